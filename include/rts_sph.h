@@ -1,0 +1,200 @@
+/*
+ * rts_sph.h -- C ABI of librtssph.so, the B200 (sm_100a) kernels behind the
+ * RTS-SPH drop-in (arXiv 2009.14514; reference package rts_sph at
+ * /root/reference/pkg/src/rts_sph).
+ *
+ * The reference has no FFI: its operator seam is a set of Numba @njit loops
+ * called from Python with caller-owned arrays.  Each entry point below
+ * replaces one of those loops (or one numpy pass around them) and cites it.
+ *
+ * Conventions
+ *   - All pointers are device pointers owned by the caller (the Python host
+ *     package allocates them with torch); the library never allocates or
+ *     frees device memory.
+ *   - `stream` is a cudaStream_t passed as void*; every entry point only
+ *     enqueues work on it (asynchronous, no host synchronisation).
+ *   - Return value: 0 on success, otherwise a cudaError_t code from the
+ *     launch.  Data errors (escaped particles, overflow, non-finite
+ *     density, iteration cap) never return non-zero: kernels record them in
+ *     RtsCounters.err_flags, which the host reads once per step / minor step
+ *     and raises as NumericalError with the reference's message.
+ *   - Once a fatal flag is set, every later kernel of the step returns
+ *     immediately, so the state is left as it was when the step began, as
+ *     with the reference's exceptions.
+ *   - Particle state is fp32 (float3 rows); geometry decisions (block keys,
+ *     r^2 < h^2 membership, region levels) and the density / EOS sums are
+ *     evaluated in fp64 with un-fused operations in the reference's order.
+ */
+#ifndef RTS_SPH_H
+#define RTS_SPH_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RTS_ABI_VERSION 4
+
+/* err_flags bits */
+#define RTS_ERR_ESCAPED   0x1u  /* fluid left the padded grid or non-finite (grid.py:268-273) */
+#define RTS_ERR_OVERFLOW  0x2u  /* > width true neighbours (grid.py:327-331) */
+#define RTS_ERR_NONFINITE 0x4u  /* non-finite density (wcsph.py:286-287, pcisph.py:680-681) */
+#define RTS_ERR_ITERCAP   0x8u  /* pressure solve hit the cap (pcisph.py:711-715) */
+#define RTS_ERR_FATAL     0xFu
+
+/* Scalar constants of one solver, fp64 values computed by the Python host
+ * with the reference's own expressions (scene.py, kernels.py:58-80,
+ * wcsph.py:143-150, pcisph.py:308-321). */
+typedef struct RtsParams {
+    double origin[3];      /* grid.py:225-229 */
+    double grid_hi[3];     /* origin + dims*block, domain-check bound (grid.py:266) */
+    double block_size;
+    double inv_block;
+    double h, h2, c_poly6, c_spiky, c_visc;
+    double mass, inv_mass, rho0, b_stiff, mu;
+    double clamp_lo[3], clamp_hi[3];   /* wcsph.py:171-172 */
+    double gravity[3];
+    double dt;             /* step length of this call */
+    double dt_base, lambda_v, lambda_f, sound_speed, alpha;
+    double betas[8];       /* scene.py:130-139, index = region id */
+    double eta_max, eta_avg, rho_T, delta;   /* PCISPH (scene.py:91-93, pcisph.py:359-361) */
+    int32_t dims[3];
+    int32_t n_cells;
+    int32_t n_fluid;
+    int32_t n_bound;
+    int32_t n_bcells;      /* distinct cells holding boundary particles */
+    int32_t width;         /* neighbour table width (wcsph.py:35) */
+    int32_t n_max;         /* largest region id for assign_regions */
+    int32_t use_sound;     /* WCSPH uses the acoustic criterion */
+    int32_t pin_region;    /* 0 = off, else force every occupied block */
+    int32_t apply_correction;
+    int32_t rts;           /* 1 = regional mode, 0 = synchronous baseline */
+    int32_t n_sms;         /* grid sizing for persistent kernels */
+    int32_t pad0, pad1;
+} RtsParams;
+
+/* Device-side counters; copied to the host once per step. */
+typedef struct RtsCounters {
+    uint32_t err_flags;
+    int32_t  n_escaped;        /* count of bad fluid rows */
+    int32_t  first_escaped;    /* lowest bad index (INT32_MAX if none) */
+    int32_t  n_compute;        /* active particles this step */
+    int64_t  overflow;         /* neighbour entries beyond width */
+    int32_t  n_sorted;         /* fluid + active boundary in the CSR */
+    int32_t  n_pred;           /* PCISPH: |pred set| of the current iteration */
+    int32_t  n_force;          /* PCISPH: |force set| of the current iteration */
+    int32_t  n_list;           /* generic compacted list length */
+    uint64_t fmax_bits;        /* max |F| over fluid (baseline CFL), double bits */
+    double   sum_rho;          /* PCISPH: sum of rho* over fluid */
+    double   max_err;          /* PCISPH: max err over fluid */
+    int32_t  any_se;           /* PCISPH: any particle in S_e */
+    int32_t  pad;
+    double   reserved[8];
+} RtsCounters;
+
+/* Buffers: every pointer is caller-owned device memory. Sizes in comments,
+ * Nf = n_fluid, Nb = n_bound, Nc = n_cells, Bc = n_bcells. */
+typedef struct RtsBuffers {
+    /* canonical particle state (index = reference particle index) */
+    float   *pos;          /* (Nf+Nb, 3) */
+    float   *vel;          /* (Nf, 3) */
+    float   *acc;          /* (Nf, 3)  WCSPH */
+    float   *acc_prev;     /* (Nf, 3)  WCSPH */
+    float   *force;        /* (Nf, 3)  WCSPH force / PCISPH f_ext */
+    float   *f_p;          /* (Nf, 3)  PCISPH pressure force */
+    float   *rho;          /* (Nf)     WCSPH rho / PCISPH rho_star */
+    float   *pres;         /* (Nf)     WCSPH pres / PCISPH p */
+    double  *err;          /* (Nf)     PCISPH err (fp64: S_e threshold decisions) */
+    float   *xstar;        /* (Nf, 3)  PCISPH x* */
+    double  *dt_since;     /* (Nf) */
+    double  *dt_corr;      /* (Nf) */
+    int32_t *validity;     /* (Nf) */
+    int8_t  *region;       /* (Nf) */
+    uint8_t *compute;      /* (Nf) */
+    uint8_t *in_se;        /* (Nf) */
+    uint8_t *in_sob;       /* (Nf) */
+    /* block grid */
+    int32_t *fluid_cells;  /* (Nf) */
+    int32_t *cell_count;   /* (Nc) fluid count per block */
+    int32_t *cell_bcount;  /* (Nc) active boundary count per block (0 off boundary blocks) */
+    int32_t *starts;       /* (Nc+1) CSR starts (grid.py:291) */
+    int32_t *order;        /* (Nf+Nb) CSR members (grid.py:293) */
+    int32_t *fill;         /* (Nc) scratch */
+    int32_t *scan_tmp;     /* (>= 2*ceil(Nc/1024)+64) scratch */
+    int32_t *bcell_ids;    /* (Bc) sorted block ids holding boundary particles */
+    int32_t *bcell_start;  /* (Bc+1) CSR into bidx */
+    int32_t *bidx;         /* (Nb) boundary particle indices (Nf + b), grouped by block */
+    int32_t *bcell_of;     /* (Nb) block id of each boundary particle */
+    uint8_t *bcell_active; /* (Bc) */
+    /* block fields */
+    double  *vmax;         /* (Nc) per-block max |v| (grid.py:347) */
+    double  *fmax;         /* (Nc) per-block max |F| */
+    int8_t  *block_raw;    /* (Nc) assign_regions output */
+    int8_t  *block_field;  /* (Nc) smoothed (and expanded) region field */
+    int8_t  *block_tmp;    /* (Nc) scratch */
+    uint8_t *block_flag;   /* (Nc) scratch mask (S_e blocks / observed) */
+    /* sorted candidate copies, slot k of the CSR */
+    float   *cpos;         /* (Nf+Nb, 4)  x y z p   (p = -1 marks a boundary slot) */
+    float   *cvel;         /* (Nf+Nb, 4)  vx vy vz rho */
+    int32_t *active;       /* (Nf) compacted CSR slots of active fluid particles */
+    int32_t *list2;        /* (Nf) second compacted list */
+    /* PCISPH neighbour tables */
+    int32_t *nbr;          /* (Nf, width) neighbour particle indices (grid.py:146-149) */
+    int32_t *cnt;          /* (Nf) */
+    float   *xs4;          /* (Nf+Nb, 4) fluid: x* p ; wall: pos -1 */
+    uint8_t *pflag;        /* (Nf) per-iteration set bits (1 = force set) */
+    double  *partial;      /* (>= 4096) deterministic reduction partials */
+    float   *snap_p;       /* (Nf)    local-phase snapshot of p */
+    float   *snap_fp;      /* (Nf, 3) local-phase snapshot of f_p */
+    RtsCounters *ctr;
+} RtsBuffers;
+
+/* ---- library ---------------------------------------------------------- */
+int rts_abi_version(void);
+/* Query the current device; returns its SM count or a negative cudaError. */
+int rts_device_sms(void);
+/* Zero-filled cudaMemsetAsync helper so hosts need not link cudart. */
+int rts_memset(void *dst, int value, int64_t bytes, void *stream);
+
+/* ---- block grid (grid.py) -------------------------------------------- */
+/* One-time static binning of the boundary shell: bcell_of, and
+ * bcell_ids/bcell_start/bidx (host computes the sort; see grid.py:279-290). */
+/* Fluid block keys, domain check, occupancy counts; per-block max |v|, |F|
+ * when want_maxima (grid.py:248-277, grid.py:155-162, wcsph.py:239-240,
+ * pcisph.py:509-510 where `force` holds f_ext and f_p is added). */
+int rts_grid_keys(const RtsParams *p, const RtsBuffers *b, int want_maxima, int add_fp,
+                  void *stream);
+/* Boundary culling by 1-dilated occupancy, exclusive scan of block counts,
+ * stable scatter into (starts, order): fluid ascending then active boundary
+ * ascending within each block (grid.py:279-293, _counting_sort grid.py:70-85). */
+int rts_grid_sort(const RtsParams *p, const RtsBuffers *b, void *stream);
+/* Per-block maxima only (reduce_fluid_max, grid.py:347-351) on current
+ * fluid_cells; f_p added to force when add_fp. */
+int rts_block_maxima(const RtsParams *p, const RtsBuffers *b, int add_fp, void *stream);
+
+/* ---- region fields (regions.py) -------------------------------------- */
+/* assign_regions (regions.py:38-75) then smooth_regions (regions.py:78-91)
+ * into block_field; expand_fast_regions (regions.py:94-107) when expand;
+ * pin_region override (wcsph.py:258-259, pcisph.py:528-529). */
+int rts_block_levels(const RtsParams *p, const RtsBuffers *b, int expand, void *stream);
+
+/* ---- RTS-WCSPH (wcsph.py) -------------------------------------------- */
+/* Validity countdown / pre-emption (wcsph.py:262-266) fused with the sorted
+ * candidate gather and the active-list compaction. rts=0: all active. */
+int rts_wcsph_propagate(const RtsParams *p, const RtsBuffers *b, void *stream);
+/* Density + clamped Tait pressure for active particles (wcsph.py:45-60)
+ * over the on-the-fly 3x3x3 block search (grid.py:88-152, layers=1). */
+int rts_wcsph_density(const RtsParams *p, const RtsBuffers *b, void *stream);
+/* dt_corr/dt_since/acc_prev bookkeeping (wcsph.py:288-290), forces
+ * (wcsph.py:63-105) and acc = F/m (wcsph.py:296). */
+int rts_wcsph_forces(const RtsParams *p, const RtsBuffers *b, void *stream);
+/* Predictor for all, corrector for active, clamp (wcsph.py:299-319). */
+int rts_wcsph_integrate(const RtsParams *p, const RtsBuffers *b, void *stream);
+/* max |F| over fluid into ctr->fmax_bits (cfl_bound, wcsph.py:182-189). */
+int rts_force_max(const RtsParams *p, const RtsBuffers *b, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RTS_SPH_H */

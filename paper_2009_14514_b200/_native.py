@@ -1,0 +1,110 @@
+"""ctypes binding of ``librtssph.so`` (C ABI in ``include/rts_sph.h``).
+
+The library is the only compute path of this package: if it is missing or
+there is no CUDA device, constructing a solver raises -- there is no CPU
+fallback.  Structures mirror the header field for field.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librtssph.so")
+ABI_VERSION = 4
+
+_c = ctypes
+_D = _c.c_double
+_I = _c.c_int32
+_P = _c.c_void_p
+
+
+class RtsParams(_c.Structure):
+    _fields_ = [
+        ("origin", _D * 3), ("grid_hi", _D * 3), ("block_size", _D), ("inv_block", _D),
+        ("h", _D), ("h2", _D), ("c_poly6", _D), ("c_spiky", _D), ("c_visc", _D),
+        ("mass", _D), ("inv_mass", _D), ("rho0", _D), ("b_stiff", _D), ("mu", _D),
+        ("clamp_lo", _D * 3), ("clamp_hi", _D * 3), ("gravity", _D * 3), ("dt", _D),
+        ("dt_base", _D), ("lambda_v", _D), ("lambda_f", _D), ("sound_speed", _D), ("alpha", _D),
+        ("betas", _D * 8), ("eta_max", _D), ("eta_avg", _D), ("rho_T", _D), ("delta", _D),
+        ("dims", _I * 3), ("n_cells", _I), ("n_fluid", _I), ("n_bound", _I), ("n_bcells", _I),
+        ("width", _I), ("n_max", _I), ("use_sound", _I), ("pin_region", _I),
+        ("apply_correction", _I), ("rts", _I), ("n_sms", _I), ("pad0", _I), ("pad1", _I),
+    ]
+
+
+class RtsCounters(_c.Structure):
+    _fields_ = [
+        ("err_flags", _c.c_uint32), ("n_escaped", _I), ("first_escaped", _I), ("n_compute", _I),
+        ("overflow", _c.c_int64), ("n_sorted", _I), ("n_pred", _I), ("n_force", _I),
+        ("n_list", _I), ("fmax_bits", _c.c_uint64), ("sum_rho", _D), ("max_err", _D),
+        ("any_se", _I), ("pad", _I), ("reserved", _D * 8),
+    ]
+
+
+BUFFER_FIELDS = (
+    "pos", "vel", "acc", "acc_prev", "force", "f_p", "rho", "pres", "err", "xstar", "dt_since",
+    "dt_corr", "validity", "region", "compute", "in_se", "in_sob", "fluid_cells", "cell_count",
+    "cell_bcount", "starts", "order", "fill", "scan_tmp", "bcell_ids", "bcell_start", "bidx",
+    "bcell_of", "bcell_active", "vmax", "fmax", "block_raw", "block_field", "block_tmp",
+    "block_flag", "cpos", "cvel", "active", "list2", "nbr", "cnt", "xs4", "pflag", "partial",
+    "snap_p", "snap_fp", "ctr",
+)
+
+
+class RtsBuffers(_c.Structure):
+    _fields_ = [(name, _P) for name in BUFFER_FIELDS]
+
+
+ERR_ESCAPED, ERR_OVERFLOW, ERR_NONFINITE, ERR_ITERCAP = 0x1, 0x2, 0x4, 0x8
+
+# entry points: name -> argtypes (all return int)
+_PP = _c.POINTER(RtsParams)
+_PB = _c.POINTER(RtsBuffers)
+SIGNATURES = {
+    "rts_abi_version": [],
+    "rts_device_sms": [],
+    "rts_memset": [_P, _c.c_int, _c.c_int64, _P],
+    "rts_grid_keys": [_PP, _PB, _c.c_int, _c.c_int, _P],
+    "rts_grid_sort": [_PP, _PB, _P],
+    "rts_block_maxima": [_PP, _PB, _c.c_int, _P],
+    "rts_force_max": [_PP, _PB, _P],
+    "rts_block_levels": [_PP, _PB, _c.c_int, _P],
+    "rts_wcsph_propagate": [_PP, _PB, _P],
+    "rts_wcsph_density": [_PP, _PB, _P],
+    "rts_wcsph_forces": [_PP, _PB, _P],
+    "rts_wcsph_integrate": [_PP, _PB, _P],
+}
+
+_lib = None
+
+
+class NativeError(RuntimeError):
+    pass
+
+
+def load(path: str = LIB_PATH):
+    """Load the library (no CUDA call is made); raises if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise NativeError(
+            f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+            " (there is no CPU fallback)")
+    lib = _c.CDLL(path)
+    for name, args in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = _c.c_int
+    if lib.rts_abi_version() != ABI_VERSION:
+        raise NativeError(f"librtssph ABI {lib.rts_abi_version()} != expected {ABI_VERSION}")
+    _lib = lib
+    return lib
+
+
+def call(name: str, *args) -> None:
+    rc = getattr(load(), name)(*args)
+    if rc != 0:
+        raise NativeError(f"{name} failed with cudaError {rc}")

@@ -1,0 +1,112 @@
+// Shared device helpers for librtssph (sm_100a).
+//
+// Parity-critical arithmetic (block keys, r^2 < h^2 membership, density and
+// EOS sums, level classification) is fp64 with explicitly rounded, never
+// fused operations (__dadd_rn / __dmul_rn / ...), in the operand order of
+// the reference's Python/numba expressions, so that from a common fp32
+// state the B200 results equal the reference's fp64 results exactly (or up
+// to the final fp32 store).  The library is also compiled with
+// --fmad=false as a second line of defence.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/rts_sph.h"
+
+#define RTS_DEV __device__ __forceinline__
+
+namespace rts {
+
+RTS_DEV double xadd(double a, double b) { return __dadd_rn(a, b); }
+RTS_DEV double xsub(double a, double b) { return __dsub_rn(a, b); }
+RTS_DEV double xmul(double a, double b) { return __dmul_rn(a, b); }
+RTS_DEV double xdiv(double a, double b) { return __ddiv_rn(a, b); }
+RTS_DEV double xsqrt(double a) { return __dsqrt_rn(a); }
+
+// ((dx*dx + dy*dy) + dz*dz), the numba/numpy evaluation order.
+RTS_DEV double dist2(double dx, double dy, double dz) {
+    return xadd(xadd(xmul(dx, dx), xmul(dy, dy)), xmul(dz, dz));
+}
+
+// poly6 W(r^2) = ((c*d)*d)*d, d = h2 - r2 (kernels.py:23-32)
+RTS_DEV double poly6(double r2, double h2, double c) {
+    const double d = xsub(h2, r2);
+    if (d <= 0.0) return 0.0;
+    return xmul(xmul(xmul(c, d), d), d);
+}
+// spiky gradient factor ((c*d)*d)/r, d = h - r (kernels.py:35-46)
+RTS_DEV double spiky(double r, double h, double c) {
+    if (r <= 0.0 || r >= h) return 0.0;
+    const double d = xsub(h, r);
+    return xdiv(xmul(xmul(c, d), d), r);
+}
+// viscosity Laplacian c*(h - r) (kernels.py:49-55)
+RTS_DEV double visc_lap(double r, double h, double c) {
+    const double d = xsub(h, r);
+    if (d <= 0.0) return 0.0;
+    return xmul(c, d);
+}
+
+// np.floor((x - origin) * inv_block), clipped to [0, n-1] (grid.py:248-250)
+RTS_DEV int cell_axis(double x, double o, double inv, int n) {
+    const double v = floor(xmul(xsub(x, o), inv));
+    if (!(v >= 0.0)) return 0;  // also catches NaN (those rows are flagged anyway)
+    if (v >= (double)(n - 1)) return n - 1;
+    return (int)v;
+}
+
+RTS_DEV int cell_of(const RtsParams &p, double x, double y, double z) {
+    const int cx = cell_axis(x, p.origin[0], p.inv_block, p.dims[0]);
+    const int cy = cell_axis(y, p.origin[1], p.inv_block, p.dims[1]);
+    const int cz = cell_axis(z, p.origin[2], p.inv_block, p.dims[2]);
+    return (cx * p.dims[1] + cy) * p.dims[2] + cz;
+}
+
+// |v| = sqrt((x^2 + y^2) + z^2) in fp64 (np.linalg.norm(axis=1))
+RTS_DEV double norm3(float x, float y, float z) {
+    return xsqrt(dist2((double)x, (double)y, (double)z));
+}
+
+// max of non-negative doubles via their bit patterns (monotone for >= 0)
+RTS_DEV void atomic_max_pos(double *addr, double v) {
+    if (v > 0.0)  // NaN and 0 never raise a maximum (matches `if v > out[c]`)
+        atomicMax(reinterpret_cast<unsigned long long *>(addr),
+                  (unsigned long long)__double_as_longlong(v));
+}
+
+RTS_DEV bool fatal(const RtsCounters *c) {
+    return (*(volatile const uint32_t *)&c->err_flags) & RTS_ERR_FATAL;
+}
+
+// warp-aggregated append of `pred` lanes to list[*count]
+RTS_DEV void warp_append(bool pred, int value, int *list, int *count) {
+    const unsigned mask = __ballot_sync(0xffffffffu, pred);
+    if (!mask) return;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(mask) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(count, __popc(mask));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (pred) list[base + __popc(mask & ((1u << lane) - 1u))] = value;
+}
+
+RTS_DEV int warp_count_add(bool pred, int *count) {
+    const unsigned mask = __ballot_sync(0xffffffffu, pred);
+    const int lane = threadIdx.x & 31;
+    if (mask && lane == __ffs(mask) - 1) atomicAdd(count, __popc(mask));
+    return __popc(mask);
+}
+
+}  // namespace rts
+
+// launch helpers
+static inline int rts_blocks(long long n, int threads, int cap = 148 * 32) {
+    long long b = (n + threads - 1) / threads;
+    if (b < 1) b = 1;
+    if (b > cap) b = cap;
+    return (int)b;
+}
+
+#define RTS_LAUNCH_CHECK() \
+    do { cudaError_t e__ = cudaGetLastError(); if (e__ != cudaSuccess) return (int)e__; } while (0)

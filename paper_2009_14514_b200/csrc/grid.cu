@@ -1,0 +1,328 @@
+// Block grid on the B200: keys, occupancy, boundary culling, stable counting
+// sort into the CSR (starts, order) of the reference's BlockGrid
+// (/root/reference/pkg/src/rts_sph/grid.py:220-394).
+//
+// Data layout (HBM): per-particle rows are canonical (reference index);
+// per-block fields are dense over the padded grid dims, linearised
+// (cx*ny + cy)*nz + cz (grid.py:252-255), so the three z-adjacent blocks of
+// a 3x3x3 neighbourhood are contiguous in the CSR.
+//
+// Sort: fluid rows atomically bump their block count (integer, so
+// deterministic); an exclusive scan gives `starts`; fluid rows scatter with
+// an atomic cursor and each block's fluid run is then re-sorted by index,
+// which restores the reference's stable order (fluid ascending, then active
+// boundary ascending, grid.py:283-293) independent of atomic timing.
+#include "common.cuh"
+
+using namespace rts;
+
+namespace {
+
+constexpr int kThreads = 256;
+
+// grid.py:257-277 (+ reduce_fluid_max, grid.py:155-162 / wcsph.py:239-240)
+__global__ void k_fluid_keys(const __grid_constant__ RtsParams p, RtsBuffers b, int want_maxima,
+                             int add_fp) {
+    const int nf = p.n_fluid;
+    const int stride = gridDim.x * blockDim.x;
+    for (int base = blockIdx.x * blockDim.x; base < nf; base += stride) {
+        const int i = base + threadIdx.x;
+        if (i >= nf) break;
+        const double x = b.pos[3 * i], y = b.pos[3 * i + 1], z = b.pos[3 * i + 2];
+        const bool ok = (x >= p.origin[0]) && (x <= p.grid_hi[0]) && (y >= p.origin[1]) &&
+                        (y <= p.grid_hi[1]) && (z >= p.origin[2]) && (z <= p.grid_hi[2]) &&
+                        isfinite(x) && isfinite(y) && isfinite(z);
+        if (!ok) {
+            atomicOr(&b.ctr->err_flags, RTS_ERR_ESCAPED);
+            atomicAdd(&b.ctr->n_escaped, 1);
+            atomicMin(&b.ctr->first_escaped, i);
+        }
+        const int c = cell_of(p, x, y, z);
+        b.fluid_cells[i] = c;
+        atomicAdd(&b.cell_count[c], 1);
+        if (want_maxima) {
+            atomic_max_pos(&b.vmax[c], norm3(b.vel[3 * i], b.vel[3 * i + 1], b.vel[3 * i + 2]));
+            double fx = b.force[3 * i], fy = b.force[3 * i + 1], fz = b.force[3 * i + 2];
+            if (add_fp) {  // |f_ext + f_p| (pcisph.py:510), sum formed in fp64 like numpy
+                fx = xadd(fx, (double)b.f_p[3 * i]);
+                fy = xadd(fy, (double)b.f_p[3 * i + 1]);
+                fz = xadd(fz, (double)b.f_p[3 * i + 2]);
+                atomic_max_pos(&b.fmax[c], xsqrt(dist2(fx, fy, fz)));
+            } else {
+                atomic_max_pos(&b.fmax[c], xsqrt(dist2(fx, fy, fz)));
+            }
+        }
+    }
+}
+
+__global__ void k_block_maxima(const __grid_constant__ RtsParams p, RtsBuffers b, int add_fp) {
+    const int nf = p.n_fluid;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nf; i += gridDim.x * blockDim.x) {
+        const int c = b.fluid_cells[i];
+        atomic_max_pos(&b.vmax[c], norm3(b.vel[3 * i], b.vel[3 * i + 1], b.vel[3 * i + 2]));
+        double fx = b.force[3 * i], fy = b.force[3 * i + 1], fz = b.force[3 * i + 2];
+        if (add_fp) {
+            fx = xadd(fx, (double)b.f_p[3 * i]);
+            fy = xadd(fy, (double)b.f_p[3 * i + 1]);
+            fz = xadd(fz, (double)b.f_p[3 * i + 2]);
+        }
+        atomic_max_pos(&b.fmax[c], xsqrt(dist2(fx, fy, fz)));
+    }
+}
+
+// boundary culling: a wall block participates iff a fluid particle occupies
+// it or one of its 26 neighbours (dilate_mask(occupancy, 1), grid.py:279-290)
+__global__ void k_boundary_active(const __grid_constant__ RtsParams p, RtsBuffers b) {
+    if (fatal(b.ctr)) return;
+    const int nx = p.dims[0], ny = p.dims[1], nz = p.dims[2];
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < p.n_bcells;
+         t += gridDim.x * blockDim.x) {
+        const int c = b.bcell_ids[t];
+        const int cz = c % nz, cy = (c / nz) % ny, cx = c / (ny * nz);
+        bool allowed = false;
+        for (int ax = max(0, cx - 1); ax <= min(nx - 1, cx + 1) && !allowed; ++ax)
+            for (int ay = max(0, cy - 1); ay <= min(ny - 1, cy + 1) && !allowed; ++ay) {
+                const int base = (ax * ny + ay) * nz;
+                for (int az = max(0, cz - 1); az <= min(nz - 1, cz + 1); ++az)
+                    if (b.cell_count[base + az] > 0) { allowed = true; break; }
+            }
+        b.bcell_active[t] = allowed;
+        b.cell_bcount[c] = allowed ? (b.bcell_start[t + 1] - b.bcell_start[t]) : 0;
+    }
+}
+
+// ---- exclusive scan of (cell_count + cell_bcount) into starts ----------
+constexpr int kScanThreads = 1024;
+constexpr int kScanItems = 4;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__device__ __forceinline__ int block_incl_scan(int v, int *warp_sums) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int n = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += n;
+    }
+    if (lane == 31) warp_sums[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        int s = lane < (int)(blockDim.x >> 5) ? warp_sums[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int n = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= o) s += n;
+        }
+        warp_sums[lane] = s;
+    }
+    __syncthreads();
+    if (warp > 0) v += warp_sums[warp - 1];
+    return v;
+}
+
+template <bool kFromCounts>
+__global__ void __launch_bounds__(kScanThreads) k_scan_tiles(const int *a, const int *a2, int n,
+                                                             int *out_excl, int *tile_sums) {
+    __shared__ int warp_sums[32];
+    const int tile0 = blockIdx.x * kScanTile;
+    int v[kScanItems];
+    int local = 0;
+#pragma unroll
+    for (int q = 0; q < kScanItems; ++q) {
+        const int idx = tile0 + threadIdx.x * kScanItems + q;
+        int x = 0;
+        if (idx < n) x = kFromCounts ? (a[idx] + a2[idx]) : a[idx];
+        v[q] = x;
+        local += x;
+    }
+    const int incl = block_incl_scan(local, warp_sums);
+    int run = incl - local;
+#pragma unroll
+    for (int q = 0; q < kScanItems; ++q) {
+        const int idx = tile0 + threadIdx.x * kScanItems + q;
+        if (idx < n) out_excl[idx] = run;
+        run += v[q];
+    }
+    if (threadIdx.x == blockDim.x - 1) tile_sums[blockIdx.x] = incl;
+}
+
+__global__ void k_scan_add(int *out, int n, const int *tile_offsets) {
+    const int tile = blockIdx.x;
+    const int add = tile_offsets[tile];
+    if (add == 0) return;
+    for (int q = threadIdx.x; q < kScanTile; q += blockDim.x) {
+        const int idx = tile * kScanTile + q;
+        if (idx < n) out[idx] += add;
+    }
+}
+
+__global__ void k_scan_finish(const __grid_constant__ RtsParams p, RtsBuffers b) {
+    // starts[n_cells] = total members
+    const int nc = p.n_cells;
+    const int last = b.starts[nc - 1] + b.cell_count[nc - 1] + b.cell_bcount[nc - 1];
+    b.starts[nc] = last;
+    b.ctr->n_sorted = last;
+}
+
+// recursive tile scan: exclusive scan of a[0..n) into out (a2 added when kFromCounts)
+int scan_exclusive(const int *a, const int *a2, int n, int *out, int *tmp, cudaStream_t s,
+                   bool from_counts) {
+    const int tiles = (n + kScanTile - 1) / kScanTile;
+    int *sums = tmp;
+    int *offs = tmp + tiles;
+    if (from_counts)
+        k_scan_tiles<true><<<tiles, kScanThreads, 0, s>>>(a, a2, n, out, sums);
+    else
+        k_scan_tiles<false><<<tiles, kScanThreads, 0, s>>>(a, a2, n, out, sums);
+    RTS_LAUNCH_CHECK();
+    if (tiles > 1) {
+        int rc = scan_exclusive(sums, nullptr, tiles, offs, tmp + 2 * tiles, s, false);
+        if (rc) return rc;
+        k_scan_add<<<tiles, 256, 0, s>>>(out, n, offs);
+        RTS_LAUNCH_CHECK();
+    }
+    return 0;
+}
+
+// stable scatter, step 1: atomic cursor per block
+__global__ void k_scatter_fluid(const __grid_constant__ RtsParams p, RtsBuffers b) {
+    if (fatal(b.ctr)) return;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.n_fluid;
+         i += gridDim.x * blockDim.x) {
+        const int c = b.fluid_cells[i];
+        const int slot = b.starts[c] + atomicAdd(&b.fill[c], 1);
+        b.order[slot] = i;
+    }
+}
+
+// step 2: restore ascending index order inside each block's fluid run
+__global__ void k_sort_runs(const __grid_constant__ RtsParams p, RtsBuffers b) {
+    if (fatal(b.ctr)) return;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < p.n_cells;
+         c += gridDim.x * blockDim.x) {
+        const int n = b.cell_count[c];
+        if (n < 2) continue;
+        int *run = b.order + b.starts[c];
+        if (n <= 32) {
+            int v[32];
+            for (int q = 0; q < n; ++q) v[q] = run[q];
+            for (int q = 1; q < n; ++q) {
+                const int key = v[q];
+                int r = q - 1;
+                while (r >= 0 && v[r] > key) { v[r + 1] = v[r]; --r; }
+                v[r + 1] = key;
+            }
+            for (int q = 0; q < n; ++q) run[q] = v[q];
+        } else {
+            for (int q = 1; q < n; ++q) {
+                const int key = run[q];
+                int r = q - 1;
+                while (r >= 0 && run[r] > key) { run[r + 1] = run[r]; --r; }
+                run[r + 1] = key;
+            }
+        }
+    }
+}
+
+// step 3: active wall blocks append their (statically sorted) boundary rows
+__global__ void k_scatter_boundary(const __grid_constant__ RtsParams p, RtsBuffers b) {
+    if (fatal(b.ctr)) return;
+    // one warp per wall block
+    const int lane = threadIdx.x & 31;
+    const int warps = (gridDim.x * blockDim.x) >> 5;
+    for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < p.n_bcells; t += warps) {
+        if (!b.bcell_active[t]) continue;
+        const int c = b.bcell_ids[t];
+        const int dst = b.starts[c] + b.cell_count[c];
+        const int s0 = b.bcell_start[t], s1 = b.bcell_start[t + 1];
+        for (int q = s0 + lane; q < s1; q += 32) b.order[dst + (q - s0)] = b.bidx[q];
+    }
+}
+
+__global__ void k_force_max(const __grid_constant__ RtsParams p, RtsBuffers b) {
+    double m = 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.n_fluid;
+         i += gridDim.x * blockDim.x) {
+        const double f = norm3(b.force[3 * i], b.force[3 * i + 1], b.force[3 * i + 2]);
+        if (f > m) m = f;
+    }
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m > 0.0)
+        atomicMax(reinterpret_cast<unsigned long long *>(&b.ctr->fmax_bits),
+                  (unsigned long long)__double_as_longlong(m));
+}
+
+}  // namespace
+
+extern "C" {
+
+int rts_grid_keys(const RtsParams *p, const RtsBuffers *b, int want_maxima, int add_fp,
+                  void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaMemsetAsync(b->cell_count, 0, sizeof(int) * (size_t)p->n_cells, s);
+    if (want_maxima) {
+        cudaMemsetAsync(b->vmax, 0, sizeof(double) * (size_t)p->n_cells, s);
+        cudaMemsetAsync(b->fmax, 0, sizeof(double) * (size_t)p->n_cells, s);
+    }
+    k_fluid_keys<<<rts_blocks(p->n_fluid, kThreads), kThreads, 0, s>>>(*p, *b, want_maxima,
+                                                                        add_fp);
+    RTS_LAUNCH_CHECK();
+    return 0;
+}
+
+int rts_block_maxima(const RtsParams *p, const RtsBuffers *b, int add_fp, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaMemsetAsync(b->vmax, 0, sizeof(double) * (size_t)p->n_cells, s);
+    cudaMemsetAsync(b->fmax, 0, sizeof(double) * (size_t)p->n_cells, s);
+    k_block_maxima<<<rts_blocks(p->n_fluid, kThreads), kThreads, 0, s>>>(*p, *b, add_fp);
+    RTS_LAUNCH_CHECK();
+    return 0;
+}
+
+int rts_grid_sort(const RtsParams *p, const RtsBuffers *b, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (p->n_bcells > 0) {
+        k_boundary_active<<<rts_blocks(p->n_bcells, kThreads), kThreads, 0, s>>>(*p, *b);
+        RTS_LAUNCH_CHECK();
+    }
+    int rc = scan_exclusive(b->cell_count, b->cell_bcount, p->n_cells, b->starts, b->scan_tmp, s,
+                            true);
+    if (rc) return rc;
+    k_scan_finish<<<1, 1, 0, s>>>(*p, *b);
+    RTS_LAUNCH_CHECK();
+    cudaMemsetAsync(b->fill, 0, sizeof(int) * (size_t)p->n_cells, s);
+    k_scatter_fluid<<<rts_blocks(p->n_fluid, kThreads), kThreads, 0, s>>>(*p, *b);
+    RTS_LAUNCH_CHECK();
+    k_sort_runs<<<rts_blocks(p->n_cells, kThreads), kThreads, 0, s>>>(*p, *b);
+    RTS_LAUNCH_CHECK();
+    if (p->n_bcells > 0) {
+        k_scatter_boundary<<<rts_blocks((long long)p->n_bcells * 32, kThreads), kThreads, 0, s>>>(
+            *p, *b);
+        RTS_LAUNCH_CHECK();
+    }
+    return 0;
+}
+
+int rts_force_max(const RtsParams *p, const RtsBuffers *b, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    k_force_max<<<rts_blocks(p->n_fluid, kThreads, 148 * 8), kThreads, 0, s>>>(*p, *b);
+    RTS_LAUNCH_CHECK();
+    return 0;
+}
+
+int rts_abi_version(void) { return RTS_ABI_VERSION; }
+
+int rts_device_sms(void) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return -(int)e;
+    int sms = 0;
+    e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return -(int)e;
+    return sms;
+}
+
+int rts_memset(void *dst, int value, int64_t bytes, void *stream) {
+    return (int)cudaMemsetAsync(dst, value, (size_t)bytes, (cudaStream_t)stream);
+}
+
+}  // extern "C"

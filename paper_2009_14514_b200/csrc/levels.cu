@@ -1,0 +1,141 @@
+// Region fields on the B200 (reference: /root/reference/pkg/src/rts_sph/regions.py).
+//
+// assign_regions (regions.py:38-75) is evaluated per block in fp64 with the
+// reference's operation order, so levels are bit-identical given the same
+// per-block maxima.  smooth_regions (regions.py:78-91) is a 26-neighbour min
+// stencil; expand_fast_regions (regions.py:94-107) is a Chebyshev-4
+// dilation done as three separable width-9 passes over a 2-bit mask.
+#include "common.cuh"
+
+using namespace rts;
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int8_t kEmpty = 127;  // regions.py:35
+
+__global__ void k_assign(const __grid_constant__ RtsParams p, RtsBuffers b) {
+    if (fatal(b.ctr)) return;
+    const double r = p.block_size;
+    const double sound_bound = xdiv(xmul(p.lambda_v, r), p.sound_speed);
+    const double rm = xmul(r, p.mass);
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < p.n_cells;
+         c += gridDim.x * blockDim.x) {
+        const bool occ = b.cell_count[c] > 0;
+        int8_t region = occ ? 1 : 0;
+        if (occ) {
+            const double vmax = b.vmax[c], fmax = b.fmax[c];
+            // lambda_f * sqrt(r*m / f_max); f_max == 0 -> inf (numpy divide)
+            const double fb = xmul(p.lambda_f, xsqrt(xdiv(rm, fmax)));
+            for (int n = 2; n <= p.n_max; ++n) {
+                const double dt_n = xmul((double)n, p.dt_base);
+                if (p.use_sound && !(dt_n <= sound_bound)) break;
+                bool ok = (region == n - 1);
+                ok = ok && ((fmax == 0.0) || (dt_n <= fb));
+                const double beta = p.betas[n];
+                if (isfinite(beta)) ok = ok && (xdiv(xmul(dt_n, vmax), r) <= xmul(p.alpha, beta));
+                if (ok) region = (int8_t)n;
+            }
+        }
+        b.block_raw[c] = region;
+    }
+}
+
+// new = min(own, min over 26 occupied neighbours), empty stays 0
+__global__ void k_smooth(const __grid_constant__ RtsParams p, RtsBuffers b, int8_t *out) {
+    if (fatal(b.ctr)) return;
+    const int nx = p.dims[0], ny = p.dims[1], nz = p.dims[2];
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < p.n_cells;
+         c += gridDim.x * blockDim.x) {
+        const int8_t f = b.block_raw[c];
+        int8_t res = 0;
+        if (f > 0) {
+            if (p.pin_region) {
+                res = (int8_t)p.pin_region;
+            } else {
+                const int cz = c % nz, cy = (c / nz) % ny, cx = c / (ny * nz);
+                int8_t m = kEmpty;
+                for (int ax = max(0, cx - 1); ax <= min(nx - 1, cx + 1); ++ax)
+                    for (int ay = max(0, cy - 1); ay <= min(ny - 1, cy + 1); ++ay) {
+                        const int base = (ax * ny + ay) * nz;
+                        for (int az = max(0, cz - 1); az <= min(nz - 1, cz + 1); ++az) {
+                            const int q = base + az;
+                            if (q == c) continue;
+                            const int8_t v = b.block_raw[q];
+                            if (v > 0 && v < m) m = v;
+                        }
+                    }
+                res = f < m ? f : m;
+            }
+        }
+        out[c] = res;
+    }
+}
+
+// separable Chebyshev dilation of the two masks {f==2 -> bit0, f==1 -> bit1}
+__global__ void k_dilate_axis(const __grid_constant__ RtsParams p, const int8_t *field,
+                              const uint8_t *in, uint8_t *out, int axis, int layers,
+                              int from_field) {
+    const int nx = p.dims[0], ny = p.dims[1], nz = p.dims[2];
+    const int dim = p.dims[axis];
+    const int stride = axis == 0 ? ny * nz : (axis == 1 ? nz : 1);
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < p.n_cells;
+         c += gridDim.x * blockDim.x) {
+        const int coord = axis == 0 ? c / (ny * nz) : (axis == 1 ? (c / nz) % ny : c % nz);
+        uint8_t acc = 0;
+        const int lo = max(0, coord - layers), hi = min(dim - 1, coord + layers);
+        for (int q = lo; q <= hi; ++q) {
+            const int cc = c + (q - coord) * stride;
+            uint8_t v;
+            if (from_field) {
+                const int8_t f = field[cc];
+                v = (uint8_t)((f == 2 ? 1 : 0) | (f == 1 ? 2 : 0));
+            } else {
+                v = in[cc];
+            }
+            acc |= v;
+        }
+        out[c] = acc;
+    }
+    (void)nx;
+}
+
+// regions.py:101-107: occupied blocks with a larger region inside a dilated
+// mask drop to 2, then (taking precedence) to 1
+__global__ void k_expand_apply(const __grid_constant__ RtsParams p, const int8_t *field,
+                               const uint8_t *near, int8_t *out) {
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < p.n_cells;
+         c += gridDim.x * blockDim.x) {
+        const int8_t f = field[c];
+        int8_t v = f;
+        if (f > 2 && (near[c] & 1)) v = 2;
+        if (f > 1 && (near[c] & 2)) v = 1;
+        out[c] = v;
+    }
+}
+
+}  // namespace
+
+extern "C" int rts_block_levels(const RtsParams *p, const RtsBuffers *b, int expand,
+                                void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    const int blocks = rts_blocks(p->n_cells, kThreads);
+    k_assign<<<blocks, kThreads, 0, s>>>(*p, *b);
+    RTS_LAUNCH_CHECK();
+    if (!expand || p->pin_region) {
+        k_smooth<<<blocks, kThreads, 0, s>>>(*p, *b, b->block_field);
+        RTS_LAUNCH_CHECK();
+        return 0;
+    }
+    // smoothed field into block_tmp, then expansion into block_field
+    k_smooth<<<blocks, kThreads, 0, s>>>(*p, *b, b->block_tmp);
+    RTS_LAUNCH_CHECK();
+    uint8_t *m0 = b->block_flag;
+    uint8_t *m1 = reinterpret_cast<uint8_t *>(b->block_field);  // scratch until final write
+    k_dilate_axis<<<blocks, kThreads, 0, s>>>(*p, b->block_tmp, nullptr, m0, 2, 4, 1);
+    k_dilate_axis<<<blocks, kThreads, 0, s>>>(*p, nullptr, m0, m1, 1, 4, 0);
+    k_dilate_axis<<<blocks, kThreads, 0, s>>>(*p, nullptr, m1, m0, 0, 4, 0);
+    k_expand_apply<<<blocks, kThreads, 0, s>>>(*p, b->block_tmp, m0, b->block_field);
+    RTS_LAUNCH_CHECK();
+    return 0;
+}

@@ -1,0 +1,283 @@
+// RTS-WCSPH step kernels (reference: /root/reference/pkg/src/rts_sph/wcsph.py).
+//
+// Neighbourhoods are never materialised: the density and force kernels walk
+// the 3x3x3 block neighbourhood of each active particle directly in the CSR
+// (the three z-adjacent blocks of each (x, y) column are one contiguous
+// span, so nine spans), reading the sorted candidate copies `cpos`
+// (x y z p) / `cvel` (v rho) written by the propagate pass.  The set of j
+// with r^2 < h^2 (fp64, un-fused) and the visiting order (blocks in
+// (ax, ay, az) order, CSR order inside a block) are exactly those of the
+// reference's table fill (grid.py:133-149) followed by its table walk
+// (wcsph.py:50-56, 75-101), so the fp64 sums are bit-identical to the
+// reference's from a common state; only the final fp32 store rounds.
+#include "common.cuh"
+
+using namespace rts;
+
+namespace {
+
+constexpr int kThreads = 128;
+
+// wcsph.py:262-266 (validity / pre-emption) + sorted-copy gather + active list
+__global__ void k_propagate(const __grid_constant__ RtsParams p, RtsBuffers b) {
+    if (fatal(b.ctr)) return;
+    const int n_sorted = b.ctr->n_sorted;
+    const int stride = gridDim.x * blockDim.x;
+    for (int base = blockIdx.x * blockDim.x; base < n_sorted; base += stride) {
+        const int k = base + threadIdx.x;
+        bool act = false;
+        if (k < n_sorted) {
+            const int j = b.order[k];
+            const float x = b.pos[3 * j], y = b.pos[3 * j + 1], z = b.pos[3 * j + 2];
+            if (j < p.n_fluid) {
+                reinterpret_cast<float4 *>(b.cpos)[k] = make_float4(x, y, z, b.pres[j]);
+                reinterpret_cast<float4 *>(b.cvel)[k] =
+                    make_float4(b.vel[3 * j], b.vel[3 * j + 1], b.vel[3 * j + 2], b.rho[j]);
+                if (p.rts) {
+                    const int8_t blk = b.block_field[b.fluid_cells[j]];
+                    int v = b.validity[j] - 1;
+                    const int8_t reg = b.region[j];
+                    act = (v <= 0) || (blk != reg);
+                    if (act) {
+                        b.region[j] = blk;
+                        v = blk;
+                    }
+                    b.validity[j] = v;
+                    b.compute[j] = act;
+                } else {
+                    act = true;
+                }
+            } else {
+                reinterpret_cast<float4 *>(b.cpos)[k] = make_float4(x, y, z, -1.0f);
+                reinterpret_cast<float4 *>(b.cvel)[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
+        warp_append(act, k, b.active, &b.ctr->n_compute);
+    }
+}
+
+struct Span {
+    int k0, k1;
+};
+
+// the nine CSR spans of the 3x3x3 neighbourhood of block c, (ax, ay) order
+__device__ __forceinline__ int block_spans(const RtsParams &p, const int *starts, int c,
+                                           Span *sp) {
+    const int nx = p.dims[0], ny = p.dims[1], nz = p.dims[2];
+    const int cz = c % nz, cy = (c / nz) % ny, cx = c / (ny * nz);
+    const int z0 = max(0, cz - 1), z1 = min(nz - 1, cz + 1);
+    int n = 0;
+    for (int ax = max(0, cx - 1); ax <= min(nx - 1, cx + 1); ++ax)
+        for (int ay = max(0, cy - 1); ay <= min(ny - 1, cy + 1); ++ay) {
+            const int base = (ax * ny + ay) * nz;
+            sp[n].k0 = starts[base + z0];
+            sp[n].k1 = starts[base + z1 + 1];
+            ++n;
+        }
+    return n;
+}
+
+// fp32 pre-test with a margin that can only admit, never reject, a true
+// neighbour; the fp64 test below decides membership exactly.
+__device__ __forceinline__ bool maybe_near(float4 a, float4 q, float h2_loose) {
+    const float dx = a.x - q.x, dy = a.y - q.y, dz = a.z - q.z;
+    return __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz)) <=
+           h2_loose;
+}
+
+// wcsph.py:45-60 over the on-the-fly search of grid.py:88-152
+__global__ void __launch_bounds__(kThreads) k_density(const __grid_constant__ RtsParams p,
+                                                      RtsBuffers b) {
+    if (fatal(b.ctr)) return;
+    const int n_act = b.ctr->n_compute;
+    const float4 *cpos = reinterpret_cast<const float4 *>(b.cpos);
+    const float h2_loose = (float)(p.h2 * 1.00001);
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n_act; t += gridDim.x * blockDim.x) {
+        const int k = b.active[t];
+        const int j = b.order[k];
+        const float4 a = cpos[k];
+        const double xi = a.x, yi = a.y, zi = a.z;
+        Span sp[9];
+        const int ns = block_spans(p, b.starts, b.fluid_cells[j], sp);
+        double acc = 0.0;
+        int n = 0;
+        for (int s = 0; s < ns; ++s) {
+            for (int q = sp[s].k0; q < sp[s].k1; ++q) {
+                const float4 o = cpos[q];
+                if (!maybe_near(a, o, h2_loose)) continue;
+                const double r2 = dist2(xsub(xi, (double)o.x), xsub(yi, (double)o.y),
+                                        xsub(zi, (double)o.z));
+                if (r2 < p.h2) {
+                    acc = xadd(acc, poly6(r2, p.h2, p.c_poly6));
+                    ++n;
+                }
+            }
+        }
+        if (n > p.width) {
+            atomicOr(&b.ctr->err_flags, RTS_ERR_OVERFLOW);
+            atomicAdd((unsigned long long *)&b.ctr->overflow, (unsigned long long)(n - p.width));
+        }
+        const double rho = xmul(p.mass, acc);
+        const double ratio = xdiv(rho, p.rho0);
+        const double r2 = xmul(ratio, ratio);
+        const double r4 = xmul(r2, r2);
+        double pr = xmul(p.b_stiff, xsub(xmul(xmul(ratio, r2), r4), 1.0));
+        pr = pr > 0.0 ? pr : 0.0;
+        if (!isfinite(rho)) atomicOr(&b.ctr->err_flags, RTS_ERR_NONFINITE);
+        b.rho[j] = (float)rho;
+        b.pres[j] = (float)pr;
+        // publish for the force pass (only .w of slot k changes; the
+        // concurrent readers of cpos in this kernel use .xyz only)
+        reinterpret_cast<float *>(b.cpos)[4 * k + 3] = (float)pr;
+        reinterpret_cast<float *>(b.cvel)[4 * k + 3] = (float)rho;
+    }
+}
+
+// wcsph.py:288-296 + _forces wcsph.py:63-105
+__global__ void __launch_bounds__(kThreads) k_forces(const __grid_constant__ RtsParams p,
+                                                     RtsBuffers b) {
+    if (fatal(b.ctr)) return;
+    const int n_act = b.ctr->n_compute;
+    const float4 *cpos = reinterpret_cast<const float4 *>(b.cpos);
+    const float4 *cvel = reinterpret_cast<const float4 *>(b.cvel);
+    const float h2_loose = (float)(p.h2 * 1.00001);
+    const double m2 = xmul(p.mass, p.mass);
+    const double inv_rho0_sq = xdiv(1.0, xmul(p.rho0, p.rho0));
+    const double mum2 = xmul(p.mu, m2);
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n_act; t += gridDim.x * blockDim.x) {
+        const int k = b.active[t];
+        const int j = b.order[k];
+        const float4 a = cpos[k];
+        const float4 va = cvel[k];
+        const double xi = a.x, yi = a.y, zi = a.z;
+        const double rho_i = va.w, p_i = a.w;
+        const double term_i = xdiv(p_i, xmul(rho_i, rho_i));
+        const double wall_term = xadd(term_i, xmul(p_i, inv_rho0_sq));
+        Span sp[9];
+        const int ns = block_spans(p, b.starts, b.fluid_cells[j], sp);
+        double fx = 0.0, fy = 0.0, fz = 0.0;
+        for (int s = 0; s < ns; ++s) {
+            for (int q = sp[s].k0; q < sp[s].k1; ++q) {
+                if (q == k) continue;
+                const float4 o = cpos[q];
+                if (!maybe_near(a, o, h2_loose)) continue;
+                const double dx = xsub(xi, (double)o.x), dy = xsub(yi, (double)o.y),
+                             dz = xsub(zi, (double)o.z);
+                const double r2 = dist2(dx, dy, dz);
+                if (!(r2 < p.h2)) continue;
+                const double r = xsqrt(r2);
+                if (r >= p.h) continue;
+                if (o.w >= 0.0f) {  // fluid neighbour
+                    const float4 vo = cvel[q];
+                    const double rho_j = vo.w;
+                    const double term = xadd(term_i, xdiv((double)o.w, xmul(rho_j, rho_j)));
+                    const double sc = xmul(xmul(m2, term), spiky(r, p.h, p.c_spiky));
+                    fx = xsub(fx, xmul(sc, dx));
+                    fy = xsub(fy, xmul(sc, dy));
+                    fz = xsub(fz, xmul(sc, dz));
+                    const double lap =
+                        xdiv(xmul(mum2, visc_lap(r, p.h, p.c_visc)), xmul(rho_i, rho_j));
+                    fx = xadd(fx, xmul(lap, xsub((double)vo.x, (double)va.x)));
+                    fy = xadd(fy, xmul(lap, xsub((double)vo.y, (double)va.y)));
+                    fz = xadd(fz, xmul(lap, xsub((double)vo.z, (double)va.z)));
+                } else {  // static wall sample, mirrored pressure
+                    const double sc = xmul(xmul(m2, wall_term), spiky(r, p.h, p.c_spiky));
+                    fx = xsub(fx, xmul(sc, dx));
+                    fy = xsub(fy, xmul(sc, dy));
+                    fz = xsub(fz, xmul(sc, dz));
+                }
+            }
+        }
+        fx = xadd(fx, xmul(p.mass, p.gravity[0]));
+        fy = xadd(fy, xmul(p.mass, p.gravity[1]));
+        fz = xadd(fz, xmul(p.mass, p.gravity[2]));
+        // bookkeeping of wcsph.py:288-290 for this active particle
+        b.dt_corr[j] = b.dt_since[j];
+        b.dt_since[j] = 0.0;
+        float *ap = b.acc_prev + 3 * j;
+        float *ac = b.acc + 3 * j;
+        ap[0] = ac[0];
+        ap[1] = ac[1];
+        ap[2] = ac[2];
+        float *fo = b.force + 3 * j;
+        fo[0] = (float)fx;
+        fo[1] = (float)fy;
+        fo[2] = (float)fz;
+        ac[0] = (float)xdiv(fx, p.mass);
+        ac[1] = (float)xdiv(fy, p.mass);
+        ac[2] = (float)xdiv(fz, p.mass);
+    }
+}
+
+// wcsph.py:299-319: predictor for all, corrector (after it) for active, clamp
+__global__ void k_integrate(const __grid_constant__ RtsParams p, RtsBuffers b) {
+    if (fatal(b.ctr)) return;
+    const double dt = p.dt;
+    const double half_dt2 = xmul(xmul(0.5, dt), dt);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.n_fluid;
+         i += gridDim.x * blockDim.x) {
+        const bool act = p.rts ? (b.compute[i] != 0) : true;
+        const double dtc = b.dt_corr[i];
+        const double corr_x = xdiv(xmul(dtc, dtc), 6.0);
+        const double corr_v = xdiv(dtc, 2.0);
+        const bool correct = p.apply_correction && act;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            double x = b.pos[3 * i + a];
+            double v = b.vel[3 * i + a];
+            const double ac = b.acc[3 * i + a];
+            x = xadd(x, xadd(xmul(v, dt), xmul(ac, half_dt2)));
+            v = xadd(v, xmul(ac, dt));
+            if (correct) {
+                const double da = xsub(ac, (double)b.acc_prev[3 * i + a]);
+                x = xadd(x, xmul(da, corr_x));
+                v = xadd(v, xmul(da, corr_v));
+            }
+            if (x < p.clamp_lo[a]) {
+                x = p.clamp_lo[a];
+                v = 0.0;
+            } else if (x > p.clamp_hi[a]) {
+                x = p.clamp_hi[a];
+                v = 0.0;
+            }
+            b.pos[3 * i + a] = (float)x;
+            b.vel[3 * i + a] = (float)v;
+        }
+        b.dt_since[i] = xadd(b.dt_since[i], dt);
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int rts_wcsph_propagate(const RtsParams *p, const RtsBuffers *b, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaMemsetAsync(&b->ctr->n_compute, 0, sizeof(int), s);
+    k_propagate<<<rts_blocks(p->n_fluid + p->n_bound, 256), 256, 0, s>>>(*p, *b);
+    RTS_LAUNCH_CHECK();
+    return 0;
+}
+
+int rts_wcsph_density(const RtsParams *p, const RtsBuffers *b, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    k_density<<<rts_blocks(p->n_fluid, kThreads), kThreads, 0, s>>>(*p, *b);
+    RTS_LAUNCH_CHECK();
+    return 0;
+}
+
+int rts_wcsph_forces(const RtsParams *p, const RtsBuffers *b, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    k_forces<<<rts_blocks(p->n_fluid, kThreads), kThreads, 0, s>>>(*p, *b);
+    RTS_LAUNCH_CHECK();
+    return 0;
+}
+
+int rts_wcsph_integrate(const RtsParams *p, const RtsBuffers *b, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    k_integrate<<<rts_blocks(p->n_fluid, 256), 256, 0, s>>>(*p, *b);
+    RTS_LAUNCH_CHECK();
+    return 0;
+}
+
+}  // extern "C"

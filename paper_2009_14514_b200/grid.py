@@ -1,0 +1,223 @@
+"""Uniform block grid on the B200 -- drop-in for ``rts_sph.grid.BlockGrid``
+(/root/reference/pkg/src/rts_sph/grid.py:220-394).
+
+Geometry (origin, dims, inv_block) is computed on the host with the
+reference's expressions (grid.py:223-244).  ``rebuild`` runs the librtssph
+kernels: fp64 block keys with the domain check, occupancy counts, boundary
+culling by the 1-dilated occupancy, a tile scan, and the stable counting
+sort into ``starts``/``order`` (bit-identical to the reference's CSR:
+fluid ascending, then active boundary ascending, inside every block).
+
+All per-particle and per-block arrays are device tensors (int32 indices,
+bool masks); ``order`` holds reference particle indices (fluid first,
+boundary as ``n_fluid + b``).
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import _native as N
+from ._device import Arena, Counters, as_device_f32, raise_on_errors, require_cuda
+
+__all__ = ["BlockGrid", "neighbor_min", "dilate_mask"]
+
+
+def neighbor_min(field: np.ndarray, pad_value) -> np.ndarray:
+    """Host helper kept for API parity (grid.py:33-45): min over the 26
+    adjacent cells, ``pad_value`` outside."""
+    f = np.asarray(field)
+    padded = np.pad(f, 1, constant_values=pad_value)
+    out = np.full_like(f, pad_value)
+    nx, ny, nz = f.shape
+    for dx in (-1, 0, 1):
+        for dy in (-1, 0, 1):
+            for dz in (-1, 0, 1):
+                if dx or dy or dz:
+                    np.minimum(out, padded[1 + dx:1 + dx + nx, 1 + dy:1 + dy + ny,
+                                           1 + dz:1 + dz + nz], out=out)
+    return out
+
+
+def dilate_mask(mask: np.ndarray, layers: int = 1) -> np.ndarray:
+    """Host helper kept for API parity (grid.py:48-62): Chebyshev dilation."""
+    cur = np.asarray(mask, dtype=bool)
+    for _ in range(layers):
+        padded = np.pad(cur, 1, constant_values=False)
+        nxt = cur.copy()
+        nx, ny, nz = cur.shape
+        for dx in (-1, 0, 1):
+            for dy in (-1, 0, 1):
+                for dz in (-1, 0, 1):
+                    if dx or dy or dz:
+                        nxt |= padded[1 + dx:1 + dx + nx, 1 + dy:1 + dy + ny, 1 + dz:1 + dz + nz]
+        cur = nxt
+    return cur
+
+
+class BlockGrid:
+    """Block decomposition of the padded domain at a fixed block edge."""
+
+    def __init__(self, domain_min, domain_max, block_size: float, pad: float = 0.0,
+                 device="cuda", arena: Arena | None = None):
+        lo = np.asarray(domain_min, dtype=np.float64) - pad
+        hi = np.asarray(domain_max, dtype=np.float64) + pad
+        self.block_size = float(block_size)
+        self.inv_block = 1.0 / self.block_size
+        self.origin = lo
+        self.dims = tuple(max(1, int(math.ceil((b - a) / self.block_size - 1e-12)))
+                          for a, b in zip(lo, hi))
+        self.n_cells = int(np.prod(self.dims))
+        if self.n_cells >= 2**31 - 1:
+            raise ValueError("grid has more than 2^31 blocks")
+        self.device = require_cuda(device)
+        self.arena = arena if arena is not None else Arena(self.device)
+        self._own_counters = arena is None
+        self.counters = Counters(self.arena) if arena is None else None
+        self.n_fluid = 0
+        self.n_bound = -1
+        self.n_sorted = 0
+        self._alloc_cells()
+        self.params = N.RtsParams()
+        self.fill_params(self.params)
+
+    @classmethod
+    def for_scene(cls, scene, mode: str, device="cuda", arena=None) -> "BlockGrid":
+        return cls(scene.domain_min, scene.domain_max, scene.block_size(mode),
+                   pad=scene.boundary_layers * scene.spacing, device=device, arena=arena)
+
+    # -- geometry -----------------------------------------------------------
+    def fill_params(self, p: N.RtsParams) -> None:
+        hi = self.origin + np.asarray(self.dims) * self.block_size
+        for a in range(3):
+            p.origin[a] = float(self.origin[a])
+            p.grid_hi[a] = float(hi[a])
+            p.dims[a] = int(self.dims[a])
+        p.block_size = self.block_size
+        p.inv_block = self.inv_block
+        p.n_cells = self.n_cells
+
+    def cell_coords(self, positions) -> np.ndarray:
+        x = np.asarray(positions, dtype=np.float64)
+        c = np.floor((x - self.origin) * self.inv_block).astype(np.int64)
+        return np.clip(c, 0, np.asarray(self.dims) - 1)
+
+    def cell_ids(self, positions) -> np.ndarray:
+        c = self.cell_coords(positions)
+        _, ny, nz = self.dims
+        return (c[:, 0] * ny + c[:, 1]) * nz + c[:, 2]
+
+    # -- buffers ------------------------------------------------------------
+    def _alloc_cells(self) -> None:
+        A, nc = self.arena, self.n_cells
+        i32, i8, u8 = torch.int32, torch.int8, torch.uint8
+        A.alloc("cell_count", (nc,), i32, 0)
+        A.alloc("cell_bcount", (nc,), i32, 0)
+        A.alloc("starts", (nc + 1,), i32, 0)
+        A.alloc("fill", (nc,), i32, 0)
+        tiles = -(-nc // 4096)
+        A.alloc("scan_tmp", (4 * tiles + 64,), i32, 0)
+        A.alloc("vmax", (nc,), torch.float64, 0)
+        A.alloc("fmax", (nc,), torch.float64, 0)
+        A.alloc("block_raw", (nc,), i8, 0)
+        A.alloc("block_field", (nc,), i8, 0)
+        A.alloc("block_tmp", (nc,), i8, 0)
+        A.alloc("block_flag", (nc,), u8, 0)
+
+    def _ensure_particles(self, n_fluid: int, n_total: int) -> None:
+        A = self.arena
+        if n_fluid != self.n_fluid or "fluid_cells" not in A.t:
+            A.alloc("fluid_cells", (max(n_fluid, 1),), torch.int32, 0)
+            self.n_fluid = n_fluid
+        if "order" not in A.t or A["order"].numel() < max(n_total, 1):
+            A.alloc("order", (max(n_total, 1),), torch.int32, 0)
+
+    def bind_boundary(self, boundary_pos, n_fluid: int) -> None:
+        """Static binning of the wall shell (done once per solver): blocks
+        holding wall samples, their CSR of wall indices (ascending), so each
+        rebuild only decides which wall blocks are active (grid.py:279-290)."""
+        A = self.arena
+        bpos = np.asarray(boundary_pos, dtype=np.float64).reshape(-1, 3)
+        nb = len(bpos)
+        self.n_bound = nb
+        A["cell_bcount"].zero_()
+        if nb == 0:
+            self.n_bcells = 0
+            for name in ("bcell_ids", "bcell_start", "bidx", "bcell_of", "bcell_active"):
+                A.alloc(name, (1,), torch.int32 if name != "bcell_active" else torch.uint8, 0)
+            self._bslot = torch.zeros(0, dtype=torch.int64, device=self.device)
+            return
+        cells = self.cell_ids(bpos)
+        srt = np.argsort(cells, kind="stable")
+        ids, first = np.unique(cells[srt], return_index=True)
+        starts = np.append(first, nb).astype(np.int32)
+        slot = np.searchsorted(ids, cells)
+        self.n_bcells = len(ids)
+        dev = self.device
+        A.bind("bcell_ids", torch.as_tensor(ids.astype(np.int32), device=dev))
+        A.bind("bcell_start", torch.as_tensor(starts, device=dev))
+        A.bind("bidx", torch.as_tensor((n_fluid + srt).astype(np.int32), device=dev))
+        A.bind("bcell_of", torch.as_tensor(cells.astype(np.int32), device=dev))
+        A.alloc("bcell_active", (self.n_bcells,), torch.uint8, 0)
+        self._bslot = torch.as_tensor(slot.astype(np.int64), device=dev)
+
+    # -- device passes (async, used by the solvers) -----------------------------
+    def launch_rebuild(self, p, stream, want_maxima=False, add_fp=False) -> None:
+        s = stream.cuda_stream
+        N.call("rts_grid_keys", p, self.arena.buf, int(want_maxima), int(add_fp), s)
+        N.call("rts_grid_sort", p, self.arena.buf, s)
+
+    # -- reference-facing API -------------------------------------------------
+    def rebuild(self, pos, n_fluid: int) -> None:
+        """Re-bin ``pos`` (fluid rows first, boundary after); raises
+        NumericalError if fluid left the padded grid or is non-finite."""
+        x = as_device_f32(pos, self.device).reshape(-1, 3)
+        n_total = x.shape[0]
+        nb = n_total - n_fluid
+        self._ensure_particles(n_fluid, n_total)
+        self.bind_boundary(x[n_fluid:].cpu().numpy(), n_fluid)
+        self.arena.bind("pos", x)
+        self._pos_ref = x
+        p = self.params
+        p.n_fluid = n_fluid
+        p.n_bound = nb
+        p.n_bcells = self.n_bcells
+        stream = torch.cuda.current_stream(self.device)
+        ctr = self.counters
+        ctr.reset(stream)
+        self.launch_rebuild(p, stream)
+        c = ctr.read(stream)
+        raise_on_errors(c)
+        self.n_sorted = int(c.n_sorted)
+
+    @property
+    def fluid_cells(self) -> torch.Tensor:
+        return self.arena["fluid_cells"][: self.n_fluid]
+
+    @property
+    def starts(self) -> torch.Tensor:
+        return self.arena["starts"]
+
+    @property
+    def order(self) -> torch.Tensor:
+        return self.arena["order"][: self.n_sorted]
+
+    @property
+    def occupancy(self) -> torch.Tensor:
+        return (self.arena["cell_count"] > 0).reshape(self.dims)
+
+    @property
+    def boundary_active(self) -> torch.Tensor:
+        if self.n_bound <= 0:
+            return torch.zeros(0, dtype=torch.bool, device=self.device)
+        return self.arena["bcell_active"][self._bslot].bool()
+
+    def reduce_fluid_max(self, values) -> torch.Tensor:
+        """Per-block max of a fluid scalar, zeros in empty blocks (grid.py:347-351)."""
+        v = torch.as_tensor(values, device=self.device).to(torch.float64).reshape(-1)
+        out = torch.zeros(self.n_cells, dtype=torch.float64, device=self.device)
+        idx = self.fluid_cells.to(torch.int64)
+        return out.scatter_reduce(0, idx, v, reduce="amax", include_self=True)

@@ -1,0 +1,249 @@
+"""RTS-WCSPH on the B200 -- drop-in for ``rts_sph.wcsph.WcsphSolver``
+(/root/reference/pkg/src/rts_sph/wcsph.py:108-319; Algorithm 1 of
+arXiv 2009.14514 with the Serna predictor-corrector).
+
+One ``step()`` enqueues, on the current CUDA stream:
+
+  rts_grid_keys        block keys + domain check + per-block max |v|, |F|
+  rts_grid_sort        boundary culling, scan, stable CSR scatter
+  rts_block_levels     assign_regions + smooth_regions (RTS mode)
+  rts_wcsph_propagate  validity countdown / pre-emption, sorted copies,
+                       active-list compaction
+  rts_wcsph_density    density + Tait over the 3x3x3 block neighbourhood
+  rts_wcsph_forces     pressure + viscosity + gravity, corrector bookkeeping
+  rts_wcsph_integrate  predictor (all), corrector (active), clamp
+
+and synchronises once at the end to read the counters block (errors,
+n_compute) for the returned StepStats.  State attributes are fp32 CUDA
+tensors in the reference's particle order, writable in place
+(``solver.vel[i] = ...`` works as with the numpy reference).
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import _native as N
+from ._device import Arena, Counters, PhaseTimer, raise_on_errors, require_cuda
+from .grid import BlockGrid
+from .kernels import KernelSet
+from .scene import TAIT_GAMMA, Scene, seed_particles
+from .stats import StepStats
+
+__all__ = ["WcsphSolver", "tait_pressure", "NEIGHBOR_WIDTH"]
+
+NEIGHBOR_WIDTH = 128
+
+
+def tait_pressure(rho: float, rest_density: float, sound_speed: float) -> float:
+    """Host form of the clamped Tait EOS (wcsph.py:38-42)."""
+    b = rest_density * sound_speed * sound_speed / TAIT_GAMMA
+    p = b * ((rho / rest_density) ** TAIT_GAMMA - 1.0)
+    return p if p > 0.0 else 0.0
+
+
+class _DeviceSolver:
+    """Shared construction: seeding, device buffers, grid, RtsParams."""
+
+    def _setup_common(self, scene: Scene, grid_mode: str, device):
+        self.scene = scene
+        self.device = require_cuda(device)
+        self.kernel = KernelSet(scene.support_radius)
+        self.mass = scene.particle_mass
+        self.mu = scene.viscosity * scene.rest_density
+        fluid, wall = seed_particles(scene)
+        nf = self.n_fluid = len(fluid)
+        self.n_bound = len(wall)
+        A = self.arena = Arena(self.device)
+        init = np.concatenate([fluid, wall]) if len(wall) else fluid
+        self._pos = A.alloc("pos", (max(nf + self.n_bound, 1), 3), torch.float32, 0)
+        self._pos[: nf + self.n_bound].copy_(torch.as_tensor(init, dtype=torch.float32))
+        self.counters = Counters(A)
+        self.grid = BlockGrid.for_scene(scene, grid_mode, device=self.device, arena=A)
+        self.grid.counters = self.counters
+        self.grid._ensure_particles(nf, nf + self.n_bound)
+        self.grid.bind_boundary(self._pos[nf:nf + self.n_bound].cpu().numpy(), nf)
+        self.grid.n_fluid = nf
+        self.gravity = np.asarray(scene.gravity, dtype=np.float64)
+        self._clamp_lo = np.asarray(scene.domain_min) + 0.1 * scene.spacing
+        self._clamp_hi = np.asarray(scene.domain_max) - 0.1 * scene.spacing
+        p = self.params = N.RtsParams()
+        self.grid.fill_params(p)
+        k = self.kernel
+        p.h, p.h2, p.c_poly6, p.c_spiky, p.c_visc = k.h, k.h2, k.c_poly6, k.c_spiky, k.c_visc
+        p.mass = self.mass
+        p.inv_mass = 1.0 / self.mass
+        p.rho0 = scene.rest_density
+        p.mu = self.mu
+        for a in range(3):
+            p.clamp_lo[a] = float(self._clamp_lo[a])
+            p.clamp_hi[a] = float(self._clamp_hi[a])
+        p.n_fluid = nf
+        p.n_bound = self.n_bound
+        p.n_bcells = self.grid.n_bcells
+        p.width = NEIGHBOR_WIDTH
+        p.lambda_v = scene.lambda_v
+        p.lambda_f = scene.lambda_f
+        p.sound_speed = scene.sound_speed
+        p.eta_max, p.eta_avg, p.rho_T = scene.eta_max, scene.eta_avg, scene.rho_T
+        sms = N.load().rts_device_sms()
+        p.n_sms = sms if sms > 0 else 148
+        A.alloc("cpos", (max(nf + self.n_bound, 1), 4), torch.float32, 0)
+        A.alloc("cvel", (max(nf + self.n_bound, 1), 4), torch.float32, 0)
+        A.alloc("active", (max(nf, 1),), torch.int32, 0)
+        A.alloc("list2", (max(nf, 1),), torch.int32, 0)
+        self.step_index = 0
+        self.sim_time = 0.0
+        self.missed_neighbors_total = 0
+        self._timers = {"neighbor": 0.0, "physics": 0.0, "rts": 0.0}
+        self.timer = PhaseTimer(True)
+
+    def _set_betas(self, n_regions: int, alpha: float):
+        betas = self.scene.betas(n_regions)
+        p = self.params
+        for q in range(8):
+            p.betas[q] = float(betas[q]) if q < len(betas) else math.nan
+        p.alpha = alpha
+        self.betas = betas
+        self.alpha = alpha
+
+    def _sync_params(self):
+        p = self.params
+        g = np.asarray(self.gravity, dtype=np.float64).reshape(3)
+        for a in range(3):
+            p.gravity[a] = float(g[a])
+
+    @property
+    def pos(self) -> torch.Tensor:
+        return self._pos[: self.n_fluid + self.n_bound]
+
+    def host(self, name: str) -> np.ndarray:
+        """fp64 numpy snapshot of a state attribute (for parity checks)."""
+        t = getattr(self, name)
+        t = t.detach().cpu()
+        return t.numpy().astype(np.float64) if t.is_floating_point() else t.numpy()
+
+
+class WcsphSolver(_DeviceSolver):
+    """Weakly compressible SPH, ``mode`` "baseline" or "rts" (wcsph.py:108)."""
+
+    mode_names = ("baseline", "rts")
+
+    def __init__(self, scene: Scene, mode: str = "rts", dt_cap: float | None = None,
+                 pin_region: int | None = None, apply_correction: bool = True,
+                 track_rho_variance: bool = False, audit_neighbors: bool = False,
+                 n_regions: int = 4, device="cuda"):
+        if mode not in self.mode_names:
+            raise ValueError(f"unknown wcsph mode {mode!r}")
+        self.mode = mode
+        self.pin_region = pin_region
+        self.apply_correction = apply_correction
+        self.track_rho_variance = track_rho_variance
+        self.audit_neighbors = audit_neighbors
+        self.n_regions = n_regions
+        self._setup_common(scene, "wcsph", device)
+        self.dt_base = scene.base_dt("wcsph")
+        self.dt_cap = self.dt_base if dt_cap is None else dt_cap
+        self.b_stiff = scene.rest_density * scene.sound_speed**2 / TAIT_GAMMA
+        self._set_betas(n_regions, scene.alpha_for("wcsph"))
+        p = self.params
+        p.b_stiff = self.b_stiff
+        p.dt_base = self.dt_base
+        p.n_max = n_regions
+        p.use_sound = 1
+        p.rts = 1 if mode == "rts" else 0
+        nf = self.n_fluid
+        A = self.arena
+        f32 = torch.float32
+        self.vel = A.alloc("vel", (max(nf, 1), 3), f32, 0)[:nf]
+        self.acc = A.alloc("acc", (max(nf, 1), 3), f32, 0)[:nf]
+        self.acc_prev = A.alloc("acc_prev", (max(nf, 1), 3), f32, 0)[:nf]
+        self.force = A.alloc("force", (max(nf, 1), 3), f32, 0)[:nf]
+        self.rho = A.alloc("rho", (max(nf, 1),), f32, scene.rest_density)[:nf]
+        self.pres = A.alloc("pres", (max(nf, 1),), f32, 0)[:nf]
+        self.dt_since = A.alloc("dt_since", (max(nf, 1),), torch.float64, 0)[:nf]
+        self.dt_corr = A.alloc("dt_corr", (max(nf, 1),), torch.float64, 0)[:nf]
+        self.validity = A.alloc("validity", (max(nf, 1),), torch.int32, 0)[:nf]
+        self.region = A.alloc("region", (max(nf, 1),), torch.int8, 1)[:nf]
+        self.compute = A.alloc("compute", (max(nf, 1),), torch.bool, True)[:nf]
+        self._missed_last = 0
+
+    # ------------------------------------------------------------------
+    def cfl_bound(self) -> float:
+        """Global step bound from max |F| (wcsph.py:182-189)."""
+        sc = self.scene
+        r = self.grid.block_size
+        eq1 = sc.lambda_v * r / sc.sound_speed
+        f_max = self._force_max()
+        eq2 = sc.lambda_f * math.sqrt(r * self.mass / f_max) if f_max > 0.0 else math.inf
+        return min(eq1, eq2)
+
+    def _force_max(self) -> float:
+        if not self.n_fluid:
+            return 0.0
+        stream = torch.cuda.current_stream(self.device)
+        self.counters.reset(stream)
+        N.call("rts_force_max", self.params, self.arena.buf, stream.cuda_stream)
+        c = self.counters.read(stream)
+        return float(np.array([c.fmax_bits], dtype=np.uint64).view(np.float64)[0])
+
+    def particle_regions(self) -> torch.Tensor:
+        if self.mode == "rts":
+            return self.region
+        return torch.ones(self.n_fluid, dtype=torch.int8, device=self.device)
+
+    def advance(self) -> list[StepStats]:
+        return [self.step()]
+
+    def step(self) -> StepStats:
+        if self.mode == "rts":
+            dt = self.dt_base
+        else:
+            dt = min(self.cfl_bound(), self.dt_cap)
+        c = self._enqueue_step(dt)
+        raise_on_errors(c, NEIGHBOR_WIDTH)
+        n_compute = int(c.n_compute)
+        self.step_index += 1
+        self.sim_time += dt
+        self._timers = self.timer.totals()
+        st = StepStats(step=self.step_index, time=self.sim_time, dt=dt, n_compute=n_compute,
+                       frac_compute=n_compute / max(1, self.n_fluid),
+                       missed_neighbors=self._missed_last,
+                       t_neighbor=self._timers["neighbor"], t_physics=self._timers["physics"],
+                       t_rts=self._timers["rts"])
+        if self.track_rho_variance:
+            st.rho_var = float(torch.var(self.rho.double(), unbiased=False))
+        return st
+
+    def _enqueue_step(self, dt: float, read: bool = True):
+        """Enqueue one step (no host sync unless ``read``)."""
+        self._sync_params()
+        p = self.params
+        p.dt = dt
+        p.pin_region = int(self.pin_region or 0)
+        p.apply_correction = int(bool(self.apply_correction))
+        buf = self.arena.buf
+        stream = torch.cuda.current_stream(self.device)
+        s = stream.cuda_stream
+        tm = self.timer
+        self.counters.reset(stream)
+        tm.start(stream)
+        rts = self.mode == "rts"
+        self.grid.launch_rebuild(p, stream, want_maxima=rts)
+        tm.mark("neighbor", stream)
+        if rts:
+            N.call("rts_block_levels", p, buf, 0, s)
+        N.call("rts_wcsph_propagate", p, buf, s)
+        tm.mark("rts", stream)
+        N.call("rts_wcsph_density", p, buf, s)
+        N.call("rts_wcsph_forces", p, buf, s)
+        N.call("rts_wcsph_integrate", p, buf, s)
+        tm.mark("physics", stream)
+        if not read:
+            return None
+        c = self.counters.read(stream)
+        self.grid.n_sorted = int(c.n_sorted)
+        return c
