@@ -176,8 +176,45 @@ int rts_block_maxima(const RtsParams *p, const RtsBuffers *b, int add_fp, void *
 /* ---- region fields (regions.py) -------------------------------------- */
 /* assign_regions (regions.py:38-75) then smooth_regions (regions.py:78-91)
  * into block_field; expand_fast_regions (regions.py:94-107) when expand;
- * pin_region override (wcsph.py:258-259, pcisph.py:528-529). */
+ * pin_region override (wcsph.py:258-259, pcisph.py:528-529).  expand=2:
+ * assign_regions only (required levels of _mark_timestep_updates). */
 int rts_block_levels(const RtsParams *p, const RtsBuffers *b, int expand, void *stream);
+
+/* ---- RTS-PCISPH (pcisph.py) ------------------------------------------- */
+/* Wall rows of xs4 (static positions, marker -1). */
+int rts_pci_walls(const RtsParams *p, const RtsBuffers *b, void *stream);
+/* _assign_major_regions particle tail (pcisph.py:531-534): region, validity
+ * = VALIDITY_PERIOD[region], compute = 1, S_e = empty. */
+int rts_pci_major_particles(const RtsParams *p, const RtsBuffers *b, void *stream);
+/* search_into on the stale major grid for compute/all particles, layers 2
+ * for region 1 when two_layer_r1 (grid.py:88-152, pcisph.py:553-557), fused
+ * with _ext_forces (pcisph.py:174-199). */
+int rts_pci_refresh(const RtsParams *p, const RtsBuffers *b, int all, int two_layer_r1,
+                    void *stream);
+/* _predict_motion (pcisph.py:202-213): all fluid, or the last force list. */
+int rts_pci_motion(const RtsParams *p, const RtsBuffers *b, int all, void *stream);
+/* turn | S_e | S_ob membership (pcisph.py:634-643) -> pred list (active),
+ * force list (list2); all_pred=1 for the synchronous baselines. */
+int rts_pci_sets(const RtsParams *p, const RtsBuffers *b, int row_mask, int all_pred,
+                 void *stream);
+/* _predict_density + _accumulate_pressure (pcisph.py:216-235, 432-437). */
+int rts_pci_density(const RtsParams *p, const RtsBuffers *b, void *stream);
+/* S_e = err > eta_max/2 and its blocks (with_se), max err, sum rho*,
+ * any(S_e) into the counters (pcisph.py:662, 421-430, 682-683). */
+int rts_pci_se_reduce(const RtsParams *p, const RtsBuffers *b, int with_se, void *stream);
+/* derive_observed (regions.py:110-125) into block_tmp; S_ob refresh. */
+int rts_pci_observed(const RtsParams *p, const RtsBuffers *b, int with_se, void *stream);
+int rts_pci_sob(const RtsParams *p, const RtsBuffers *b, void *stream);
+/* _pressure_forces over the force list (pcisph.py:238-271). */
+int rts_pci_pforces(const RtsParams *p, const RtsBuffers *b, void *stream);
+/* _integrate (pcisph.py:759-768) + validity countdown (pcisph.py:580-584). */
+int rts_pci_integrate(const RtsParams *p, const RtsBuffers *b, int countdown, void *stream);
+/* _mark_timestep_updates (pcisph.py:718-755); block_raw = required levels. */
+int rts_pci_mark_updates(const RtsParams *p, const RtsBuffers *b, void *stream);
+/* local-phase snapshot (restore=0) / revert (restore=1) of p, f_p (pcisph.py:694-707). */
+int rts_pci_snapshot(const RtsParams *p, const RtsBuffers *b, int restore, void *stream);
+/* max |v| over fluid into ctr->fmax_bits (_adapt_dt, pcisph.py:470-476). */
+int rts_vel_max(const RtsParams *p, const RtsBuffers *b, void *stream);
 
 /* ---- RTS-WCSPH (wcsph.py) -------------------------------------------- */
 /* Validity countdown / pre-emption (wcsph.py:262-266) fused with the sorted

@@ -72,6 +72,20 @@ SIGNATURES = {
     "rts_force_max": [_PP, _PB, _P],
     "rts_block_levels": [_PP, _PB, _c.c_int, _P],
     "rts_wcsph_propagate": [_PP, _PB, _P],
+    "rts_pci_walls": [_PP, _PB, _P],
+    "rts_pci_major_particles": [_PP, _PB, _P],
+    "rts_pci_refresh": [_PP, _PB, _c.c_int, _c.c_int, _P],
+    "rts_pci_motion": [_PP, _PB, _c.c_int, _P],
+    "rts_pci_sets": [_PP, _PB, _c.c_int, _c.c_int, _P],
+    "rts_pci_density": [_PP, _PB, _P],
+    "rts_pci_se_reduce": [_PP, _PB, _c.c_int, _P],
+    "rts_pci_observed": [_PP, _PB, _c.c_int, _P],
+    "rts_pci_sob": [_PP, _PB, _P],
+    "rts_pci_pforces": [_PP, _PB, _P],
+    "rts_pci_integrate": [_PP, _PB, _c.c_int, _P],
+    "rts_pci_mark_updates": [_PP, _PB, _P],
+    "rts_pci_snapshot": [_PP, _PB, _c.c_int, _P],
+    "rts_vel_max": [_PP, _PB, _P],
     "rts_wcsph_density": [_PP, _PB, _P],
     "rts_wcsph_forces": [_PP, _PB, _P],
     "rts_wcsph_integrate": [_PP, _PB, _P],

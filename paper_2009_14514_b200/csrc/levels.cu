@@ -122,6 +122,7 @@ extern "C" int rts_block_levels(const RtsParams *p, const RtsBuffers *b, int exp
     const int blocks = rts_blocks(p->n_cells, kThreads);
     k_assign<<<blocks, kThreads, 0, s>>>(*p, *b);
     RTS_LAUNCH_CHECK();
+    if (expand == 2) return 0;  // assign only (required levels, pcisph.py:726-740)
     if (!expand || p->pin_region) {
         k_smooth<<<blocks, kThreads, 0, s>>>(*p, *b, b->block_field);
         RTS_LAUNCH_CHECK();

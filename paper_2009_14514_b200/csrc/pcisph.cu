@@ -1,2 +1,600 @@
-// PCISPH kernels (filled in below)
+// RTS-PCISPH kernels (reference: /root/reference/pkg/src/rts_sph/pcisph.py).
+//
+// Neighbour tables are materialised (the minor steps deliberately reuse
+// stale tables, pcisph.py:7-10, 553-557): `nbr` row i holds reference
+// particle indices in the reference's fill order, `cnt[i]` its length.
+// Predicted positions live in `xs4` (fluid rows: x* and p; wall rows: the
+// static position and -1), so every pair kernel reads one float4 per
+// neighbour regardless of its kind.
+//
+// Per correction iteration the host enqueues
+//   motion   x* for all fluid (first iteration / after a revert) or only for
+//            the previous force set (x* depends on f_p alone, which changed
+//            only there -- bit-identical to recomputing all, pcisph.py:202-213)
+//   sets     turn | S_e | S_ob membership -> compact pred/force lists, S_ob
+//            refresh from the observed-block mask (pcisph.py:637-643)
+//   density  rho*, err over the pred list; Jacobi pressure update for force
+//            members (pcisph.py:216-235, 432-437)
+//   se       S_e = err > eta_max/2, S_e blocks, max err, sum rho* (fixed-order
+//            two-level reduction: deterministic), any(S_e) (pcisph.py:662-684)
+//   observed observed-block mask (regions.py:110-125)
+//   pforces  pressure forces over the force list (pcisph.py:238-271)
 #include "common.cuh"
+
+using namespace rts;
+
+namespace {
+
+constexpr int kThreads = 128;
+constexpr int kRedBlocks = 1024;  // fixed partial count -> deterministic sums
+
+__constant__ int kValidity[5] = {0, 1, 2, 4, 4};  // pcisph.py:66
+
+RTS_DEV int trunc_axis(double x, double o, double inv, int n) {
+    // int((x - o) * inv) then clamp (grid.py:116-131)
+    const double v = xmul(xsub(x, o), inv);
+    if (!(v >= 0.0)) return 0;
+    if (v >= (double)(n - 1)) return n - 1;
+    return (int)v;
+}
+
+// wall rows of xs4 (static positions, marker -1)
+__global__ void k_xs4_walls(const __grid_constant__ RtsParams p, RtsBuffers b) {
+    const int nb = p.n_bound;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nb; t += gridDim.x * blockDim.x) {
+        const int j = p.n_fluid + t;
+        reinterpret_cast<float4 *>(b.xs4)[j] =
+            make_float4(b.pos[3 * j], b.pos[3 * j + 1], b.pos[3 * j + 2], -1.0f);
+    }
+}
+
+// _assign_major_regions per-particle tail (pcisph.py:531-534)
+__global__ void k_major_particles(const __grid_constant__ RtsParams p, RtsBuffers b) {
+    if (fatal(b.ctr)) return;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.n_fluid;
+         i += gridDim.x * blockDim.x) {
+        const int8_t r = b.block_field[b.fluid_cells[i]];
+        b.region[i] = r;
+        b.validity[i] = kValidity[r < 0 ? 0 : (r > 4 ? 4 : r)];
+        b.compute[i] = 1;
+        b.in_se[i] = 0;
+    }
+}
+
+// refresh list: particles whose tables are renewed this minor step
+__global__ void k_refresh_list(const __grid_constant__ RtsParams p, RtsBuffers b, int all) {
+    if (fatal(b.ctr)) return;
+    const int nf = p.n_fluid;
+    const int stride = gridDim.x * blockDim.x;
+    for (int base = blockIdx.x * blockDim.x; base < nf; base += stride) {
+        const int i = base + threadIdx.x;
+        const bool r = i < nf && (all || b.compute[i]);
+        warp_append(r, i, b.active, &b.ctr->n_compute);
+    }
+}
+
+// search_into on the (stale) major grid (grid.py:88-152) fused with the
+// external forces of the refreshed particle (pcisph.py:174-199): the
+// viscosity sum visits the table entries in the order they are written.
+__global__ void __launch_bounds__(kThreads) k_refresh(const __grid_constant__ RtsParams p,
+                                                      RtsBuffers b, int two_layer_r1) {
+    if (fatal(b.ctr)) return;
+    const int n = b.ctr->n_compute;
+    const int nx = p.dims[0], ny = p.dims[1], nz = p.dims[2];
+    const float h2_loose = (float)(p.h2 * 1.00001);
+    const double m2 = xmul(p.mass, p.mass);
+    const double inv_rho0_sq = xdiv(1.0, xmul(p.rho0, p.rho0));
+    const double mum2 = xmul(p.mu, m2);
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        const int i = b.active[t];
+        const float fxi = b.pos[3 * i], fyi = b.pos[3 * i + 1], fzi = b.pos[3 * i + 2];
+        const double xi = fxi, yi = fyi, zi = fzi;
+        const double vxi = b.vel[3 * i], vyi = b.vel[3 * i + 1], vzi = b.vel[3 * i + 2];
+        const int lay = (two_layer_r1 && b.region[i] == 1) ? 2 : 1;
+        const int cx = trunc_axis(xi, p.origin[0], p.inv_block, nx);
+        const int cy = trunc_axis(yi, p.origin[1], p.inv_block, ny);
+        const int cz = trunc_axis(zi, p.origin[2], p.inv_block, nz);
+        const int z0 = max(0, cz - lay), z1 = min(nz - 1, cz + lay);
+        int cntn = 0;
+        long long lost = 0;
+        int *row = b.nbr + (size_t)i * p.width;
+        double fx = 0.0, fy = 0.0, fz = 0.0;
+        for (int ax = max(0, cx - lay); ax <= min(nx - 1, cx + lay); ++ax)
+            for (int ay = max(0, cy - lay); ay <= min(ny - 1, cy + lay); ++ay) {
+                const int base = (ax * ny + ay) * nz;
+                const int k0 = b.starts[base + z0], k1 = b.starts[base + z1 + 1];
+                for (int k = k0; k < k1; ++k) {
+                    const int j = b.order[k];
+                    const float px = b.pos[3 * j], py = b.pos[3 * j + 1], pz = b.pos[3 * j + 2];
+                    {
+                        const float dx = fxi - px, dy = fyi - py, dz = fzi - pz;
+                        if (__fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)),
+                                      __fmul_rn(dz, dz)) > h2_loose)
+                            continue;
+                    }
+                    const double dx = xsub(xi, (double)px), dy = xsub(yi, (double)py),
+                                 dz = xsub(zi, (double)pz);
+                    const double r2 = dist2(dx, dy, dz);
+                    if (!(r2 < p.h2)) continue;
+                    if (cntn < p.width) {
+                        row[cntn++] = j;
+                    } else {
+                        ++lost;
+                        continue;
+                    }
+                    if (j >= p.n_fluid || j == i) continue;
+                    const double r = xsqrt(r2);
+                    if (r >= p.h) continue;
+                    const double lap = xmul(xmul(mum2, visc_lap(r, p.h, p.c_visc)), inv_rho0_sq);
+                    fx = xadd(fx, xmul(lap, xsub((double)b.vel[3 * j], vxi)));
+                    fy = xadd(fy, xmul(lap, xsub((double)b.vel[3 * j + 1], vyi)));
+                    fz = xadd(fz, xmul(lap, xsub((double)b.vel[3 * j + 2], vzi)));
+                }
+            }
+        b.cnt[i] = cntn;
+        if (lost) {
+            atomicOr(&b.ctr->err_flags, RTS_ERR_OVERFLOW);
+            atomicAdd((unsigned long long *)&b.ctr->overflow, (unsigned long long)lost);
+        }
+        b.force[3 * i] = (float)xadd(fx, xmul(p.mass, p.gravity[0]));
+        b.force[3 * i + 1] = (float)xadd(fy, xmul(p.mass, p.gravity[1]));
+        b.force[3 * i + 2] = (float)xadd(fz, xmul(p.mass, p.gravity[2]));
+    }
+}
+
+// x* = pos + dt * (vel + dt/m (f_ext + f_p)) (pcisph.py:202-213); xs4.w = p
+RTS_DEV void motion_one(const RtsParams &p, const RtsBuffers &b, int i, double dt_inv_m) {
+    float xs[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double f = xadd((double)b.force[3 * i + a], (double)b.f_p[3 * i + a]);
+        const double v = xadd((double)b.vel[3 * i + a], xmul(dt_inv_m, f));
+        xs[a] = (float)xadd((double)b.pos[3 * i + a], xmul(p.dt, v));
+        b.xstar[3 * i + a] = xs[a];
+    }
+    reinterpret_cast<float4 *>(b.xs4)[i] = make_float4(xs[0], xs[1], xs[2], b.pres[i]);
+}
+
+__global__ void k_motion_all(const __grid_constant__ RtsParams p, RtsBuffers b) {
+    if (fatal(b.ctr)) return;
+    const double dim = xmul(p.dt, p.inv_mass);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.n_fluid;
+         i += gridDim.x * blockDim.x)
+        motion_one(p, b, i, dim);
+}
+
+__global__ void k_motion_list(const __grid_constant__ RtsParams p, RtsBuffers b) {
+    if (fatal(b.ctr)) return;
+    const double dim = xmul(p.dt, p.inv_mass);
+    const int n = b.ctr->n_force;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x)
+        motion_one(p, b, b.list2[t], dim);
+}
+
+// set membership for one iteration (pcisph.py:634-643); row_mask bit n set
+// when region n is scheduled; S_ob refreshed from the observed mask first
+__global__ void k_sets(const __grid_constant__ RtsParams p, RtsBuffers b, int row_mask,
+                       int all_pred) {
+    if (fatal(b.ctr)) return;
+    const int nf = p.n_fluid;
+    const int stride = gridDim.x * blockDim.x;
+    for (int base = blockIdx.x * blockDim.x; base < nf; base += stride) {
+        const int i = base + threadIdx.x;
+        bool pred = false, force = false;
+        if (i < nf) {
+            if (all_pred) {
+                pred = force = true;
+            } else {
+                const bool sob = b.block_tmp[b.fluid_cells[i]] != 0;
+                b.in_sob[i] = sob;
+                const bool turn = (row_mask >> b.region[i]) & 1;
+                const bool se = b.in_se[i] != 0;
+                pred = turn || se || sob;
+                force = turn || se;
+            }
+            b.pflag[i] = force;
+        }
+        warp_append(pred, i, b.active, &b.ctr->n_pred);
+        warp_append(force, i, b.list2, &b.ctr->n_force);
+    }
+}
+
+// S_ob = observed[fluid_cells] for every fluid particle (pcisph.py:537-542)
+__global__ void k_sob(const __grid_constant__ RtsParams p, RtsBuffers b) {
+    if (fatal(b.ctr)) return;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.n_fluid;
+         i += gridDim.x * blockDim.x)
+        b.in_sob[i] = b.block_tmp[b.fluid_cells[i]] != 0;
+}
+
+// rho*, err over the pred list; p += delta (rho* - rho0) on force members
+__global__ void __launch_bounds__(kThreads) k_density(const __grid_constant__ RtsParams p,
+                                                      RtsBuffers b) {
+    if (fatal(b.ctr)) return;
+    const int n = b.ctr->n_pred;
+    const float4 *xs4 = reinterpret_cast<const float4 *>(b.xs4);
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        const int i = b.active[t];
+        const float4 a = xs4[i];
+        const double xi = a.x, yi = a.y, zi = a.z;
+        const int c = b.cnt[i];
+        const int *row = b.nbr + (size_t)i * p.width;
+        double acc = 0.0;
+        for (int q = 0; q < c; ++q) {
+            const float4 o = xs4[row[q]];
+            acc = xadd(acc, poly6(dist2(xsub(xi, (double)o.x), xsub(yi, (double)o.y),
+                                        xsub(zi, (double)o.z)),
+                                  p.h2, p.c_poly6));
+        }
+        const double rho = xmul(p.mass, acc);
+        const double diff = xsub(rho, p.rho0);
+        b.rho[i] = (float)rho;
+        b.err[i] = diff > 0.0 ? xdiv(diff, p.rho0) : 0.0;
+        if (!isfinite(rho)) atomicOr(&b.ctr->err_flags, RTS_ERR_NONFINITE);
+        if (b.pflag[i]) {
+            double pr = xadd((double)b.pres[i], xmul(p.delta, diff));
+            pr = pr > 0.0 ? pr : 0.0;
+            b.pres[i] = (float)pr;
+            reinterpret_cast<float *>(b.xs4)[4 * i + 3] = (float)pr;  // .w only
+        }
+    }
+}
+
+// S_e, S_e blocks, max err, sum rho* (deterministic), any S_e
+__global__ void __launch_bounds__(256) k_se_reduce(const __grid_constant__ RtsParams p,
+                                                   RtsBuffers b, int with_se) {
+    if (fatal(b.ctr)) return;
+    __shared__ double ssum[8];
+    const int nf = p.n_fluid;
+    const double thr = xmul(0.5, p.eta_max);
+    // contiguous chunk per block, fixed tree inside -> order-independent of timing
+    const int chunk = (nf + gridDim.x - 1) / gridDim.x;
+    const int i0 = blockIdx.x * chunk, i1 = min(nf, i0 + chunk);
+    double s = 0.0, m = 0.0;
+    int any = 0;
+    for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+        const double e = b.err[i];
+        const bool se = with_se && e > thr;
+        if (with_se) b.in_se[i] = se;
+        if (se) {
+            b.block_flag[b.fluid_cells[i]] = 1;
+            any = 1;
+        }
+        if (e > m) m = e;
+        s = xadd(s, (double)b.rho[i]);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        s = xadd(s, __shfl_down_sync(0xffffffffu, s, o));
+        m = fmax(m, __shfl_down_sync(0xffffffffu, m, o));
+    }
+    any = __any_sync(0xffffffffu, any);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) {
+        ssum[warp] = s;
+        if (m > 0.0)
+            atomicMax(reinterpret_cast<unsigned long long *>(&b.ctr->max_err),
+                      (unsigned long long)__double_as_longlong(m));
+        if (any) atomicOr(&b.ctr->any_se, 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t = xadd(t, ssum[w]);
+        b.partial[blockIdx.x] = t;
+    }
+}
+
+__global__ void k_sum_partials(RtsBuffers b, int n) {
+    __shared__ double ssum[32];
+    double s = 0.0;
+    for (int q = threadIdx.x; q < n; q += blockDim.x) s = xadd(s, b.partial[q]);
+    for (int o = 16; o > 0; o >>= 1) s = xadd(s, __shfl_down_sync(0xffffffffu, s, o));
+    if ((threadIdx.x & 31) == 0) ssum[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t = xadd(t, ssum[w]);
+        b.ctr->sum_rho = t;
+    }
+}
+
+// observed blocks (regions.py:110-125): occupied and (bordering a strictly
+// smaller region, or bordering an S_e block without being one); -> block_tmp
+__global__ void k_observed(const __grid_constant__ RtsParams p, RtsBuffers b, int with_se) {
+    if (fatal(b.ctr)) return;
+    const int nx = p.dims[0], ny = p.dims[1], nz = p.dims[2];
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < p.n_cells;
+         c += gridDim.x * blockDim.x) {
+        const int8_t f = b.block_field[c];
+        bool obs = false;
+        if (f > 0) {
+            const int cz = c % nz, cy = (c / nz) % ny, cx = c / (ny * nz);
+            int8_t m = 127;
+            bool near_se = false;
+            for (int ax = max(0, cx - 1); ax <= min(nx - 1, cx + 1); ++ax)
+                for (int ay = max(0, cy - 1); ay <= min(ny - 1, cy + 1); ++ay) {
+                    const int base = (ax * ny + ay) * nz;
+                    for (int az = max(0, cz - 1); az <= min(nz - 1, cz + 1); ++az) {
+                        const int q = base + az;
+                        if (q == c) continue;
+                        const int8_t v = b.block_field[q];
+                        if (v > 0 && v < m) m = v;
+                        if (with_se && b.block_flag[q]) near_se = true;
+                    }
+                }
+            obs = (m < f) || (with_se && near_se && !b.block_flag[c]);
+        }
+        b.block_tmp[c] = obs;
+    }
+}
+
+// pressure forces at x* over the force list (pcisph.py:238-271)
+__global__ void __launch_bounds__(kThreads) k_pforces(const __grid_constant__ RtsParams p,
+                                                      RtsBuffers b) {
+    if (fatal(b.ctr)) return;
+    const int n = b.ctr->n_force;
+    const float4 *xs4 = reinterpret_cast<const float4 *>(b.xs4);
+    const double m2 = xmul(p.mass, p.mass);
+    const double inv_rho0_sq = xdiv(1.0, xmul(p.rho0, p.rho0));
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        const int i = b.list2[t];
+        const float4 a = xs4[i];
+        const double xi = a.x, yi = a.y, zi = a.z;
+        const double term_i = xmul((double)b.pres[i], inv_rho0_sq);
+        const double wall = xadd(term_i, term_i);
+        const int c = b.cnt[i];
+        const int *row = b.nbr + (size_t)i * p.width;
+        double fx = 0.0, fy = 0.0, fz = 0.0;
+        for (int q = 0; q < c; ++q) {
+            const int j = row[q];
+            if (j == i) continue;
+            const float4 o = xs4[j];
+            const double dx = xsub(xi, (double)o.x), dy = xsub(yi, (double)o.y),
+                         dz = xsub(zi, (double)o.z);
+            const double term = j < p.n_fluid ? xadd(term_i, xmul((double)o.w, inv_rho0_sq)) : wall;
+            const double r = xsqrt(dist2(dx, dy, dz));
+            if (r <= 0.0 || r >= p.h) continue;
+            const double s = xmul(xmul(m2, term), spiky(r, p.h, p.c_spiky));
+            fx = xsub(fx, xmul(s, dx));
+            fy = xsub(fy, xmul(s, dy));
+            fz = xsub(fz, xmul(s, dz));
+        }
+        b.f_p[3 * i] = (float)fx;
+        b.f_p[3 * i + 1] = (float)fy;
+        b.f_p[3 * i + 2] = (float)fz;
+    }
+}
+
+// _integrate (pcisph.py:759-768) + validity countdown (pcisph.py:580-584)
+__global__ void k_integrate(const __grid_constant__ RtsParams p, RtsBuffers b, int countdown) {
+    if (fatal(b.ctr)) return;
+    const double dim = xmul(p.dt, p.inv_mass);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.n_fluid;
+         i += gridDim.x * blockDim.x) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const double f = xadd((double)b.force[3 * i + a], (double)b.f_p[3 * i + a]);
+            double v = xadd((double)b.vel[3 * i + a], xmul(f, dim));
+            double x = xadd((double)b.pos[3 * i + a], xmul(v, p.dt));
+            if (x < p.clamp_lo[a]) {
+                x = p.clamp_lo[a];
+                v = 0.0;
+            } else if (x > p.clamp_hi[a]) {
+                x = p.clamp_hi[a];
+                v = 0.0;
+            }
+            b.pos[3 * i + a] = (float)x;
+            b.vel[3 * i + a] = (float)v;
+        }
+        if (countdown) {
+            int v = b.validity[i] - 1;
+            const bool expired = v <= 0;
+            if (expired) {
+                const int8_t r = b.region[i];
+                v = kValidity[r < 0 ? 0 : (r > 4 ? 4 : r)];
+            }
+            b.validity[i] = v;
+            b.compute[i] = expired;
+        }
+    }
+}
+
+// _mark_timestep_updates (pcisph.py:718-755), block part: block_raw holds the
+// required levels; new field -> block_tmp, changed mask -> block_flag
+__global__ void k_mark_blocks(const __grid_constant__ RtsParams p, RtsBuffers b) {
+    if (fatal(b.ctr)) return;
+    const int nx = p.dims[0], ny = p.dims[1], nz = p.dims[2];
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < p.n_cells;
+         c += gridDim.x * blockDim.x) {
+        const bool occ = b.cell_count[c] > 0;
+        const int8_t cur = b.block_field[c];
+        int8_t nw = 0;
+        if (occ) {
+            // spread = min(vfield, min over 26 neighbours of vfield), vfield =
+            // required where violating else 127
+            const int cz = c % nz, cy = (c / nz) % ny, cx = c / (ny * nz);
+            int8_t spread = 127;
+            for (int ax = max(0, cx - 1); ax <= min(nx - 1, cx + 1); ++ax)
+                for (int ay = max(0, cy - 1); ay <= min(ny - 1, cy + 1); ++ay) {
+                    const int base = (ax * ny + ay) * nz;
+                    for (int az = max(0, cz - 1); az <= min(nz - 1, cz + 1); ++az) {
+                        const int q = base + az;
+                        const int8_t cq = b.block_field[q];
+                        const int8_t rq = b.block_raw[q];
+                        const bool viol = (b.cell_count[q] > 0) && (rq < cq) && (cq > 0);
+                        if (viol && rq < spread) spread = rq;
+                    }
+                }
+            nw = cur < spread ? cur : spread;
+        }
+        b.block_tmp[c] = nw;
+        b.block_flag[c] = nw < cur;
+    }
+}
+
+__global__ void k_mark_apply(const __grid_constant__ RtsParams p, RtsBuffers b) {
+    if (fatal(b.ctr)) return;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < p.n_cells;
+         c += gridDim.x * blockDim.x)
+        b.block_field[c] = b.block_tmp[c];
+}
+
+__global__ void k_mark_particles(const __grid_constant__ RtsParams p, RtsBuffers b) {
+    if (fatal(b.ctr)) return;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.n_fluid;
+         i += gridDim.x * blockDim.x) {
+        const int c = b.fluid_cells[i];
+        if (b.block_flag[c]) {
+            const int8_t r = b.block_field[c];
+            b.region[i] = r;
+            b.compute[i] = 1;
+            b.validity[i] = kValidity[r < 0 ? 0 : (r > 4 ? 4 : r)];
+        }
+    }
+}
+
+__global__ void k_vel_max(const __grid_constant__ RtsParams p, RtsBuffers b) {
+    double m = 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.n_fluid;
+         i += gridDim.x * blockDim.x) {
+        const double v = norm3(b.vel[3 * i], b.vel[3 * i + 1], b.vel[3 * i + 2]);
+        if (v > m) m = v;
+    }
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m > 0.0)
+        atomicMax(reinterpret_cast<unsigned long long *>(&b.ctr->fmax_bits),
+                  (unsigned long long)__double_as_longlong(m));
+}
+
+__global__ void k_snapshot(const __grid_constant__ RtsParams p, RtsBuffers b, int restore) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.n_fluid;
+         i += gridDim.x * blockDim.x) {
+        if (!restore) {
+            b.snap_p[i] = b.pres[i];
+            b.snap_fp[3 * i] = b.f_p[3 * i];
+            b.snap_fp[3 * i + 1] = b.f_p[3 * i + 1];
+            b.snap_fp[3 * i + 2] = b.f_p[3 * i + 2];
+        } else {
+            b.pres[i] = b.snap_p[i];
+            b.f_p[3 * i] = b.snap_fp[3 * i];
+            b.f_p[3 * i + 1] = b.snap_fp[3 * i + 1];
+            b.f_p[3 * i + 2] = b.snap_fp[3 * i + 2];
+        }
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int rts_pci_walls(const RtsParams *p, const RtsBuffers *b, void *stream) {
+    if (p->n_bound <= 0) return 0;
+    k_xs4_walls<<<rts_blocks(p->n_bound, 256), 256, 0, (cudaStream_t)stream>>>(*p, *b);
+    RTS_LAUNCH_CHECK();
+    return 0;
+}
+
+int rts_pci_major_particles(const RtsParams *p, const RtsBuffers *b, void *stream) {
+    k_major_particles<<<rts_blocks(p->n_fluid, 256), 256, 0, (cudaStream_t)stream>>>(*p, *b);
+    RTS_LAUNCH_CHECK();
+    return 0;
+}
+
+int rts_pci_refresh(const RtsParams *p, const RtsBuffers *b, int all, int two_layer_r1,
+                    void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaMemsetAsync(&b->ctr->n_compute, 0, sizeof(int), s);
+    k_refresh_list<<<rts_blocks(p->n_fluid, 256), 256, 0, s>>>(*p, *b, all);
+    RTS_LAUNCH_CHECK();
+    k_refresh<<<rts_blocks(p->n_fluid, kThreads), kThreads, 0, s>>>(*p, *b, two_layer_r1);
+    RTS_LAUNCH_CHECK();
+    return 0;
+}
+
+int rts_pci_motion(const RtsParams *p, const RtsBuffers *b, int all, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (all)
+        k_motion_all<<<rts_blocks(p->n_fluid, 256), 256, 0, s>>>(*p, *b);
+    else
+        k_motion_list<<<rts_blocks(p->n_fluid, 256), 256, 0, s>>>(*p, *b);
+    RTS_LAUNCH_CHECK();
+    return 0;
+}
+
+int rts_pci_sets(const RtsParams *p, const RtsBuffers *b, int row_mask, int all_pred,
+                 void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaMemsetAsync(&b->ctr->n_pred, 0, 2 * sizeof(int), s);  // n_pred, n_force
+    k_sets<<<rts_blocks(p->n_fluid, 256), 256, 0, s>>>(*p, *b, row_mask, all_pred);
+    RTS_LAUNCH_CHECK();
+    return 0;
+}
+
+int rts_pci_density(const RtsParams *p, const RtsBuffers *b, void *stream) {
+    k_density<<<rts_blocks(p->n_fluid, kThreads), kThreads, 0, (cudaStream_t)stream>>>(*p, *b);
+    RTS_LAUNCH_CHECK();
+    return 0;
+}
+
+int rts_pci_se_reduce(const RtsParams *p, const RtsBuffers *b, int with_se, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (with_se) cudaMemsetAsync(b->block_flag, 0, (size_t)p->n_cells, s);
+    cudaMemsetAsync(&b->ctr->max_err, 0, sizeof(double) + 2 * sizeof(int), s);  // max_err, any_se
+    int blocks = (p->n_fluid + 255) / 256;
+    if (blocks > kRedBlocks) blocks = kRedBlocks;
+    if (blocks < 1) blocks = 1;
+    k_se_reduce<<<blocks, 256, 0, s>>>(*p, *b, with_se);
+    RTS_LAUNCH_CHECK();
+    k_sum_partials<<<1, 1024, 0, s>>>(*b, blocks);
+    RTS_LAUNCH_CHECK();
+    return 0;
+}
+
+int rts_pci_observed(const RtsParams *p, const RtsBuffers *b, int with_se, void *stream) {
+    k_observed<<<rts_blocks(p->n_cells, 256), 256, 0, (cudaStream_t)stream>>>(*p, *b, with_se);
+    RTS_LAUNCH_CHECK();
+    return 0;
+}
+
+int rts_pci_sob(const RtsParams *p, const RtsBuffers *b, void *stream) {
+    k_sob<<<rts_blocks(p->n_fluid, 256), 256, 0, (cudaStream_t)stream>>>(*p, *b);
+    RTS_LAUNCH_CHECK();
+    return 0;
+}
+
+int rts_pci_pforces(const RtsParams *p, const RtsBuffers *b, void *stream) {
+    k_pforces<<<rts_blocks(p->n_fluid, kThreads), kThreads, 0, (cudaStream_t)stream>>>(*p, *b);
+    RTS_LAUNCH_CHECK();
+    return 0;
+}
+
+int rts_pci_integrate(const RtsParams *p, const RtsBuffers *b, int countdown, void *stream) {
+    k_integrate<<<rts_blocks(p->n_fluid, 256), 256, 0, (cudaStream_t)stream>>>(*p, *b,
+                                                                               countdown);
+    RTS_LAUNCH_CHECK();
+    return 0;
+}
+
+int rts_pci_mark_updates(const RtsParams *p, const RtsBuffers *b, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    const int cb = rts_blocks(p->n_cells, 256);
+    k_mark_blocks<<<cb, 256, 0, s>>>(*p, *b);
+    k_mark_apply<<<cb, 256, 0, s>>>(*p, *b);
+    k_mark_particles<<<rts_blocks(p->n_fluid, 256), 256, 0, s>>>(*p, *b);
+    RTS_LAUNCH_CHECK();
+    return 0;
+}
+
+int rts_pci_snapshot(const RtsParams *p, const RtsBuffers *b, int restore, void *stream) {
+    k_snapshot<<<rts_blocks(p->n_fluid, 256), 256, 0, (cudaStream_t)stream>>>(*p, *b, restore);
+    RTS_LAUNCH_CHECK();
+    return 0;
+}
+
+int rts_vel_max(const RtsParams *p, const RtsBuffers *b, void *stream) {
+    k_vel_max<<<rts_blocks(p->n_fluid, 256, 148 * 8), 256, 0, (cudaStream_t)stream>>>(*p, *b);
+    RTS_LAUNCH_CHECK();
+    return 0;
+}
+
+}  // extern "C"
