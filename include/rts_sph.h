@@ -154,6 +154,8 @@ typedef struct RtsBuffers {
 int rts_abi_version(void);
 /* Query the current device; returns its SM count or a negative cudaError. */
 int rts_device_sms(void);
+/* Number of librtssph kernels launched by this process so far. */
+long long rts_launch_count(void);
 /* Zero-filled cudaMemsetAsync helper so hosts need not link cudart. */
 int rts_memset(void *dst, int value, int64_t bytes, void *stream);
 

@@ -112,10 +112,16 @@ def load(path: str = LIB_PATH):
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = _c.c_int
+    lib.rts_launch_count.argtypes = []
+    lib.rts_launch_count.restype = _c.c_longlong
     if lib.rts_abi_version() != ABI_VERSION:
         raise NativeError(f"librtssph ABI {lib.rts_abi_version()} != expected {ABI_VERSION}")
     _lib = lib
     return lib
+
+
+def launch_count() -> int:
+    return int(load().rts_launch_count())
 
 
 def call(name: str, *args) -> None:

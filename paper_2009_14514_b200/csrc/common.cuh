@@ -100,6 +100,9 @@ RTS_DEV int warp_count_add(bool pred, int *count) {
 
 }  // namespace rts
 
+// kernel-launch counter (reported by bench.py as gpu_launches)
+extern "C" void rts_note_launch(void);
+
 // launch helpers
 static inline int rts_blocks(long long n, int threads, int cap = 148 * 32) {
     long long b = (n + threads - 1) / threads;

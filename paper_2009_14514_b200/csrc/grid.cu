@@ -170,14 +170,14 @@ int scan_exclusive(const int *a, const int *a2, int n, int *out, int *tmp, cudaS
     int *sums = tmp;
     int *offs = tmp + tiles;
     if (from_counts)
-        k_scan_tiles<true><<<tiles, kScanThreads, 0, s>>>(a, a2, n, out, sums);
+        rts_note_launch(), k_scan_tiles<true><<<tiles, kScanThreads, 0, s>>>(a, a2, n, out, sums);
     else
-        k_scan_tiles<false><<<tiles, kScanThreads, 0, s>>>(a, a2, n, out, sums);
+        rts_note_launch(), k_scan_tiles<false><<<tiles, kScanThreads, 0, s>>>(a, a2, n, out, sums);
     RTS_LAUNCH_CHECK();
     if (tiles > 1) {
         int rc = scan_exclusive(sums, nullptr, tiles, offs, tmp + 2 * tiles, s, false);
         if (rc) return rc;
-        k_scan_add<<<tiles, 256, 0, s>>>(out, n, offs);
+        rts_note_launch(), k_scan_add<<<tiles, 256, 0, s>>>(out, n, offs);
         RTS_LAUNCH_CHECK();
     }
     return 0;
@@ -263,7 +263,7 @@ int rts_grid_keys(const RtsParams *p, const RtsBuffers *b, int want_maxima, int 
         cudaMemsetAsync(b->vmax, 0, sizeof(double) * (size_t)p->n_cells, s);
         cudaMemsetAsync(b->fmax, 0, sizeof(double) * (size_t)p->n_cells, s);
     }
-    k_fluid_keys<<<rts_blocks(p->n_fluid, kThreads), kThreads, 0, s>>>(*p, *b, want_maxima,
+    rts_note_launch(), k_fluid_keys<<<rts_blocks(p->n_fluid, kThreads), kThreads, 0, s>>>(*p, *b, want_maxima,
                                                                         add_fp);
     RTS_LAUNCH_CHECK();
     return 0;
@@ -273,7 +273,7 @@ int rts_block_maxima(const RtsParams *p, const RtsBuffers *b, int add_fp, void *
     cudaStream_t s = (cudaStream_t)stream;
     cudaMemsetAsync(b->vmax, 0, sizeof(double) * (size_t)p->n_cells, s);
     cudaMemsetAsync(b->fmax, 0, sizeof(double) * (size_t)p->n_cells, s);
-    k_block_maxima<<<rts_blocks(p->n_fluid, kThreads), kThreads, 0, s>>>(*p, *b, add_fp);
+    rts_note_launch(), k_block_maxima<<<rts_blocks(p->n_fluid, kThreads), kThreads, 0, s>>>(*p, *b, add_fp);
     RTS_LAUNCH_CHECK();
     return 0;
 }
@@ -281,21 +281,21 @@ int rts_block_maxima(const RtsParams *p, const RtsBuffers *b, int add_fp, void *
 int rts_grid_sort(const RtsParams *p, const RtsBuffers *b, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
     if (p->n_bcells > 0) {
-        k_boundary_active<<<rts_blocks(p->n_bcells, kThreads), kThreads, 0, s>>>(*p, *b);
+        rts_note_launch(), k_boundary_active<<<rts_blocks(p->n_bcells, kThreads), kThreads, 0, s>>>(*p, *b);
         RTS_LAUNCH_CHECK();
     }
     int rc = scan_exclusive(b->cell_count, b->cell_bcount, p->n_cells, b->starts, b->scan_tmp, s,
                             true);
     if (rc) return rc;
-    k_scan_finish<<<1, 1, 0, s>>>(*p, *b);
+    rts_note_launch(), k_scan_finish<<<1, 1, 0, s>>>(*p, *b);
     RTS_LAUNCH_CHECK();
     cudaMemsetAsync(b->fill, 0, sizeof(int) * (size_t)p->n_cells, s);
-    k_scatter_fluid<<<rts_blocks(p->n_fluid, kThreads), kThreads, 0, s>>>(*p, *b);
+    rts_note_launch(), k_scatter_fluid<<<rts_blocks(p->n_fluid, kThreads), kThreads, 0, s>>>(*p, *b);
     RTS_LAUNCH_CHECK();
-    k_sort_runs<<<rts_blocks(p->n_cells, kThreads), kThreads, 0, s>>>(*p, *b);
+    rts_note_launch(), k_sort_runs<<<rts_blocks(p->n_cells, kThreads), kThreads, 0, s>>>(*p, *b);
     RTS_LAUNCH_CHECK();
     if (p->n_bcells > 0) {
-        k_scatter_boundary<<<rts_blocks((long long)p->n_bcells * 32, kThreads), kThreads, 0, s>>>(
+        rts_note_launch(), k_scatter_boundary<<<rts_blocks((long long)p->n_bcells * 32, kThreads), kThreads, 0, s>>>(
             *p, *b);
         RTS_LAUNCH_CHECK();
     }
@@ -304,10 +304,14 @@ int rts_grid_sort(const RtsParams *p, const RtsBuffers *b, void *stream) {
 
 int rts_force_max(const RtsParams *p, const RtsBuffers *b, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
-    k_force_max<<<rts_blocks(p->n_fluid, kThreads, 148 * 8), kThreads, 0, s>>>(*p, *b);
+    rts_note_launch(), k_force_max<<<rts_blocks(p->n_fluid, kThreads, 148 * 8), kThreads, 0, s>>>(*p, *b);
     RTS_LAUNCH_CHECK();
     return 0;
 }
+
+static unsigned long long g_launches = 0;
+void rts_note_launch(void) { __atomic_fetch_add(&g_launches, 1ull, __ATOMIC_RELAXED); }
+long long rts_launch_count(void) { return (long long)__atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
 
 int rts_abi_version(void) { return RTS_ABI_VERSION; }
 

@@ -120,23 +120,23 @@ extern "C" int rts_block_levels(const RtsParams *p, const RtsBuffers *b, int exp
                                 void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
     const int blocks = rts_blocks(p->n_cells, kThreads);
-    k_assign<<<blocks, kThreads, 0, s>>>(*p, *b);
+    rts_note_launch(), k_assign<<<blocks, kThreads, 0, s>>>(*p, *b);
     RTS_LAUNCH_CHECK();
     if (expand == 2) return 0;  // assign only (required levels, pcisph.py:726-740)
     if (!expand || p->pin_region) {
-        k_smooth<<<blocks, kThreads, 0, s>>>(*p, *b, b->block_field);
+        rts_note_launch(), k_smooth<<<blocks, kThreads, 0, s>>>(*p, *b, b->block_field);
         RTS_LAUNCH_CHECK();
         return 0;
     }
     // smoothed field into block_tmp, then expansion into block_field
-    k_smooth<<<blocks, kThreads, 0, s>>>(*p, *b, b->block_tmp);
+    rts_note_launch(), k_smooth<<<blocks, kThreads, 0, s>>>(*p, *b, b->block_tmp);
     RTS_LAUNCH_CHECK();
     uint8_t *m0 = b->block_flag;
     uint8_t *m1 = reinterpret_cast<uint8_t *>(b->block_field);  // scratch until final write
-    k_dilate_axis<<<blocks, kThreads, 0, s>>>(*p, b->block_tmp, nullptr, m0, 2, 4, 1);
-    k_dilate_axis<<<blocks, kThreads, 0, s>>>(*p, nullptr, m0, m1, 1, 4, 0);
-    k_dilate_axis<<<blocks, kThreads, 0, s>>>(*p, nullptr, m1, m0, 0, 4, 0);
-    k_expand_apply<<<blocks, kThreads, 0, s>>>(*p, b->block_tmp, m0, b->block_field);
+    rts_note_launch(), k_dilate_axis<<<blocks, kThreads, 0, s>>>(*p, b->block_tmp, nullptr, m0, 2, 4, 1);
+    rts_note_launch(), k_dilate_axis<<<blocks, kThreads, 0, s>>>(*p, nullptr, m0, m1, 1, 4, 0);
+    rts_note_launch(), k_dilate_axis<<<blocks, kThreads, 0, s>>>(*p, nullptr, m1, m0, 0, 4, 0);
+    rts_note_launch(), k_expand_apply<<<blocks, kThreads, 0, s>>>(*p, b->block_tmp, m0, b->block_field);
     RTS_LAUNCH_CHECK();
     return 0;
 }

@@ -489,13 +489,13 @@ extern "C" {
 
 int rts_pci_walls(const RtsParams *p, const RtsBuffers *b, void *stream) {
     if (p->n_bound <= 0) return 0;
-    k_xs4_walls<<<rts_blocks(p->n_bound, 256), 256, 0, (cudaStream_t)stream>>>(*p, *b);
+    rts_note_launch(), k_xs4_walls<<<rts_blocks(p->n_bound, 256), 256, 0, (cudaStream_t)stream>>>(*p, *b);
     RTS_LAUNCH_CHECK();
     return 0;
 }
 
 int rts_pci_major_particles(const RtsParams *p, const RtsBuffers *b, void *stream) {
-    k_major_particles<<<rts_blocks(p->n_fluid, 256), 256, 0, (cudaStream_t)stream>>>(*p, *b);
+    rts_note_launch(), k_major_particles<<<rts_blocks(p->n_fluid, 256), 256, 0, (cudaStream_t)stream>>>(*p, *b);
     RTS_LAUNCH_CHECK();
     return 0;
 }
@@ -504,9 +504,9 @@ int rts_pci_refresh(const RtsParams *p, const RtsBuffers *b, int all, int two_la
                     void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
     cudaMemsetAsync(&b->ctr->n_compute, 0, sizeof(int), s);
-    k_refresh_list<<<rts_blocks(p->n_fluid, 256), 256, 0, s>>>(*p, *b, all);
+    rts_note_launch(), k_refresh_list<<<rts_blocks(p->n_fluid, 256), 256, 0, s>>>(*p, *b, all);
     RTS_LAUNCH_CHECK();
-    k_refresh<<<rts_blocks(p->n_fluid, kThreads), kThreads, 0, s>>>(*p, *b, two_layer_r1);
+    rts_note_launch(), k_refresh<<<rts_blocks(p->n_fluid, kThreads), kThreads, 0, s>>>(*p, *b, two_layer_r1);
     RTS_LAUNCH_CHECK();
     return 0;
 }
@@ -514,9 +514,9 @@ int rts_pci_refresh(const RtsParams *p, const RtsBuffers *b, int all, int two_la
 int rts_pci_motion(const RtsParams *p, const RtsBuffers *b, int all, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
     if (all)
-        k_motion_all<<<rts_blocks(p->n_fluid, 256), 256, 0, s>>>(*p, *b);
+        rts_note_launch(), k_motion_all<<<rts_blocks(p->n_fluid, 256), 256, 0, s>>>(*p, *b);
     else
-        k_motion_list<<<rts_blocks(p->n_fluid, 256), 256, 0, s>>>(*p, *b);
+        rts_note_launch(), k_motion_list<<<rts_blocks(p->n_fluid, 256), 256, 0, s>>>(*p, *b);
     RTS_LAUNCH_CHECK();
     return 0;
 }
@@ -525,13 +525,13 @@ int rts_pci_sets(const RtsParams *p, const RtsBuffers *b, int row_mask, int all_
                  void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
     cudaMemsetAsync(&b->ctr->n_pred, 0, 2 * sizeof(int), s);  // n_pred, n_force
-    k_sets<<<rts_blocks(p->n_fluid, 256), 256, 0, s>>>(*p, *b, row_mask, all_pred);
+    rts_note_launch(), k_sets<<<rts_blocks(p->n_fluid, 256), 256, 0, s>>>(*p, *b, row_mask, all_pred);
     RTS_LAUNCH_CHECK();
     return 0;
 }
 
 int rts_pci_density(const RtsParams *p, const RtsBuffers *b, void *stream) {
-    k_density<<<rts_blocks(p->n_fluid, kThreads), kThreads, 0, (cudaStream_t)stream>>>(*p, *b);
+    rts_note_launch(), k_density<<<rts_blocks(p->n_fluid, kThreads), kThreads, 0, (cudaStream_t)stream>>>(*p, *b);
     RTS_LAUNCH_CHECK();
     return 0;
 }
@@ -543,33 +543,33 @@ int rts_pci_se_reduce(const RtsParams *p, const RtsBuffers *b, int with_se, void
     int blocks = (p->n_fluid + 255) / 256;
     if (blocks > kRedBlocks) blocks = kRedBlocks;
     if (blocks < 1) blocks = 1;
-    k_se_reduce<<<blocks, 256, 0, s>>>(*p, *b, with_se);
+    rts_note_launch(), k_se_reduce<<<blocks, 256, 0, s>>>(*p, *b, with_se);
     RTS_LAUNCH_CHECK();
-    k_sum_partials<<<1, 1024, 0, s>>>(*b, blocks);
+    rts_note_launch(), k_sum_partials<<<1, 1024, 0, s>>>(*b, blocks);
     RTS_LAUNCH_CHECK();
     return 0;
 }
 
 int rts_pci_observed(const RtsParams *p, const RtsBuffers *b, int with_se, void *stream) {
-    k_observed<<<rts_blocks(p->n_cells, 256), 256, 0, (cudaStream_t)stream>>>(*p, *b, with_se);
+    rts_note_launch(), k_observed<<<rts_blocks(p->n_cells, 256), 256, 0, (cudaStream_t)stream>>>(*p, *b, with_se);
     RTS_LAUNCH_CHECK();
     return 0;
 }
 
 int rts_pci_sob(const RtsParams *p, const RtsBuffers *b, void *stream) {
-    k_sob<<<rts_blocks(p->n_fluid, 256), 256, 0, (cudaStream_t)stream>>>(*p, *b);
+    rts_note_launch(), k_sob<<<rts_blocks(p->n_fluid, 256), 256, 0, (cudaStream_t)stream>>>(*p, *b);
     RTS_LAUNCH_CHECK();
     return 0;
 }
 
 int rts_pci_pforces(const RtsParams *p, const RtsBuffers *b, void *stream) {
-    k_pforces<<<rts_blocks(p->n_fluid, kThreads), kThreads, 0, (cudaStream_t)stream>>>(*p, *b);
+    rts_note_launch(), k_pforces<<<rts_blocks(p->n_fluid, kThreads), kThreads, 0, (cudaStream_t)stream>>>(*p, *b);
     RTS_LAUNCH_CHECK();
     return 0;
 }
 
 int rts_pci_integrate(const RtsParams *p, const RtsBuffers *b, int countdown, void *stream) {
-    k_integrate<<<rts_blocks(p->n_fluid, 256), 256, 0, (cudaStream_t)stream>>>(*p, *b,
+    rts_note_launch(), k_integrate<<<rts_blocks(p->n_fluid, 256), 256, 0, (cudaStream_t)stream>>>(*p, *b,
                                                                                countdown);
     RTS_LAUNCH_CHECK();
     return 0;
@@ -578,21 +578,21 @@ int rts_pci_integrate(const RtsParams *p, const RtsBuffers *b, int countdown, vo
 int rts_pci_mark_updates(const RtsParams *p, const RtsBuffers *b, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
     const int cb = rts_blocks(p->n_cells, 256);
-    k_mark_blocks<<<cb, 256, 0, s>>>(*p, *b);
-    k_mark_apply<<<cb, 256, 0, s>>>(*p, *b);
-    k_mark_particles<<<rts_blocks(p->n_fluid, 256), 256, 0, s>>>(*p, *b);
+    rts_note_launch(), k_mark_blocks<<<cb, 256, 0, s>>>(*p, *b);
+    rts_note_launch(), k_mark_apply<<<cb, 256, 0, s>>>(*p, *b);
+    rts_note_launch(), k_mark_particles<<<rts_blocks(p->n_fluid, 256), 256, 0, s>>>(*p, *b);
     RTS_LAUNCH_CHECK();
     return 0;
 }
 
 int rts_pci_snapshot(const RtsParams *p, const RtsBuffers *b, int restore, void *stream) {
-    k_snapshot<<<rts_blocks(p->n_fluid, 256), 256, 0, (cudaStream_t)stream>>>(*p, *b, restore);
+    rts_note_launch(), k_snapshot<<<rts_blocks(p->n_fluid, 256), 256, 0, (cudaStream_t)stream>>>(*p, *b, restore);
     RTS_LAUNCH_CHECK();
     return 0;
 }
 
 int rts_vel_max(const RtsParams *p, const RtsBuffers *b, void *stream) {
-    k_vel_max<<<rts_blocks(p->n_fluid, 256, 148 * 8), 256, 0, (cudaStream_t)stream>>>(*p, *b);
+    rts_note_launch(), k_vel_max<<<rts_blocks(p->n_fluid, 256, 148 * 8), 256, 0, (cudaStream_t)stream>>>(*p, *b);
     RTS_LAUNCH_CHECK();
     return 0;
 }

@@ -254,28 +254,28 @@ extern "C" {
 int rts_wcsph_propagate(const RtsParams *p, const RtsBuffers *b, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
     cudaMemsetAsync(&b->ctr->n_compute, 0, sizeof(int), s);
-    k_propagate<<<rts_blocks(p->n_fluid + p->n_bound, 256), 256, 0, s>>>(*p, *b);
+    rts_note_launch(), k_propagate<<<rts_blocks(p->n_fluid + p->n_bound, 256), 256, 0, s>>>(*p, *b);
     RTS_LAUNCH_CHECK();
     return 0;
 }
 
 int rts_wcsph_density(const RtsParams *p, const RtsBuffers *b, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
-    k_density<<<rts_blocks(p->n_fluid, kThreads), kThreads, 0, s>>>(*p, *b);
+    rts_note_launch(), k_density<<<rts_blocks(p->n_fluid, kThreads), kThreads, 0, s>>>(*p, *b);
     RTS_LAUNCH_CHECK();
     return 0;
 }
 
 int rts_wcsph_forces(const RtsParams *p, const RtsBuffers *b, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
-    k_forces<<<rts_blocks(p->n_fluid, kThreads), kThreads, 0, s>>>(*p, *b);
+    rts_note_launch(), k_forces<<<rts_blocks(p->n_fluid, kThreads), kThreads, 0, s>>>(*p, *b);
     RTS_LAUNCH_CHECK();
     return 0;
 }
 
 int rts_wcsph_integrate(const RtsParams *p, const RtsBuffers *b, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
-    k_integrate<<<rts_blocks(p->n_fluid, 256), 256, 0, s>>>(*p, *b);
+    rts_note_launch(), k_integrate<<<rts_blocks(p->n_fluid, 256), 256, 0, s>>>(*p, *b);
     RTS_LAUNCH_CHECK();
     return 0;
 }

@@ -185,6 +185,7 @@ class PcisphSolver(_DeviceSolver):
         A.alloc("snap_fp", (n1, 3), f32, 0)
         self.local_entered_total = 0
         self.local_reverted_total = 0
+        self._force_total = 0
         p = self.params
         p.dt_base = self.dt
         p.use_sound = 0
@@ -220,7 +221,7 @@ class PcisphSolver(_DeviceSolver):
         return torch.cuda.current_stream(self.device)
 
     def _call(self, name, *args):
-        N.call(name, self.params, self.arena.buf, *args, self._stream().cuda_stream)
+        self._launch(name, *args)
 
     def _prepare(self, dt: float) -> None:
         self._sync_params()
@@ -422,6 +423,7 @@ class PcisphSolver(_DeviceSolver):
             motion_all = False
             it += 1
             corrected += int(c.n_pred)
+            self._force_total += int(c.n_force)
             if local_active:
                 local_run += 1
             else:

@@ -116,6 +116,31 @@ class _DeviceSolver:
         for a in range(3):
             p.gravity[a] = float(g[a])
 
+    # -- kernel launch with optional CUDA-event timing (bench roofline) -----
+    _ktimes: dict | None = None
+
+    def time_kernels(self, names) -> None:
+        """Record CUDA events around every launch of the named entry points
+        (used by bench.py for the live roofline of the dominant kernel)."""
+        self._ktimes = {n: [] for n in names}
+
+    def kernel_times(self, name: str) -> list[float]:
+        """Durations (s) of the recorded launches of ``name`` (syncs)."""
+        return [a.elapsed_time(b) * 1e-3 for a, b in (self._ktimes or {}).get(name, [])]
+
+    def _launch(self, name: str, *args) -> None:
+        stream = torch.cuda.current_stream(self.device)
+        kt = self._ktimes
+        if kt is not None and name in kt:
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            N.call(name, self.params, self.arena.buf, *args, stream.cuda_stream)
+            b.record(stream)
+            kt[name].append((a, b))
+        else:
+            N.call(name, self.params, self.arena.buf, *args, stream.cuda_stream)
+
     @property
     def pos(self) -> torch.Tensor:
         return self._pos[: self.n_fluid + self.n_bound]
@@ -235,12 +260,12 @@ class WcsphSolver(_DeviceSolver):
         self.grid.launch_rebuild(p, stream, want_maxima=rts)
         tm.mark("neighbor", stream)
         if rts:
-            N.call("rts_block_levels", p, buf, 0, s)
-        N.call("rts_wcsph_propagate", p, buf, s)
+            self._launch("rts_block_levels", 0)
+        self._launch("rts_wcsph_propagate")
         tm.mark("rts", stream)
-        N.call("rts_wcsph_density", p, buf, s)
-        N.call("rts_wcsph_forces", p, buf, s)
-        N.call("rts_wcsph_integrate", p, buf, s)
+        self._launch("rts_wcsph_density")
+        self._launch("rts_wcsph_forces")
+        self._launch("rts_wcsph_integrate")
         tm.mark("physics", stream)
         if not read:
             return None
