@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define RTS_ABI_VERSION 4
+#define RTS_ABI_VERSION 5
 
 /* err_flags bits */
 #define RTS_ERR_ESCAPED   0x1u  /* fluid left the padded grid or non-finite (grid.py:268-273) */
@@ -147,6 +147,7 @@ typedef struct RtsBuffers {
     double  *partial;      /* (>= 4096) deterministic reduction partials */
     float   *snap_p;       /* (Nf)    local-phase snapshot of p */
     float   *snap_fp;      /* (Nf, 3) local-phase snapshot of f_p */
+    int32_t *slot_of;      /* (Nf) CSR slot of each fluid particle (inverse of order) */
     RtsCounters *ctr;
 } RtsBuffers;
 
@@ -185,6 +186,10 @@ int rts_block_levels(const RtsParams *p, const RtsBuffers *b, int expand, void *
 /* ---- RTS-PCISPH (pcisph.py) ------------------------------------------- */
 /* Wall rows of xs4 (static positions, marker -1). */
 int rts_pci_walls(const RtsParams *p, const RtsBuffers *b, void *stream);
+/* Sorted candidate positions cpos[k] = pos[order[k]] and slot_of, at major
+ * start; k_integrate keeps them current so the stale-grid search of later
+ * minor steps reads current positions (grid.py:140-143) contiguously. */
+int rts_pci_gather(const RtsParams *p, const RtsBuffers *b, void *stream);
 /* _assign_major_regions particle tail (pcisph.py:531-534): region, validity
  * = VALIDITY_PERIOD[region], compute = 1, S_e = empty. */
 int rts_pci_major_particles(const RtsParams *p, const RtsBuffers *b, void *stream);

@@ -12,7 +12,7 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "librtssph.so")
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 _c = ctypes
 _D = _c.c_double
@@ -49,7 +49,7 @@ BUFFER_FIELDS = (
     "cell_bcount", "starts", "order", "fill", "scan_tmp", "bcell_ids", "bcell_start", "bidx",
     "bcell_of", "bcell_active", "vmax", "fmax", "block_raw", "block_field", "block_tmp",
     "block_flag", "cpos", "cvel", "active", "list2", "nbr", "cnt", "xs4", "pflag", "partial",
-    "snap_p", "snap_fp", "ctr",
+    "snap_p", "snap_fp", "slot_of", "ctr",
 )
 
 
@@ -73,6 +73,7 @@ SIGNATURES = {
     "rts_block_levels": [_PP, _PB, _c.c_int, _P],
     "rts_wcsph_propagate": [_PP, _PB, _P],
     "rts_pci_walls": [_PP, _PB, _P],
+    "rts_pci_gather": [_PP, _PB, _P],
     "rts_pci_major_particles": [_PP, _PB, _P],
     "rts_pci_refresh": [_PP, _PB, _c.c_int, _c.c_int, _P],
     "rts_pci_motion": [_PP, _PB, _c.c_int, _P],

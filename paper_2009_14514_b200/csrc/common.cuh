@@ -91,6 +91,41 @@ RTS_DEV void warp_append(bool pred, int value, int *list, int *count) {
     if (pred) list[base + __popc(mask & ((1u << lane) - 1u))] = value;
 }
 
+// Block-aggregated append of up to two predicates per thread: one global
+// atomic per block and list (the loop around it must be block-uniform).
+// Within a block the output keeps thread order.
+template <int NT>
+RTS_DEV void block_append2(bool p0, int v0, int *list0, int *count0, bool p1, int v1,
+                           int *list1, int *count1) {
+    constexpr int NW = NT / 32;
+    __shared__ int s_w0[NW], s_w1[NW], s_base[2];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned m0 = __ballot_sync(0xffffffffu, p0);
+    const unsigned m1 = __ballot_sync(0xffffffffu, p1);
+    if (lane == 0) {
+        s_w0[warp] = __popc(m0);
+        s_w1[warp] = __popc(m1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int a = 0, c = 0;
+        for (int w = 0; w < NW; ++w) {
+            const int x = s_w0[w], y = s_w1[w];
+            s_w0[w] = a;
+            s_w1[w] = c;
+            a += x;
+            c += y;
+        }
+        s_base[0] = a && list0 ? atomicAdd(count0, a) : 0;
+        s_base[1] = c && list1 ? atomicAdd(count1, c) : 0;
+    }
+    __syncthreads();
+    const unsigned lt = (1u << lane) - 1u;
+    if (p0) list0[s_base[0] + s_w0[warp] + __popc(m0 & lt)] = v0;
+    if (p1) list1[s_base[1] + s_w1[warp] + __popc(m1 & lt)] = v1;
+    __syncthreads();  // shared slots are reused by the next loop trip
+}
+
 RTS_DEV int warp_count_add(bool pred, int *count) {
     const unsigned mask = __ballot_sync(0xffffffffu, pred);
     const int lane = threadIdx.x & 31;

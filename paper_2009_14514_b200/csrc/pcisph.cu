@@ -48,6 +48,18 @@ __global__ void k_xs4_walls(const __grid_constant__ RtsParams p, RtsBuffers b) {
     }
 }
 
+// candidate copies of the major grid: cpos[k] = pos[order[k]], slot_of
+__global__ void k_gather(const __grid_constant__ RtsParams p, RtsBuffers b) {
+    if (fatal(b.ctr)) return;
+    const int n = b.ctr->n_sorted;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const int j = b.order[k];
+        reinterpret_cast<float4 *>(b.cpos)[k] =
+            make_float4(b.pos[3 * j], b.pos[3 * j + 1], b.pos[3 * j + 2], 0.0f);
+        if (j < p.n_fluid) b.slot_of[j] = k;
+    }
+}
+
 // _assign_major_regions per-particle tail (pcisph.py:531-534)
 __global__ void k_major_particles(const __grid_constant__ RtsParams p, RtsBuffers b) {
     if (fatal(b.ctr)) return;
@@ -62,14 +74,15 @@ __global__ void k_major_particles(const __grid_constant__ RtsParams p, RtsBuffer
 }
 
 // refresh list: particles whose tables are renewed this minor step
-__global__ void k_refresh_list(const __grid_constant__ RtsParams p, RtsBuffers b, int all) {
+__global__ void __launch_bounds__(256) k_refresh_list(const __grid_constant__ RtsParams p,
+                                                      RtsBuffers b, int all) {
     if (fatal(b.ctr)) return;
     const int nf = p.n_fluid;
     const int stride = gridDim.x * blockDim.x;
     for (int base = blockIdx.x * blockDim.x; base < nf; base += stride) {
         const int i = base + threadIdx.x;
         const bool r = i < nf && (all || b.compute[i]);
-        warp_append(r, i, b.active, &b.ctr->n_compute);
+        block_append2<256>(r, i, b.active, &b.ctr->n_compute, false, 0, nullptr, nullptr);
     }
 }
 
@@ -99,13 +112,14 @@ __global__ void __launch_bounds__(kThreads) k_refresh(const __grid_constant__ Rt
         long long lost = 0;
         int *row = b.nbr + (size_t)i * p.width;
         double fx = 0.0, fy = 0.0, fz = 0.0;
+        const float4 *cpos = reinterpret_cast<const float4 *>(b.cpos);
         for (int ax = max(0, cx - lay); ax <= min(nx - 1, cx + lay); ++ax)
             for (int ay = max(0, cy - lay); ay <= min(ny - 1, cy + lay); ++ay) {
                 const int base = (ax * ny + ay) * nz;
                 const int k0 = b.starts[base + z0], k1 = b.starts[base + z1 + 1];
                 for (int k = k0; k < k1; ++k) {
-                    const int j = b.order[k];
-                    const float px = b.pos[3 * j], py = b.pos[3 * j + 1], pz = b.pos[3 * j + 2];
+                    const float4 o = cpos[k];
+                    const float px = o.x, py = o.y, pz = o.z;
                     {
                         const float dx = fxi - px, dy = fyi - py, dz = fzi - pz;
                         if (__fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)),
@@ -116,6 +130,7 @@ __global__ void __launch_bounds__(kThreads) k_refresh(const __grid_constant__ Rt
                                  dz = xsub(zi, (double)pz);
                     const double r2 = dist2(dx, dy, dz);
                     if (!(r2 < p.h2)) continue;
+                    const int j = b.order[k];
                     if (cntn < p.width) {
                         row[cntn++] = j;
                     } else {
@@ -173,8 +188,8 @@ __global__ void k_motion_list(const __grid_constant__ RtsParams p, RtsBuffers b)
 
 // set membership for one iteration (pcisph.py:634-643); row_mask bit n set
 // when region n is scheduled; S_ob refreshed from the observed mask first
-__global__ void k_sets(const __grid_constant__ RtsParams p, RtsBuffers b, int row_mask,
-                       int all_pred) {
+__global__ void __launch_bounds__(256) k_sets(const __grid_constant__ RtsParams p, RtsBuffers b,
+                                              int row_mask, int all_pred) {
     if (fatal(b.ctr)) return;
     const int nf = p.n_fluid;
     const int stride = gridDim.x * blockDim.x;
@@ -194,8 +209,7 @@ __global__ void k_sets(const __grid_constant__ RtsParams p, RtsBuffers b, int ro
             }
             b.pflag[i] = force;
         }
-        warp_append(pred, i, b.active, &b.ctr->n_pred);
-        warp_append(force, i, b.list2, &b.ctr->n_force);
+        block_append2<256>(pred, i, b.active, &b.ctr->n_pred, force, i, b.list2, &b.ctr->n_force);
     }
 }
 
@@ -218,13 +232,21 @@ __global__ void __launch_bounds__(kThreads) k_density(const __grid_constant__ Rt
         const float4 a = xs4[i];
         const double xi = a.x, yi = a.y, zi = a.z;
         const int c = b.cnt[i];
-        const int *row = b.nbr + (size_t)i * p.width;
+        const int4 *row4 = reinterpret_cast<const int4 *>(b.nbr + (size_t)i * p.width);
         double acc = 0.0;
-        for (int q = 0; q < c; ++q) {
-            const float4 o = xs4[row[q]];
-            acc = xadd(acc, poly6(dist2(xsub(xi, (double)o.x), xsub(yi, (double)o.y),
-                                        xsub(zi, (double)o.z)),
-                                  p.h2, p.c_poly6));
+        for (int q = 0; q < c; q += 4) {
+            const int4 jj = row4[q >> 2];
+            const int j4[4] = {jj.x, jj.y, jj.z, jj.w};
+            float4 o[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) o[u] = xs4[q + u < c ? j4[u] : i];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (q + u < c)
+                    acc = xadd(acc, poly6(dist2(xsub(xi, (double)o[u].x), xsub(yi, (double)o[u].y),
+                                                xsub(zi, (double)o[u].z)),
+                                          p.h2, p.c_poly6));
+            }
         }
         const double rho = xmul(p.mass, acc);
         const double diff = xsub(rho, p.rho0);
@@ -343,21 +365,30 @@ __global__ void __launch_bounds__(kThreads) k_pforces(const __grid_constant__ Rt
         const double term_i = xmul((double)b.pres[i], inv_rho0_sq);
         const double wall = xadd(term_i, term_i);
         const int c = b.cnt[i];
-        const int *row = b.nbr + (size_t)i * p.width;
+        const int4 *row4 = reinterpret_cast<const int4 *>(b.nbr + (size_t)i * p.width);
         double fx = 0.0, fy = 0.0, fz = 0.0;
-        for (int q = 0; q < c; ++q) {
-            const int j = row[q];
-            if (j == i) continue;
-            const float4 o = xs4[j];
-            const double dx = xsub(xi, (double)o.x), dy = xsub(yi, (double)o.y),
-                         dz = xsub(zi, (double)o.z);
-            const double term = j < p.n_fluid ? xadd(term_i, xmul((double)o.w, inv_rho0_sq)) : wall;
-            const double r = xsqrt(dist2(dx, dy, dz));
-            if (r <= 0.0 || r >= p.h) continue;
-            const double s = xmul(xmul(m2, term), spiky(r, p.h, p.c_spiky));
-            fx = xsub(fx, xmul(s, dx));
-            fy = xsub(fy, xmul(s, dy));
-            fz = xsub(fz, xmul(s, dz));
+        for (int q = 0; q < c; q += 4) {
+            const int4 jj = row4[q >> 2];
+            const int j4[4] = {jj.x, jj.y, jj.z, jj.w};
+            float4 o4[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) o4[u] = xs4[q + u < c ? j4[u] : i];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int j = j4[u];
+                if (q + u >= c || j == i) continue;
+                const float4 o = o4[u];
+                const double dx = xsub(xi, (double)o.x), dy = xsub(yi, (double)o.y),
+                             dz = xsub(zi, (double)o.z);
+                const double term =
+                    j < p.n_fluid ? xadd(term_i, xmul((double)o.w, inv_rho0_sq)) : wall;
+                const double r = xsqrt(dist2(dx, dy, dz));
+                if (r <= 0.0 || r >= p.h) continue;
+                const double s = xmul(xmul(m2, term), spiky(r, p.h, p.c_spiky));
+                fx = xsub(fx, xmul(s, dx));
+                fy = xsub(fy, xmul(s, dy));
+                fz = xsub(fz, xmul(s, dz));
+            }
         }
         b.f_p[3 * i] = (float)fx;
         b.f_p[3 * i + 1] = (float)fy;
@@ -385,6 +416,7 @@ __global__ void k_integrate(const __grid_constant__ RtsParams p, RtsBuffers b, i
             }
             b.pos[3 * i + a] = (float)x;
             b.vel[3 * i + a] = (float)v;
+            if (countdown) b.cpos[4 * b.slot_of[i] + a] = (float)x;
         }
         if (countdown) {
             int v = b.validity[i] - 1;
@@ -494,6 +526,13 @@ int rts_pci_walls(const RtsParams *p, const RtsBuffers *b, void *stream) {
     return 0;
 }
 
+int rts_pci_gather(const RtsParams *p, const RtsBuffers *b, void *stream) {
+    rts_note_launch(), k_gather<<<rts_blocks(p->n_fluid + p->n_bound, 256), 256, 0,
+                                   (cudaStream_t)stream>>>(*p, *b);
+    RTS_LAUNCH_CHECK();
+    return 0;
+}
+
 int rts_pci_major_particles(const RtsParams *p, const RtsBuffers *b, void *stream) {
     rts_note_launch(), k_major_particles<<<rts_blocks(p->n_fluid, 256), 256, 0, (cudaStream_t)stream>>>(*p, *b);
     RTS_LAUNCH_CHECK();
@@ -504,7 +543,7 @@ int rts_pci_refresh(const RtsParams *p, const RtsBuffers *b, int all, int two_la
                     void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
     cudaMemsetAsync(&b->ctr->n_compute, 0, sizeof(int), s);
-    rts_note_launch(), k_refresh_list<<<rts_blocks(p->n_fluid, 256), 256, 0, s>>>(*p, *b, all);
+    rts_note_launch(), k_refresh_list<<<rts_blocks(p->n_fluid, 256, 148 * 4), 256, 0, s>>>(*p, *b, all);
     RTS_LAUNCH_CHECK();
     rts_note_launch(), k_refresh<<<rts_blocks(p->n_fluid, kThreads), kThreads, 0, s>>>(*p, *b, two_layer_r1);
     RTS_LAUNCH_CHECK();
@@ -525,7 +564,7 @@ int rts_pci_sets(const RtsParams *p, const RtsBuffers *b, int row_mask, int all_
                  void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
     cudaMemsetAsync(&b->ctr->n_pred, 0, 2 * sizeof(int), s);  // n_pred, n_force
-    rts_note_launch(), k_sets<<<rts_blocks(p->n_fluid, 256), 256, 0, s>>>(*p, *b, row_mask, all_pred);
+    rts_note_launch(), k_sets<<<rts_blocks(p->n_fluid, 256, 148 * 4), 256, 0, s>>>(*p, *b, row_mask, all_pred);
     RTS_LAUNCH_CHECK();
     return 0;
 }

@@ -19,7 +19,8 @@ namespace {
 constexpr int kThreads = 128;
 
 // wcsph.py:262-266 (validity / pre-emption) + sorted-copy gather + active list
-__global__ void k_propagate(const __grid_constant__ RtsParams p, RtsBuffers b) {
+__global__ void __launch_bounds__(256) k_propagate(const __grid_constant__ RtsParams p,
+                                                   RtsBuffers b) {
     if (fatal(b.ctr)) return;
     const int n_sorted = b.ctr->n_sorted;
     const int stride = gridDim.x * blockDim.x;
@@ -52,7 +53,7 @@ __global__ void k_propagate(const __grid_constant__ RtsParams p, RtsBuffers b) {
                 reinterpret_cast<float4 *>(b.cvel)[k] = make_float4(0.f, 0.f, 0.f, 0.f);
             }
         }
-        warp_append(act, k, b.active, &b.ctr->n_compute);
+        block_append2<256>(act, k, b.active, &b.ctr->n_compute, false, 0, nullptr, nullptr);
     }
 }
 
@@ -254,7 +255,7 @@ extern "C" {
 int rts_wcsph_propagate(const RtsParams *p, const RtsBuffers *b, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
     cudaMemsetAsync(&b->ctr->n_compute, 0, sizeof(int), s);
-    rts_note_launch(), k_propagate<<<rts_blocks(p->n_fluid + p->n_bound, 256), 256, 0, s>>>(*p, *b);
+    rts_note_launch(), k_propagate<<<rts_blocks(p->n_fluid + p->n_bound, 256, 148 * 4), 256, 0, s>>>(*p, *b);
     RTS_LAUNCH_CHECK();
     return 0;
 }

@@ -183,6 +183,7 @@ class PcisphSolver(_DeviceSolver):
         A.alloc("partial", (4096,), torch.float64, 0)
         A.alloc("snap_p", (n1,), f32, 0)
         A.alloc("snap_fp", (n1, 3), f32, 0)
+        A.alloc("slot_of", (n1,), torch.int32, 0)
         self.local_entered_total = 0
         self.local_reverted_total = 0
         self._force_total = 0
@@ -253,6 +254,7 @@ class PcisphSolver(_DeviceSolver):
         self.counters.reset(self._stream())
         self.grid.launch_rebuild(self.params, self._stream(), want_maxima=want_maxima,
                                  add_fp=True)
+        self._call("rts_pci_gather")
 
     def _zero_pressure(self) -> None:
         s = self._stream().cuda_stream
