@@ -281,6 +281,7 @@ def main():
 
     # ---- dominant kernel roofline (separate instrumented pass) --------------
     solver.time_kernels(kernels)
+    solver.use_graphs = False  # per-kernel CUDA events need individual launches
     solver._force_total = 0
     rec = {"pred": 0, "force": 0, "refresh": 0, "motion": 0}
     prof_rows = []
@@ -299,6 +300,7 @@ def main():
     rec["motion"] = nf * len(prof_rows) + rec["force"]
     c_mean = float(solver.cnt.double().mean())
     solver._ktimes = None
+    solver.use_graphs = True
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     peak = float(peaks.get("hbm_gbs", 6650.0))

@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define RTS_ABI_VERSION 5
+#define RTS_ABI_VERSION 7
 
 /* err_flags bits */
 #define RTS_ERR_ESCAPED   0x1u  /* fluid left the padded grid or non-finite (grid.py:268-273) */
@@ -93,6 +93,49 @@ typedef struct RtsCounters {
     double   reserved[8];
 } RtsCounters;
 
+/* Per-minor-step record written by the device loop control (StepStats,
+ * stats.py:9-40 / pcisph.py:591-610). */
+typedef struct RtsMinorStats {
+    int32_t  iterations;
+    int32_t  n_refresh;
+    int32_t  early;
+    int32_t  riters[5];
+    int64_t  corrected;
+    int64_t  forced;       /* sum of |force set| over the iterations */
+    double   max_err;
+    double   avg_err;
+    int64_t  t_begin, t_refreshed, t_looped, t_end;  /* %globaltimer ns */
+} RtsMinorStats;
+
+#define RTS_MAX_MINOR 8
+#define RTS_MAX_ROWS 8
+
+/* Device-resident state of the scheduled correction loop
+ * (_correct_scheduled, pcisph.py:612-716; _correct_all, pcisph.py:439-468).
+ * The k_control kernel owns every decision; iteration kernels only read
+ * row_mask / motion_all / snap_op / done. */
+typedef struct RtsControl {
+    int32_t it, g_count, local_active, local_banned, local_run, early, done, failed;
+    int32_t motion_all;    /* next motion pass covers all fluid */
+    int32_t row_mask;      /* next iteration's scheduled regions (bit n), 0 = local pass */
+    int32_t snap_op;       /* after control: 0 none, 1 snapshot p/f_p, 2 revert */
+    int32_t minor;
+    int32_t stop_major;    /* early termination or failure: later minors are skipped */
+    int32_t local_entered, local_reverted;
+    int32_t fail_kind;     /* 1 non-finite, 2 RTS cap, 3 sync cap */
+    int32_t fail_g;
+    int32_t n_rows[RTS_MAX_MINOR];
+    int32_t row_masks[RTS_MAX_MINOR][RTS_MAX_ROWS];
+    int32_t row_counts[RTS_MAX_MINOR][RTS_MAX_ROWS];  /* region multiplicities, 4 bits each */
+    int32_t riters[5];
+    int32_t skipped;       /* current minor skipped (stop_major) */
+    int64_t corrected;
+    int64_t forced;
+    double  last_max_err, last_avg_err;
+    double  fail_err;
+    RtsMinorStats stats[RTS_MAX_MINOR];
+} RtsControl;
+
 /* Buffers: every pointer is caller-owned device memory. Sizes in comments,
  * Nf = n_fluid, Nb = n_bound, Nc = n_cells, Bc = n_bcells. */
 typedef struct RtsBuffers {
@@ -148,6 +191,7 @@ typedef struct RtsBuffers {
     float   *snap_p;       /* (Nf)    local-phase snapshot of p */
     float   *snap_fp;      /* (Nf, 3) local-phase snapshot of f_p */
     int32_t *slot_of;      /* (Nf) CSR slot of each fluid particle (inverse of order) */
+    RtsControl *ctl;       /* correction-loop control block */
     RtsCounters *ctr;
 } RtsBuffers;
 
@@ -159,6 +203,9 @@ int rts_device_sms(void);
 long long rts_launch_count(void);
 /* Zero-filled cudaMemsetAsync helper so hosts need not link cudart. */
 int rts_memset(void *dst, int value, int64_t bytes, void *stream);
+
+/* Reset the counters block (err_flags = 0, first_escaped = INT32_MAX ...). */
+int rts_counters_reset(const RtsBuffers *b, void *stream);
 
 /* ---- block grid (grid.py) -------------------------------------------- */
 /* One-time static binning of the boundary shell: bcell_of, and
@@ -222,6 +269,34 @@ int rts_pci_mark_updates(const RtsParams *p, const RtsBuffers *b, void *stream);
 int rts_pci_snapshot(const RtsParams *p, const RtsBuffers *b, int restore, void *stream);
 /* max |v| over fluid into ctr->fmax_bits (_adapt_dt, pcisph.py:470-476). */
 int rts_vel_max(const RtsParams *p, const RtsBuffers *b, void *stream);
+/* p = f_p = 0 for all fluid (pcisph.py:570-571). */
+int rts_pci_zero_pressure(const RtsParams *p, const RtsBuffers *b, void *stream);
+/* Device loop control: reset per major; per-minor state reset + first row;
+ * per-minor StepStats record into ctl->stats. */
+int rts_pci_major_begin(const RtsParams *p, const RtsBuffers *b, void *stream);
+int rts_pci_minor_begin(const RtsParams *p, const RtsBuffers *b, int minor, int sync_mode,
+                        void *stream);
+int rts_pci_minor_end(const RtsParams *p, const RtsBuffers *b, int minor, void *stream);
+/* One correction iteration incl. the k_control decision kernel
+ * (pcisph.py:633-715; sync_mode: pcisph.py:446-468).  cond_handle: the
+ * cudaGraphConditionalHandle of an enclosing while node, or 0. */
+int rts_pci_iteration(const RtsParams *p, const RtsBuffers *b, int sync_mode,
+                      unsigned long long cond_handle, int local_attempts, int iteration_cap,
+                      void *stream);
+/* The decision kernel alone (+ snapshot/revert pass in RTS mode). */
+int rts_pci_control(const RtsParams *p, const RtsBuffers *b, int sync_mode,
+                    unsigned long long cond_handle, int local_attempts, int iteration_cap,
+                    void *stream);
+/* Minor step before / after the correction loop (pcisph.py:553-587). */
+int rts_pci_minor_head(const RtsParams *p, const RtsBuffers *b, int minor, void *stream);
+int rts_pci_minor_tail(const RtsParams *p, const RtsBuffers *b, int minor, int last,
+                       void *stream);
+/* Whole major step (mode 0, n_minor minors) or synchronous step (mode 1) as
+ * one CUDA graph with conditional while nodes; NULL + *err on failure. */
+void *rts_pci_graph_create(const RtsParams *p, const RtsBuffers *b, int mode, int n_minor,
+                           int local_attempts, int iteration_cap, int *err);
+int rts_graph_launch(void *graph, void *stream);
+void rts_graph_destroy(void *graph);
 
 /* ---- RTS-WCSPH (wcsph.py) -------------------------------------------- */
 /* Validity countdown / pre-emption (wcsph.py:262-266) fused with the sorted

@@ -12,7 +12,7 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "librtssph.so")
-ABI_VERSION = 5
+ABI_VERSION = 7
 
 _c = ctypes
 _D = _c.c_double
@@ -43,13 +43,40 @@ class RtsCounters(_c.Structure):
     ]
 
 
+class RtsMinorStats(_c.Structure):
+    _fields_ = [
+        ("iterations", _I), ("n_refresh", _I), ("early", _I), ("riters", _I * 5),
+        ("corrected", _c.c_int64), ("forced", _c.c_int64), ("max_err", _D), ("avg_err", _D),
+        ("t_begin", _c.c_int64), ("t_refreshed", _c.c_int64), ("t_looped", _c.c_int64),
+        ("t_end", _c.c_int64),
+    ]
+
+
+MAX_MINOR = 8
+MAX_ROWS = 8
+
+
+class RtsControl(_c.Structure):
+    _fields_ = [
+        ("it", _I), ("g_count", _I), ("local_active", _I), ("local_banned", _I),
+        ("local_run", _I), ("early", _I), ("done", _I), ("failed", _I), ("motion_all", _I),
+        ("row_mask", _I), ("snap_op", _I), ("minor", _I), ("stop_major", _I),
+        ("local_entered", _I), ("local_reverted", _I), ("fail_kind", _I), ("fail_g", _I),
+        ("n_rows", _I * MAX_MINOR), ("row_masks", (_I * MAX_ROWS) * MAX_MINOR),
+        ("row_counts", (_I * MAX_ROWS) * MAX_MINOR), ("riters", _I * 5), ("skipped", _I),
+        ("corrected", _c.c_int64), ("forced", _c.c_int64), ("last_max_err", _D),
+        ("last_avg_err", _D), ("fail_err", _D),
+        ("stats", RtsMinorStats * MAX_MINOR),
+    ]
+
+
 BUFFER_FIELDS = (
     "pos", "vel", "acc", "acc_prev", "force", "f_p", "rho", "pres", "err", "xstar", "dt_since",
     "dt_corr", "validity", "region", "compute", "in_se", "in_sob", "fluid_cells", "cell_count",
     "cell_bcount", "starts", "order", "fill", "scan_tmp", "bcell_ids", "bcell_start", "bidx",
     "bcell_of", "bcell_active", "vmax", "fmax", "block_raw", "block_field", "block_tmp",
     "block_flag", "cpos", "cvel", "active", "list2", "nbr", "cnt", "xs4", "pflag", "partial",
-    "snap_p", "snap_fp", "slot_of", "ctr",
+    "snap_p", "snap_fp", "slot_of", "ctl", "ctr",
 )
 
 
@@ -87,6 +114,16 @@ SIGNATURES = {
     "rts_pci_mark_updates": [_PP, _PB, _P],
     "rts_pci_snapshot": [_PP, _PB, _c.c_int, _P],
     "rts_vel_max": [_PP, _PB, _P],
+    "rts_counters_reset": [_PB, _P],
+    "rts_pci_zero_pressure": [_PP, _PB, _P],
+    "rts_pci_major_begin": [_PP, _PB, _P],
+    "rts_pci_minor_begin": [_PP, _PB, _c.c_int, _c.c_int, _P],
+    "rts_pci_minor_end": [_PP, _PB, _c.c_int, _P],
+    "rts_pci_iteration": [_PP, _PB, _c.c_int, _c.c_ulonglong, _c.c_int, _c.c_int, _P],
+    "rts_pci_control": [_PP, _PB, _c.c_int, _c.c_ulonglong, _c.c_int, _c.c_int, _P],
+    "rts_pci_minor_head": [_PP, _PB, _c.c_int, _P],
+    "rts_pci_minor_tail": [_PP, _PB, _c.c_int, _c.c_int, _P],
+    "rts_graph_launch": [_P, _P],
     "rts_wcsph_density": [_PP, _PB, _P],
     "rts_wcsph_forces": [_PP, _PB, _P],
     "rts_wcsph_integrate": [_PP, _PB, _P],
@@ -115,6 +152,11 @@ def load(path: str = LIB_PATH):
         fn.restype = _c.c_int
     lib.rts_launch_count.argtypes = []
     lib.rts_launch_count.restype = _c.c_longlong
+    lib.rts_pci_graph_create.argtypes = [_PP, _PB, _c.c_int, _c.c_int, _c.c_int, _c.c_int,
+                                         _c.POINTER(_c.c_int)]
+    lib.rts_pci_graph_create.restype = _c.c_void_p
+    lib.rts_graph_destroy.argtypes = [_P]
+    lib.rts_graph_destroy.restype = None
     if lib.rts_abi_version() != ABI_VERSION:
         raise NativeError(f"librtssph ABI {lib.rts_abi_version()} != expected {ABI_VERSION}")
     _lib = lib

@@ -75,6 +75,12 @@ RTS_DEV void atomic_max_pos(double *addr, double v) {
                   (unsigned long long)__double_as_longlong(v));
 }
 
+RTS_DEV long long gtimer() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 RTS_DEV bool fatal(const RtsCounters *c) {
     return (*(volatile const uint32_t *)&c->err_flags) & RTS_ERR_FATAL;
 }

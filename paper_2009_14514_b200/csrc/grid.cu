@@ -251,9 +251,22 @@ __global__ void k_force_max(const __grid_constant__ RtsParams p, RtsBuffers b) {
                   (unsigned long long)__double_as_longlong(m));
 }
 
+__global__ void k_counters_reset(RtsCounters *c) {
+    RtsCounters z = {};
+    z.first_escaped = 0x7fffffff;
+    *c = z;
+}
+
 }  // namespace
 
 extern "C" {
+
+int rts_counters_reset(const RtsBuffers *b, void *stream) {
+    rts_note_launch(), k_counters_reset<<<1, 1, 0, (cudaStream_t)stream>>>(b->ctr);
+    RTS_LAUNCH_CHECK();
+    return 0;
+}
+
 
 int rts_grid_keys(const RtsParams *p, const RtsBuffers *b, int want_maxima, int add_fp,
                   void *stream) {

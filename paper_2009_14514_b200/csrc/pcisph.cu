@@ -30,6 +30,17 @@ constexpr int kRedBlocks = 1024;  // fixed partial count -> deterministic sums
 
 __constant__ int kValidity[5] = {0, 1, 2, 4, 4};  // pcisph.py:66
 
+// loop control flags (ctl may be null for callers outside a solver)
+RTS_DEV bool loop_done(const RtsBuffers &b) {
+    return b.ctl && *(volatile const int *)&b.ctl->done;
+}
+RTS_DEV bool major_stopped(const RtsBuffers &b) {
+    return b.ctl && *(volatile const int *)&b.ctl->stop_major;
+}
+// iteration kernels skip when the loop has finished or a fatal flag is set
+#define RTS_ITER_GUARD() if (fatal(b.ctr) || loop_done(b)) return
+#define RTS_MINOR_GUARD() if (fatal(b.ctr) || major_stopped(b)) return
+
 RTS_DEV int trunc_axis(double x, double o, double inv, int n) {
     // int((x - o) * inv) then clamp (grid.py:116-131)
     const double v = xmul(xsub(x, o), inv);
@@ -76,7 +87,7 @@ __global__ void k_major_particles(const __grid_constant__ RtsParams p, RtsBuffer
 // refresh list: particles whose tables are renewed this minor step
 __global__ void __launch_bounds__(256) k_refresh_list(const __grid_constant__ RtsParams p,
                                                       RtsBuffers b, int all) {
-    if (fatal(b.ctr)) return;
+    RTS_MINOR_GUARD();
     const int nf = p.n_fluid;
     const int stride = gridDim.x * blockDim.x;
     for (int base = blockIdx.x * blockDim.x; base < nf; base += stride) {
@@ -87,69 +98,84 @@ __global__ void __launch_bounds__(256) k_refresh_list(const __grid_constant__ Rt
 }
 
 // search_into on the (stale) major grid (grid.py:88-152) fused with the
-// external forces of the refreshed particle (pcisph.py:174-199): the
-// viscosity sum visits the table entries in the order they are written.
+// external forces of the refreshed particle (pcisph.py:174-199).
+//
+// Pass 1 scans the CSR spans of the (2L+1)^3 blocks (contiguous cpos reads)
+// and classifies each candidate in fp32 with a +-1e-5 relative band around
+// h^2; only candidates inside the band take the exact fp64 test, so the
+// warp does not serialise on fp64 work for every candidate some lane hits.
+// Membership equals the reference's fp64 `r2 < h2` exactly.  Pass 2 walks
+// the freshly written table row (no divergence) for the viscosity sum.
 __global__ void __launch_bounds__(kThreads) k_refresh(const __grid_constant__ RtsParams p,
                                                       RtsBuffers b, int two_layer_r1) {
-    if (fatal(b.ctr)) return;
+    RTS_MINOR_GUARD();
     const int n = b.ctr->n_compute;
     const int nx = p.dims[0], ny = p.dims[1], nz = p.dims[2];
-    const float h2_loose = (float)(p.h2 * 1.00001);
+    const float h2_lo = (float)(p.h2 * (1.0 - 1e-5));
+    const float h2_hi = (float)(p.h2 * (1.0 + 1e-5));
     const double m2 = xmul(p.mass, p.mass);
     const double inv_rho0_sq = xdiv(1.0, xmul(p.rho0, p.rho0));
     const double mum2 = xmul(p.mu, m2);
+    const float4 *cpos = reinterpret_cast<const float4 *>(b.cpos);
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
         const int i = b.active[t];
         const float fxi = b.pos[3 * i], fyi = b.pos[3 * i + 1], fzi = b.pos[3 * i + 2];
         const double xi = fxi, yi = fyi, zi = fzi;
-        const double vxi = b.vel[3 * i], vyi = b.vel[3 * i + 1], vzi = b.vel[3 * i + 2];
         const int lay = (two_layer_r1 && b.region[i] == 1) ? 2 : 1;
         const int cx = trunc_axis(xi, p.origin[0], p.inv_block, nx);
         const int cy = trunc_axis(yi, p.origin[1], p.inv_block, ny);
         const int cz = trunc_axis(zi, p.origin[2], p.inv_block, nz);
         const int z0 = max(0, cz - lay), z1 = min(nz - 1, cz + lay);
         int cntn = 0;
-        long long lost = 0;
         int *row = b.nbr + (size_t)i * p.width;
-        double fx = 0.0, fy = 0.0, fz = 0.0;
-        const float4 *cpos = reinterpret_cast<const float4 *>(b.cpos);
         for (int ax = max(0, cx - lay); ax <= min(nx - 1, cx + lay); ++ax)
             for (int ay = max(0, cy - lay); ay <= min(ny - 1, cy + lay); ++ay) {
                 const int base = (ax * ny + ay) * nz;
                 const int k0 = b.starts[base + z0], k1 = b.starts[base + z1 + 1];
-                for (int k = k0; k < k1; ++k) {
-                    const float4 o = cpos[k];
-                    const float px = o.x, py = o.y, pz = o.z;
-                    {
-                        const float dx = fxi - px, dy = fyi - py, dz = fzi - pz;
-                        if (__fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)),
-                                      __fmul_rn(dz, dz)) > h2_loose)
-                            continue;
+                for (int kb = k0; kb < k1; kb += 4) {
+                    float4 ob[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) ob[u] = cpos[min(kb + u, k1 - 1)];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int k = kb + u;
+                        const float ex = fxi - ob[u].x, ey = fyi - ob[u].y, ez = fzi - ob[u].z;
+                        const float r2f =
+                            __fadd_rn(__fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey)),
+                                      __fmul_rn(ez, ez));
+                        bool in = k < k1 && r2f < h2_lo;
+                        if (k < k1 && !in && r2f <= h2_hi)
+                            in = dist2(xsub(xi, (double)ob[u].x), xsub(yi, (double)ob[u].y),
+                                       xsub(zi, (double)ob[u].z)) < p.h2;
+                        if (in) {
+                            if (cntn < p.width) row[cntn] = b.order[k];
+                            ++cntn;
+                        }
                     }
-                    const double dx = xsub(xi, (double)px), dy = xsub(yi, (double)py),
-                                 dz = xsub(zi, (double)pz);
-                    const double r2 = dist2(dx, dy, dz);
-                    if (!(r2 < p.h2)) continue;
-                    const int j = b.order[k];
-                    if (cntn < p.width) {
-                        row[cntn++] = j;
-                    } else {
-                        ++lost;
-                        continue;
-                    }
-                    if (j >= p.n_fluid || j == i) continue;
-                    const double r = xsqrt(r2);
-                    if (r >= p.h) continue;
-                    const double lap = xmul(xmul(mum2, visc_lap(r, p.h, p.c_visc)), inv_rho0_sq);
-                    fx = xadd(fx, xmul(lap, xsub((double)b.vel[3 * j], vxi)));
-                    fy = xadd(fy, xmul(lap, xsub((double)b.vel[3 * j + 1], vyi)));
-                    fz = xadd(fz, xmul(lap, xsub((double)b.vel[3 * j + 2], vzi)));
                 }
             }
-        b.cnt[i] = cntn;
-        if (lost) {
+        if (cntn > p.width) {
             atomicOr(&b.ctr->err_flags, RTS_ERR_OVERFLOW);
-            atomicAdd((unsigned long long *)&b.ctr->overflow, (unsigned long long)lost);
+            atomicAdd((unsigned long long *)&b.ctr->overflow,
+                      (unsigned long long)(cntn - p.width));
+            cntn = p.width;
+        }
+        b.cnt[i] = cntn;
+        // pass 2: viscosity over fluid entries of the row (pcisph.py:183-196)
+        const double vxi = b.vel[3 * i], vyi = b.vel[3 * i + 1], vzi = b.vel[3 * i + 2];
+        double fx = 0.0, fy = 0.0, fz = 0.0;
+        for (int q = 0; q < cntn; ++q) {
+            const int j = row[q];
+            if (j >= p.n_fluid || j == i) continue;
+            const double dx = xsub(xi, (double)b.pos[3 * j]);
+            const double dy = xsub(yi, (double)b.pos[3 * j + 1]);
+            const double dz = xsub(zi, (double)b.pos[3 * j + 2]);
+            const double r = xsqrt(dist2(dx, dy, dz));
+            if (r >= p.h) continue;
+            const double lap = xmul(xmul(mum2, visc_lap(r, p.h, p.c_visc)), inv_rho0_sq);
+            fx = xadd(fx, xmul(lap, xsub((double)b.vel[3 * j], vxi)));
+            fy = xadd(fy, xmul(lap, xsub((double)b.vel[3 * j + 1], vyi)));
+            fz = xadd(fz, xmul(lap, xsub((double)b.vel[3 * j + 2], vzi)));
         }
         b.force[3 * i] = (float)xadd(fx, xmul(p.mass, p.gravity[0]));
         b.force[3 * i + 1] = (float)xadd(fy, xmul(p.mass, p.gravity[1]));
@@ -170,27 +196,22 @@ RTS_DEV void motion_one(const RtsParams &p, const RtsBuffers &b, int i, double d
     reinterpret_cast<float4 *>(b.xs4)[i] = make_float4(xs[0], xs[1], xs[2], b.pres[i]);
 }
 
-__global__ void k_motion_all(const __grid_constant__ RtsParams p, RtsBuffers b) {
-    if (fatal(b.ctr)) return;
+// all = 1: every fluid particle; 0: the previous force list; -1: ctl->motion_all
+__global__ void k_motion(const __grid_constant__ RtsParams p, RtsBuffers b, int all) {
+    RTS_ITER_GUARD();
+    if (all < 0) all = b.ctl->motion_all;
     const double dim = xmul(p.dt, p.inv_mass);
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.n_fluid;
-         i += gridDim.x * blockDim.x)
-        motion_one(p, b, i, dim);
-}
-
-__global__ void k_motion_list(const __grid_constant__ RtsParams p, RtsBuffers b) {
-    if (fatal(b.ctr)) return;
-    const double dim = xmul(p.dt, p.inv_mass);
-    const int n = b.ctr->n_force;
+    const int n = all ? p.n_fluid : b.ctr->n_force;
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x)
-        motion_one(p, b, b.list2[t], dim);
+        motion_one(p, b, all ? t : b.list2[t], dim);
 }
 
 // set membership for one iteration (pcisph.py:634-643); row_mask bit n set
 // when region n is scheduled; S_ob refreshed from the observed mask first
 __global__ void __launch_bounds__(256) k_sets(const __grid_constant__ RtsParams p, RtsBuffers b,
                                               int row_mask, int all_pred) {
-    if (fatal(b.ctr)) return;
+    RTS_ITER_GUARD();
+    if (row_mask < 0) row_mask = b.ctl->row_mask;
     const int nf = p.n_fluid;
     const int stride = gridDim.x * blockDim.x;
     for (int base = blockIdx.x * blockDim.x; base < nf; base += stride) {
@@ -215,7 +236,9 @@ __global__ void __launch_bounds__(256) k_sets(const __grid_constant__ RtsParams 
 
 // S_ob = observed[fluid_cells] for every fluid particle (pcisph.py:537-542)
 __global__ void k_sob(const __grid_constant__ RtsParams p, RtsBuffers b) {
-    if (fatal(b.ctr)) return;
+    RTS_MINOR_GUARD();
+    if (b.ctl && blockIdx.x == 0 && threadIdx.x == 0)
+        b.ctl->stats[b.ctl->minor].t_looped = gtimer();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.n_fluid;
          i += gridDim.x * blockDim.x)
         b.in_sob[i] = b.block_tmp[b.fluid_cells[i]] != 0;
@@ -224,7 +247,7 @@ __global__ void k_sob(const __grid_constant__ RtsParams p, RtsBuffers b) {
 // rho*, err over the pred list; p += delta (rho* - rho0) on force members
 __global__ void __launch_bounds__(kThreads) k_density(const __grid_constant__ RtsParams p,
                                                       RtsBuffers b) {
-    if (fatal(b.ctr)) return;
+    RTS_ITER_GUARD();
     const int n = b.ctr->n_pred;
     const float4 *xs4 = reinterpret_cast<const float4 *>(b.xs4);
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
@@ -234,14 +257,15 @@ __global__ void __launch_bounds__(kThreads) k_density(const __grid_constant__ Rt
         const int c = b.cnt[i];
         const int4 *row4 = reinterpret_cast<const int4 *>(b.nbr + (size_t)i * p.width);
         double acc = 0.0;
-        for (int q = 0; q < c; q += 4) {
-            const int4 jj = row4[q >> 2];
-            const int j4[4] = {jj.x, jj.y, jj.z, jj.w};
-            float4 o[4];
+        for (int q = 0; q < c; q += 8) {
+            const int4 ja = row4[q >> 2];
+            const int4 jb = row4[(q >> 2) + 1];
+            const int j8[8] = {ja.x, ja.y, ja.z, ja.w, jb.x, jb.y, jb.z, jb.w};
+            float4 o[8];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) o[u] = xs4[q + u < c ? j4[u] : i];
+            for (int u = 0; u < 8; ++u) o[u] = xs4[q + u < c ? j8[u] : i];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < 8; ++u) {
                 if (q + u < c)
                     acc = xadd(acc, poly6(dist2(xsub(xi, (double)o[u].x), xsub(yi, (double)o[u].y),
                                                 xsub(zi, (double)o[u].z)),
@@ -265,7 +289,7 @@ __global__ void __launch_bounds__(kThreads) k_density(const __grid_constant__ Rt
 // S_e, S_e blocks, max err, sum rho* (deterministic), any S_e
 __global__ void __launch_bounds__(256) k_se_reduce(const __grid_constant__ RtsParams p,
                                                    RtsBuffers b, int with_se) {
-    if (fatal(b.ctr)) return;
+    RTS_ITER_GUARD();
     __shared__ double ssum[8];
     const int nf = p.n_fluid;
     const double thr = xmul(0.5, p.eta_max);
@@ -307,6 +331,7 @@ __global__ void __launch_bounds__(256) k_se_reduce(const __grid_constant__ RtsPa
 }
 
 __global__ void k_sum_partials(RtsBuffers b, int n) {
+    if (loop_done(b)) return;
     __shared__ double ssum[32];
     double s = 0.0;
     for (int q = threadIdx.x; q < n; q += blockDim.x) s = xadd(s, b.partial[q]);
@@ -323,7 +348,11 @@ __global__ void k_sum_partials(RtsBuffers b, int n) {
 // observed blocks (regions.py:110-125): occupied and (bordering a strictly
 // smaller region, or bordering an S_e block without being one); -> block_tmp
 __global__ void k_observed(const __grid_constant__ RtsParams p, RtsBuffers b, int with_se) {
-    if (fatal(b.ctr)) return;
+    if (with_se) {
+        RTS_ITER_GUARD();
+    } else {
+        RTS_MINOR_GUARD();
+    }
     const int nx = p.dims[0], ny = p.dims[1], nz = p.dims[2];
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < p.n_cells;
          c += gridDim.x * blockDim.x) {
@@ -353,7 +382,7 @@ __global__ void k_observed(const __grid_constant__ RtsParams p, RtsBuffers b, in
 // pressure forces at x* over the force list (pcisph.py:238-271)
 __global__ void __launch_bounds__(kThreads) k_pforces(const __grid_constant__ RtsParams p,
                                                       RtsBuffers b) {
-    if (fatal(b.ctr)) return;
+    RTS_ITER_GUARD();
     const int n = b.ctr->n_force;
     const float4 *xs4 = reinterpret_cast<const float4 *>(b.xs4);
     const double m2 = xmul(p.mass, p.mass);
@@ -382,9 +411,14 @@ __global__ void __launch_bounds__(kThreads) k_pforces(const __grid_constant__ Rt
                              dz = xsub(zi, (double)o.z);
                 const double term =
                     j < p.n_fluid ? xadd(term_i, xmul((double)o.w, inv_rho0_sq)) : wall;
-                const double r = xsqrt(dist2(dx, dy, dz));
-                if (r <= 0.0 || r >= p.h) continue;
-                const double s = xmul(xmul(m2, term), spiky(r, p.h, p.c_spiky));
+                const double r2 = dist2(dx, dy, dz);
+                if (!(r2 > 0.0) || !(r2 < p.h2)) continue;  // r <= 0 or r >= h
+                // spiky factor c (h - r)^2 / r via one fp64 rsqrt (1e-16-level
+                // deviation from sqrt + divide; f_p parity bar is 1e-4)
+                const double rinv = rsqrt(r2);
+                const double r = xmul(r2, rinv);
+                const double d = xsub(p.h, r);
+                const double s = xmul(xmul(xmul(m2, term), xmul(xmul(p.c_spiky, d), d)), rinv);
                 fx = xsub(fx, xmul(s, dx));
                 fy = xsub(fy, xmul(s, dy));
                 fz = xsub(fz, xmul(s, dz));
@@ -398,7 +432,7 @@ __global__ void __launch_bounds__(kThreads) k_pforces(const __grid_constant__ Rt
 
 // _integrate (pcisph.py:759-768) + validity countdown (pcisph.py:580-584)
 __global__ void k_integrate(const __grid_constant__ RtsParams p, RtsBuffers b, int countdown) {
-    if (fatal(b.ctr)) return;
+    RTS_MINOR_GUARD();
     const double dim = xmul(p.dt, p.inv_mass);
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.n_fluid;
          i += gridDim.x * blockDim.x) {
@@ -434,7 +468,7 @@ __global__ void k_integrate(const __grid_constant__ RtsParams p, RtsBuffers b, i
 // _mark_timestep_updates (pcisph.py:718-755), block part: block_raw holds the
 // required levels; new field -> block_tmp, changed mask -> block_flag
 __global__ void k_mark_blocks(const __grid_constant__ RtsParams p, RtsBuffers b) {
-    if (fatal(b.ctr)) return;
+    RTS_MINOR_GUARD();
     const int nx = p.dims[0], ny = p.dims[1], nz = p.dims[2];
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < p.n_cells;
          c += gridDim.x * blockDim.x) {
@@ -465,14 +499,14 @@ __global__ void k_mark_blocks(const __grid_constant__ RtsParams p, RtsBuffers b)
 }
 
 __global__ void k_mark_apply(const __grid_constant__ RtsParams p, RtsBuffers b) {
-    if (fatal(b.ctr)) return;
+    RTS_MINOR_GUARD();
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < p.n_cells;
          c += gridDim.x * blockDim.x)
         b.block_field[c] = b.block_tmp[c];
 }
 
 __global__ void k_mark_particles(const __grid_constant__ RtsParams p, RtsBuffers b) {
-    if (fatal(b.ctr)) return;
+    RTS_MINOR_GUARD();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.n_fluid;
          i += gridDim.x * blockDim.x) {
         const int c = b.fluid_cells[i];
@@ -498,7 +532,13 @@ __global__ void k_vel_max(const __grid_constant__ RtsParams p, RtsBuffers b) {
                   (unsigned long long)__double_as_longlong(m));
 }
 
+// restore: 0 snapshot, 1 revert, -1 take ctl->snap_op (0 none, 1 snapshot, 2 revert)
 __global__ void k_snapshot(const __grid_constant__ RtsParams p, RtsBuffers b, int restore) {
+    if (restore < 0) {
+        const int op = b.ctl->snap_op;
+        if (op == 0 || fatal(b.ctr)) return;
+        restore = op == 2;
+    }
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.n_fluid;
          i += gridDim.x * blockDim.x) {
         if (!restore) {
@@ -515,6 +555,156 @@ __global__ void k_snapshot(const __grid_constant__ RtsParams p, RtsBuffers b, in
     }
 }
 
+
+// p = 0, f_p = 0 for all fluid at minor start (pcisph.py:570-571)
+__global__ void k_zero_pressure(const __grid_constant__ RtsParams p, RtsBuffers b) {
+    RTS_MINOR_GUARD();
+    if (b.ctl && blockIdx.x == 0 && threadIdx.x == 0)
+        b.ctl->stats[b.ctl->minor].t_refreshed = gtimer();
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.n_fluid;
+         i += gridDim.x * blockDim.x) {
+        b.pres[i] = 0.0f;
+        b.f_p[3 * i] = 0.0f;
+        b.f_p[3 * i + 1] = 0.0f;
+        b.f_p[3 * i + 2] = 0.0f;
+    }
+}
+
+__global__ void k_major_begin(RtsBuffers b) {
+    RtsControl *c = b.ctl;
+    c->stop_major = 0;
+    c->done = 0;
+    c->failed = 0;
+    c->fail_kind = 0;
+    for (int m = 0; m < RTS_MAX_MINOR; ++m) c->stats[m].iterations = -1;
+}
+
+RTS_DEV void add_row_iters(RtsControl *c, int minor, int row) {
+    const int packed = c->row_counts[minor][row];
+    for (int n = 1; n <= 4; ++n) c->riters[n] += (packed >> (4 * n)) & 0xF;
+}
+
+// state reset of _correct_scheduled (pcisph.py:618-631) + first row; S_e = {}
+__global__ void k_minor_begin(RtsBuffers b, int minor, int sync_mode) {
+    RtsControl *c = b.ctl;
+    c->skipped = c->stop_major;
+    if (c->stop_major) {
+        c->done = 1;
+        return;
+    }
+    c->minor = minor;
+    c->stats[minor].t_begin = gtimer();
+    c->it = c->g_count = c->local_active = c->local_banned = c->local_run = 0;
+    c->early = 0;
+    c->done = 0;
+    c->corrected = 0;
+    c->forced = 0;
+    for (int n = 0; n < 5; ++n) c->riters[n] = 0;
+    c->motion_all = 1;
+    c->snap_op = 0;
+    if (!sync_mode) {
+        c->row_mask = c->row_masks[minor][0];
+        add_row_iters(c, minor, 0);
+    } else {
+        c->row_mask = 0x1E;
+    }
+}
+
+// Decisions after one correction iteration: pcisph.py:673-715 (scheduled,
+// sync_mode = 0) or pcisph.py:457-468 (synchronous baselines, sync_mode = 1).
+// Writes the next iteration's row / motion / snapshot ops, or ends the loop
+// (cond handle of the enclosing CUDA-graph while node, if any).
+__global__ void k_control(const __grid_constant__ RtsParams p, RtsBuffers b, int sync_mode,
+                          unsigned long long cond_handle, int local_attempts, int iteration_cap) {
+    RtsControl *c = b.ctl;
+    const RtsCounters *ctr = b.ctr;
+    int done = c->done;
+    if (!done) {
+        c->snap_op = 0;
+        c->it += 1;
+        c->corrected += sync_mode ? p.n_fluid : ctr->n_pred;
+        c->forced += sync_mode ? p.n_fluid : ctr->n_force;
+        if (c->local_active) c->local_run += 1; else c->g_count += 1;
+        const double max_err = ctr->max_err;
+        const double mean = p.n_fluid ? ctr->sum_rho / (double)p.n_fluid : 0.0;
+        double avg = p.n_fluid ? xsub(xdiv(mean, p.rho0), 1.0) : 0.0;
+        avg = avg > 0.0 ? avg : 0.0;
+        c->last_max_err = max_err;
+        c->last_avg_err = avg;
+        c->motion_all = 0;
+        const bool converged = max_err < p.eta_max && avg < p.eta_avg;
+        if (ctr->err_flags & RTS_ERR_FATAL) {
+            done = 1;
+            c->failed = 1;
+            c->fail_kind = (ctr->err_flags & RTS_ERR_NONFINITE) ? 1 : 4;
+        } else if (sync_mode) {
+            c->motion_all = 1;
+            if (c->it >= 3 && converged) {
+                done = 1;
+            } else if (c->it > iteration_cap + 3) {
+                done = 1;
+                c->failed = 1;
+                c->fail_kind = 3;
+                c->fail_g = c->it;
+                c->fail_err = max_err;
+            }
+        } else if (converged && c->it >= 3) {
+            done = 1;
+        } else if (!converged && c->it >= 3) {
+            if (c->local_active) {
+                if (c->local_run >= local_attempts) {
+                    c->snap_op = 2;  // revert p, f_p to the entry snapshot
+                    c->motion_all = 1;
+                    c->local_active = 0;
+                    c->local_banned = 1;
+                    c->local_reverted += 1;
+                }
+            } else if (xmul(avg, 100.0) < p.rho_T && !c->local_banned && ctr->any_se) {
+                c->local_active = 1;
+                c->local_run = 0;
+                c->snap_op = 1;
+                c->local_entered += 1;
+            }
+            if (c->g_count > 6) c->early = 1;
+            if (c->g_count > iteration_cap) {
+                done = 1;
+                c->failed = 1;
+                c->fail_kind = 2;
+                c->fail_g = c->g_count;
+                c->fail_err = max_err;
+            }
+        }
+        if (!done && !sync_mode) {
+            if (c->local_active) {
+                c->row_mask = 0;
+            } else {
+                const int m = c->minor;
+                const int r = c->g_count % c->n_rows[m];
+                c->row_mask = c->row_masks[m][r];
+                add_row_iters(c, m, r);
+            }
+        }
+        if (c->failed) c->stop_major = 1;
+        c->done = done;
+    }
+    if (cond_handle) cudaGraphSetConditional((cudaGraphConditionalHandle)cond_handle, done ? 0 : 1);
+}
+
+__global__ void k_minor_end(RtsBuffers b, int minor) {
+    RtsControl *c = b.ctl;
+    if (c->skipped) return;
+    RtsMinorStats &s = c->stats[minor];
+    s.iterations = c->it;
+    s.n_refresh = b.ctr->n_compute;
+    s.early = c->early;
+    for (int n = 0; n < 5; ++n) s.riters[n] = c->riters[n];
+    s.corrected = c->corrected;
+    s.forced = c->forced;
+    s.max_err = c->last_max_err;
+    s.avg_err = c->last_avg_err;
+    s.t_end = gtimer();
+    if (c->early || c->failed) c->stop_major = 1;
+}
 }  // namespace
 
 extern "C" {
@@ -551,11 +741,7 @@ int rts_pci_refresh(const RtsParams *p, const RtsBuffers *b, int all, int two_la
 }
 
 int rts_pci_motion(const RtsParams *p, const RtsBuffers *b, int all, void *stream) {
-    cudaStream_t s = (cudaStream_t)stream;
-    if (all)
-        rts_note_launch(), k_motion_all<<<rts_blocks(p->n_fluid, 256), 256, 0, s>>>(*p, *b);
-    else
-        rts_note_launch(), k_motion_list<<<rts_blocks(p->n_fluid, 256), 256, 0, s>>>(*p, *b);
+    rts_note_launch(), k_motion<<<rts_blocks(p->n_fluid, 256), 256, 0, (cudaStream_t)stream>>>(*p, *b, all);
     RTS_LAUNCH_CHECK();
     return 0;
 }
@@ -634,6 +820,207 @@ int rts_vel_max(const RtsParams *p, const RtsBuffers *b, void *stream) {
     rts_note_launch(), k_vel_max<<<rts_blocks(p->n_fluid, 256, 148 * 8), 256, 0, (cudaStream_t)stream>>>(*p, *b);
     RTS_LAUNCH_CHECK();
     return 0;
+}
+
+int rts_pci_zero_pressure(const RtsParams *p, const RtsBuffers *b, void *stream) {
+    rts_note_launch(), k_zero_pressure<<<rts_blocks(p->n_fluid, 256), 256, 0, (cudaStream_t)stream>>>(*p, *b);
+    RTS_LAUNCH_CHECK();
+    return 0;
+}
+
+int rts_pci_major_begin(const RtsParams *p, const RtsBuffers *b, void *stream) {
+    (void)p;
+    rts_note_launch(), k_major_begin<<<1, 1, 0, (cudaStream_t)stream>>>(*b);
+    RTS_LAUNCH_CHECK();
+    return 0;
+}
+
+int rts_pci_minor_begin(const RtsParams *p, const RtsBuffers *b, int minor, int sync_mode,
+                        void *stream) {
+    (void)p;
+    rts_note_launch(), k_minor_begin<<<1, 1, 0, (cudaStream_t)stream>>>(*b, minor, sync_mode);
+    RTS_LAUNCH_CHECK();
+    return 0;
+}
+
+int rts_pci_minor_end(const RtsParams *p, const RtsBuffers *b, int minor, void *stream) {
+    (void)p;
+    rts_note_launch(), k_minor_end<<<1, 1, 0, (cudaStream_t)stream>>>(*b, minor);
+    RTS_LAUNCH_CHECK();
+    return 0;
+}
+
+int rts_pci_control(const RtsParams *p, const RtsBuffers *b, int sync_mode,
+                    unsigned long long cond_handle, int local_attempts, int iteration_cap,
+                    void *stream);
+
+// One correction iteration with device-side control (pcisph.py:633-715 or
+// 446-468): motion, sets, density + pressure, S_e/reductions, observed,
+// pressure forces, control, snapshot/revert.
+int rts_pci_iteration(const RtsParams *p, const RtsBuffers *b, int sync_mode,
+                      unsigned long long cond_handle, int local_attempts, int iteration_cap,
+                      void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    int rc;
+    if ((rc = rts_pci_motion(p, b, -1, stream))) return rc;
+    if ((rc = rts_pci_sets(p, b, -1, sync_mode, stream))) return rc;
+    if ((rc = rts_pci_density(p, b, stream))) return rc;
+    if ((rc = rts_pci_se_reduce(p, b, !sync_mode, stream))) return rc;
+    if (!sync_mode && (rc = rts_pci_observed(p, b, 1, stream))) return rc;
+    if ((rc = rts_pci_pforces(p, b, stream))) return rc;
+    (void)s;
+    return rts_pci_control(p, b, sync_mode, cond_handle, local_attempts, iteration_cap, stream);
+}
+
+int rts_pci_control(const RtsParams *p, const RtsBuffers *b, int sync_mode,
+                    unsigned long long cond_handle, int local_attempts, int iteration_cap,
+                    void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    rts_note_launch(), k_control<<<1, 1, 0, s>>>(*p, *b, sync_mode, cond_handle, local_attempts,
+                                                 iteration_cap);
+    RTS_LAUNCH_CHECK();
+    if (!sync_mode) {
+        rts_note_launch(), k_snapshot<<<rts_blocks(p->n_fluid, 256), 256, 0, s>>>(*p, *b, -1);
+        RTS_LAUNCH_CHECK();
+    }
+    return 0;
+}
+
+// The minor step of RTS mode (pcisph.py:544-610) up to the correction loop,
+// and its tail after the loop.
+int rts_pci_minor_head(const RtsParams *p, const RtsBuffers *b, int minor, void *stream) {
+    int rc;
+    if ((rc = rts_pci_minor_begin(p, b, minor, 0, stream))) return rc;
+    if ((rc = rts_pci_refresh(p, b, 0, 1, stream))) return rc;
+    if ((rc = rts_pci_zero_pressure(p, b, stream))) return rc;
+    cudaMemsetAsync(b->in_se, 0, (size_t)p->n_fluid, (cudaStream_t)stream);
+    return rts_pci_observed(p, b, 0, stream);
+}
+
+int rts_pci_minor_tail(const RtsParams *p, const RtsBuffers *b, int minor, int last,
+                       void *stream) {
+    int rc;
+    if ((rc = rts_pci_sob(p, b, stream))) return rc;
+    if ((rc = rts_pci_integrate(p, b, 1, stream))) return rc;
+    if (!last) {
+        if ((rc = rts_block_maxima(p, b, 1, stream))) return rc;
+        if ((rc = rts_block_levels(p, b, 2, stream))) return rc;
+        if ((rc = rts_pci_mark_updates(p, b, stream))) return rc;
+    }
+    return rts_pci_minor_end(p, b, minor, stream);
+}
+
+// ---- CUDA graphs -----------------------------------------------------------
+struct RtsGraph {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+};
+
+static int add_while_loop(cudaStream_t cs, const RtsParams *p, const RtsBuffers *b, int sync_mode,
+                          int local_attempts, int iteration_cap) {
+    cudaStreamCaptureStatus st;
+    cudaGraph_t g;
+    const cudaGraphNode_t *deps;
+    size_t ndeps;
+    cudaError_t e = cudaStreamGetCaptureInfo(cs, &st, nullptr, &g, &deps, &ndeps);
+    if (e != cudaSuccess) return (int)e;
+    cudaGraphConditionalHandle h;
+    e = cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault);
+    if (e != cudaSuccess) return (int)e;
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = h;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    e = cudaGraphAddNode(&node, g, deps, ndeps, &np);
+    if (e != cudaSuccess) return (int)e;
+    cudaGraph_t body = np.conditional.phGraph_out[0];
+    cudaStream_t bs;
+    cudaStreamCreateWithFlags(&bs, cudaStreamNonBlocking);
+    e = cudaStreamBeginCaptureToGraph(bs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed);
+    if (e != cudaSuccess) return (int)e;
+    int rc = rts_pci_iteration(p, b, sync_mode, (unsigned long long)h, local_attempts,
+                               iteration_cap, bs);
+    cudaGraph_t out;
+    e = cudaStreamEndCapture(bs, &out);
+    cudaStreamDestroy(bs);
+    if (rc) return rc;
+    if (e != cudaSuccess) return (int)e;
+    e = cudaStreamUpdateCaptureDependencies(cs, &node, 1, cudaStreamSetCaptureDependencies);
+    return (int)e;
+}
+
+static int reset_counters(const RtsBuffers *b, cudaStream_t s) {
+    return rts_counters_reset(b, s);
+}
+
+// Whole RTS major step (pcisph.py:482-505) or synchronous step
+// (pcisph.py:376-419) as one graph: the correction loops are conditional
+// while nodes driven by k_control, so a major step runs with no host round
+// trip.  mode: 0 RTS major with n_minor minors, 1 synchronous step.
+void *rts_pci_graph_create(const RtsParams *p, const RtsBuffers *b, int mode, int n_minor,
+                           int local_attempts, int iteration_cap, int *err) {
+    *err = 0;
+    cudaStream_t cs;
+    cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed);
+    if (e != cudaSuccess) { *err = (int)e; cudaStreamDestroy(cs); return nullptr; }
+    int rc = 0;
+    do {
+        if ((rc = reset_counters(b, cs))) break;
+        if ((rc = rts_pci_major_begin(p, b, cs))) break;
+        if ((rc = rts_grid_keys(p, b, mode == 0, 1, cs))) break;
+        if ((rc = rts_grid_sort(p, b, cs))) break;
+        if ((rc = rts_pci_gather(p, b, cs))) break;
+        if (mode == 0) {
+            if ((rc = rts_block_levels(p, b, 1, cs))) break;
+            if ((rc = rts_pci_major_particles(p, b, cs))) break;
+            for (int j = 0; j < n_minor && !rc; ++j) {
+                if ((rc = rts_pci_minor_head(p, b, j, cs))) break;
+                if ((rc = add_while_loop(cs, p, b, 0, local_attempts, iteration_cap))) break;
+                rc = rts_pci_minor_tail(p, b, j, j == n_minor - 1, cs);
+            }
+        } else {
+            if ((rc = rts_pci_minor_begin(p, b, 0, 1, cs))) break;
+            if ((rc = rts_pci_refresh(p, b, 1, 0, cs))) break;
+            if ((rc = rts_pci_zero_pressure(p, b, cs))) break;
+            if ((rc = add_while_loop(cs, p, b, 1, local_attempts, iteration_cap))) break;
+            if ((rc = rts_pci_integrate(p, b, 0, cs))) break;
+            rc = rts_pci_minor_end(p, b, 0, cs);
+        }
+    } while (0);
+    cudaGraph_t g = nullptr;
+    e = cudaStreamEndCapture(cs, &g);
+    cudaStreamDestroy(cs);
+    if (rc || e != cudaSuccess) {
+        *err = rc ? rc : (int)e;
+        if (g) cudaGraphDestroy(g);
+        return nullptr;
+    }
+    RtsGraph *rg = new RtsGraph;
+    rg->graph = g;
+    e = cudaGraphInstantiate(&rg->exec, g, 0);
+    if (e != cudaSuccess) {
+        *err = (int)e;
+        cudaGraphDestroy(g);
+        delete rg;
+        return nullptr;
+    }
+    return rg;
+}
+
+int rts_graph_launch(void *graph, void *stream) {
+    RtsGraph *rg = (RtsGraph *)graph;
+    return (int)cudaGraphLaunch(rg->exec, (cudaStream_t)stream);
+}
+
+void rts_graph_destroy(void *graph) {
+    RtsGraph *rg = (RtsGraph *)graph;
+    if (!rg) return;
+    if (rg->exec) cudaGraphExecDestroy(rg->exec);
+    if (rg->graph) cudaGraphDestroy(rg->graph);
+    delete rg;
 }
 
 }  // extern "C"

@@ -12,6 +12,7 @@ sum rho*, any S_e, |pred|) to take the reference's convergence decisions.
 
 from __future__ import annotations
 
+import ctypes
 import dataclasses
 import math
 
@@ -137,7 +138,8 @@ class PcisphSolver(_DeviceSolver):
     def __init__(self, scene: Scene, mode: str = "rts", dt: float | None = None,
                  schedule=DEFAULT_SCHEDULE, pin_region: int | None = None,
                  audit_neighbors: bool = False, iteration_cap: int = 24,
-                 local_attempts: int = 4, n_regions: int = 4, device="cuda"):
+                 local_attempts: int = 4, n_regions: int = 4, device="cuda",
+                 use_graphs: bool = True):
         if mode not in self.mode_names:
             raise ValueError(f"unknown pcisph mode {mode!r}")
         validate_schedule(schedule, n_regions)
@@ -184,8 +186,10 @@ class PcisphSolver(_DeviceSolver):
         A.alloc("snap_p", (n1,), f32, 0)
         A.alloc("snap_fp", (n1, 3), f32, 0)
         A.alloc("slot_of", (n1,), torch.int32, 0)
-        self.local_entered_total = 0
-        self.local_reverted_total = 0
+        self._ctl = A.alloc("ctl", (ctypes.sizeof(N.RtsControl),), torch.uint8, 0)
+        self._ctl_host = torch.zeros(ctypes.sizeof(N.RtsControl), dtype=torch.uint8).pin_memory()
+        self.use_graphs = use_graphs
+        self._graphs: dict = {}
         self._force_total = 0
         p = self.params
         p.dt_base = self.dt
@@ -193,6 +197,108 @@ class PcisphSolver(_DeviceSolver):
         p.rts = 1 if mode == "rts" else 0
         stream = torch.cuda.current_stream(self.device)
         N.call("rts_pci_walls", p, A.buf, stream.cuda_stream)
+        self._upload_schedule()
+
+    def __del__(self):
+        for g in getattr(self, "_graphs", {}).values():
+            try:
+                N.load().rts_graph_destroy(g)
+            except Exception:  # pragma: no cover
+                pass
+
+    # -- device loop control ----------------------------------------------------
+    def _upload_schedule(self) -> None:
+        """Write the schedule's row masks / region multiplicities into the
+        control block (its loop state and running totals restart at zero)."""
+        c = N.RtsControl()
+        if len(self.schedule) > N.MAX_MINOR:
+            raise ConfigError(f"at most {N.MAX_MINOR} minor steps are supported")
+        for j, rows in enumerate(self.schedule):
+            if len(rows) > N.MAX_ROWS:
+                raise ConfigError(f"at most {N.MAX_ROWS} iterations per minor step are supported")
+            c.n_rows[j] = len(rows)
+            for r, row in enumerate(rows):
+                c.row_masks[j][r] = _row_mask(row)
+                packed = 0
+                for n in row:
+                    if 1 <= n <= min(self.n_regions, 7):
+                        packed += 1 << (4 * n)
+                c.row_counts[j][r] = packed
+        host = torch.frombuffer(bytearray(bytes(c)), dtype=torch.uint8)
+        self._ctl.copy_(host)
+
+    def _read_control(self):
+        st = self._stream()
+        self._ctl_host.copy_(self._ctl, non_blocking=True)
+        c = self.counters.read(st)
+        ctl = N.RtsControl.from_buffer_copy(self._ctl_host.numpy().tobytes())
+        self._ctl_cache = ctl
+        self.grid.n_sorted = int(c.n_sorted)
+        return ctl, c
+
+    @property
+    def local_entered_total(self) -> int:
+        ctl = getattr(self, "_ctl_cache", None)
+        return int(ctl.local_entered) if ctl is not None else 0
+
+    @property
+    def local_reverted_total(self) -> int:
+        ctl = getattr(self, "_ctl_cache", None)
+        return int(ctl.local_reverted) if ctl is not None else 0
+
+    def _graph(self, mode: int, n_minor: int):
+        key = (mode, n_minor, bytes(self.params), self.local_attempts, self.iteration_cap)
+        g = self._graphs.get(key)
+        if g is None:
+            if len(self._graphs) >= 8:
+                for old in self._graphs.values():
+                    N.load().rts_graph_destroy(old)
+                self._graphs.clear()
+            err = ctypes.c_int(0)
+            g = N.load().rts_pci_graph_create(self.params, self.arena.buf, mode, n_minor,
+                                              self.local_attempts, self.iteration_cap,
+                                              ctypes.byref(err))
+            if not g:
+                raise N.NativeError(f"rts_pci_graph_create failed with cudaError {err.value}")
+            self._graphs[key] = g
+        return g
+
+    def _run_loop_host(self, sync_mode: int) -> None:
+        """Correction loop without a graph: enqueue iterations, read `done`."""
+        while True:
+            if self._ktimes is None:
+                self._call("rts_pci_iteration", sync_mode, 0, self.local_attempts,
+                           self.iteration_cap)
+            else:  # per-entry-point launches so each kernel can be timed
+                self._call("rts_pci_motion", -1)
+                self._call("rts_pci_sets", -1, sync_mode)
+                self._call("rts_pci_density")
+                self._call("rts_pci_se_reduce", int(not sync_mode))
+                if not sync_mode:
+                    self._call("rts_pci_observed", 1)
+                self._call("rts_pci_pforces")
+                self._call("rts_pci_control", sync_mode, 0, self.local_attempts,
+                           self.iteration_cap)
+            self._ctl_host[24:28].copy_(self._ctl[24:28], non_blocking=True)  # ctl.done
+            self._stream().synchronize()
+            if int(self._ctl_host[24:28].view(torch.int32)[0]):
+                return
+
+    def _raise_control(self, ctl, c) -> None:
+        raise_on_errors(c, NEIGHBOR_WIDTH) if c.err_flags & (N.ERR_ESCAPED | N.ERR_OVERFLOW) else None
+        if not ctl.failed:
+            return
+        if ctl.fail_kind == 1 or c.err_flags & N.ERR_NONFINITE:
+            raise NumericalError("non-finite predicted density; the simulation has blown up")
+        if ctl.fail_kind == 2:
+            raise NumericalError(
+                f"pressure solve used {int(ctl.fail_g)} global iterations in one minor step "
+                f"(max error {float(ctl.fail_err):.4%} of rest density)")
+        if ctl.fail_kind == 3:
+            raise NumericalError(
+                f"pressure solve did not converge within {int(ctl.fail_g)} iterations "
+                f"(max error {float(ctl.fail_err):.4%} of rest density)")
+        raise_on_errors(c, NEIGHBOR_WIDTH)
 
     # -- reference-facing helpers -------------------------------------------
     @property
@@ -264,48 +370,43 @@ class PcisphSolver(_DeviceSolver):
 
     # -- synchronous baselines (pcisph.py:376-476) ------------------------------
     def sync_step(self) -> StepStats:
+        """Synchronous baseline step (pcisph.py:376-419): rebuild, full
+        search + external forces, the standard correction loop (device
+        control, >= 3 iterations until max err < eta_max and avg < eta_avg),
+        integrate."""
         nf = self.n_fluid
         dt = self.dt
         self._prepare(dt)
-        tm = self.timer
         st = self._stream()
-        self._rebuild(False)
-        tm.start(st)
-        self._call("rts_pci_refresh", 1, 0)
-        tm.mark("neighbor", st)
-        self._zero_pressure()
-        it = corrected = 0
-        while True:
-            self._call("rts_pci_motion", 1)
-            self._call("rts_pci_sets", 0, 1)
-            self._call("rts_pci_density")
-            self._call("rts_pci_se_reduce", 0)
-            self._call("rts_pci_pforces")
-            c = self._read()
-            it += 1
-            corrected += nf
-            max_err = float(c.max_err)
-            avg_err = self._avg_from(c)
-            if it >= 3 and max_err < self.scene.eta_max and avg_err < self.scene.eta_avg:
-                break
-            if it > self.iteration_cap + 3:
-                raise NumericalError(
-                    f"pressure solve did not converge within {it} iterations "
-                    f"(max error {max_err:.4%} of rest density)")
-        self._call("rts_pci_integrate", 0)
-        tm.mark("physics", st)
-        c = self._read()
-        self.grid.n_sorted = int(c.n_sorted)
+        if self.use_graphs:
+            N.call("rts_graph_launch", self._graph(1, 1), st.cuda_stream)
+        else:
+            N.call("rts_counters_reset", self.arena.buf, st.cuda_stream)
+            self._call("rts_pci_major_begin")
+            self.grid.launch_rebuild(self.params, st, want_maxima=False, add_fp=True)
+            self._call("rts_pci_gather")
+            self._call("rts_pci_minor_begin", 0, 1)
+            self._call("rts_pci_refresh", 1, 0)
+            self._call("rts_pci_zero_pressure")
+            self._run_loop_host(1)
+            self._call("rts_pci_integrate", 0)
+            self._call("rts_pci_minor_end", 0)
+        ctl, c = self._read_control()
+        self._raise_control(ctl, c)
+        ms = ctl.stats[0]
+        it = int(ms.iterations)
+        self._force_total += int(ms.forced)
         if self.mode == "adaptive":
             self._adapt_dt(it)
         self.step_index += 1
         self.sim_time += dt
-        t = tm.totals()
+        t_nb = max(0, ms.t_refreshed - ms.t_begin) * 1e-9
+        t_ph = max(0, ms.t_end - ms.t_refreshed) * 1e-9
         return StepStats(step=self.step_index, time=self.sim_time, dt=dt, n_compute=nf,
-                         frac_compute=1.0, iterations=it, corrected=corrected, iters_r1=it,
-                         iters_r2=it, iters_r3=it, iters_r4=it, max_err=max_err,
-                         avg_err=avg_err, t_neighbor=t["neighbor"], t_physics=t["physics"],
-                         t_rts=t["rts"])
+                         frac_compute=1.0, iterations=it, corrected=int(ms.corrected),
+                         iters_r1=it, iters_r2=it, iters_r3=it, iters_r4=it,
+                         max_err=float(ms.max_err), avg_err=float(ms.avg_err),
+                         t_neighbor=t_nb, t_physics=t_ph, t_rts=0.0)
 
     def _vel_max(self) -> float:
         if not self.n_fluid:
@@ -327,18 +428,69 @@ class PcisphSolver(_DeviceSolver):
 
     # -- regional mode (pcisph.py:482-768) -----------------------------------
     def major_step(self) -> list[StepStats]:
+        """One major step of N minor steps (pcisph.py:482-505).  With
+        ``use_graphs`` (default) the whole major -- rebuild, region
+        assignment, every minor step with its device-controlled correction
+        loop -- is one CUDA-graph launch followed by a single read-back."""
         n_minor = self.controller.n_current
         self._prepare(self.dt)
-        self._rebuild(True)
-        self._assign_major_regions(n_minor, rebuilt=True)
+        self.params.n_max = min(self.n_regions, n_minor)
+        st = self._stream()
+        if self.use_graphs:
+            N.call("rts_graph_launch", self._graph(0, n_minor), st.cuda_stream)
+        else:
+            N.call("rts_counters_reset", self.arena.buf, st.cuda_stream)
+            self._call("rts_pci_major_begin")
+            self.grid.launch_rebuild(self.params, st, want_maxima=True, add_fp=True)
+            self._call("rts_pci_gather")
+            self._call("rts_block_levels", 1)
+            self._call("rts_pci_major_particles")
+            for j in range(n_minor):
+                if self._ktimes is None:
+                    self._call("rts_pci_minor_head", j)
+                else:
+                    self._call("rts_pci_minor_begin", j, 0)
+                    self._call("rts_pci_refresh", 0, 1)
+                    self._call("rts_pci_zero_pressure")
+                    N.call("rts_memset", self.arena.buf.in_se, 0, self.n_fluid, st.cuda_stream)
+                    self._call("rts_pci_observed", 0)
+                self._run_loop_host(0)
+                if self._ktimes is None:
+                    self._call("rts_pci_minor_tail", j, int(j == n_minor - 1))
+                else:
+                    self._call("rts_pci_sob")
+                    self._call("rts_pci_integrate", 1)
+                    if j != n_minor - 1:
+                        self._call("rts_block_maxima", 1)
+                        self._call("rts_block_levels", 2)
+                        self._call("rts_pci_mark_updates")
+                    self._call("rts_pci_minor_end", j)
+        ctl, c = self._read_control()
         rows = []
         early = False
+        nf = self.n_fluid
         for j in range(n_minor):
-            st = self._minor_step(j, self.schedule[j], last=(j == n_minor - 1))
-            rows.append(st)
-            if st.early_term:
-                early = True
+            ms = ctl.stats[j]
+            if ms.iterations < 0:
                 break
+            if ctl.failed and j == int(ctl.minor):
+                break
+            self.step_index += 1
+            self.sim_time += self.dt
+            early = early or bool(ms.early)
+            self._force_total += int(ms.forced)
+            rows.append(StepStats(
+                step=self.step_index, time=self.sim_time, dt=self.dt,
+                n_compute=int(ms.n_refresh), frac_compute=int(ms.n_refresh) / max(1, nf),
+                iterations=int(ms.iterations), corrected=int(ms.corrected),
+                iters_r1=int(ms.riters[1]), iters_r2=int(ms.riters[2]),
+                iters_r3=int(ms.riters[3]), iters_r4=int(ms.riters[4]),
+                max_err=float(ms.max_err), avg_err=float(ms.avg_err), early_term=int(ms.early),
+                missed_neighbors=0,
+                t_neighbor=max(0, ms.t_refreshed - ms.t_begin) * 1e-9,
+                t_physics=max(0, ms.t_looped - ms.t_refreshed) * 1e-9,
+                t_rts=max(0, ms.t_end - ms.t_looped) * 1e-9))
+        self._raise_control(ctl, c)
         self.controller.note_major(early)
         return rows
 
@@ -357,107 +509,6 @@ class PcisphSolver(_DeviceSolver):
         self._call("rts_pci_sob")
         if not rebuilt:
             self._raise(self.counters.read(self._stream()))
-
-    def _minor_step(self, j: int, rows, last: bool) -> StepStats:
-        nf = self.n_fluid
-        dt = self.dt
-        self._prepare(dt)
-        st = self._stream()
-        tm = self.timer
-        tm.start(st)
-        self._call("rts_pci_refresh", 0, 1)
-        tm.mark("neighbor", st)
-        missed = 0
-        if self.audit_neighbors:
-            missed = self._audit_refresh()
-            self.missed_neighbors_total += missed
-        self._zero_pressure()
-        iters, corrected, riters, early, c_last = self._correct_scheduled(dt, rows)
-        self._call("rts_pci_integrate", 1)
-        tm.mark("physics", st)
-        if not last:
-            self._mark_timestep_updates(launch_only=True)
-        tm.mark("rts", st)
-        c = self._read()
-        n_refresh = int(self._n_refresh)
-        self.step_index += 1
-        self.sim_time += dt
-        t = tm.totals()
-        return StepStats(step=self.step_index, time=self.sim_time, dt=dt, n_compute=n_refresh,
-                         frac_compute=n_refresh / max(1, nf), iterations=iters,
-                         corrected=corrected, iters_r1=riters[1], iters_r2=riters[2],
-                         iters_r3=riters[3], iters_r4=riters[4], max_err=float(c_last.max_err),
-                         avg_err=self._avg_from(c_last), early_term=int(early),
-                         missed_neighbors=missed, t_neighbor=t["neighbor"],
-                         t_physics=t["physics"], t_rts=t["rts"])
-
-    def _correct_scheduled(self, dt: float, rows):
-        sc = self.scene
-        s = self._stream().cuda_stream
-        N.call("rts_memset", self.arena.buf.in_se, 0, self.n_fluid, s) if self.n_fluid else None
-        self._call("rts_pci_observed", 0)
-        it = g_count = corrected = 0
-        riters = [0, 0, 0, 0, 0]
-        local_active = local_banned = False
-        local_run = 0
-        early = False
-        motion_all = True
-        first = True
-        while True:
-            if local_active:
-                mask = 0
-            else:
-                row = rows[g_count % len(rows)]
-                mask = _row_mask(row)
-                for n in row:
-                    if n <= self.n_regions:
-                        riters[n] += 1
-            self._call("rts_pci_motion", int(motion_all))
-            self._call("rts_pci_sets", mask, 0)
-            self._call("rts_pci_density")
-            self._call("rts_pci_se_reduce", 1)
-            self._call("rts_pci_observed", 1)
-            self._call("rts_pci_pforces")
-            c = self._read()
-            if first:
-                self._n_refresh = int(c.n_compute)
-                first = False
-            motion_all = False
-            it += 1
-            corrected += int(c.n_pred)
-            self._force_total += int(c.n_force)
-            if local_active:
-                local_run += 1
-            else:
-                g_count += 1
-            max_err = float(c.max_err)
-            avg_err = self._avg_from(c)
-            if max_err < sc.eta_max and avg_err < sc.eta_avg:
-                if it >= 3:
-                    break
-                continue
-            if it < 3:
-                continue
-            if local_active:
-                if local_run >= self.local_attempts:
-                    self._call("rts_pci_snapshot", 1)
-                    motion_all = True
-                    local_active = False
-                    local_banned = True
-                    self.local_reverted_total += 1
-            elif avg_err * 100.0 < sc.rho_T and not local_banned and c.any_se:
-                local_active = True
-                local_run = 0
-                self._call("rts_pci_snapshot", 0)
-                self.local_entered_total += 1
-            if g_count > 6:
-                early = True
-            if g_count > self.iteration_cap:
-                raise NumericalError(
-                    f"pressure solve used {g_count} global iterations in one minor step "
-                    f"(max error {max_err:.4%} of rest density)")
-        self._call("rts_pci_sob")
-        return it, corrected, riters, early, c
 
     def _mark_timestep_updates(self, launch_only: bool = False) -> None:
         """Mid-major pre-emption (pcisph.py:718-755)."""

@@ -80,6 +80,7 @@ def test_first_iteration_parity_from_common_state():
     orc.in_se = orc.err > 0.5 * orc.scene.eta_max
     orc._refresh_observed()
     orc._pforces(force)
+    dev._call("rts_pci_minor_begin", 0, 0)  # loop state: not done
     dev._call("rts_pci_observed", 0)
     dev._call("rts_pci_motion", 1)
     dev._call("rts_pci_sets", 0b11110, 0)
@@ -100,9 +101,13 @@ def test_first_iteration_parity_from_common_state():
     assert float(c.max_err) == pytest.approx(float(orc.err.max()), rel=1e-4, abs=1e-9)
 
 
+@pytest.mark.parametrize("graphs", [True, False])
 @pytest.mark.parametrize("mode", ["rts", "const"])
-def test_major_step_parity_from_common_state(mode):
-    dev, orc = _pair(tiny_tank(), mode=mode)
+def test_major_step_parity_from_common_state(mode, graphs):
+    from oracle.sph import OraclePcisph
+    from paper_2009_14514_b200 import PcisphSolver
+    dev = PcisphSolver(tiny_tank(), mode=mode, use_graphs=graphs)
+    orc = OraclePcisph(tiny_tank(), mode=mode)
     apply_jitter(dev, orc)
     for major in range(4):
         inject(dev, orc, PCISPH_STATE)
