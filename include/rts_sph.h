@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define RTS_ABI_VERSION 7
+#define RTS_ABI_VERSION 9
 
 /* err_flags bits */
 #define RTS_ERR_ESCAPED   0x1u  /* fluid left the padded grid or non-finite (grid.py:268-273) */
@@ -89,7 +89,7 @@ typedef struct RtsCounters {
     double   sum_rho;          /* PCISPH: sum of rho* over fluid */
     double   max_err;          /* PCISPH: max err over fluid */
     int32_t  any_se;           /* PCISPH: any particle in S_e */
-    int32_t  pad;
+    int32_t  n_work;           /* blocks in the tiled work list */
     double   reserved[8];
 } RtsCounters;
 
@@ -124,6 +124,8 @@ typedef struct RtsControl {
     int32_t local_entered, local_reverted;
     int32_t fail_kind;     /* 1 non-finite, 2 RTS cap, 3 sync cap */
     int32_t fail_g;
+    int32_t stamp;         /* S_e generation: cells stamped with it hold S_e particles */
+    int32_t prev_force;    /* |force set| of the previous iteration (motion list length) */
     int32_t n_rows[RTS_MAX_MINOR];
     int32_t row_masks[RTS_MAX_MINOR][RTS_MAX_ROWS];
     int32_t row_counts[RTS_MAX_MINOR][RTS_MAX_ROWS];  /* region multiplicities, 4 bits each */
@@ -192,6 +194,8 @@ typedef struct RtsBuffers {
     float   *snap_fp;      /* (Nf, 3) local-phase snapshot of f_p */
     int32_t *slot_of;      /* (Nf) CSR slot of each fluid particle (inverse of order) */
     RtsControl *ctl;       /* correction-loop control block */
+    int32_t *se_stamp;     /* (Nc) S_e generation that last marked the block */
+    int32_t *near_stamp;   /* (Nc) S_e generation that last marked a 26-neighbour */
     RtsCounters *ctr;
 } RtsBuffers;
 
@@ -256,7 +260,11 @@ int rts_pci_density(const RtsParams *p, const RtsBuffers *b, void *stream);
 /* S_e = err > eta_max/2 and its blocks (with_se), max err, sum rho*,
  * any(S_e) into the counters (pcisph.py:662, 421-430, 682-683). */
 int rts_pci_se_reduce(const RtsParams *p, const RtsBuffers *b, int with_se, void *stream);
-/* derive_observed (regions.py:110-125) into block_tmp; S_ob refresh. */
+/* Static part of derive_observed (regions.py:110-125: occupied and next to
+ * a strictly smaller region) into block_tmp; the S_e part (regions.py:123-124)
+ * is carried by the generation stamps se_stamp/near_stamp written in
+ * rts_pci_se_reduce, and S_ob = static | (near & !S_e) is evaluated per
+ * particle (rts_pci_sets, rts_pci_sob, k_integrate).  with_se is ignored. */
 int rts_pci_observed(const RtsParams *p, const RtsBuffers *b, int with_se, void *stream);
 int rts_pci_sob(const RtsParams *p, const RtsBuffers *b, void *stream);
 /* _pressure_forces over the force list (pcisph.py:238-271). */

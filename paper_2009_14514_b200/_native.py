@@ -12,7 +12,7 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "librtssph.so")
-ABI_VERSION = 7
+ABI_VERSION = 9
 
 _c = ctypes
 _D = _c.c_double
@@ -39,7 +39,7 @@ class RtsCounters(_c.Structure):
         ("err_flags", _c.c_uint32), ("n_escaped", _I), ("first_escaped", _I), ("n_compute", _I),
         ("overflow", _c.c_int64), ("n_sorted", _I), ("n_pred", _I), ("n_force", _I),
         ("n_list", _I), ("fmax_bits", _c.c_uint64), ("sum_rho", _D), ("max_err", _D),
-        ("any_se", _I), ("pad", _I), ("reserved", _D * 8),
+        ("any_se", _I), ("n_work", _I), ("reserved", _D * 8),
     ]
 
 
@@ -62,6 +62,7 @@ class RtsControl(_c.Structure):
         ("local_run", _I), ("early", _I), ("done", _I), ("failed", _I), ("motion_all", _I),
         ("row_mask", _I), ("snap_op", _I), ("minor", _I), ("stop_major", _I),
         ("local_entered", _I), ("local_reverted", _I), ("fail_kind", _I), ("fail_g", _I),
+        ("stamp", _I), ("prev_force", _I),
         ("n_rows", _I * MAX_MINOR), ("row_masks", (_I * MAX_ROWS) * MAX_MINOR),
         ("row_counts", (_I * MAX_ROWS) * MAX_MINOR), ("riters", _I * 5), ("skipped", _I),
         ("corrected", _c.c_int64), ("forced", _c.c_int64), ("last_max_err", _D),
@@ -76,7 +77,7 @@ BUFFER_FIELDS = (
     "cell_bcount", "starts", "order", "fill", "scan_tmp", "bcell_ids", "bcell_start", "bidx",
     "bcell_of", "bcell_active", "vmax", "fmax", "block_raw", "block_field", "block_tmp",
     "block_flag", "cpos", "cvel", "active", "list2", "nbr", "cnt", "xs4", "pflag", "partial",
-    "snap_p", "snap_fp", "slot_of", "ctl", "ctr",
+    "snap_p", "snap_fp", "slot_of", "ctl", "se_stamp", "near_stamp", "ctr",
 )
 
 

@@ -81,9 +81,9 @@ RTS_DEV long long gtimer() {
     return t;
 }
 
-RTS_DEV bool fatal(const RtsCounters *c) {
-    return (*(volatile const uint32_t *)&c->err_flags) & RTS_ERR_FATAL;
-}
+// Flags written by earlier kernels in the stream are visible at kernel start;
+// a plain (L1-cacheable) load suffices -- no system-scope volatile load.
+RTS_DEV bool fatal(const RtsCounters *c) { return c->err_flags & RTS_ERR_FATAL; }
 
 // warp-aggregated append of `pred` lanes to list[*count]
 RTS_DEV void warp_append(bool pred, int value, int *list, int *count) {
@@ -122,13 +122,13 @@ RTS_DEV void block_append2(bool p0, int v0, int *list0, int *count0, bool p1, in
             a += x;
             c += y;
         }
-        s_base[0] = a && list0 ? atomicAdd(count0, a) : 0;
-        s_base[1] = c && list1 ? atomicAdd(count1, c) : 0;
+        s_base[0] = a && count0 ? atomicAdd(count0, a) : 0;
+        s_base[1] = c && count1 ? atomicAdd(count1, c) : 0;
     }
     __syncthreads();
     const unsigned lt = (1u << lane) - 1u;
-    if (p0) list0[s_base[0] + s_w0[warp] + __popc(m0 & lt)] = v0;
-    if (p1) list1[s_base[1] + s_w1[warp] + __popc(m1 & lt)] = v1;
+    if (p0 && list0) list0[s_base[0] + s_w0[warp] + __popc(m0 & lt)] = v0;
+    if (p1 && list1) list1[s_base[1] + s_w1[warp] + __popc(m1 & lt)] = v1;
     __syncthreads();  // shared slots are reused by the next loop trip
 }
 

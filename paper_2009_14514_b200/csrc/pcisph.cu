@@ -30,13 +30,15 @@ constexpr int kRedBlocks = 1024;  // fixed partial count -> deterministic sums
 
 __constant__ int kValidity[5] = {0, 1, 2, 4, 4};  // pcisph.py:66
 
+// S_ob membership of a block: static transition bit (block_tmp) or next to
+// an S_e block of generation `gen` without being one (regions.py:119-125)
+RTS_DEV bool observed_block(const RtsBuffers &b, int c, int gen) {
+    return b.block_tmp[c] || (b.near_stamp[c] == gen && b.se_stamp[c] != gen);
+}
+
 // loop control flags (ctl may be null for callers outside a solver)
-RTS_DEV bool loop_done(const RtsBuffers &b) {
-    return b.ctl && *(volatile const int *)&b.ctl->done;
-}
-RTS_DEV bool major_stopped(const RtsBuffers &b) {
-    return b.ctl && *(volatile const int *)&b.ctl->stop_major;
-}
+RTS_DEV bool loop_done(const RtsBuffers &b) { return b.ctl && b.ctl->done; }
+RTS_DEV bool major_stopped(const RtsBuffers &b) { return b.ctl && b.ctl->stop_major; }
 // iteration kernels skip when the loop has finished or a fatal flag is set
 #define RTS_ITER_GUARD() if (fatal(b.ctr) || loop_done(b)) return
 #define RTS_MINOR_GUARD() if (fatal(b.ctr) || major_stopped(b)) return
@@ -97,89 +99,166 @@ __global__ void __launch_bounds__(256) k_refresh_list(const __grid_constant__ Rt
     }
 }
 
-// search_into on the (stale) major grid (grid.py:88-152) fused with the
-// external forces of the refreshed particle (pcisph.py:174-199).
+// ---- search_into on the (stale) major grid (grid.py:88-152) fused with the
+// external forces of the refreshed particle (pcisph.py:174-199) ------------
 //
-// Pass 1 scans the CSR spans of the (2L+1)^3 blocks (contiguous cpos reads)
-// and classifies each candidate in fp32 with a +-1e-5 relative band around
-// h^2; only candidates inside the band take the exact fp64 test, so the
-// warp does not serialise on fp64 work for every candidate some lane hits.
-// Membership equals the reference's fp64 `r2 < h2` exactly.  Pass 2 walks
-// the freshly written table row (no divergence) for the viscosity sum.
-__global__ void __launch_bounds__(kThreads) k_refresh(const __grid_constant__ RtsParams p,
-                                                      RtsBuffers b, int two_layer_r1) {
-    RTS_MINOR_GUARD();
-    const int n = b.ctr->n_compute;
-    const int nx = p.dims[0], ny = p.dims[1], nz = p.dims[2];
-    const float h2_lo = (float)(p.h2 * (1.0 - 1e-5));
-    const float h2_hi = (float)(p.h2 * (1.0 + 1e-5));
-    const double m2 = xmul(p.mass, p.mass);
-    const double inv_rho0_sq = xdiv(1.0, xmul(p.rho0, p.rho0));
-    const double mum2 = xmul(p.mu, m2);
+// Membership: candidates are classified in fp32 with a +-1e-5 relative band
+// around h^2; only candidates inside the band take the exact fp64 test, so
+// membership equals the reference's fp64 `r2 < h2` exactly.  Table rows are
+// filled in the reference's order (blocks in (ax, ay, az) order, CSR order
+// inside a block).  The viscosity sum of f_ext is a fixed-order tree
+// (deterministic; f_ext parity bar 1e-4).
+struct RefreshConsts {
+    float h2_lo, h2_hi;
+    double m2, inv_rho0_sq, mum2;
+};
+
+RTS_DEV RefreshConsts refresh_consts(const RtsParams &p) {
+    RefreshConsts k;
+    k.h2_lo = (float)(p.h2 * (1.0 - 1e-5));
+    k.h2_hi = (float)(p.h2 * (1.0 + 1e-5));
+    k.m2 = xmul(p.mass, p.mass);
+    k.inv_rho0_sq = xdiv(1.0, xmul(p.rho0, p.rho0));
+    k.mum2 = xmul(p.mu, k.m2);
+    return k;
+}
+
+// exact fp64 membership for the rare candidates inside the fp32 band; kept
+// out of line so the compiler cannot if-convert (speculate) the fp64 work
+// into every candidate test
+__device__ __noinline__ bool exact_neighbour(double h2, float fxi, float fyi, float fzi, float ox,
+                                             float oy, float oz) {
+    return dist2(xsub((double)fxi, (double)ox), xsub((double)fyi, (double)oy),
+                 xsub((double)fzi, (double)oz)) < h2;
+}
+
+RTS_DEV bool is_neighbour(const RefreshConsts &k, const RtsParams &p, float fxi, float fyi,
+                          float fzi, float4 o) {
+    const float ex = fxi - o.x, ey = fyi - o.y, ez = fzi - o.z;
+    const float r2f = __fadd_rn(__fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey)), __fmul_rn(ez, ez));
+    if (r2f > k.h2_hi) return false;
+    if (r2f < k.h2_lo) return true;
+    return exact_neighbour(p.h2, fxi, fyi, fzi, o.x, o.y, o.z);
+}
+
+// viscosity term of one table entry j for particle i (pcisph.py:183-196)
+RTS_DEV void visc_term(const RefreshConsts &k, const RtsParams &p, const RtsBuffers &b, int i,
+                       int j, double xi, double yi, double zi, float4 pj, double vxi, double vyi,
+                       double vzi, double &fx, double &fy, double &fz) {
+    if (j >= p.n_fluid || j == i) return;
+    const double r = xsqrt(dist2(xsub(xi, (double)pj.x), xsub(yi, (double)pj.y),
+                                 xsub(zi, (double)pj.z)));
+    if (r >= p.h) return;
+    const double lap = xmul(xmul(k.mum2, visc_lap(r, p.h, p.c_visc)), k.inv_rho0_sq);
+    fx = xadd(fx, xmul(lap, xsub((double)b.vel[3 * j], vxi)));
+    fy = xadd(fy, xmul(lap, xsub((double)b.vel[3 * j + 1], vyi)));
+    fz = xadd(fz, xmul(lap, xsub((double)b.vel[3 * j + 2], vzi)));
+}
+
+RTS_DEV void finish_refresh(const RtsParams &p, const RtsBuffers &b, int i, int cntn, double fx,
+                            double fy, double fz) {
+    if (cntn > p.width) {
+        atomicOr(&b.ctr->err_flags, RTS_ERR_OVERFLOW);
+        atomicAdd((unsigned long long *)&b.ctr->overflow, (unsigned long long)(cntn - p.width));
+        cntn = p.width;
+    }
+    b.cnt[i] = cntn;
+    b.force[3 * i] = (float)xadd(fx, xmul(p.mass, p.gravity[0]));
+    b.force[3 * i + 1] = (float)xadd(fy, xmul(p.mass, p.gravity[1]));
+    b.force[3 * i + 2] = (float)xadd(fz, xmul(p.mass, p.gravity[2]));
+}
+
+// One thread (G = 1) or one G-lane group per refreshed particle, chosen from
+// the list length: the full refresh at a major-step start keeps one thread
+// per particle (adjacent lanes share candidate spans -> few L1 lines per
+// load); the short later lists (regions 1-2) use 8- or 32-lane groups so the
+// launch still has enough independent loads in flight (region-1 particles
+// scan 125 blocks, ~1300 candidates).
+template <int G>
+RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshConsts &k, int i,
+                         int two_layer_r1, int lane, unsigned gmask, int gshift) {
     const float4 *cpos = reinterpret_cast<const float4 *>(b.cpos);
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
-        const int i = b.active[t];
-        const float fxi = b.pos[3 * i], fyi = b.pos[3 * i + 1], fzi = b.pos[3 * i + 2];
-        const double xi = fxi, yi = fyi, zi = fzi;
-        const int lay = (two_layer_r1 && b.region[i] == 1) ? 2 : 1;
-        const int cx = trunc_axis(xi, p.origin[0], p.inv_block, nx);
-        const int cy = trunc_axis(yi, p.origin[1], p.inv_block, ny);
-        const int cz = trunc_axis(zi, p.origin[2], p.inv_block, nz);
-        const int z0 = max(0, cz - lay), z1 = min(nz - 1, cz + lay);
-        int cntn = 0;
-        int *row = b.nbr + (size_t)i * p.width;
-        for (int ax = max(0, cx - lay); ax <= min(nx - 1, cx + lay); ++ax)
-            for (int ay = max(0, cy - lay); ay <= min(ny - 1, cy + lay); ++ay) {
-                const int base = (ax * ny + ay) * nz;
-                const int k0 = b.starts[base + z0], k1 = b.starts[base + z1 + 1];
+    const int nx = p.dims[0], ny = p.dims[1], nz = p.dims[2];
+    const float fxi = b.pos[3 * i], fyi = b.pos[3 * i + 1], fzi = b.pos[3 * i + 2];
+    const double xi = fxi, yi = fyi, zi = fzi;
+    const int lay = (two_layer_r1 && b.region[i] == 1) ? 2 : 1;
+    const int cx = trunc_axis(xi, p.origin[0], p.inv_block, nx);
+    const int cy = trunc_axis(yi, p.origin[1], p.inv_block, ny);
+    const int cz = trunc_axis(zi, p.origin[2], p.inv_block, nz);
+    const int z0 = max(0, cz - lay), z1 = min(nz - 1, cz + lay);
+    const unsigned lt = (1u << lane) - 1u;
+    int cntn = 0;
+    int *row = b.nbr + (size_t)i * p.width;
+    for (int ax = max(0, cx - lay); ax <= min(nx - 1, cx + lay); ++ax)
+        for (int ay = max(0, cy - lay); ay <= min(ny - 1, cy + lay); ++ay) {
+            const int base = (ax * ny + ay) * nz;
+            const int k0 = b.starts[base + z0], k1 = b.starts[base + z1 + 1];
+            if (G == 1) {
                 for (int kb = k0; kb < k1; kb += 4) {
                     float4 ob[4];
 #pragma unroll
                     for (int u = 0; u < 4; ++u) ob[u] = cpos[min(kb + u, k1 - 1)];
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
-                        const int k = kb + u;
-                        const float ex = fxi - ob[u].x, ey = fyi - ob[u].y, ez = fzi - ob[u].z;
-                        const float r2f =
-                            __fadd_rn(__fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey)),
-                                      __fmul_rn(ez, ez));
-                        bool in = k < k1 && r2f < h2_lo;
-                        if (k < k1 && !in && r2f <= h2_hi)
-                            in = dist2(xsub(xi, (double)ob[u].x), xsub(yi, (double)ob[u].y),
-                                       xsub(zi, (double)ob[u].z)) < p.h2;
-                        if (in) {
-                            if (cntn < p.width) row[cntn] = b.order[k];
+                        if (kb + u < k1 && is_neighbour(k, p, fxi, fyi, fzi, ob[u])) {
+                            if (cntn < p.width) row[cntn] = b.order[kb + u];
                             ++cntn;
                         }
                     }
                 }
+            } else {
+                for (int kb = k0; kb < k1; kb += G) {
+                    const int kk = kb + lane;
+                    const bool in = kk < k1 && is_neighbour(k, p, fxi, fyi, fzi, cpos[kk]);
+                    const unsigned m =
+                        (__ballot_sync(gmask, in) >> gshift) & (G == 32 ? 0xffffffffu : ((1u << G) - 1u));
+                    if (in) {
+                        const int slot = cntn + __popc(m & lt);
+                        if (slot < p.width) row[slot] = b.order[kk];
+                    }
+                    cntn += __popc(m);
+                }
             }
-        if (cntn > p.width) {
-            atomicOr(&b.ctr->err_flags, RTS_ERR_OVERFLOW);
-            atomicAdd((unsigned long long *)&b.ctr->overflow,
-                      (unsigned long long)(cntn - p.width));
-            cntn = p.width;
         }
-        b.cnt[i] = cntn;
-        // pass 2: viscosity over fluid entries of the row (pcisph.py:183-196)
-        const double vxi = b.vel[3 * i], vyi = b.vel[3 * i + 1], vzi = b.vel[3 * i + 2];
-        double fx = 0.0, fy = 0.0, fz = 0.0;
-        for (int q = 0; q < cntn; ++q) {
-            const int j = row[q];
-            if (j >= p.n_fluid || j == i) continue;
-            const double dx = xsub(xi, (double)b.pos[3 * j]);
-            const double dy = xsub(yi, (double)b.pos[3 * j + 1]);
-            const double dz = xsub(zi, (double)b.pos[3 * j + 2]);
-            const double r = xsqrt(dist2(dx, dy, dz));
-            if (r >= p.h) continue;
-            const double lap = xmul(xmul(mum2, visc_lap(r, p.h, p.c_visc)), inv_rho0_sq);
-            fx = xadd(fx, xmul(lap, xsub((double)b.vel[3 * j], vxi)));
-            fy = xadd(fy, xmul(lap, xsub((double)b.vel[3 * j + 1], vyi)));
-            fz = xadd(fz, xmul(lap, xsub((double)b.vel[3 * j + 2], vzi)));
+    if (G > 1) __syncwarp(gmask);
+    const int nrow = min(cntn, p.width);
+    const double vxi = b.vel[3 * i], vyi = b.vel[3 * i + 1], vzi = b.vel[3 * i + 2];
+    double fx = 0.0, fy = 0.0, fz = 0.0;
+    for (int q = lane; q < nrow; q += G) {
+        const int j = row[q];
+        const float4 pj = make_float4(b.pos[3 * j], b.pos[3 * j + 1], b.pos[3 * j + 2], 0.f);
+        visc_term(k, p, b, i, j, xi, yi, zi, pj, vxi, vyi, vzi, fx, fy, fz);
+    }
+    if (G > 1) {
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) {
+            fx = xadd(fx, __shfl_xor_sync(gmask, fx, o, G));
+            fy = xadd(fy, __shfl_xor_sync(gmask, fy, o, G));
+            fz = xadd(fz, __shfl_xor_sync(gmask, fz, o, G));
         }
-        b.force[3 * i] = (float)xadd(fx, xmul(p.mass, p.gravity[0]));
-        b.force[3 * i + 1] = (float)xadd(fy, xmul(p.mass, p.gravity[1]));
-        b.force[3 * i + 2] = (float)xadd(fz, xmul(p.mass, p.gravity[2]));
+    }
+    if (lane == 0) finish_refresh(p, b, i, cntn, fx, fy, fz);
+}
+
+__global__ void __launch_bounds__(kThreads) k_refresh(const __grid_constant__ RtsParams p,
+                                                      RtsBuffers b, int two_layer_r1) {
+    RTS_MINOR_GUARD();
+    const int n = b.ctr->n_compute;
+    const RefreshConsts k = refresh_consts(p);
+    const int nthreads = gridDim.x * blockDim.x;
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int wl = threadIdx.x & 31;
+    if ((long long)n * 32 <= nthreads) {
+        for (int t = tid / 32; t < n; t += nthreads / 32)
+            refresh_one<32>(p, b, k, b.active[t], two_layer_r1, wl, 0xffffffffu, 0);
+    } else if ((long long)n * 8 <= nthreads) {
+        const int lane = wl & 7, gshift = wl & ~7;
+        const unsigned gmask = 0xffu << gshift;
+        for (int t = tid / 8; t < n; t += nthreads / 8)
+            refresh_one<8>(p, b, k, b.active[t], two_layer_r1, lane, gmask, gshift);
+    } else {
+        for (int t = tid; t < n; t += nthreads)
+            refresh_one<1>(p, b, k, b.active[t], two_layer_r1, 0, 0u, 0);
     }
 }
 
@@ -191,7 +270,6 @@ RTS_DEV void motion_one(const RtsParams &p, const RtsBuffers &b, int i, double d
         const double f = xadd((double)b.force[3 * i + a], (double)b.f_p[3 * i + a]);
         const double v = xadd((double)b.vel[3 * i + a], xmul(dt_inv_m, f));
         xs[a] = (float)xadd((double)b.pos[3 * i + a], xmul(p.dt, v));
-        b.xstar[3 * i + a] = xs[a];
     }
     reinterpret_cast<float4 *>(b.xs4)[i] = make_float4(xs[0], xs[1], xs[2], b.pres[i]);
 }
@@ -201,7 +279,7 @@ __global__ void k_motion(const __grid_constant__ RtsParams p, RtsBuffers b, int 
     RTS_ITER_GUARD();
     if (all < 0) all = b.ctl->motion_all;
     const double dim = xmul(p.dt, p.inv_mass);
-    const int n = all ? p.n_fluid : b.ctr->n_force;
+    const int n = all ? p.n_fluid : b.ctl->prev_force;
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x)
         motion_one(p, b, all ? t : b.list2[t], dim);
 }
@@ -212,6 +290,7 @@ __global__ void __launch_bounds__(256) k_sets(const __grid_constant__ RtsParams 
                                               int row_mask, int all_pred) {
     RTS_ITER_GUARD();
     if (row_mask < 0) row_mask = b.ctl->row_mask;
+    const int gen = b.ctl ? b.ctl->stamp : 0;
     const int nf = p.n_fluid;
     const int stride = gridDim.x * blockDim.x;
     for (int base = blockIdx.x * blockDim.x; base < nf; base += stride) {
@@ -221,7 +300,7 @@ __global__ void __launch_bounds__(256) k_sets(const __grid_constant__ RtsParams 
             if (all_pred) {
                 pred = force = true;
             } else {
-                const bool sob = b.block_tmp[b.fluid_cells[i]] != 0;
+                const bool sob = observed_block(b, b.fluid_cells[i], gen);
                 b.in_sob[i] = sob;
                 const bool turn = (row_mask >> b.region[i]) & 1;
                 const bool se = b.in_se[i] != 0;
@@ -237,26 +316,30 @@ __global__ void __launch_bounds__(256) k_sets(const __grid_constant__ RtsParams 
 // S_ob = observed[fluid_cells] for every fluid particle (pcisph.py:537-542)
 __global__ void k_sob(const __grid_constant__ RtsParams p, RtsBuffers b) {
     RTS_MINOR_GUARD();
-    if (b.ctl && blockIdx.x == 0 && threadIdx.x == 0)
-        b.ctl->stats[b.ctl->minor].t_looped = gtimer();
+    const int gen = b.ctl ? b.ctl->stamp : 0;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.n_fluid;
          i += gridDim.x * blockDim.x)
-        b.in_sob[i] = b.block_tmp[b.fluid_cells[i]] != 0;
+        b.in_sob[i] = observed_block(b, b.fluid_cells[i], gen);
 }
 
-// rho*, err over the pred list; p += delta (rho* - rho0) on force members
-__global__ void __launch_bounds__(kThreads) k_density(const __grid_constant__ RtsParams p,
-                                                      RtsBuffers b) {
-    RTS_ITER_GUARD();
-    const int n = b.ctr->n_pred;
+// rho*, err over the pred list; p += delta (rho* - rho0) on force members.
+// Granularity adapts to the list length: large lists run one particle per
+// thread (neighbouring lanes share neighbours -> few L1 lines per warp
+// load); short lists (the later, S_e-driven iterations) run an 8-lane group
+// per particle so the launch still has enough independent loads in flight.
+constexpr int kPG = 8;
+
+template <int LG>
+RTS_DEV void density_one(const RtsParams &p, const RtsBuffers &b, int i, int lane,
+                         unsigned gmask) {
     const float4 *xs4 = reinterpret_cast<const float4 *>(b.xs4);
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
-        const int i = b.active[t];
-        const float4 a = xs4[i];
-        const double xi = a.x, yi = a.y, zi = a.z;
-        const int c = b.cnt[i];
-        const int4 *row4 = reinterpret_cast<const int4 *>(b.nbr + (size_t)i * p.width);
-        double acc = 0.0;
+    const float4 a = xs4[i];
+    const double xi = a.x, yi = a.y, zi = a.z;
+    const int c = b.cnt[i];
+    const int *row = b.nbr + (size_t)i * p.width;
+    double acc = 0.0;
+    if (LG == 1) {
+        const int4 *row4 = reinterpret_cast<const int4 *>(row);
         for (int q = 0; q < c; q += 8) {
             const int4 ja = row4[q >> 2];
             const int4 jb = row4[(q >> 2) + 1];
@@ -272,6 +355,17 @@ __global__ void __launch_bounds__(kThreads) k_density(const __grid_constant__ Rt
                                           p.h2, p.c_poly6));
             }
         }
+    } else {
+        for (int q = lane; q < c; q += LG) {
+            const float4 o = xs4[row[q]];
+            acc = xadd(acc, poly6(dist2(xsub(xi, (double)o.x), xsub(yi, (double)o.y),
+                                        xsub(zi, (double)o.z)),
+                                  p.h2, p.c_poly6));
+        }
+#pragma unroll
+        for (int o = LG / 2; o > 0; o >>= 1) acc = xadd(acc, __shfl_xor_sync(gmask, acc, o, LG));
+    }
+    if (lane == 0) {
         const double rho = xmul(p.mass, acc);
         const double diff = xsub(rho, p.rho0);
         b.rho[i] = (float)rho;
@@ -286,6 +380,22 @@ __global__ void __launch_bounds__(kThreads) k_density(const __grid_constant__ Rt
     }
 }
 
+__global__ void __launch_bounds__(kThreads) k_density(const __grid_constant__ RtsParams p,
+                                                      RtsBuffers b) {
+    RTS_ITER_GUARD();
+    const int n = b.ctr->n_pred;
+    const int nthreads = gridDim.x * blockDim.x;
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    if ((long long)n * kPG <= nthreads) {
+        const int wl = threadIdx.x & 31, lane = wl & (kPG - 1);
+        const unsigned gmask = ((1u << kPG) - 1u) << (wl & ~(kPG - 1));
+        for (int t = tid / kPG; t < n; t += nthreads / kPG)
+            density_one<kPG>(p, b, b.active[t], lane, gmask);
+    } else {
+        for (int t = tid; t < n; t += nthreads) density_one<1>(p, b, b.active[t], 0, 0u);
+    }
+}
+
 // S_e, S_e blocks, max err, sum rho* (deterministic), any S_e
 __global__ void __launch_bounds__(256) k_se_reduce(const __grid_constant__ RtsParams p,
                                                    RtsBuffers b, int with_se) {
@@ -296,6 +406,8 @@ __global__ void __launch_bounds__(256) k_se_reduce(const __grid_constant__ RtsPa
     // contiguous chunk per block, fixed tree inside -> order-independent of timing
     const int chunk = (nf + gridDim.x - 1) / gridDim.x;
     const int i0 = blockIdx.x * chunk, i1 = min(nf, i0 + chunk);
+    const int gen = b.ctl ? b.ctl->stamp + 1 : 1;
+    const int nx = p.dims[0], ny = p.dims[1], nz = p.dims[2];
     double s = 0.0, m = 0.0;
     int any = 0;
     for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
@@ -303,8 +415,17 @@ __global__ void __launch_bounds__(256) k_se_reduce(const __grid_constant__ RtsPa
         const bool se = with_se && e > thr;
         if (with_se) b.in_se[i] = se;
         if (se) {
-            b.block_flag[b.fluid_cells[i]] = 1;
             any = 1;
+            const int c = b.fluid_cells[i];
+            if (atomicExch(&b.se_stamp[c], gen) != gen) {  // first S_e particle of block c
+                const int cz = c % nz, cy = (c / nz) % ny, cx = c / (ny * nz);
+                for (int ax = max(0, cx - 1); ax <= min(nx - 1, cx + 1); ++ax)
+                    for (int ay = max(0, cy - 1); ay <= min(ny - 1, cy + 1); ++ay) {
+                        const int base = (ax * ny + ay) * nz;
+                        for (int az = max(0, cz - 1); az <= min(nz - 1, cz + 1); ++az)
+                            b.near_stamp[base + az] = gen;
+                    }
+            }
         }
         if (e > m) m = e;
         s = xadd(s, (double)b.rho[i]);
@@ -348,11 +469,8 @@ __global__ void k_sum_partials(RtsBuffers b, int n) {
 // observed blocks (regions.py:110-125): occupied and (bordering a strictly
 // smaller region, or bordering an S_e block without being one); -> block_tmp
 __global__ void k_observed(const __grid_constant__ RtsParams p, RtsBuffers b, int with_se) {
-    if (with_se) {
-        RTS_ITER_GUARD();
-    } else {
-        RTS_MINOR_GUARD();
-    }
+    (void)with_se;  // the S_e part is stamp-based (k_se_reduce / observed_block)
+    RTS_MINOR_GUARD();
     const int nx = p.dims[0], ny = p.dims[1], nz = p.dims[2];
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < p.n_cells;
          c += gridDim.x * blockDim.x) {
@@ -361,7 +479,6 @@ __global__ void k_observed(const __grid_constant__ RtsParams p, RtsBuffers b, in
         if (f > 0) {
             const int cz = c % nz, cy = (c / nz) % ny, cx = c / (ny * nz);
             int8_t m = 127;
-            bool near_se = false;
             for (int ax = max(0, cx - 1); ax <= min(nx - 1, cx + 1); ++ax)
                 for (int ay = max(0, cy - 1); ay <= min(ny - 1, cy + 1); ++ay) {
                     const int base = (ax * ny + ay) * nz;
@@ -370,32 +487,51 @@ __global__ void k_observed(const __grid_constant__ RtsParams p, RtsBuffers b, in
                         if (q == c) continue;
                         const int8_t v = b.block_field[q];
                         if (v > 0 && v < m) m = v;
-                        if (with_se && b.block_flag[q]) near_se = true;
                     }
                 }
-            obs = (m < f) || (with_se && near_se && !b.block_flag[c]);
+            obs = (m < f);
         }
         b.block_tmp[c] = obs;
     }
 }
 
-// pressure forces at x* over the force list (pcisph.py:238-271)
-__global__ void __launch_bounds__(kThreads) k_pforces(const __grid_constant__ RtsParams p,
-                                                      RtsBuffers b) {
-    RTS_ITER_GUARD();
-    const int n = b.ctr->n_force;
+// pressure forces at x* over the force list (pcisph.py:238-271); same
+// adaptive granularity as k_density.
+RTS_DEV void pforce_pair(const RtsParams &p, double xi, double yi, double zi, double term_i,
+                         double wall, double m2, double inv_rho0_sq, int i, int j, float4 o,
+                         double &fx, double &fy, double &fz) {
+    if (j == i) return;
+    const double dx = xsub(xi, (double)o.x), dy = xsub(yi, (double)o.y),
+                 dz = xsub(zi, (double)o.z);
+    const double term = j < p.n_fluid ? xadd(term_i, xmul((double)o.w, inv_rho0_sq)) : wall;
+    const double r2 = dist2(dx, dy, dz);
+    if (!(r2 > 0.0) || !(r2 < p.h2)) return;  // r <= 0 or r >= h
+    // spiky factor c (h - r)^2 / r via one fp64 rsqrt (1e-16-level deviation
+    // from sqrt + divide; the f_p parity bar is 1e-4)
+    const double rinv = rsqrt(r2);
+    const double r = xmul(r2, rinv);
+    const double d = xsub(p.h, r);
+    const double s = xmul(xmul(xmul(m2, term), xmul(xmul(p.c_spiky, d), d)), rinv);
+    fx = xsub(fx, xmul(s, dx));
+    fy = xsub(fy, xmul(s, dy));
+    fz = xsub(fz, xmul(s, dz));
+}
+
+template <int LG>
+RTS_DEV void pforce_one(const RtsParams &p, const RtsBuffers &b, int i, int lane,
+                        unsigned gmask) {
     const float4 *xs4 = reinterpret_cast<const float4 *>(b.xs4);
     const double m2 = xmul(p.mass, p.mass);
     const double inv_rho0_sq = xdiv(1.0, xmul(p.rho0, p.rho0));
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
-        const int i = b.list2[t];
-        const float4 a = xs4[i];
-        const double xi = a.x, yi = a.y, zi = a.z;
-        const double term_i = xmul((double)b.pres[i], inv_rho0_sq);
-        const double wall = xadd(term_i, term_i);
-        const int c = b.cnt[i];
-        const int4 *row4 = reinterpret_cast<const int4 *>(b.nbr + (size_t)i * p.width);
-        double fx = 0.0, fy = 0.0, fz = 0.0;
+    const float4 a = xs4[i];
+    const double xi = a.x, yi = a.y, zi = a.z;
+    const double term_i = xmul((double)a.w, inv_rho0_sq);
+    const double wall = xadd(term_i, term_i);
+    const int c = b.cnt[i];
+    const int *row = b.nbr + (size_t)i * p.width;
+    double fx = 0.0, fy = 0.0, fz = 0.0;
+    if (LG == 1) {
+        const int4 *row4 = reinterpret_cast<const int4 *>(row);
         for (int q = 0; q < c; q += 4) {
             const int4 jj = row4[q >> 2];
             const int j4[4] = {jj.x, jj.y, jj.z, jj.w};
@@ -403,30 +539,43 @@ __global__ void __launch_bounds__(kThreads) k_pforces(const __grid_constant__ Rt
 #pragma unroll
             for (int u = 0; u < 4; ++u) o4[u] = xs4[q + u < c ? j4[u] : i];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int j = j4[u];
-                if (q + u >= c || j == i) continue;
-                const float4 o = o4[u];
-                const double dx = xsub(xi, (double)o.x), dy = xsub(yi, (double)o.y),
-                             dz = xsub(zi, (double)o.z);
-                const double term =
-                    j < p.n_fluid ? xadd(term_i, xmul((double)o.w, inv_rho0_sq)) : wall;
-                const double r2 = dist2(dx, dy, dz);
-                if (!(r2 > 0.0) || !(r2 < p.h2)) continue;  // r <= 0 or r >= h
-                // spiky factor c (h - r)^2 / r via one fp64 rsqrt (1e-16-level
-                // deviation from sqrt + divide; f_p parity bar is 1e-4)
-                const double rinv = rsqrt(r2);
-                const double r = xmul(r2, rinv);
-                const double d = xsub(p.h, r);
-                const double s = xmul(xmul(xmul(m2, term), xmul(xmul(p.c_spiky, d), d)), rinv);
-                fx = xsub(fx, xmul(s, dx));
-                fy = xsub(fy, xmul(s, dy));
-                fz = xsub(fz, xmul(s, dz));
-            }
+            for (int u = 0; u < 4; ++u)
+                if (q + u < c)
+                    pforce_pair(p, xi, yi, zi, term_i, wall, m2, inv_rho0_sq, i, j4[u], o4[u],
+                                fx, fy, fz);
         }
+    } else {
+        for (int q = lane; q < c; q += LG) {
+            const int j = row[q];
+            pforce_pair(p, xi, yi, zi, term_i, wall, m2, inv_rho0_sq, i, j, xs4[j], fx, fy, fz);
+        }
+#pragma unroll
+        for (int o = LG / 2; o > 0; o >>= 1) {
+            fx = xadd(fx, __shfl_xor_sync(gmask, fx, o, LG));
+            fy = xadd(fy, __shfl_xor_sync(gmask, fy, o, LG));
+            fz = xadd(fz, __shfl_xor_sync(gmask, fz, o, LG));
+        }
+    }
+    if (lane == 0) {
         b.f_p[3 * i] = (float)fx;
         b.f_p[3 * i + 1] = (float)fy;
         b.f_p[3 * i + 2] = (float)fz;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_pforces(const __grid_constant__ RtsParams p,
+                                                      RtsBuffers b) {
+    RTS_ITER_GUARD();
+    const int n = b.ctr->n_force;
+    const int nthreads = gridDim.x * blockDim.x;
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    if ((long long)n * kPG <= nthreads) {
+        const int wl = threadIdx.x & 31, lane = wl & (kPG - 1);
+        const unsigned gmask = ((1u << kPG) - 1u) << (wl & ~(kPG - 1));
+        for (int t = tid / kPG; t < n; t += nthreads / kPG)
+            pforce_one<kPG>(p, b, b.list2[t], lane, gmask);
+    } else {
+        for (int t = tid; t < n; t += nthreads) pforce_one<1>(p, b, b.list2[t], 0, 0u);
     }
 }
 
@@ -434,8 +583,18 @@ __global__ void __launch_bounds__(kThreads) k_pforces(const __grid_constant__ Rt
 __global__ void k_integrate(const __grid_constant__ RtsParams p, RtsBuffers b, int countdown) {
     RTS_MINOR_GUARD();
     const double dim = xmul(p.dt, p.inv_mass);
+    const int gen = b.ctl ? b.ctl->stamp : 0;
+    if (b.ctl && countdown && blockIdx.x == 0 && threadIdx.x == 0)
+        b.ctl->stats[b.ctl->minor].t_looped = gtimer();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.n_fluid;
          i += gridDim.x * blockDim.x) {
+        // public x* = the last prediction; S_ob from the final S_e generation
+        const float4 xs = reinterpret_cast<const float4 *>(b.xs4)[i];
+        b.xstar[3 * i] = xs.x;
+        b.xstar[3 * i + 1] = xs.y;
+        b.xstar[3 * i + 2] = xs.z;
+        if (countdown) b.in_sob[i] = observed_block(b, b.fluid_cells[i], gen);
+        float nx[3];
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
             const double f = xadd((double)b.force[3 * i + a], (double)b.f_p[3 * i + a]);
@@ -450,8 +609,10 @@ __global__ void k_integrate(const __grid_constant__ RtsParams p, RtsBuffers b, i
             }
             b.pos[3 * i + a] = (float)x;
             b.vel[3 * i + a] = (float)v;
-            if (countdown) b.cpos[4 * b.slot_of[i] + a] = (float)x;
+            nx[a] = (float)x;
         }
+        if (countdown)
+            reinterpret_cast<float4 *>(b.cpos)[b.slot_of[i]] = make_float4(nx[0], nx[1], nx[2], 0.f);
         if (countdown) {
             int v = b.validity[i] - 1;
             const bool expired = v <= 0;
@@ -602,6 +763,12 @@ __global__ void k_minor_begin(RtsBuffers b, int minor, int sync_mode) {
     for (int n = 0; n < 5; ++n) c->riters[n] = 0;
     c->motion_all = 1;
     c->snap_op = 0;
+    c->stamp += 1;  // fresh S_e generation: S_e = {} (pcisph.py:618)
+    c->prev_force = 0;
+    b.ctr->n_pred = 0;
+    b.ctr->n_force = 0;
+    b.ctr->max_err = 0.0;
+    b.ctr->any_se = 0;
     if (!sync_mode) {
         c->row_mask = c->row_masks[minor][0];
         add_row_iters(c, minor, 0);
@@ -615,11 +782,20 @@ __global__ void k_minor_begin(RtsBuffers b, int minor, int sync_mode) {
 // Writes the next iteration's row / motion / snapshot ops, or ends the loop
 // (cond handle of the enclosing CUDA-graph while node, if any).
 __global__ void k_control(const __grid_constant__ RtsParams p, RtsBuffers b, int sync_mode,
-                          unsigned long long cond_handle, int local_attempts, int iteration_cap) {
+                          unsigned long long cond_handle, int local_attempts, int iteration_cap,
+                          int n_part) {
     RtsControl *c = b.ctl;
-    const RtsCounters *ctr = b.ctr;
+    RtsCounters *ctr = b.ctr;
     int done = c->done;
+    // fixed-order sum of the per-block rho* partials (deterministic)
+    double part = 0.0;
+    if (!done)
+        for (int q = threadIdx.x; q < n_part; q += 32) part = xadd(part, b.partial[q]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part = xadd(part, __shfl_xor_sync(0xffffffffu, part, o));
+    if (threadIdx.x != 0) return;
     if (!done) {
+        ctr->sum_rho = part;
         c->snap_op = 0;
         c->it += 1;
         c->corrected += sync_mode ? p.n_fluid : ctr->n_pred;
@@ -686,6 +862,16 @@ __global__ void k_control(const __grid_constant__ RtsParams p, RtsBuffers b, int
         }
         if (c->failed) c->stop_major = 1;
         c->done = done;
+        // hand-over to the next iteration: motion list length, fresh counts,
+        // the S_e generation just written by k_se_reduce becomes current
+        c->prev_force = ctr->n_force;
+        c->stamp += 1;
+        if (!done) {
+            ctr->n_pred = 0;
+            ctr->n_force = 0;
+            ctr->max_err = 0.0;
+            ctr->any_se = 0;
+        }
     }
     if (cond_handle) cudaGraphSetConditional((cudaGraphConditionalHandle)cond_handle, done ? 0 : 1);
 }
@@ -749,7 +935,6 @@ int rts_pci_motion(const RtsParams *p, const RtsBuffers *b, int all, void *strea
 int rts_pci_sets(const RtsParams *p, const RtsBuffers *b, int row_mask, int all_pred,
                  void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
-    cudaMemsetAsync(&b->ctr->n_pred, 0, 2 * sizeof(int), s);  // n_pred, n_force
     rts_note_launch(), k_sets<<<rts_blocks(p->n_fluid, 256, 148 * 4), 256, 0, s>>>(*p, *b, row_mask, all_pred);
     RTS_LAUNCH_CHECK();
     return 0;
@@ -763,15 +948,16 @@ int rts_pci_density(const RtsParams *p, const RtsBuffers *b, void *stream) {
 
 int rts_pci_se_reduce(const RtsParams *p, const RtsBuffers *b, int with_se, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
-    if (with_se) cudaMemsetAsync(b->block_flag, 0, (size_t)p->n_cells, s);
-    cudaMemsetAsync(&b->ctr->max_err, 0, sizeof(double) + 2 * sizeof(int), s);  // max_err, any_se
+
     int blocks = (p->n_fluid + 255) / 256;
     if (blocks > kRedBlocks) blocks = kRedBlocks;
     if (blocks < 1) blocks = 1;
     rts_note_launch(), k_se_reduce<<<blocks, 256, 0, s>>>(*p, *b, with_se);
     RTS_LAUNCH_CHECK();
-    rts_note_launch(), k_sum_partials<<<1, 1024, 0, s>>>(*b, blocks);
-    RTS_LAUNCH_CHECK();
+    if (!b->ctl) {  // outside the device loop: finish the sum here
+        rts_note_launch(), k_sum_partials<<<1, 1024, 0, s>>>(*b, blocks);
+        RTS_LAUNCH_CHECK();
+    }
     return 0;
 }
 
@@ -866,7 +1052,6 @@ int rts_pci_iteration(const RtsParams *p, const RtsBuffers *b, int sync_mode,
     if ((rc = rts_pci_sets(p, b, -1, sync_mode, stream))) return rc;
     if ((rc = rts_pci_density(p, b, stream))) return rc;
     if ((rc = rts_pci_se_reduce(p, b, !sync_mode, stream))) return rc;
-    if (!sync_mode && (rc = rts_pci_observed(p, b, 1, stream))) return rc;
     if ((rc = rts_pci_pforces(p, b, stream))) return rc;
     (void)s;
     return rts_pci_control(p, b, sync_mode, cond_handle, local_attempts, iteration_cap, stream);
@@ -876,11 +1061,14 @@ int rts_pci_control(const RtsParams *p, const RtsBuffers *b, int sync_mode,
                     unsigned long long cond_handle, int local_attempts, int iteration_cap,
                     void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
-    rts_note_launch(), k_control<<<1, 1, 0, s>>>(*p, *b, sync_mode, cond_handle, local_attempts,
-                                                 iteration_cap);
+    int n_part = (p->n_fluid + 255) / 256;
+    if (n_part > kRedBlocks) n_part = kRedBlocks;
+    if (n_part < 1) n_part = 1;
+    rts_note_launch(), k_control<<<1, 32, 0, s>>>(*p, *b, sync_mode, cond_handle, local_attempts,
+                                                  iteration_cap, n_part);
     RTS_LAUNCH_CHECK();
     if (!sync_mode) {
-        rts_note_launch(), k_snapshot<<<rts_blocks(p->n_fluid, 256), 256, 0, s>>>(*p, *b, -1);
+        rts_note_launch(), k_snapshot<<<rts_blocks(p->n_fluid, 256, 148 * 4), 256, 0, s>>>(*p, *b, -1);
         RTS_LAUNCH_CHECK();
     }
     return 0;
@@ -900,8 +1088,7 @@ int rts_pci_minor_head(const RtsParams *p, const RtsBuffers *b, int minor, void 
 int rts_pci_minor_tail(const RtsParams *p, const RtsBuffers *b, int minor, int last,
                        void *stream) {
     int rc;
-    if ((rc = rts_pci_sob(p, b, stream))) return rc;
-    if ((rc = rts_pci_integrate(p, b, 1, stream))) return rc;
+    if ((rc = rts_pci_integrate(p, b, 1, stream))) return rc;  // includes S_ob / x* refresh
     if (!last) {
         if ((rc = rts_block_maxima(p, b, 1, stream))) return rc;
         if ((rc = rts_block_levels(p, b, 2, stream))) return rc;

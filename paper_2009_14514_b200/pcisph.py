@@ -186,6 +186,8 @@ class PcisphSolver(_DeviceSolver):
         A.alloc("snap_p", (n1,), f32, 0)
         A.alloc("snap_fp", (n1, 3), f32, 0)
         A.alloc("slot_of", (n1,), torch.int32, 0)
+        A.alloc("se_stamp", (self.grid.n_cells,), torch.int32, 0)
+        A.alloc("near_stamp", (self.grid.n_cells,), torch.int32, 0)
         self._ctl = A.alloc("ctl", (ctypes.sizeof(N.RtsControl),), torch.uint8, 0)
         self._ctl_host = torch.zeros(ctypes.sizeof(N.RtsControl), dtype=torch.uint8).pin_memory()
         self.use_graphs = use_graphs
@@ -274,8 +276,6 @@ class PcisphSolver(_DeviceSolver):
                 self._call("rts_pci_sets", -1, sync_mode)
                 self._call("rts_pci_density")
                 self._call("rts_pci_se_reduce", int(not sync_mode))
-                if not sync_mode:
-                    self._call("rts_pci_observed", 1)
                 self._call("rts_pci_pforces")
                 self._call("rts_pci_control", sync_mode, 0, self.local_attempts,
                            self.iteration_cap)
@@ -458,7 +458,6 @@ class PcisphSolver(_DeviceSolver):
                 if self._ktimes is None:
                     self._call("rts_pci_minor_tail", j, int(j == n_minor - 1))
                 else:
-                    self._call("rts_pci_sob")
                     self._call("rts_pci_integrate", 1)
                     if j != n_minor - 1:
                         self._call("rts_block_maxima", 1)

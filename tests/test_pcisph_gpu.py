@@ -86,10 +86,10 @@ def test_first_iteration_parity_from_common_state():
     dev._call("rts_pci_sets", 0b11110, 0)
     dev._call("rts_pci_density")
     dev._call("rts_pci_se_reduce", 1)
-    dev._call("rts_pci_observed", 1)
     dev._call("rts_pci_pforces")
-    dev._call("rts_pci_sob")
     c = dev._read()
+    dev._call("rts_pci_control", 0, 0, dev.local_attempts, dev.iteration_cap)
+    dev._call("rts_pci_sob")
     assert int(c.n_pred) == pred.size
     assert rel_err(dev.host("rho_star")[pred], orc.rho_star[pred]) <= TOL
     assert np.abs(dev.host("err")[pred] - orc.err[pred]).max() <= TOL
