@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define RTS_ABI_VERSION 9
+#define RTS_ABI_VERSION 10
 
 /* err_flags bits */
 #define RTS_ERR_ESCAPED   0x1u  /* fluid left the padded grid or non-finite (grid.py:268-273) */
@@ -71,7 +71,8 @@ typedef struct RtsParams {
     int32_t apply_correction;
     int32_t rts;           /* 1 = regional mode, 0 = synchronous baseline */
     int32_t n_sms;         /* grid sizing for persistent kernels */
-    int32_t pad0, pad1;
+    int32_t n_regions;     /* region ids 1..n_regions (pcisph.py:294) */
+    int32_t pad1;
 } RtsParams;
 
 /* Device-side counters; copied to the host once per step. */
@@ -89,7 +90,7 @@ typedef struct RtsCounters {
     double   sum_rho;          /* PCISPH: sum of rho* over fluid */
     double   max_err;          /* PCISPH: max err over fluid */
     int32_t  any_se;           /* PCISPH: any particle in S_e */
-    int32_t  n_work;           /* blocks in the tiled work list */
+    int32_t  lists_all;        /* PCISPH: this iteration's pred = force = all fluid (no lists) */
     double   reserved[8];
 } RtsCounters;
 

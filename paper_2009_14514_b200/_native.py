@@ -12,7 +12,7 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "librtssph.so")
-ABI_VERSION = 9
+ABI_VERSION = 10
 
 _c = ctypes
 _D = _c.c_double
@@ -30,7 +30,7 @@ class RtsParams(_c.Structure):
         ("betas", _D * 8), ("eta_max", _D), ("eta_avg", _D), ("rho_T", _D), ("delta", _D),
         ("dims", _I * 3), ("n_cells", _I), ("n_fluid", _I), ("n_bound", _I), ("n_bcells", _I),
         ("width", _I), ("n_max", _I), ("use_sound", _I), ("pin_region", _I),
-        ("apply_correction", _I), ("rts", _I), ("n_sms", _I), ("pad0", _I), ("pad1", _I),
+        ("apply_correction", _I), ("rts", _I), ("n_sms", _I), ("n_regions", _I), ("pad1", _I),
     ]
 
 
@@ -39,7 +39,7 @@ class RtsCounters(_c.Structure):
         ("err_flags", _c.c_uint32), ("n_escaped", _I), ("first_escaped", _I), ("n_compute", _I),
         ("overflow", _c.c_int64), ("n_sorted", _I), ("n_pred", _I), ("n_force", _I),
         ("n_list", _I), ("fmax_bits", _c.c_uint64), ("sum_rho", _D), ("max_err", _D),
-        ("any_se", _I), ("n_work", _I), ("reserved", _D * 8),
+        ("any_se", _I), ("lists_all", _I), ("reserved", _D * 8),
     ]
 
 

@@ -26,7 +26,7 @@ using namespace rts;
 namespace {
 
 constexpr int kThreads = 128;
-constexpr int kRedBlocks = 1024;  // fixed partial count -> deterministic sums
+constexpr int kRedBlocks = 296;  // fixed partial count -> deterministic sums
 
 __constant__ int kValidity[5] = {0, 1, 2, 4, 4};  // pcisph.py:66
 
@@ -292,21 +292,27 @@ __global__ void __launch_bounds__(256) k_sets(const __grid_constant__ RtsParams 
     if (row_mask < 0) row_mask = b.ctl->row_mask;
     const int gen = b.ctl ? b.ctl->stamp : 0;
     const int nf = p.n_fluid;
+    // every region scheduled (or a synchronous baseline): pred = force = all
+    // fluid; the pair kernels then walk 0..nf-1 directly (no lists)
+    const int all_mask = ((1 << (p.n_regions + 1)) - 1) & ~1;
+    if (all_pred || (p.n_regions > 0 && (row_mask & all_mask) == all_mask)) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            b.ctr->n_pred = nf;
+            b.ctr->n_force = nf;
+            b.ctr->lists_all = 1;
+        }
+        return;
+    }
     const int stride = gridDim.x * blockDim.x;
     for (int base = blockIdx.x * blockDim.x; base < nf; base += stride) {
         const int i = base + threadIdx.x;
         bool pred = false, force = false;
         if (i < nf) {
-            if (all_pred) {
-                pred = force = true;
-            } else {
-                const bool sob = observed_block(b, b.fluid_cells[i], gen);
-                b.in_sob[i] = sob;
-                const bool turn = (row_mask >> b.region[i]) & 1;
-                const bool se = b.in_se[i] != 0;
-                pred = turn || se || sob;
-                force = turn || se;
-            }
+            const bool sob = observed_block(b, b.fluid_cells[i], gen);
+            const bool turn = (row_mask >> b.region[i]) & 1;
+            const bool se = b.in_se[i] != 0;
+            pred = turn || se || sob;
+            force = turn || se;
             b.pflag[i] = force;
         }
         block_append2<256>(pred, i, b.active, &b.ctr->n_pred, force, i, b.list2, &b.ctr->n_force);
@@ -371,7 +377,7 @@ RTS_DEV void density_one(const RtsParams &p, const RtsBuffers &b, int i, int lan
         b.rho[i] = (float)rho;
         b.err[i] = diff > 0.0 ? xdiv(diff, p.rho0) : 0.0;
         if (!isfinite(rho)) atomicOr(&b.ctr->err_flags, RTS_ERR_NONFINITE);
-        if (b.pflag[i]) {
+        if (b.ctr->lists_all || b.pflag[i]) {
             double pr = xadd((double)b.pres[i], xmul(p.delta, diff));
             pr = pr > 0.0 ? pr : 0.0;
             b.pres[i] = (float)pr;
@@ -384,15 +390,16 @@ __global__ void __launch_bounds__(kThreads) k_density(const __grid_constant__ Rt
                                                       RtsBuffers b) {
     RTS_ITER_GUARD();
     const int n = b.ctr->n_pred;
+    const bool all = b.ctr->lists_all;
     const int nthreads = gridDim.x * blockDim.x;
     const int tid = blockIdx.x * blockDim.x + threadIdx.x;
     if ((long long)n * kPG <= nthreads) {
         const int wl = threadIdx.x & 31, lane = wl & (kPG - 1);
         const unsigned gmask = ((1u << kPG) - 1u) << (wl & ~(kPG - 1));
         for (int t = tid / kPG; t < n; t += nthreads / kPG)
-            density_one<kPG>(p, b, b.active[t], lane, gmask);
+            density_one<kPG>(p, b, all ? t : b.active[t], lane, gmask);
     } else {
-        for (int t = tid; t < n; t += nthreads) density_one<1>(p, b, b.active[t], 0, 0u);
+        for (int t = tid; t < n; t += nthreads) density_one<1>(p, b, all ? t : b.active[t], 0, 0u);
     }
 }
 
@@ -567,15 +574,16 @@ __global__ void __launch_bounds__(kThreads) k_pforces(const __grid_constant__ Rt
                                                       RtsBuffers b) {
     RTS_ITER_GUARD();
     const int n = b.ctr->n_force;
+    const bool all = b.ctr->lists_all;
     const int nthreads = gridDim.x * blockDim.x;
     const int tid = blockIdx.x * blockDim.x + threadIdx.x;
     if ((long long)n * kPG <= nthreads) {
         const int wl = threadIdx.x & 31, lane = wl & (kPG - 1);
         const unsigned gmask = ((1u << kPG) - 1u) << (wl & ~(kPG - 1));
         for (int t = tid / kPG; t < n; t += nthreads / kPG)
-            pforce_one<kPG>(p, b, b.list2[t], lane, gmask);
+            pforce_one<kPG>(p, b, all ? t : b.list2[t], lane, gmask);
     } else {
-        for (int t = tid; t < n; t += nthreads) pforce_one<1>(p, b, b.list2[t], 0, 0u);
+        for (int t = tid; t < n; t += nthreads) pforce_one<1>(p, b, all ? t : b.list2[t], 0, 0u);
     }
 }
 
@@ -767,6 +775,7 @@ __global__ void k_minor_begin(RtsBuffers b, int minor, int sync_mode) {
     c->prev_force = 0;
     b.ctr->n_pred = 0;
     b.ctr->n_force = 0;
+    b.ctr->lists_all = 0;
     b.ctr->max_err = 0.0;
     b.ctr->any_se = 0;
     if (!sync_mode) {
@@ -865,8 +874,10 @@ __global__ void k_control(const __grid_constant__ RtsParams p, RtsBuffers b, int
         // hand-over to the next iteration: motion list length, fresh counts,
         // the S_e generation just written by k_se_reduce becomes current
         c->prev_force = ctr->n_force;
+        if (ctr->lists_all) c->motion_all = 1;  // the force set was every particle
         c->stamp += 1;
         if (!done) {
+            ctr->lists_all = 0;
             ctr->n_pred = 0;
             ctr->n_force = 0;
             ctr->max_err = 0.0;

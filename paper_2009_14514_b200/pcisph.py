@@ -195,6 +195,7 @@ class PcisphSolver(_DeviceSolver):
         self._force_total = 0
         p = self.params
         p.dt_base = self.dt
+        p.n_regions = n_regions
         p.use_sound = 0
         p.rts = 1 if mode == "rts" else 0
         stream = torch.cuda.current_stream(self.device)
