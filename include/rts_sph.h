@@ -319,6 +319,9 @@ int rts_wcsph_density(const RtsParams *p, const RtsBuffers *b, void *stream);
 int rts_wcsph_forces(const RtsParams *p, const RtsBuffers *b, void *stream);
 /* Predictor for all, corrector for active, clamp (wcsph.py:299-319). */
 int rts_wcsph_integrate(const RtsParams *p, const RtsBuffers *b, void *stream);
+/* One whole RTS-WCSPH step as a CUDA graph (launch with rts_graph_launch,
+ * destroy with rts_graph_destroy); NULL + *err on failure. */
+void *rts_wcsph_graph_create(const RtsParams *p, const RtsBuffers *b, int *err);
 /* max |F| over fluid into ctr->fmax_bits (cfl_bound, wcsph.py:182-189). */
 int rts_force_max(const RtsParams *p, const RtsBuffers *b, void *stream);
 

@@ -156,6 +156,8 @@ def load(path: str = LIB_PATH):
     lib.rts_pci_graph_create.argtypes = [_PP, _PB, _c.c_int, _c.c_int, _c.c_int, _c.c_int,
                                          _c.POINTER(_c.c_int)]
     lib.rts_pci_graph_create.restype = _c.c_void_p
+    lib.rts_wcsph_graph_create.argtypes = [_PP, _PB, _c.POINTER(_c.c_int)]
+    lib.rts_wcsph_graph_create.restype = _c.c_void_p
     lib.rts_graph_destroy.argtypes = [_P]
     lib.rts_graph_destroy.restype = None
     if lib.rts_abi_version() != ABI_VERSION:

@@ -68,6 +68,39 @@ RTS_DEV double norm3(float x, float y, float z) {
     return xsqrt(dist2((double)x, (double)y, (double)z));
 }
 
+// ---- exact neighbour membership ------------------------------------------
+// The reference keeps j iff fp64 ((dx^2 + dy^2) + dz^2) < h^2 (grid.py:140-144).
+// Candidates are first classified in fp32 with a +-1e-5 relative band around
+// h^2 (fp32 rounding of r^2 is < 3e-7 relative), only in-band candidates take
+// the exact fp64 test, kept out of line so the compiler cannot speculate the
+// fp64 work into every candidate test.
+static __device__ __noinline__ bool exact_neighbour(double h2, float fxi, float fyi, float fzi,
+                                                    float ox, float oy, float oz) {
+    return dist2(xsub((double)fxi, (double)ox), xsub((double)fyi, (double)oy),
+                 xsub((double)fzi, (double)oz)) < h2;
+}
+
+struct Band {
+    float lo, hi;
+    double h2;
+};
+
+RTS_DEV Band make_band(double h2) {
+    Band b;
+    b.lo = (float)(h2 * (1.0 - 1e-5));
+    b.hi = (float)(h2 * (1.0 + 1e-5));
+    b.h2 = h2;
+    return b;
+}
+
+RTS_DEV bool in_support(const Band &bd, float fxi, float fyi, float fzi, float4 o) {
+    const float ex = fxi - o.x, ey = fyi - o.y, ez = fzi - o.z;
+    const float r2f = __fadd_rn(__fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey)), __fmul_rn(ez, ez));
+    if (r2f > bd.hi) return false;
+    if (r2f < bd.lo) return true;
+    return exact_neighbour(bd.h2, fxi, fyi, fzi, o.x, o.y, o.z);
+}
+
 // max of non-negative doubles via their bit patterns (monotone for >= 0)
 RTS_DEV void atomic_max_pos(double *addr, double v) {
     if (v > 0.0)  // NaN and 0 never raise a maximum (matches `if v > out[c]`)
@@ -143,6 +176,12 @@ RTS_DEV int warp_count_add(bool pred, int *count) {
 
 // kernel-launch counter (reported by bench.py as gpu_launches)
 extern "C" void rts_note_launch(void);
+
+// owned CUDA graph (rts_pci_graph_create / rts_wcsph_graph_create)
+struct RtsGraph {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+};
 
 // launch helpers
 static inline int rts_blocks(long long n, int threads, int cap = 148 * 32) {

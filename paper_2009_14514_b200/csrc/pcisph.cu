@@ -123,15 +123,6 @@ RTS_DEV RefreshConsts refresh_consts(const RtsParams &p) {
     return k;
 }
 
-// exact fp64 membership for the rare candidates inside the fp32 band; kept
-// out of line so the compiler cannot if-convert (speculate) the fp64 work
-// into every candidate test
-__device__ __noinline__ bool exact_neighbour(double h2, float fxi, float fyi, float fzi, float ox,
-                                             float oy, float oz) {
-    return dist2(xsub((double)fxi, (double)ox), xsub((double)fyi, (double)oy),
-                 xsub((double)fzi, (double)oz)) < h2;
-}
-
 RTS_DEV bool is_neighbour(const RefreshConsts &k, const RtsParams &p, float fxi, float fyi,
                           float fzi, float4 o) {
     const float ex = fxi - o.x, ey = fyi - o.y, ez = fzi - o.z;
@@ -1109,11 +1100,6 @@ int rts_pci_minor_tail(const RtsParams *p, const RtsBuffers *b, int minor, int l
 }
 
 // ---- CUDA graphs -----------------------------------------------------------
-struct RtsGraph {
-    cudaGraph_t graph = nullptr;
-    cudaGraphExec_t exec = nullptr;
-};
-
 static int add_while_loop(cudaStream_t cs, const RtsParams *p, const RtsBuffers *b, int sync_mode,
                           int local_attempts, int iteration_cap) {
     cudaStreamCaptureStatus st;

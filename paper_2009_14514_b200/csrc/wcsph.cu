@@ -78,45 +78,79 @@ __device__ __forceinline__ int block_spans(const RtsParams &p, const int *starts
     return n;
 }
 
-// fp32 pre-test with a margin that can only admit, never reject, a true
-// neighbour; the fp64 test below decides membership exactly.
-__device__ __forceinline__ bool maybe_near(float4 a, float4 q, float h2_loose) {
-    const float dx = a.x - q.x, dy = a.y - q.y, dz = a.z - q.z;
-    return __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz)) <=
-           h2_loose;
+// ---- pair kernels: two passes per active particle ----------------------
+// Pass 1 walks the nine CSR spans with four float4 candidates in flight and
+// collects the slots of true neighbours (exact reference membership, see
+// in_support) into a per-thread shared-memory list, in reference order.
+// Pass 2 evaluates the fp64 pair terms over that list without divergence
+// and sums them sequentially in that order, so rho / force equal the
+// reference's fp64 values from a common state (up to the fp32 store).
+constexpr int kHitCap = 64;  // list entries per thread (overflow -> direct path)
+
+RTS_DEV int collect_hits(const RtsParams &p, const RtsBuffers &b, const float4 *cpos, int cell,
+                         float4 a, const Band &bd, int *hits, int *n_all) {
+    Span sp[9];
+    const int ns = block_spans(p, b.starts, cell, sp);
+    int n = 0;
+    for (int s = 0; s < ns; ++s) {
+        const int k0 = sp[s].k0, k1 = sp[s].k1;
+        for (int kb = k0; kb < k1; kb += 4) {
+            float4 ob[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) ob[u] = cpos[min(kb + u, k1 - 1)];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (kb + u < k1 && in_support(bd, a.x, a.y, a.z, ob[u])) {
+                    if (n < kHitCap) hits[n * kThreads] = kb + u;
+                    ++n;
+                }
+            }
+        }
+    }
+    *n_all = n;
+    return min(n, kHitCap);
 }
 
 // wcsph.py:45-60 over the on-the-fly search of grid.py:88-152
 __global__ void __launch_bounds__(kThreads) k_density(const __grid_constant__ RtsParams p,
                                                       RtsBuffers b) {
     if (fatal(b.ctr)) return;
+    __shared__ int s_hits[kHitCap * kThreads];
+    int *hits = s_hits + threadIdx.x;
     const int n_act = b.ctr->n_compute;
     const float4 *cpos = reinterpret_cast<const float4 *>(b.cpos);
-    const float h2_loose = (float)(p.h2 * 1.00001);
+    const Band bd = make_band(p.h2);
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n_act; t += gridDim.x * blockDim.x) {
         const int k = b.active[t];
         const int j = b.order[k];
         const float4 a = cpos[k];
         const double xi = a.x, yi = a.y, zi = a.z;
-        Span sp[9];
-        const int ns = block_spans(p, b.starts, b.fluid_cells[j], sp);
+        int n_all;
+        const int nh = collect_hits(p, b, cpos, b.fluid_cells[j], a, bd, hits, &n_all);
         double acc = 0.0;
-        int n = 0;
-        for (int s = 0; s < ns; ++s) {
-            for (int q = sp[s].k0; q < sp[s].k1; ++q) {
-                const float4 o = cpos[q];
-                if (!maybe_near(a, o, h2_loose)) continue;
-                const double r2 = dist2(xsub(xi, (double)o.x), xsub(yi, (double)o.y),
-                                        xsub(zi, (double)o.z));
-                if (r2 < p.h2) {
-                    acc = xadd(acc, poly6(r2, p.h2, p.c_poly6));
-                    ++n;
-                }
+        if (n_all <= kHitCap) {
+            for (int q = 0; q < nh; ++q) {
+                const float4 o = cpos[hits[q * kThreads]];
+                acc = xadd(acc, poly6(dist2(xsub(xi, (double)o.x), xsub(yi, (double)o.y),
+                                            xsub(zi, (double)o.z)),
+                                      p.h2, p.c_poly6));
             }
+        } else {  // crowded neighbourhood: direct pass over the spans
+            Span sp[9];
+            const int ns = block_spans(p, b.starts, b.fluid_cells[j], sp);
+            for (int s = 0; s < ns; ++s)
+                for (int q = sp[s].k0; q < sp[s].k1; ++q)
+                    if (in_support(bd, a.x, a.y, a.z, cpos[q])) {
+                        const float4 o = cpos[q];
+                        acc = xadd(acc, poly6(dist2(xsub(xi, (double)o.x), xsub(yi, (double)o.y),
+                                                    xsub(zi, (double)o.z)),
+                                              p.h2, p.c_poly6));
+                    }
         }
-        if (n > p.width) {
+        if (n_all > p.width) {
             atomicOr(&b.ctr->err_flags, RTS_ERR_OVERFLOW);
-            atomicAdd((unsigned long long *)&b.ctr->overflow, (unsigned long long)(n - p.width));
+            atomicAdd((unsigned long long *)&b.ctr->overflow,
+                      (unsigned long long)(n_all - p.width));
         }
         const double rho = xmul(p.mass, acc);
         const double ratio = xdiv(rho, p.rho0);
@@ -134,14 +168,43 @@ __global__ void __launch_bounds__(kThreads) k_density(const __grid_constant__ Rt
     }
 }
 
+// one pair term of _forces (wcsph.py:75-101), fp64 in the reference's order
+RTS_DEV void force_pair(const RtsParams &p, double xi, double yi, double zi, float4 va,
+                        double rho_i, double term_i, double wall_term, double m2, double mum2,
+                        float4 o, float4 vo, double &fx, double &fy, double &fz) {
+    const double dx = xsub(xi, (double)o.x), dy = xsub(yi, (double)o.y),
+                 dz = xsub(zi, (double)o.z);
+    const double r = xsqrt(dist2(dx, dy, dz));
+    if (r >= p.h) return;
+    if (o.w >= 0.0f) {  // fluid neighbour
+        const double rho_j = vo.w;
+        const double term = xadd(term_i, xdiv((double)o.w, xmul(rho_j, rho_j)));
+        const double sc = xmul(xmul(m2, term), spiky(r, p.h, p.c_spiky));
+        fx = xsub(fx, xmul(sc, dx));
+        fy = xsub(fy, xmul(sc, dy));
+        fz = xsub(fz, xmul(sc, dz));
+        const double lap = xdiv(xmul(mum2, visc_lap(r, p.h, p.c_visc)), xmul(rho_i, rho_j));
+        fx = xadd(fx, xmul(lap, xsub((double)vo.x, (double)va.x)));
+        fy = xadd(fy, xmul(lap, xsub((double)vo.y, (double)va.y)));
+        fz = xadd(fz, xmul(lap, xsub((double)vo.z, (double)va.z)));
+    } else {  // static wall sample, mirrored pressure
+        const double sc = xmul(xmul(m2, wall_term), spiky(r, p.h, p.c_spiky));
+        fx = xsub(fx, xmul(sc, dx));
+        fy = xsub(fy, xmul(sc, dy));
+        fz = xsub(fz, xmul(sc, dz));
+    }
+}
+
 // wcsph.py:288-296 + _forces wcsph.py:63-105
 __global__ void __launch_bounds__(kThreads) k_forces(const __grid_constant__ RtsParams p,
                                                      RtsBuffers b) {
     if (fatal(b.ctr)) return;
+    __shared__ int s_hits[kHitCap * kThreads];
+    int *hits = s_hits + threadIdx.x;
     const int n_act = b.ctr->n_compute;
     const float4 *cpos = reinterpret_cast<const float4 *>(b.cpos);
     const float4 *cvel = reinterpret_cast<const float4 *>(b.cvel);
-    const float h2_loose = (float)(p.h2 * 1.00001);
+    const Band bd = make_band(p.h2);
     const double m2 = xmul(p.mass, p.mass);
     const double inv_rho0_sq = xdiv(1.0, xmul(p.rho0, p.rho0));
     const double mum2 = xmul(p.mu, m2);
@@ -154,40 +217,24 @@ __global__ void __launch_bounds__(kThreads) k_forces(const __grid_constant__ Rts
         const double rho_i = va.w, p_i = a.w;
         const double term_i = xdiv(p_i, xmul(rho_i, rho_i));
         const double wall_term = xadd(term_i, xmul(p_i, inv_rho0_sq));
-        Span sp[9];
-        const int ns = block_spans(p, b.starts, b.fluid_cells[j], sp);
+        int n_all;
+        const int nh = collect_hits(p, b, cpos, b.fluid_cells[j], a, bd, hits, &n_all);
         double fx = 0.0, fy = 0.0, fz = 0.0;
-        for (int s = 0; s < ns; ++s) {
-            for (int q = sp[s].k0; q < sp[s].k1; ++q) {
-                if (q == k) continue;
-                const float4 o = cpos[q];
-                if (!maybe_near(a, o, h2_loose)) continue;
-                const double dx = xsub(xi, (double)o.x), dy = xsub(yi, (double)o.y),
-                             dz = xsub(zi, (double)o.z);
-                const double r2 = dist2(dx, dy, dz);
-                if (!(r2 < p.h2)) continue;
-                const double r = xsqrt(r2);
-                if (r >= p.h) continue;
-                if (o.w >= 0.0f) {  // fluid neighbour
-                    const float4 vo = cvel[q];
-                    const double rho_j = vo.w;
-                    const double term = xadd(term_i, xdiv((double)o.w, xmul(rho_j, rho_j)));
-                    const double sc = xmul(xmul(m2, term), spiky(r, p.h, p.c_spiky));
-                    fx = xsub(fx, xmul(sc, dx));
-                    fy = xsub(fy, xmul(sc, dy));
-                    fz = xsub(fz, xmul(sc, dz));
-                    const double lap =
-                        xdiv(xmul(mum2, visc_lap(r, p.h, p.c_visc)), xmul(rho_i, rho_j));
-                    fx = xadd(fx, xmul(lap, xsub((double)vo.x, (double)va.x)));
-                    fy = xadd(fy, xmul(lap, xsub((double)vo.y, (double)va.y)));
-                    fz = xadd(fz, xmul(lap, xsub((double)vo.z, (double)va.z)));
-                } else {  // static wall sample, mirrored pressure
-                    const double sc = xmul(xmul(m2, wall_term), spiky(r, p.h, p.c_spiky));
-                    fx = xsub(fx, xmul(sc, dx));
-                    fy = xsub(fy, xmul(sc, dy));
-                    fz = xsub(fz, xmul(sc, dz));
-                }
+        if (n_all <= kHitCap) {
+            for (int q = 0; q < nh; ++q) {
+                const int kq = hits[q * kThreads];
+                if (kq == k) continue;
+                force_pair(p, xi, yi, zi, va, rho_i, term_i, wall_term, m2, mum2, cpos[kq],
+                           cvel[kq], fx, fy, fz);
             }
+        } else {
+            Span sp[9];
+            const int ns = block_spans(p, b.starts, b.fluid_cells[j], sp);
+            for (int s = 0; s < ns; ++s)
+                for (int q = sp[s].k0; q < sp[s].k1; ++q)
+                    if (q != k && in_support(bd, a.x, a.y, a.z, cpos[q]))
+                        force_pair(p, xi, yi, zi, va, rho_i, term_i, wall_term, m2, mum2, cpos[q],
+                                   cvel[q], fx, fy, fz);
         }
         fx = xadd(fx, xmul(p.mass, p.gravity[0]));
         fy = xadd(fy, xmul(p.mass, p.gravity[1]));
@@ -279,6 +326,45 @@ int rts_wcsph_integrate(const RtsParams *p, const RtsBuffers *b, void *stream) {
     rts_note_launch(), k_integrate<<<rts_blocks(p->n_fluid, 256), 256, 0, s>>>(*p, *b);
     RTS_LAUNCH_CHECK();
     return 0;
+}
+
+// One RTS-WCSPH step (wcsph.py:199-233) captured as a CUDA graph: counters
+// reset, rebuild, levels, propagate, density, forces, integrate.
+void *rts_wcsph_graph_create(const RtsParams *p, const RtsBuffers *b, int *err) {
+    *err = 0;
+    cudaStream_t cs;
+    cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed);
+    if (e != cudaSuccess) { *err = (int)e; cudaStreamDestroy(cs); return nullptr; }
+    int rc = 0;
+    do {
+        if ((rc = rts_counters_reset(b, cs))) break;
+        if ((rc = rts_grid_keys(p, b, p->rts, 0, cs))) break;
+        if ((rc = rts_grid_sort(p, b, cs))) break;
+        if (p->rts && (rc = rts_block_levels(p, b, 0, cs))) break;
+        if ((rc = rts_wcsph_propagate(p, b, cs))) break;
+        if ((rc = rts_wcsph_density(p, b, cs))) break;
+        if ((rc = rts_wcsph_forces(p, b, cs))) break;
+        rc = rts_wcsph_integrate(p, b, cs);
+    } while (0);
+    cudaGraph_t g = nullptr;
+    e = cudaStreamEndCapture(cs, &g);
+    cudaStreamDestroy(cs);
+    if (rc || e != cudaSuccess) {
+        *err = rc ? rc : (int)e;
+        if (g) cudaGraphDestroy(g);
+        return nullptr;
+    }
+    RtsGraph *rg = new RtsGraph;
+    rg->graph = g;
+    e = cudaGraphInstantiate(&rg->exec, g, 0);
+    if (e != cudaSuccess) {
+        *err = (int)e;
+        cudaGraphDestroy(g);
+        delete rg;
+        return nullptr;
+    }
+    return rg;
 }
 
 }  // extern "C"

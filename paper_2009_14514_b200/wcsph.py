@@ -160,7 +160,7 @@ class WcsphSolver(_DeviceSolver):
     def __init__(self, scene: Scene, mode: str = "rts", dt_cap: float | None = None,
                  pin_region: int | None = None, apply_correction: bool = True,
                  track_rho_variance: bool = False, audit_neighbors: bool = False,
-                 n_regions: int = 4, device="cuda"):
+                 n_regions: int = 4, device="cuda", use_graphs: bool = True):
         if mode not in self.mode_names:
             raise ValueError(f"unknown wcsph mode {mode!r}")
         self.mode = mode
@@ -195,6 +195,31 @@ class WcsphSolver(_DeviceSolver):
         self.region = A.alloc("region", (max(nf, 1),), torch.int8, 1)[:nf]
         self.compute = A.alloc("compute", (max(nf, 1),), torch.bool, True)[:nf]
         self._missed_last = 0
+        self.use_graphs = use_graphs
+        self._graphs: dict = {}
+
+    def __del__(self):
+        for g in getattr(self, "_graphs", {}).values():
+            try:
+                N.load().rts_graph_destroy(g)
+            except Exception:  # pragma: no cover
+                pass
+
+    def _graph(self):
+        import ctypes
+        key = bytes(self.params)
+        g = self._graphs.get(key)
+        if g is None:
+            if len(self._graphs) >= 8:
+                for old in self._graphs.values():
+                    N.load().rts_graph_destroy(old)
+                self._graphs.clear()
+            err = ctypes.c_int(0)
+            g = N.load().rts_wcsph_graph_create(self.params, self.arena.buf, ctypes.byref(err))
+            if not g:
+                raise N.NativeError(f"rts_wcsph_graph_create failed with cudaError {err.value}")
+            self._graphs[key] = g
+        return g
 
     # ------------------------------------------------------------------
     def cfl_bound(self) -> float:
@@ -250,13 +275,20 @@ class WcsphSolver(_DeviceSolver):
         p.dt = dt
         p.pin_region = int(self.pin_region or 0)
         p.apply_correction = int(bool(self.apply_correction))
-        buf = self.arena.buf
         stream = torch.cuda.current_stream(self.device)
-        s = stream.cuda_stream
         tm = self.timer
+        rts = self.mode == "rts"
+        if self.use_graphs and rts and self._ktimes is None:  # baseline dt varies per step
+            tm.start(stream)
+            N.call("rts_graph_launch", self._graph(), stream.cuda_stream)
+            tm.mark("physics", stream)
+            if not read:
+                return None
+            c = self.counters.read(stream)
+            self.grid.n_sorted = int(c.n_sorted)
+            return c
         self.counters.reset(stream)
         tm.start(stream)
-        rts = self.mode == "rts"
         self.grid.launch_rebuild(p, stream, want_maxima=rts)
         tm.mark("neighbor", stream)
         if rts:

@@ -42,9 +42,13 @@ def test_grid_rebuild_bit_exact():
     assert np.array_equal(_np(dev.grid.boundary_active), orc.grid.boundary_active)
 
 
+@pytest.mark.parametrize("graphs", [True, False])
 @pytest.mark.parametrize("mode", ["rts", "baseline"])
-def test_one_step_parity_from_common_state(mode):
-    dev, orc = _pair(tiny_tank(), mode=mode)
+def test_one_step_parity_from_common_state(mode, graphs):
+    from oracle.sph import OracleWcsph
+    from paper_2009_14514_b200 import WcsphSolver
+    dev = WcsphSolver(tiny_tank(), mode=mode, use_graphs=graphs)
+    orc = OracleWcsph(tiny_tank(), mode=mode)
     apply_jitter(dev, orc)
     worst = {}
     for step in range(12):
