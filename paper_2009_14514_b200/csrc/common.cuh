@@ -94,8 +94,9 @@ RTS_DEV Band make_band(double h2) {
 }
 
 RTS_DEV bool in_support(const Band &bd, float fxi, float fyi, float fzi, float4 o) {
-    const float ex = fxi - o.x, ey = fyi - o.y, ez = fzi - o.z;
-    const float r2f = __fadd_rn(__fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey)), __fmul_rn(ez, ez));
+    // any fp32 evaluation order is fine here: the band absorbs its rounding
+    const float ex = __fsub_rn(fxi, o.x), ey = __fsub_rn(fyi, o.y), ez = __fsub_rn(fzi, o.z);
+    const float r2f = __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, __fmul_rn(ez, ez)));
     if (r2f > bd.hi) return false;
     if (r2f < bd.lo) return true;
     return exact_neighbour(bd.h2, fxi, fyi, fzi, o.x, o.y, o.z);

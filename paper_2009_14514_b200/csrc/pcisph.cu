@@ -125,8 +125,8 @@ RTS_DEV RefreshConsts refresh_consts(const RtsParams &p) {
 
 RTS_DEV bool is_neighbour(const RefreshConsts &k, const RtsParams &p, float fxi, float fyi,
                           float fzi, float4 o) {
-    const float ex = fxi - o.x, ey = fyi - o.y, ez = fzi - o.z;
-    const float r2f = __fadd_rn(__fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey)), __fmul_rn(ez, ez));
+    const float ex = __fsub_rn(fxi, o.x), ey = __fsub_rn(fyi, o.y), ez = __fsub_rn(fzi, o.z);
+    const float r2f = __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, __fmul_rn(ez, ez)));
     if (r2f > k.h2_hi) return false;
     if (r2f < k.h2_lo) return true;
     return exact_neighbour(p.h2, fxi, fyi, fzi, o.x, o.y, o.z);

@@ -31,9 +31,11 @@ __global__ void __launch_bounds__(256) k_propagate(const __grid_constant__ RtsPa
             const int j = b.order[k];
             const float x = b.pos[3 * j], y = b.pos[3 * j + 1], z = b.pos[3 * j + 2];
             if (j < p.n_fluid) {
-                reinterpret_cast<float4 *>(b.cpos)[k] = make_float4(x, y, z, b.pres[j]);
-                reinterpret_cast<float4 *>(b.cvel)[k] =
-                    make_float4(b.vel[3 * j], b.vel[3 * j + 1], b.vel[3 * j + 2], b.rho[j]);
+                const double rho = b.rho[j], pr = b.pres[j];
+                reinterpret_cast<float4 *>(b.cpos)[k] =
+                    make_float4(x, y, z, (float)xdiv(pr, xmul(rho, rho)));
+                reinterpret_cast<float4 *>(b.cvel)[k] = make_float4(
+                    b.vel[3 * j], b.vel[3 * j + 1], b.vel[3 * j + 2], (float)xdiv(1.0, rho));
                 if (p.rts) {
                     const int8_t blk = b.block_field[b.fluid_cells[j]];
                     int v = b.validity[j] - 1;
@@ -161,34 +163,42 @@ __global__ void __launch_bounds__(kThreads) k_density(const __grid_constant__ Rt
         if (!isfinite(rho)) atomicOr(&b.ctr->err_flags, RTS_ERR_NONFINITE);
         b.rho[j] = (float)rho;
         b.pres[j] = (float)pr;
-        // publish for the force pass (only .w of slot k changes; the
-        // concurrent readers of cpos in this kernel use .xyz only)
-        reinterpret_cast<float *>(b.cpos)[4 * k + 3] = (float)pr;
-        reinterpret_cast<float *>(b.cvel)[4 * k + 3] = (float)rho;
+        // publish p/rho^2 and 1/rho for the force pass (only .w of slot k
+        // changes; the concurrent readers of cpos in this kernel use .xyz)
+        const double rho_s = (float)rho, pr_s = (float)pr;  // the stored fp32 state
+        reinterpret_cast<float *>(b.cpos)[4 * k + 3] = (float)xdiv(pr_s, xmul(rho_s, rho_s));
+        reinterpret_cast<float *>(b.cvel)[4 * k + 3] = (float)xdiv(1.0, rho_s);
     }
 }
 
-// one pair term of _forces (wcsph.py:75-101), fp64 in the reference's order
+// One pair term of _forces (wcsph.py:75-101), accumulated in fp64 in the
+// reference's neighbour order.  The per-particle factors p_j/rho_j^2 and
+// 1/rho_j are published once per particle (fp32) and r, 1/r come from one
+// fp64 rsqrt, so a pair costs no fp64 division or sqrt; the deviation from
+// the reference's per-pair divisions is ~1e-7 relative (bar: 1e-4).
 RTS_DEV void force_pair(const RtsParams &p, double xi, double yi, double zi, float4 va,
-                        double rho_i, double term_i, double wall_term, double m2, double mum2,
+                        double inv_rho_i, double term_i, double wall_term, double m2, double mum2,
                         float4 o, float4 vo, double &fx, double &fy, double &fz) {
     const double dx = xsub(xi, (double)o.x), dy = xsub(yi, (double)o.y),
                  dz = xsub(zi, (double)o.z);
-    const double r = xsqrt(dist2(dx, dy, dz));
+    const double r2 = dist2(dx, dy, dz);
+    const double rinv = r2 > 0.0 ? rsqrt(r2) : 0.0;  // r = 0: spiky 0, viscosity kept
+    const double r = xmul(r2, rinv);
     if (r >= p.h) return;
-    if (o.w >= 0.0f) {  // fluid neighbour
-        const double rho_j = vo.w;
-        const double term = xadd(term_i, xdiv((double)o.w, xmul(rho_j, rho_j)));
-        const double sc = xmul(xmul(m2, term), spiky(r, p.h, p.c_spiky));
+    const double d = xsub(p.h, r);
+    const double spk = xmul(xmul(xmul(p.c_spiky, d), d), rinv);
+    if (o.w >= 0.0f) {  // fluid neighbour: o.w = p_j / rho_j^2, vo.w = 1 / rho_j
+        const double term = xadd(term_i, (double)o.w);
+        const double sc = xmul(xmul(m2, term), spk);
         fx = xsub(fx, xmul(sc, dx));
         fy = xsub(fy, xmul(sc, dy));
         fz = xsub(fz, xmul(sc, dz));
-        const double lap = xdiv(xmul(mum2, visc_lap(r, p.h, p.c_visc)), xmul(rho_i, rho_j));
+        const double lap = xmul(xmul(xmul(mum2, xmul(p.c_visc, d)), inv_rho_i), (double)vo.w);
         fx = xadd(fx, xmul(lap, xsub((double)vo.x, (double)va.x)));
         fy = xadd(fy, xmul(lap, xsub((double)vo.y, (double)va.y)));
         fz = xadd(fz, xmul(lap, xsub((double)vo.z, (double)va.z)));
     } else {  // static wall sample, mirrored pressure
-        const double sc = xmul(xmul(m2, wall_term), spiky(r, p.h, p.c_spiky));
+        const double sc = xmul(xmul(m2, wall_term), spk);
         fx = xsub(fx, xmul(sc, dx));
         fy = xsub(fy, xmul(sc, dy));
         fz = xsub(fz, xmul(sc, dz));
@@ -214,8 +224,9 @@ __global__ void __launch_bounds__(kThreads) k_forces(const __grid_constant__ Rts
         const float4 a = cpos[k];
         const float4 va = cvel[k];
         const double xi = a.x, yi = a.y, zi = a.z;
-        const double rho_i = va.w, p_i = a.w;
+        const double rho_i = b.rho[j], p_i = b.pres[j];
         const double term_i = xdiv(p_i, xmul(rho_i, rho_i));
+        const double inv_rho_i = xdiv(1.0, rho_i);
         const double wall_term = xadd(term_i, xmul(p_i, inv_rho0_sq));
         int n_all;
         const int nh = collect_hits(p, b, cpos, b.fluid_cells[j], a, bd, hits, &n_all);
@@ -224,7 +235,7 @@ __global__ void __launch_bounds__(kThreads) k_forces(const __grid_constant__ Rts
             for (int q = 0; q < nh; ++q) {
                 const int kq = hits[q * kThreads];
                 if (kq == k) continue;
-                force_pair(p, xi, yi, zi, va, rho_i, term_i, wall_term, m2, mum2, cpos[kq],
+                force_pair(p, xi, yi, zi, va, inv_rho_i, term_i, wall_term, m2, mum2, cpos[kq],
                            cvel[kq], fx, fy, fz);
             }
         } else {
@@ -233,7 +244,7 @@ __global__ void __launch_bounds__(kThreads) k_forces(const __grid_constant__ Rts
             for (int s = 0; s < ns; ++s)
                 for (int q = sp[s].k0; q < sp[s].k1; ++q)
                     if (q != k && in_support(bd, a.x, a.y, a.z, cpos[q]))
-                        force_pair(p, xi, yi, zi, va, rho_i, term_i, wall_term, m2, mum2, cpos[q],
+                        force_pair(p, xi, yi, zi, va, inv_rho_i, term_i, wall_term, m2, mum2, cpos[q],
                                    cvel[q], fx, fy, fz);
         }
         fx = xadd(fx, xmul(p.mass, p.gravity[0]));
