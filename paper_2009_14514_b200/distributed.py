@@ -1,0 +1,261 @@
+"""Multi-GPU RTS-SPH by x-slab decomposition.
+
+One process per GPU (``torch.distributed``, NCCL over NVLink; gloo works for
+CPU tests).  The padded block grid of the whole scene (grid.py:223-244) is
+cut into x-slabs aligned to block faces; a rank owns the fluid particles
+whose block column lies in its slab.  Each step:
+
+1. **ghost exchange** -- every rank sends the full state of its particles in
+   the ``halo`` block columns next to each neighbour (2 for WCSPH: the
+   first band's densities need the second band's positions, and the first
+   band's smoothed levels need the second band's raw levels);
+2. **local step** -- the B200 solver runs on owned + ghost particles (sorted
+   by global id, so every within-block order -- and therefore every sum --
+   is the single-domain order) and the wall samples of the slab + halo; the
+   ghosts are recomputed redundantly and discarded, so no second exchange
+   is needed inside the step;
+3. **migration** -- owned particles whose block column left the slab are
+   sent to the new owner.
+
+Owned results are therefore bit-identical to the single-domain run
+(``tests/test_distributed_cpu.py`` checks this with gloo on CPU ranks, the
+GPU test with two processes on one device).  The only global reduction of
+RTS-WCSPH is none (the base step is global by construction); the baseline's
+CFL bound is an all-reduce MAX of |F|.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from .scene import Scene, seed_particles
+
+# per-particle WCSPH state carried by ghosts and migrants, in pack order
+WCSPH_FIELDS = (("pos", 3), ("vel", 3), ("acc", 3), ("acc_prev", 3), ("force", 3), ("rho", 1),
+                ("pres", 1), ("dt_since", 1), ("dt_corr", 1), ("validity", 1), ("region", 1),
+                ("compute", 1))
+WCSPH_WIDTH = 1 + sum(w for _, w in WCSPH_FIELDS)  # + global id
+
+
+@dataclass
+class SlabPartition:
+    """Block-aligned x-slabs of the padded grid of ``scene``."""
+
+    origin_x: float
+    inv_block: float
+    nx: int
+    world: int
+    halo: int
+
+    @classmethod
+    def for_scene(cls, scene: Scene, mode: str, world: int, halo: int = 2) -> "SlabPartition":
+        pad = scene.boundary_layers * scene.spacing
+        lo = scene.domain_min[0] - pad
+        hi = scene.domain_max[0] + pad
+        block = scene.block_size(mode)
+        nx = max(1, int(math.ceil((hi - lo) / block - 1e-12)))
+        return cls(origin_x=lo, inv_block=1.0 / block, nx=nx, world=world, halo=halo)
+
+    def bounds(self, rank: int) -> tuple[int, int]:
+        """[first, last) block columns owned by ``rank`` (even split)."""
+        base, rem = divmod(self.nx, self.world)
+        lo = rank * base + min(rank, rem)
+        return lo, lo + base + (1 if rank < rem else 0)
+
+    def block_x(self, x) -> torch.Tensor | np.ndarray:
+        """np.floor((x - origin) * inv_block), clipped (grid.py:248-250)."""
+        if isinstance(x, torch.Tensor):
+            c = torch.floor((x.double() - self.origin_x) * self.inv_block).long()
+            return c.clamp(0, self.nx - 1)
+        c = np.floor((np.asarray(x, dtype=np.float64) - self.origin_x) * self.inv_block)
+        return np.clip(c.astype(np.int64), 0, self.nx - 1)
+
+    def owner(self, bx):
+        ranks = torch.arange(self.world) if isinstance(bx, torch.Tensor) else np.arange(self.world)
+        highs = [self.bounds(r)[1] for r in range(self.world)]
+        if isinstance(bx, torch.Tensor):
+            h = torch.tensor(highs, device=bx.device)
+            return torch.bucketize(bx, h, right=True).clamp(max=self.world - 1)
+        return np.clip(np.searchsorted(np.asarray(highs), bx, side="right"), 0, self.world - 1)
+
+
+def pack(state: dict, gid: torch.Tensor, fields=WCSPH_FIELDS) -> torch.Tensor:
+    cols = [gid.double().reshape(-1, 1)]
+    for name, w in fields:
+        cols.append(state[name].double().reshape(-1, w))
+    return torch.cat(cols, dim=1)
+
+
+def unpack(rows: torch.Tensor, fields=WCSPH_FIELDS, dtypes=None) -> tuple[torch.Tensor, dict]:
+    gid = rows[:, 0].long()
+    out, c = {}, 1
+    for name, w in fields:
+        v = rows[:, c:c + w]
+        out[name] = v if w > 1 else v.reshape(-1)
+        c += w
+    return gid, out
+
+
+class Exchanger:
+    """Paired neighbour send/recv of packed particle rows (counts first).
+
+    ``device`` is where the rows live; ``comm_device`` where the transport
+    wants them (the CUDA device for NCCL; "cpu" for gloo)."""
+
+    def __init__(self, rank: int, world: int, device, comm_device=None):
+        self.rank, self.world = rank, world
+        self.compute_device = torch.device(device)
+        self.device = torch.device(comm_device) if comm_device is not None else self.compute_device
+
+    def _sendrecv(self, send: dict, width: int) -> list:
+        """send: {peer: rows}; returns received row blocks from every peer
+        that has a matching entry in its own ``send`` (symmetric pattern)."""
+        peers = sorted(send)
+        counts_out = {q: torch.tensor([send[q].shape[0]], dtype=torch.int64, device=self.device)
+                      for q in peers}
+        counts_in = {q: torch.zeros(1, dtype=torch.int64, device=self.device) for q in peers}
+        ops = []
+        for q in peers:
+            ops.append(dist.P2POp(dist.isend, counts_out[q], q))
+            ops.append(dist.P2POp(dist.irecv, counts_in[q], q))
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+        bufs = {q: torch.empty((int(counts_in[q].item()), width), dtype=torch.float64,
+                               device=self.device) for q in peers}
+        ops = []
+        for q in peers:
+            if send[q].shape[0]:
+                ops.append(dist.P2POp(dist.isend, send[q].to(self.device).contiguous(), q))
+            if bufs[q].shape[0]:
+                ops.append(dist.P2POp(dist.irecv, bufs[q], q))
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+        return [bufs[q].to(self.compute_device) for q in peers]
+
+    def neighbours(self) -> list[int]:
+        return [q for q in (self.rank - 1, self.rank + 1) if 0 <= q < self.world]
+
+
+class SlabDriver:
+    """Owns the rank's particles and runs the ghost / migrate protocol around
+    a local step function ``local_step(fluid_state, gid) -> fluid_state``.
+
+    The local step is the B200 solver in production (``DistributedWcsph``);
+    the CPU tests plug the oracle in to check the protocol bit for bit.
+    """
+
+    def __init__(self, part: SlabPartition, rank: int, device, fields=WCSPH_FIELDS,
+                 comm_device=None):
+        self.part, self.rank, self.device, self.fields = part, rank, device, fields
+        self.width = 1 + sum(w for _, w in fields)
+        self.x = Exchanger(rank, part.world, device, comm_device)
+        self.lo, self.hi = part.bounds(rank)
+
+    def ghost_rows(self, gid, state) -> tuple[torch.Tensor, dict]:
+        bx = self.part.block_x(state["pos"][:, 0])
+        send = {}
+        for q in self.x.neighbours():
+            if q < self.rank:
+                m = bx < self.lo + self.part.halo
+            else:
+                m = bx >= self.hi - self.part.halo
+            idx = torch.nonzero(m).reshape(-1)
+            send[q] = pack({k: v[idx] for k, v in state.items()}, gid[idx], self.fields)
+        recv = self.x._sendrecv(send, self.width)
+        rows = torch.cat(recv, 0) if recv else torch.zeros((0, self.width), dtype=torch.float64,
+                                                           device=self.device)
+        return unpack(rows, self.fields)
+
+    def migrate(self, gid, state) -> tuple[torch.Tensor, dict]:
+        bx = self.part.block_x(state["pos"][:, 0])
+        own = self.part.owner(bx)
+        keep = own == self.rank
+        send = {}
+        for q in self.x.neighbours():
+            idx = torch.nonzero(own == q).reshape(-1)
+            send[q] = pack({k: v[idx] for k, v in state.items()}, gid[idx], self.fields)
+        far = (~keep) & torch.isin(own, torch.tensor(self.x.neighbours() or [-1],
+                                                     device=own.device), invert=True)
+        if bool(far.any()):
+            raise RuntimeError("a particle crossed more than one slab in one step")
+        recv = self.x._sendrecv(send, self.width)
+        kidx = torch.nonzero(keep).reshape(-1)
+        rows = [pack({k: v[kidx] for k, v in state.items()}, gid[kidx], self.fields)] + recv
+        rows = torch.cat(rows, 0)
+        rows = rows[torch.argsort(rows[:, 0])]
+        return unpack(rows, self.fields)
+
+    def merged(self, gid, state, ggid, gstate):
+        """Owned + ghosts sorted by global id (the single-domain order)."""
+        allg = torch.cat([gid, ggid])
+        order = torch.argsort(allg)
+        merged = {k: torch.cat([state[k].to(gstate[k].dtype), gstate[k]])[order] for k in state}
+        is_owned = torch.cat([torch.ones_like(gid, dtype=torch.bool),
+                              torch.zeros_like(ggid, dtype=torch.bool)])[order]
+        return allg[order], merged, is_owned
+
+
+def initial_ownership(scene: Scene, part: SlabPartition, rank: int):
+    """Global ids and positions of the fluid particles ``rank`` owns at t=0,
+    and the wall samples it needs (slab + halo columns), as float64 numpy."""
+    fluid, wall = seed_particles(scene)
+    bx = part.block_x(fluid[:, 0])
+    gid = np.flatnonzero(part.owner(bx) == rank)
+    lo, hi = part.bounds(rank)
+    wb = part.block_x(wall[:, 0]) if len(wall) else np.zeros(0, dtype=np.int64)
+    wsel = np.flatnonzero((wb >= lo - part.halo - 1) & (wb < hi + part.halo + 1))
+    return gid, fluid, wall, wsel
+
+
+class DistributedWcsph:
+    """RTS-WCSPH over x-slabs: ``step()`` = ghost exchange, one B200 step on
+    owned + ghosts, extraction of the owned rows, migration."""
+
+    def __init__(self, scene: Scene, mode: str = "rts", device=None, halo: int = 2,
+                 jitter=None, local=None, comm_device=None, **kw):
+        self.rank = dist.get_rank()
+        self.world = dist.get_world_size()
+        self.device = torch.device(device) if device is not None else torch.device("cuda")
+        self.part = SlabPartition.for_scene(scene, "wcsph", self.world, halo)
+        gid, fluid, wall, wsel = initial_ownership(scene, self.part, self.rank)
+        if jitter is not None:
+            fluid = (fluid + jitter).astype(np.float32).astype(np.float64)
+        if comm_device is None and dist.get_backend() == "gloo":
+            comm_device = "cpu"
+        self.driver = SlabDriver(self.part, self.rank, self.device, comm_device=comm_device)
+        self.n_global = len(fluid)
+        if local is None:  # the B200 solver (graphs off: the particle count changes)
+            from .wcsph import WcsphSolver
+            local = WcsphSolver(scene, mode=mode, device=self.device, use_graphs=False, **kw)
+        self.solver = local
+        self.solver._set_local_particles(None, wall[wsel], capacity=None, init=True)
+        self.gid = torch.as_tensor(gid, device=self.device)
+        fl = torch.as_tensor(fluid[gid].astype(np.float32), device=self.device)
+        self.state = self.solver._fresh_state(fl)
+        self.sim_time = 0.0
+        self.step_index = 0
+
+    @property
+    def n_owned(self) -> int:
+        return int(self.gid.numel())
+
+    def step(self):
+        ggid, gstate = self.driver.ghost_rows(self.gid, self.state)
+        allg, merged, owned = self.driver.merged(self.gid, self.state, ggid, gstate)
+        self.solver._set_local_particles(merged, None)
+        st = self.solver.step()
+        out = self.solver._get_local_state()
+        idx = torch.nonzero(owned).reshape(-1)
+        state = {k: v[idx] for k, v in out.items()}
+        st.n_compute = int(state["compute"].sum())  # owned particles only
+        self.gid, self.state = self.driver.migrate(allg[idx], state)
+        self.state = self.solver._cast_state(self.state)
+        self.sim_time += st.dt
+        self.step_index += 1
+        return st

@@ -129,9 +129,9 @@ class BlockGrid:
 
     def _ensure_particles(self, n_fluid: int, n_total: int) -> None:
         A = self.arena
-        if n_fluid != self.n_fluid or "fluid_cells" not in A.t:
+        if "fluid_cells" not in A.t or A["fluid_cells"].numel() < max(n_fluid, 1):
             A.alloc("fluid_cells", (max(n_fluid, 1),), torch.int32, 0)
-            self.n_fluid = n_fluid
+        self.n_fluid = n_fluid
         if "order" not in A.t or A["order"].numel() < max(n_total, 1):
             A.alloc("order", (max(n_total, 1),), torch.int32, 0)
 
@@ -159,10 +159,19 @@ class BlockGrid:
         dev = self.device
         A.bind("bcell_ids", torch.as_tensor(ids.astype(np.int32), device=dev))
         A.bind("bcell_start", torch.as_tensor(starts, device=dev))
-        A.bind("bidx", torch.as_tensor((n_fluid + srt).astype(np.int32), device=dev))
+        self._bsrt = torch.as_tensor(srt.astype(np.int32), device=dev)
+        self._bidx_base = n_fluid
+        A.bind("bidx", self._bsrt + n_fluid)
         A.bind("bcell_of", torch.as_tensor(cells.astype(np.int32), device=dev))
         A.alloc("bcell_active", (self.n_bcells,), torch.uint8, 0)
         self._bslot = torch.as_tensor(slot.astype(np.int64), device=dev)
+
+    def shift_boundary(self, n_fluid: int) -> None:
+        """Wall rows follow the fluid rows: re-offset the static wall CSR when
+        the fluid count changes (distributed ranks)."""
+        if self.n_bound > 0 and n_fluid != self._bidx_base:
+            self.arena.bind("bidx", self._bsrt + n_fluid)
+            self._bidx_base = n_fluid
 
     # -- device passes (async, used by the solvers) -----------------------------
     def launch_rebuild(self, p, stream, want_maxima=False, add_fp=False) -> None:
