@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define RTS_ABI_VERSION 10
+#define RTS_ABI_VERSION 11
 
 /* err_flags bits */
 #define RTS_ERR_ESCAPED   0x1u  /* fluid left the padded grid or non-finite (grid.py:268-273) */
@@ -72,7 +72,7 @@ typedef struct RtsParams {
     int32_t rts;           /* 1 = regional mode, 0 = synchronous baseline */
     int32_t n_sms;         /* grid sizing for persistent kernels */
     int32_t n_regions;     /* region ids 1..n_regions (pcisph.py:294) */
-    int32_t pad1;
+    int32_t n_global;      /* fluid count of the whole scene (x-slab ranks); 0 = n_fluid */
 } RtsParams;
 
 /* Device-side counters; copied to the host once per step. */
@@ -197,6 +197,7 @@ typedef struct RtsBuffers {
     RtsControl *ctl;       /* correction-loop control block */
     int32_t *se_stamp;     /* (Nc) S_e generation that last marked the block */
     int32_t *near_stamp;   /* (Nc) S_e generation that last marked a 26-neighbour */
+    uint8_t *ghost;        /* (Nf) 1 = ghost row owned by another rank (or NULL) */
     RtsCounters *ctr;
 } RtsBuffers;
 

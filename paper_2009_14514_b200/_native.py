@@ -12,7 +12,7 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "librtssph.so")
-ABI_VERSION = 10
+ABI_VERSION = 11
 
 _c = ctypes
 _D = _c.c_double
@@ -30,7 +30,7 @@ class RtsParams(_c.Structure):
         ("betas", _D * 8), ("eta_max", _D), ("eta_avg", _D), ("rho_T", _D), ("delta", _D),
         ("dims", _I * 3), ("n_cells", _I), ("n_fluid", _I), ("n_bound", _I), ("n_bcells", _I),
         ("width", _I), ("n_max", _I), ("use_sound", _I), ("pin_region", _I),
-        ("apply_correction", _I), ("rts", _I), ("n_sms", _I), ("n_regions", _I), ("pad1", _I),
+        ("apply_correction", _I), ("rts", _I), ("n_sms", _I), ("n_regions", _I), ("n_global", _I),
     ]
 
 
@@ -77,7 +77,7 @@ BUFFER_FIELDS = (
     "cell_bcount", "starts", "order", "fill", "scan_tmp", "bcell_ids", "bcell_start", "bidx",
     "bcell_of", "bcell_active", "vmax", "fmax", "block_raw", "block_field", "block_tmp",
     "block_flag", "cpos", "cvel", "active", "list2", "nbr", "cnt", "xs4", "pflag", "partial",
-    "snap_p", "snap_fp", "slot_of", "ctl", "se_stamp", "near_stamp", "ctr",
+    "snap_p", "snap_fp", "slot_of", "ctl", "se_stamp", "near_stamp", "ghost", "ctr",
 )
 
 

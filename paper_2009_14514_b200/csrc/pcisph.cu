@@ -36,6 +36,10 @@ RTS_DEV bool observed_block(const RtsBuffers &b, int c, int gen) {
     return b.block_tmp[c] || (b.near_stamp[c] == gen && b.se_stamp[c] != gen);
 }
 
+// ghost rows (x-slab ranks) are neighbours only: never refreshed, predicted,
+// corrected or integrated here -- their owner computes them
+RTS_DEV bool is_ghost(const RtsBuffers &b, int i) { return b.ghost && b.ghost[i]; }
+
 // loop control flags (ctl may be null for callers outside a solver)
 RTS_DEV bool loop_done(const RtsBuffers &b) { return b.ctl && b.ctl->done; }
 RTS_DEV bool major_stopped(const RtsBuffers &b) { return b.ctl && b.ctl->stop_major; }
@@ -94,7 +98,7 @@ __global__ void __launch_bounds__(256) k_refresh_list(const __grid_constant__ Rt
     const int stride = gridDim.x * blockDim.x;
     for (int base = blockIdx.x * blockDim.x; base < nf; base += stride) {
         const int i = base + threadIdx.x;
-        const bool r = i < nf && (all || b.compute[i]);
+        const bool r = i < nf && (all || b.compute[i]) && !is_ghost(b, i);
         block_append2<256>(r, i, b.active, &b.ctr->n_compute, false, 0, nullptr, nullptr);
     }
 }
@@ -271,8 +275,10 @@ __global__ void k_motion(const __grid_constant__ RtsParams p, RtsBuffers b, int 
     if (all < 0) all = b.ctl->motion_all;
     const double dim = xmul(p.dt, p.inv_mass);
     const int n = all ? p.n_fluid : b.ctl->prev_force;
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x)
-        motion_one(p, b, all ? t : b.list2[t], dim);
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        const int i = all ? t : b.list2[t];
+        if (!is_ghost(b, i)) motion_one(p, b, i, dim);
+    }
 }
 
 // set membership for one iteration (pcisph.py:634-643); row_mask bit n set
@@ -286,7 +292,7 @@ __global__ void __launch_bounds__(256) k_sets(const __grid_constant__ RtsParams 
     // every region scheduled (or a synchronous baseline): pred = force = all
     // fluid; the pair kernels then walk 0..nf-1 directly (no lists)
     const int all_mask = ((1 << (p.n_regions + 1)) - 1) & ~1;
-    if (all_pred || (p.n_regions > 0 && (row_mask & all_mask) == all_mask)) {
+    if (!b.ghost && (all_pred || (p.n_regions > 0 && (row_mask & all_mask) == all_mask))) {
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             b.ctr->n_pred = nf;
             b.ctr->n_force = nf;
@@ -298,9 +304,9 @@ __global__ void __launch_bounds__(256) k_sets(const __grid_constant__ RtsParams 
     for (int base = blockIdx.x * blockDim.x; base < nf; base += stride) {
         const int i = base + threadIdx.x;
         bool pred = false, force = false;
-        if (i < nf) {
+        if (i < nf && !is_ghost(b, i)) {
             const bool sob = observed_block(b, b.fluid_cells[i], gen);
-            const bool turn = (row_mask >> b.region[i]) & 1;
+            const bool turn = all_pred || ((row_mask >> b.region[i]) & 1);
             const bool se = b.in_se[i] != 0;
             pred = turn || se || sob;
             force = turn || se;
@@ -329,6 +335,7 @@ constexpr int kPG = 8;
 template <int LG>
 RTS_DEV void density_one(const RtsParams &p, const RtsBuffers &b, int i, int lane,
                          unsigned gmask) {
+    if (is_ghost(b, i)) return;
     const float4 *xs4 = reinterpret_cast<const float4 *>(b.xs4);
     const float4 a = xs4[i];
     const double xi = a.x, yi = a.y, zi = a.z;
@@ -425,6 +432,7 @@ __global__ void __launch_bounds__(256) k_se_reduce(const __grid_constant__ RtsPa
                     }
             }
         }
+        if (is_ghost(b, i)) continue;  // reductions over owned particles (allreduced)
         if (e > m) m = e;
         s = xadd(s, (double)b.rho[i]);
     }
@@ -518,6 +526,7 @@ RTS_DEV void pforce_pair(const RtsParams &p, double xi, double yi, double zi, do
 template <int LG>
 RTS_DEV void pforce_one(const RtsParams &p, const RtsBuffers &b, int i, int lane,
                         unsigned gmask) {
+    if (is_ghost(b, i)) return;
     const float4 *xs4 = reinterpret_cast<const float4 *>(b.xs4);
     const double m2 = xmul(p.mass, p.mass);
     const double inv_rho0_sq = xdiv(1.0, xmul(p.rho0, p.rho0));
@@ -587,6 +596,7 @@ __global__ void k_integrate(const __grid_constant__ RtsParams p, RtsBuffers b, i
         b.ctl->stats[b.ctl->minor].t_looped = gtimer();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.n_fluid;
          i += gridDim.x * blockDim.x) {
+        if (is_ghost(b, i)) continue;
         // public x* = the last prediction; S_ob from the final S_e generation
         const float4 xs = reinterpret_cast<const float4 *>(b.xs4)[i];
         b.xstar[3 * i] = xs.x;
@@ -794,16 +804,17 @@ __global__ void k_control(const __grid_constant__ RtsParams p, RtsBuffers b, int
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) part = xadd(part, __shfl_xor_sync(0xffffffffu, part, o));
     if (threadIdx.x != 0) return;
+    const int n_all = p.n_global > 0 ? p.n_global : p.n_fluid;
     if (!done) {
-        ctr->sum_rho = part;
+        if (n_part > 0) ctr->sum_rho = part;  // n_part == 0: sum_rho already reduced (ranks)
         c->snap_op = 0;
         c->it += 1;
-        c->corrected += sync_mode ? p.n_fluid : ctr->n_pred;
-        c->forced += sync_mode ? p.n_fluid : ctr->n_force;
+        c->corrected += sync_mode ? n_all : ctr->n_pred;
+        c->forced += sync_mode ? n_all : ctr->n_force;
         if (c->local_active) c->local_run += 1; else c->g_count += 1;
         const double max_err = ctr->max_err;
-        const double mean = p.n_fluid ? ctr->sum_rho / (double)p.n_fluid : 0.0;
-        double avg = p.n_fluid ? xsub(xdiv(mean, p.rho0), 1.0) : 0.0;
+        const double mean = n_all ? ctr->sum_rho / (double)n_all : 0.0;
+        double avg = n_all ? xsub(xdiv(mean, p.rho0), 1.0) : 0.0;
         avg = avg > 0.0 ? avg : 0.0;
         c->last_max_err = max_err;
         c->last_avg_err = avg;
@@ -956,7 +967,7 @@ int rts_pci_se_reduce(const RtsParams *p, const RtsBuffers *b, int with_se, void
     if (blocks < 1) blocks = 1;
     rts_note_launch(), k_se_reduce<<<blocks, 256, 0, s>>>(*p, *b, with_se);
     RTS_LAUNCH_CHECK();
-    if (!b->ctl) {  // outside the device loop: finish the sum here
+    if (!b->ctl || p->n_global > 0) {  // outside the device loop / ranks: finish the sum here
         rts_note_launch(), k_sum_partials<<<1, 1024, 0, s>>>(*b, blocks);
         RTS_LAUNCH_CHECK();
     }
@@ -1066,6 +1077,7 @@ int rts_pci_control(const RtsParams *p, const RtsBuffers *b, int sync_mode,
     int n_part = (p->n_fluid + 255) / 256;
     if (n_part > kRedBlocks) n_part = kRedBlocks;
     if (n_part < 1) n_part = 1;
+    if (p->n_global > 0) n_part = 0;  // ranks: sum_rho was reduced across ranks already
     rts_note_launch(), k_control<<<1, 32, 0, s>>>(*p, *b, sync_mode, cond_handle, local_attempts,
                                                   iteration_cap, n_part);
     RTS_LAUNCH_CHECK();

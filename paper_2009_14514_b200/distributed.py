@@ -259,3 +259,176 @@ class DistributedWcsph:
         self.sim_time += st.dt
         self.step_index += 1
         return st
+
+
+# ---------------------------------------------------------------------------
+# RTS-PCISPH over x-slabs
+# ---------------------------------------------------------------------------
+
+PCISPH_FIELDS = (("pos", 3), ("vel", 3), ("f_ext", 3), ("f_p", 3), ("p", 1), ("rho_star", 1),
+                 ("err", 1), ("xstar", 3), ("region", 1), ("validity", 1), ("compute", 1),
+                 ("in_se", 1), ("in_sob", 1))
+
+# counters fields reduced across ranks before every k_control decision
+_CTR = None
+
+
+def _ctr_views(ctr: torch.Tensor) -> dict:
+    import ctypes
+
+    from ._native import RtsCounters
+    off = {f[0]: getattr(RtsCounters, f[0]).offset for f in RtsCounters._fields_}
+    return {"max_err": ctr[off["max_err"]:off["max_err"] + 8].view(torch.float64),
+            "sum_rho": ctr[off["sum_rho"]:off["sum_rho"] + 8].view(torch.float64),
+            "any_se": ctr[off["any_se"]:off["any_se"] + 4].view(torch.int32),
+            "n_pred": ctr[off["n_pred"]:off["n_pred"] + 4].view(torch.int32)}
+
+
+class PcisphExchange:
+    """Ghost refreshes inside a major step (hooks called by PcisphSolver's
+    host-driven loop).  Only the two inner ghost columns on each side are
+    neighbours of owned particles (two layers of 2.2s blocks cover the
+    region-1 two-layer search); deeper ghosts exist for the major-start
+    level fields only.  Per correction iteration: x* after the motion pass,
+    p / err / rho* after the density pass, then an all-reduce of the
+    convergence scalars (max err, sum rho*, any S_e, |pred|) -- the exchange
+    steps of SURVEY.md section 8e.  Per minor step: pos / vel / f_ext / f_p
+    after the integrator (next refresh, mid-major marking)."""
+
+    def __init__(self, driver: "SlabDriver", send_idx: dict, recv_idx: dict):
+        self.x = driver.x
+        self.send_idx, self.recv_idx = send_idx, recv_idx
+        self.peers = sorted(send_idx)
+
+    def _swap(self, columns_out) -> dict:
+        send = {q: columns_out(self.send_idx[q]).double() for q in self.peers}
+        width = next(iter(send.values())).shape[1] if send else 1
+        got = self.x._sendrecv(send, width)
+        return dict(zip(self.peers, got))
+
+    def after_motion(self, s) -> None:
+        xs4 = s.arena["xs4"]
+        got = self._swap(lambda idx: xs4[idx])
+        for q, rows in got.items():
+            xs4[self.recv_idx[q]] = rows.float()
+
+    def after_density(self, s) -> None:
+        A = s.arena
+        xs4, pres, err, rho = A["xs4"], A["pres"], A["err"], A["rho"]
+        got = self._swap(lambda idx: torch.stack([pres[idx].double(), err[idx],
+                                                  rho[idx].double()], 1))
+        for q, rows in got.items():
+            r = self.recv_idx[q]
+            pres[r] = rows[:, 0].float()
+            xs4[r, 3] = rows[:, 0].float()
+            err[r] = rows[:, 1]
+            rho[r] = rows[:, 2].float()
+
+    def reduce(self, s) -> None:
+        v = _ctr_views(s.arena["ctr"])
+        dev = self.x.device
+        m = torch.cat([v["max_err"], v["any_se"].double()]).to(dev)
+        a = torch.cat([v["sum_rho"], v["n_pred"].double()]).to(dev)
+        dist.all_reduce(m, op=dist.ReduceOp.MAX)
+        dist.all_reduce(a, op=dist.ReduceOp.SUM)
+        m, a = m.to(v["max_err"].device), a.to(v["max_err"].device)
+        v["max_err"].copy_(m[:1])
+        v["any_se"].copy_(m[1:2].to(torch.int32))
+        v["sum_rho"].copy_(a[:1])
+        v["n_pred"].copy_(a[1:2].to(torch.int32))
+
+    def after_integrate(self, s) -> None:
+        A = s.arena
+        pos, vel, fe, fp = A["pos"], A["vel"], A["force"], A["f_p"]
+        got = self._swap(lambda idx: torch.cat([pos[idx], vel[idx], fe[idx], fp[idx]], 1))
+        cpos, slot = A["cpos"], A["slot_of"]
+        for q, rows in got.items():
+            r = self.recv_idx[q]
+            rows = rows.float()
+            pos[r], vel[r], fe[r], fp[r] = rows[:, 0:3], rows[:, 3:6], rows[:, 6:9], rows[:, 9:12]
+            sl = slot[r].long()
+            cpos[sl, 0:3] = rows[:, 0:3]
+
+
+class DistributedPcisph:
+    """RTS-PCISPH over x-slabs: ``advance()`` = migration and 6-column ghost
+    exchange at the major-step start (region expansion reaches 4 blocks,
+    smoothing 1 more), then one B200 major step whose correction loops
+    exchange the 2 inner ghost columns and all-reduce the convergence
+    scalars every iteration."""
+
+    def __init__(self, scene: Scene, device=None, halo: int = 6, inner: int = 2, jitter=None,
+                 comm_device=None, **kw):
+        from .pcisph import PcisphSolver
+        self.rank = dist.get_rank()
+        self.world = dist.get_world_size()
+        self.device = torch.device(device) if device is not None else torch.device("cuda")
+        self.part = SlabPartition.for_scene(scene, "pcisph", self.world, halo)
+        self.inner = inner
+        gid, fluid, wall, wsel = initial_ownership(scene, self.part, self.rank)
+        if jitter is not None:
+            fluid = (fluid + jitter).astype(np.float32).astype(np.float64)
+        if comm_device is None and dist.get_backend() == "gloo":
+            comm_device = "cpu"
+        self.driver = SlabDriver(self.part, self.rank, self.device, fields=PCISPH_FIELDS,
+                                 comm_device=comm_device)
+        self.n_global = len(fluid)
+        self.solver = PcisphSolver(scene, mode="rts", device=self.device, use_graphs=False, **kw)
+        self.solver._set_local_particles(None, wall[wsel], init=True)
+        self.solver.params.n_global = self.n_global
+        self.gid = torch.as_tensor(gid, device=self.device)
+        fl = torch.as_tensor(fluid[gid].astype(np.float32), device=self.device)
+        st = self.solver._fresh_state(fl)
+        st["xstar"] = fl.clone()
+        self.state = st
+        self.sim_time = 0.0
+        self.step_index = 0
+
+    @property
+    def n_owned(self) -> int:
+        return int(self.gid.numel())
+
+    def _lists(self, allg, merged, owned):
+        bx = self.part.block_x(merged["pos"][:, 0])
+        lo, hi = self.driver.lo, self.driver.hi
+        send, recv = {}, {}
+        for q in self.driver.x.neighbours():
+            if q < self.rank:
+                s = owned & (bx < lo + self.inner)
+                r = (~owned) & (bx >= lo - self.inner) & (bx < lo)
+            else:
+                s = owned & (bx >= hi - self.inner)
+                r = (~owned) & (bx >= hi) & (bx < hi + self.inner)
+            send[q] = torch.nonzero(s).reshape(-1)
+            recv[q] = torch.nonzero(r).reshape(-1)
+        return send, recv
+
+    def advance(self):
+        s = self.solver
+        self.gid, self.state = self.driver.migrate(self.gid, self.state)
+        self.state = s._cast_state(self.state)
+        ggid, gstate = self.driver.ghost_rows(self.gid, self.state)
+        allg, merged, owned = self.driver.merged(self.gid, self.state, ggid, gstate)
+        merged = s._cast_state(merged)
+        s._set_local_particles(merged, None, ghost=~owned)
+        s.params.n_global = self.n_global
+        send, recv = self._lists(allg, merged, owned)
+        s._xch = PcisphExchange(self.driver, send, recv)
+        try:
+            rows = s.major_step()
+        finally:
+            s._xch = None
+        out = s._get_local_state()
+        idx = torch.nonzero(owned).reshape(-1)
+        self.state = {k: v[idx] for k, v in out.items()}
+        self.gid = allg[idx]
+        nref = torch.tensor([r.n_compute for r in rows], dtype=torch.float64,
+                            device=self.driver.x.device)
+        if len(rows):
+            dist.all_reduce(nref)
+        for r, n in zip(rows, nref.tolist()):
+            r.n_compute = int(n)
+            r.frac_compute = r.n_compute / max(1, self.n_global)
+        self.sim_time = s.sim_time
+        self.step_index = s.step_index
+        return rows

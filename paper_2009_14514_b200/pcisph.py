@@ -134,6 +134,36 @@ class PcisphSolver(_DeviceSolver):
     """PCISPH with ``mode`` "const", "adaptive" or "rts" (pcisph.py:279)."""
 
     mode_names = ("const", "adaptive", "rts")
+    _FIELDS = (("vel", "vel", 3, torch.float32, 0.0), ("f_ext", "force", 3, torch.float32, 0.0),
+               ("f_p", "f_p", 3, torch.float32, 0.0), ("p", "pres", 1, torch.float32, 0.0),
+               ("rho_star", "rho", 1, torch.float32, None), ("err", "err", 1, torch.float64, 0.0),
+               ("xstar", "xstar", 3, torch.float32, 0.0),
+               ("region", "region", 1, torch.int8, 1), ("validity", "validity", 1, torch.int32, 0),
+               ("compute", "compute", 1, torch.bool, True), ("in_se", "in_se", 1, torch.bool, False),
+               ("in_sob", "in_sob", 1, torch.bool, False))
+    _xch = None  # ghost-exchange hooks of a distributed rank (distributed.py)
+
+    def _realloc_extra(self, cap: int, nb: int) -> None:
+        A = self.arena
+        self._nbr = A.alloc("nbr", (cap, NEIGHBOR_WIDTH), torch.int32, 0)
+        self._cnt_full = A.alloc("cnt", (cap,), torch.int32, 0)
+        A.alloc("xs4", (cap + nb, 4), torch.float32, 0)
+        A.alloc("pflag", (cap,), torch.uint8, 0)
+        A.alloc("snap_p", (cap,), torch.float32, 0)
+        A.alloc("snap_fp", (cap, 3), torch.float32, 0)
+        A.alloc("slot_of", (cap,), torch.int32, 0)
+        A.alloc("ghost", (cap,), torch.uint8, 0)
+
+    def _set_local_particles(self, state, walls, capacity=None, init=False, ghost=None):
+        super()._set_local_particles(state, walls, capacity, init)
+        nf = self.n_fluid
+        self.cnt = self.arena["cnt"][:nf]
+        g = self.arena["ghost"]
+        g.zero_()
+        if ghost is not None and nf:
+            g[:nf].copy_(ghost.to(torch.uint8))
+        self.params.n_fluid = nf
+        N.call("rts_pci_walls", self.params, self.arena.buf, self._stream().cuda_stream)
 
     def __init__(self, scene: Scene, mode: str = "rts", dt: float | None = None,
                  schedule=DEFAULT_SCHEDULE, pin_region: int | None = None,
@@ -268,15 +298,22 @@ class PcisphSolver(_DeviceSolver):
 
     def _run_loop_host(self, sync_mode: int) -> None:
         """Correction loop without a graph: enqueue iterations, read `done`."""
+        x = self._xch
         while True:
-            if self._ktimes is None:
+            if self._ktimes is None and x is None:
                 self._call("rts_pci_iteration", sync_mode, 0, self.local_attempts,
                            self.iteration_cap)
-            else:  # per-entry-point launches so each kernel can be timed
+            else:  # per-entry-point launches: kernel timing / ghost exchanges
                 self._call("rts_pci_motion", -1)
+                if x is not None:
+                    x.after_motion(self)
                 self._call("rts_pci_sets", -1, sync_mode)
                 self._call("rts_pci_density")
+                if x is not None:
+                    x.after_density(self)
                 self._call("rts_pci_se_reduce", int(not sync_mode))
+                if x is not None:
+                    x.reduce(self)
                 self._call("rts_pci_pforces")
                 self._call("rts_pci_control", sync_mode, 0, self.local_attempts,
                            self.iteration_cap)
@@ -437,7 +474,7 @@ class PcisphSolver(_DeviceSolver):
         self._prepare(self.dt)
         self.params.n_max = min(self.n_regions, n_minor)
         st = self._stream()
-        if self.use_graphs:
+        if self.use_graphs and self._xch is None:
             N.call("rts_graph_launch", self._graph(0, n_minor), st.cuda_stream)
         else:
             N.call("rts_counters_reset", self.arena.buf, st.cuda_stream)
@@ -446,8 +483,9 @@ class PcisphSolver(_DeviceSolver):
             self._call("rts_pci_gather")
             self._call("rts_block_levels", 1)
             self._call("rts_pci_major_particles")
+            x = self._xch
             for j in range(n_minor):
-                if self._ktimes is None:
+                if self._ktimes is None and x is None:
                     self._call("rts_pci_minor_head", j)
                 else:
                     self._call("rts_pci_minor_begin", j, 0)
@@ -456,10 +494,12 @@ class PcisphSolver(_DeviceSolver):
                     N.call("rts_memset", self.arena.buf.in_se, 0, self.n_fluid, st.cuda_stream)
                     self._call("rts_pci_observed", 0)
                 self._run_loop_host(0)
-                if self._ktimes is None:
+                if self._ktimes is None and x is None:
                     self._call("rts_pci_minor_tail", j, int(j == n_minor - 1))
                 else:
                     self._call("rts_pci_integrate", 1)
+                    if x is not None:
+                        x.after_integrate(self)
                     if j != n_minor - 1:
                         self._call("rts_block_maxima", 1)
                         self._call("rts_block_levels", 2)

@@ -145,6 +145,82 @@ class _DeviceSolver:
     def pos(self) -> torch.Tensor:
         return self._pos[: self.n_fluid + self.n_bound]
 
+    # -- local particle sets (distributed ranks, distributed.py) ---------------
+    # (attribute, arena buffer, width, dtype, initial value; None = rest density)
+    _FIELDS: tuple = ()
+
+    def _fresh_state(self, pos: torch.Tensor) -> dict:
+        n = pos.shape[0]
+        out = {"pos": pos.to(torch.float32)}
+        for name, _, w, dt, fill in self._FIELDS:
+            fill = self.scene.rest_density if fill is None else fill
+            shape = (n, w) if w > 1 else (n,)
+            out[name] = torch.full(shape, fill, dtype=dt, device=self.device)
+        return out
+
+    def _cast_state(self, state: dict) -> dict:
+        out = {"pos": state["pos"].to(torch.float32).reshape(-1, 3)}
+        for name, _, w, dt, _f in self._FIELDS:
+            v = state[name]
+            if dt == torch.bool:
+                v = v != 0
+            out[name] = v.to(dt).reshape((-1, w) if w > 1 else (-1,))
+        return out
+
+    def _get_local_state(self) -> dict:
+        nf = self.n_fluid
+        out = {"pos": self._pos[:nf]}
+        for name, *_ in self._FIELDS:
+            out[name] = getattr(self, name)
+        return out
+
+    def _set_local_particles(self, state, walls, capacity=None, init=False) -> None:
+        """Replace the fluid rows (and optionally the static wall set) of this
+        solver: the distributed driver loads owned + ghost particles every
+        step.  Buffers grow geometrically; wall rows follow the fluid rows."""
+        A = self.arena
+        if walls is not None:
+            self._walls = torch.as_tensor(np.asarray(walls, dtype=np.float32),
+                                          device=self.device).reshape(-1, 3)
+        nb = self._walls.shape[0]
+        nf = 0 if state is None else int(state["pos"].shape[0])
+        cap = getattr(self, "_cap", -1)
+        if init or nf > cap or nf + nb > self._pos.shape[0]:
+            cap = max(nf, int(1.25 * nf) + 1024, capacity or 0)
+            self._cap = cap
+            self._pos = A.alloc("pos", (cap + nb, 3), torch.float32, 0)
+            for _, arena, w, dt, fill in self._FIELDS:
+                fill = self.scene.rest_density if fill is None else fill
+                A.alloc(arena, (cap, w) if w > 1 else (cap,), dt, fill)
+            for name in ("cpos", "cvel"):
+                A.alloc(name, (cap + nb, 4), torch.float32, 0)
+            for name in ("active", "list2"):
+                A.alloc(name, (cap,), torch.int32, 0)
+            self._realloc_extra(cap, nb)
+            self.grid._ensure_particles(cap, cap + nb)
+            if walls is not None or init:
+                self.grid.bind_boundary(self._walls.double().cpu().numpy(), nf)
+        if walls is not None and not init:
+            self.grid.bind_boundary(self._walls.double().cpu().numpy(), nf)
+        if nf:
+            self._pos[:nf].copy_(state["pos"])
+            for name, arena, w, dt, _ in self._FIELDS:
+                A[arena][:nf].copy_(state[name].reshape(A[arena][:nf].shape))
+        self._pos[nf:nf + nb].copy_(self._walls)
+        self.n_fluid = nf
+        self.n_bound = nb
+        for name, arena, *_ in self._FIELDS:
+            setattr(self, name, A[arena][:nf])
+        self.grid.n_fluid = nf
+        self.grid.shift_boundary(nf)
+        p = self.params
+        p.n_fluid = nf
+        p.n_bound = nb
+        p.n_bcells = self.grid.n_bcells
+
+    def _realloc_extra(self, cap: int, nb: int) -> None:
+        """Solver-specific buffers sized by the particle capacity."""
+
     def host(self, name: str) -> np.ndarray:
         """fp64 numpy snapshot of a state attribute (for parity checks)."""
         t = getattr(self, name)
@@ -156,6 +232,14 @@ class WcsphSolver(_DeviceSolver):
     """Weakly compressible SPH, ``mode`` "baseline" or "rts" (wcsph.py:108)."""
 
     mode_names = ("baseline", "rts")
+    _FIELDS = (("vel", "vel", 3, torch.float32, 0.0), ("acc", "acc", 3, torch.float32, 0.0),
+               ("acc_prev", "acc_prev", 3, torch.float32, 0.0),
+               ("force", "force", 3, torch.float32, 0.0), ("rho", "rho", 1, torch.float32, None),
+               ("pres", "pres", 1, torch.float32, 0.0),
+               ("dt_since", "dt_since", 1, torch.float64, 0.0),
+               ("dt_corr", "dt_corr", 1, torch.float64, 0.0),
+               ("validity", "validity", 1, torch.int32, 0), ("region", "region", 1, torch.int8, 1),
+               ("compute", "compute", 1, torch.bool, True))
 
     def __init__(self, scene: Scene, mode: str = "rts", dt_cap: float | None = None,
                  pin_region: int | None = None, apply_correction: bool = True,
@@ -222,82 +306,6 @@ class WcsphSolver(_DeviceSolver):
         return g
 
     # ------------------------------------------------------------------
-    # -- local particle sets (distributed ranks, distributed.py) ---------------
-    _FIELDS = (("vel", 3, torch.float32, 0.0), ("acc", 3, torch.float32, 0.0),
-               ("acc_prev", 3, torch.float32, 0.0), ("force", 3, torch.float32, 0.0),
-               ("rho", 1, torch.float32, None), ("pres", 1, torch.float32, 0.0),
-               ("dt_since", 1, torch.float64, 0.0), ("dt_corr", 1, torch.float64, 0.0),
-               ("validity", 1, torch.int32, 0), ("region", 1, torch.int8, 1),
-               ("compute", 1, torch.bool, True))
-
-    def _fresh_state(self, pos: torch.Tensor) -> dict:
-        n = pos.shape[0]
-        out = {"pos": pos.to(torch.float32)}
-        for name, w, dt, fill in self._FIELDS:
-            fill = self.scene.rest_density if fill is None else fill
-            shape = (n, w) if w > 1 else (n,)
-            out[name] = torch.full(shape, fill, dtype=dt, device=self.device)
-        return out
-
-    def _cast_state(self, state: dict) -> dict:
-        out = {"pos": state["pos"].to(torch.float32).reshape(-1, 3)}
-        for name, w, dt, _ in self._FIELDS:
-            v = state[name]
-            if dt == torch.bool:
-                v = v != 0
-            out[name] = v.to(dt).reshape((-1, w) if w > 1 else (-1,))
-        return out
-
-    def _get_local_state(self) -> dict:
-        nf = self.n_fluid
-        out = {"pos": self._pos[:nf]}
-        for name, *_ in self._FIELDS:
-            out[name] = getattr(self, name)
-        return out
-
-    def _set_local_particles(self, state, walls, capacity=None, init=False) -> None:
-        """Replace the fluid rows (and optionally the static wall set) of this
-        solver: the distributed driver loads owned + ghost particles every
-        step.  Buffers grow geometrically; wall rows follow the fluid rows."""
-        A = self.arena
-        if walls is not None:
-            self._walls = torch.as_tensor(np.asarray(walls, dtype=np.float32),
-                                          device=self.device).reshape(-1, 3)
-        nb = self._walls.shape[0]
-        nf = 0 if state is None else int(state["pos"].shape[0])
-        cap = getattr(self, "_cap", -1)
-        if init or nf > cap or nf + nb > self._pos.shape[0]:
-            cap = max(nf, int(1.25 * nf) + 1024, capacity or 0)
-            self._cap = cap
-            self._pos = A.alloc("pos", (cap + nb, 3), torch.float32, 0)
-            for name, w, dt, fill in self._FIELDS:
-                fill = self.scene.rest_density if fill is None else fill
-                A.alloc(name, (cap, w) if w > 1 else (cap,), dt, fill)
-            for name in ("cpos", "cvel"):
-                A.alloc(name, (cap + nb, 4), torch.float32, 0)
-            for name in ("active", "list2"):
-                A.alloc(name, (cap,), torch.int32, 0)
-            self.grid._ensure_particles(cap, cap + nb)
-            if walls is not None or init:
-                self.grid.bind_boundary(self._walls.double().cpu().numpy(), nf)
-        if walls is not None and not init:
-            self.grid.bind_boundary(self._walls.double().cpu().numpy(), nf)
-        if nf:
-            self._pos[:nf].copy_(state["pos"])
-            for name, w, dt, _ in self._FIELDS:
-                A[name][:nf].copy_(state[name].reshape(A[name][:nf].shape))
-        self._pos[nf:nf + nb].copy_(self._walls)
-        self.n_fluid = nf
-        self.n_bound = nb
-        for name, *_ in self._FIELDS:
-            setattr(self, name, A[name][:nf])
-        self.grid.n_fluid = nf
-        self.grid.shift_boundary(nf)
-        p = self.params
-        p.n_fluid = nf
-        p.n_bound = nb
-        p.n_bcells = self.grid.n_bcells
-
     def cfl_bound(self) -> float:
         """Global step bound from max |F| (wcsph.py:182-189)."""
         sc = self.scene

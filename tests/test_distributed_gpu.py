@@ -77,3 +77,63 @@ def test_two_ranks_on_one_gpu_match_single_gpu_bitwise():
     assert np.array_equal(np.concatenate([r[2] for r in res])[order], ref.host("pos")[:nf])
     assert np.array_equal(np.concatenate([r[3] for r in res])[order], ref.host("vel"))
     assert np.array_equal(np.concatenate([r[4] for r in res])[order], ref.host("rho"))
+
+
+def _pworker(rank, world, port, majors, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import sys
+        sys.path.insert(0, ROOT)
+        from paper_2009_14514_b200.distributed import DistributedPcisph
+        from paper_2009_14514_b200.scene import seed_particles
+        sc = _scene()
+        nf = len(seed_particles(sc)[0])
+        d = DistributedPcisph(sc, device="cuda:0", jitter=_jitter(nf) * 0.2)
+        stats = []
+        for _ in range(majors):
+            stats += [(r.n_compute, r.iterations, r.corrected, r.early_term) for r in d.advance()]
+        q.put((rank, d.gid.cpu().numpy(), d.state["pos"].cpu().numpy(),
+               d.state["rho_star"].cpu().numpy(), stats))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_pcisph_two_ranks_on_one_gpu_match_single_gpu():
+    """RTS-PCISPH over two x-slabs (per-iteration ghost x*/p/err exchange and
+    all-reduced convergence scalars) takes the single-GPU run's decisions
+    (refresh counts, iterations, corrected work per minor step) and stays
+    within fp32 rounding of its trajectory."""
+    from paper_2009_14514_b200 import PcisphSolver
+    from paper_2009_14514_b200.scene import seed_particles
+    majors = 3
+    sc = _scene()
+    ref = PcisphSolver(sc, mode="rts")
+    nf = ref.n_fluid
+    x = (seed_particles(sc)[0] + _jitter(nf) * 0.2).astype(np.float32)
+    ref.pos[:nf] = torch.as_tensor(x, device=ref.device)
+    ref.xstar[:] = ref.pos[:nf]
+    rstats = []
+    for _ in range(majors):
+        rstats += [(r.n_compute, r.iterations, r.corrected, r.early_term) for r in ref.advance()]
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_pworker, args=(r, 2, port, majors, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=600) for _ in range(2)], key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=60)
+    assert res[0][4] == rstats and res[1][4] == rstats
+    gid = np.concatenate([r[1] for r in res])
+    order = np.argsort(gid)
+    assert np.array_equal(gid[order], np.arange(nf))
+    pos = np.concatenate([r[2] for r in res])[order]
+    assert np.abs(pos - ref.host("pos")[:nf]).max() < 1e-5
+    rho = np.concatenate([r[3] for r in res])[order]
+    assert np.abs(rho - ref.host("rho_star")).max() / 1000.0 < 1e-5
