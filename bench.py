@@ -12,8 +12,11 @@ literal 1 % diverges on the reference itself).  A bench step
 is one ``advance()`` = one major step (4 minor steps); the metric counts
 N_fluid x minor steps / second.  Synthetic data; fp32 state, fp64 pair sums.
 
-Each rank (one per GPU, torchrun for N > 1) runs its own replica of the
-scene (weak scaling, no data-path collective: "replicas only").
+For N > 1 (torchrun, one rank per GPU) the scene grows along x by 1 m of
+fluid per rank (weak scaling) and is cut into x-slabs
+(paper_2009_14514_b200/distributed.py): ghost-column exchange and
+migration at every major step, ghost x*/p/err exchange and an all-reduce of
+the convergence scalars in every correction iteration (NCCL).
 Timing: W untimed majors, then K majors bracketed by barrier +
 synchronize, CUDA events on the solver stream, max over ranks.
 
@@ -42,10 +45,13 @@ UNIT = "particle-updates/s"
 SEED = 1234
 
 
-def scene_cfg2():
+def scene_cfg2(world: int = 1):
+    """configs[1] at world = 1; for weak scaling the fluid column and the
+    tank grow along x by 1 m per rank (world m of fluid in a world + 1.5 m
+    tank), so every rank's x-slab holds ~1 M particles."""
     from paper_2009_14514_b200 import Scene
-    return Scene(domain_min=(0.0, 0.0, 0.0), domain_max=(2.5, 1.25, 2.5),
-                 fluid_boxes=(((0.0, 0.0, 0.0), (1.0, 1.0, 1.0)),), spacing=0.01,
+    return Scene(domain_min=(0.0, 0.0, 0.0), domain_max=(world + 1.5, 1.25, 2.5),
+                 fluid_boxes=(((0.0, 0.0, 0.0), (float(world), 1.0, 1.0)),), spacing=0.01,
                  eta_max=0.03, eta_avg=0.015)
 
 
@@ -233,20 +239,36 @@ def main():
     import torch.distributed as dist
 
     from paper_2009_14514_b200 import _native
+    local = local % max(1, torch.cuda.device_count())  # ranks > GPUs: 1-GPU path checks
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        backend = os.environ.get("RTS_BENCH_BACKEND", "nccl")  # gloo: 1-GPU path checks
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=device)
+        else:
+            dist.init_process_group(backend)
 
     def barrier():
         if world > 1:
             dist.barrier()
 
-    solver = make_device_solver("pcisph", device)
-    nf = solver.n_fluid
+    if world == 1:
+        solver = make_device_solver("pcisph", device)
+        driver = solver
+        n_total = solver.n_fluid
+    else:  # x-slab decomposition (paper_2009_14514_b200/distributed.py)
+        from paper_2009_14514_b200.distributed import DistributedPcisph
+        from paper_2009_14514_b200.scene import seed_particles
+        sc = scene_cfg2(world)
+        n_total = len(seed_particles(sc)[0])
+        driver = DistributedPcisph(sc, device=device, jitter=jitter_np(n_total, sc.spacing),
+                                   iteration_cap=50)
+        solver = driver.solver
+    nf = n_total
     stream = torch.cuda.current_stream(device)
     for _ in range(args.warmup):
-        solver.advance()
+        driver.advance()
     torch.cuda.synchronize()
 
     # ---- timed region: K majors, device time --------------------------------
@@ -263,7 +285,7 @@ def main():
     minors = 0
     rows = []
     for _ in range(args.steps):
-        r = solver.advance()
+        r = driver.advance()
         rows.extend(r)
         minors += len(r)
     ev1.record(stream)
@@ -277,7 +299,7 @@ def main():
         tt = torch.tensor([t, float(minors)], device=device, dtype=torch.float64)
         dist.all_reduce(tt[:1], op=dist.ReduceOp.MAX)
         t = float(tt[0])
-    value = world * nf * minors / t
+    value = n_total * minors / t  # whole-job particle-updates / s
 
     # ---- dominant kernel roofline (separate instrumented pass) --------------
     solver.time_kernels(kernels)
@@ -286,7 +308,7 @@ def main():
     rec = {"pred": 0, "force": 0, "refresh": 0, "motion": 0}
     prof_rows = []
     for _ in range(max(2, min(args.steps, 8))):
-        prof_rows.extend(solver.advance())
+        prof_rows.extend(driver.advance())
     torch.cuda.synchronize()
     totals = {k: sum(solver.kernel_times(k)) for k in kernels}
     counts = {k: len(solver.kernel_times(k)) for k in kernels}
@@ -296,8 +318,9 @@ def main():
     rec["force"] = rec["pred"]  # force set is a subset; refined by counters below
     if hasattr(solver, "_force_total"):
         rec["force"] = solver._force_total
-    rec["refresh"] = sum(r.n_compute for r in prof_rows)
-    rec["motion"] = nf * len(prof_rows) + rec["force"]
+    rec["refresh"] = sum(r.n_compute for r in prof_rows) * solver.n_fluid // max(1, nf)
+    rec["pred"] = rec["pred"] * solver.n_fluid // max(1, nf)
+    rec["motion"] = solver.n_fluid * len(prof_rows) + rec["force"]
     c_mean = float(solver.cnt.double().mean())
     solver._ktimes = None
     solver.use_graphs = True
@@ -320,35 +343,49 @@ def main():
     # ---- e2e through the public API with host-owned state ----------------------
     e2e = None
     if not args.no_e2e:
-        hp = torch.empty((nf, 3), dtype=torch.float32).pin_memory()
-        hv = torch.empty((nf, 3), dtype=torch.float32).pin_memory()
-        hp.copy_(solver.pos[:nf])
-        hv.copy_(solver.vel)
-        torch.cuda.synchronize()
+        # host-owned state: the rank's fluid pos/vel live in pinned host memory,
+        # go up before and come back after every advance()
+        def dev_state():
+            if world == 1:
+                return solver.pos[:solver.n_fluid], solver.vel
+            return driver.state["pos"], driver.state["vel"]
         k_e2e = max(2, min(args.steps, 10))
+        cap = 2 * dev_state()[0].shape[0] + 1024
+        hp_all = torch.empty((cap, 3), dtype=torch.float32).pin_memory()
+        hv_all = torch.empty((cap, 3), dtype=torch.float32).pin_memory()
+        dp, dv = dev_state()
+        hp_all[:dp.shape[0]].copy_(dp)
+        hv_all[:dv.shape[0]].copy_(dv)
+        torch.cuda.synchronize()
         barrier()
         t0 = time.perf_counter()
         e_minors = 0
+        nbytes = 0
         for _ in range(k_e2e):
-            solver.pos[:nf].copy_(hp, non_blocking=True)
-            solver.vel.copy_(hv, non_blocking=True)
-            e_minors += len(solver.advance())
-            hp.copy_(solver.pos[:nf], non_blocking=True)
-            hv.copy_(solver.vel, non_blocking=True)
+            dp, dv = dev_state()
+            n = dp.shape[0]
+            dp.copy_(hp_all[:n], non_blocking=True)  # step inputs: host -> device
+            dv.copy_(hv_all[:n], non_blocking=True)
+            e_minors += len(driver.advance())
+            dp, dv = dev_state()  # results (ownership may have changed)
+            n2 = dp.shape[0]
+            hp_all[:n2].copy_(dp, non_blocking=True)
+            hv_all[:n2].copy_(dv, non_blocking=True)
+            nbytes = (n + n2) * 24
         torch.cuda.synchronize()
         te = time.perf_counter() - t0
         if world > 1:
             tt = torch.tensor([te], device=device, dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             te = float(tt[0])
-        e2e = {"value": world * nf * e_minors / te, "unit": UNIT,
-               "h2d_bytes_per_step": 2 * nf * 12, "d2h_bytes_per_step": 2 * nf * 12,
+        e2e = {"value": n_total * e_minors / te, "unit": UNIT,
+               "h2d_bytes_per_step": nbytes // 2, "d2h_bytes_per_step": nbytes // 2,
                "steps": k_e2e, "note": "pinned host pos+vel uploaded before and downloaded "
                                        "after every advance(); wall clock"}
 
     # ---- WCSPH extra (configs[2] geometry, 1M RTS-WCSPH) ----------------------
     wc = None
-    if not args.no_wcsph:
+    if not args.no_wcsph and world == 1:
         ws = make_device_solver("wcsph", device)
         for _ in range(8):
             ws.step()
@@ -389,8 +426,9 @@ def main():
                        "corrected_per_minor_over_nf": round(sum(r.corrected for r in rows) /
                                                            max(1, minors) / nf, 3),
                        "l2": "working set > L2 (neighbour tables 512 MB + state)",
-                       "parallelism": f"replicas x{world}", "arithmetic": "fp32 state, fp64 "
-                       "pair sums"},
+                       "parallelism": ("single GPU" if world == 1 else
+                                       f"x-slabs x{world} (ghost exchange + allreduce)"),
+                       "arithmetic": "fp32 state, fp64 pair sums"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk, "wcsph_rts_1m": wc,
         }

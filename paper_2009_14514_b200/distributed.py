@@ -51,18 +51,35 @@ class SlabPartition:
     nx: int
     world: int
     halo: int
+    cuts: tuple = ()  # world + 1 column boundaries; empty = even split
 
     @classmethod
-    def for_scene(cls, scene: Scene, mode: str, world: int, halo: int = 2) -> "SlabPartition":
+    def for_scene(cls, scene: Scene, mode: str, world: int, halo: int = 2,
+                  balance: bool = True) -> "SlabPartition":
         pad = scene.boundary_layers * scene.spacing
         lo = scene.domain_min[0] - pad
         hi = scene.domain_max[0] + pad
         block = scene.block_size(mode)
         nx = max(1, int(math.ceil((hi - lo) / block - 1e-12)))
-        return cls(origin_x=lo, inv_block=1.0 / block, nx=nx, world=world, halo=halo)
+        part = cls(origin_x=lo, inv_block=1.0 / block, nx=nx, world=world, halo=halo)
+        if balance and world > 1:
+            # cut at equal fluid counts of the initial state (the RTS work
+            # follows the particles; rebalancing at rebuilds is a next step)
+            fluid, _ = seed_particles(scene)
+            hist = np.bincount(part.block_x(fluid[:, 0]), minlength=nx).cumsum()
+            total = hist[-1] if len(hist) else 0
+            cuts = [0]
+            for r in range(1, world):
+                c = int(np.searchsorted(hist, r * total / world, side="left")) + 1
+                cuts.append(min(max(c, cuts[-1] + 1), nx - (world - r)))
+            cuts.append(nx)
+            part.cuts = tuple(cuts)
+        return part
 
     def bounds(self, rank: int) -> tuple[int, int]:
-        """[first, last) block columns owned by ``rank`` (even split)."""
+        """[first, last) block columns owned by ``rank``."""
+        if self.cuts:
+            return self.cuts[rank], self.cuts[rank + 1]
         base, rem = divmod(self.nx, self.world)
         lo = rank * base + min(rank, rem)
         return lo, lo + base + (1 if rank < rem else 0)
