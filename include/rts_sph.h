@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define RTS_ABI_VERSION 11
+#define RTS_ABI_VERSION 12
 
 /* err_flags bits */
 #define RTS_ERR_ESCAPED   0x1u  /* fluid left the padded grid or non-finite (grid.py:268-273) */
@@ -91,7 +91,8 @@ typedef struct RtsCounters {
     double   max_err;          /* PCISPH: max err over fluid */
     int32_t  any_se;           /* PCISPH: any particle in S_e */
     int32_t  lists_all;        /* PCISPH: this iteration's pred = force = all fluid (no lists) */
-    double   reserved[8];
+    int64_t  missing;          /* neighbour audit: true neighbours absent from tables */
+    double   reserved[7];
 } RtsCounters;
 
 /* Per-minor-step record written by the device loop control (StepStats,
@@ -279,6 +280,12 @@ int rts_pci_mark_updates(const RtsParams *p, const RtsBuffers *b, void *stream);
 int rts_pci_snapshot(const RtsParams *p, const RtsBuffers *b, int restore, void *stream);
 /* max |v| over fluid into ctr->fmax_bits (_adapt_dt, pcisph.py:470-476). */
 int rts_vel_max(const RtsParams *p, const RtsBuffers *b, void *stream);
+/* Neighbour audit (count_missing_neighbors, grid.py:165-212, 353-394): `a`
+ * describes a grid freshly rebuilt at the current positions (its cpos filled
+ * by rts_pci_gather); for every particle of `b`'s refresh list, count the
+ * true neighbours (fp64 r^2 < h^2 over one block layer of `a`) absent from
+ * its table row; the total goes to b->ctr->missing. */
+int rts_pci_audit(const RtsParams *pa, const RtsBuffers *a, const RtsBuffers *b, void *stream);
 /* p = f_p = 0 for all fluid (pcisph.py:570-571). */
 int rts_pci_zero_pressure(const RtsParams *p, const RtsBuffers *b, void *stream);
 /* Device loop control: reset per major; per-minor state reset + first row;

@@ -904,9 +904,53 @@ __global__ void k_minor_end(RtsBuffers b, int minor) {
     s.t_end = gtimer();
     if (c->early || c->failed) c->stop_major = 1;
 }
+// count_missing (grid.py:165-212): one block layer of the fresh audit grid
+// `a` around the particle's current block; true neighbours (fp64) missing
+// from the table row of the refresh particle
+__global__ void k_audit(const __grid_constant__ RtsParams pa, RtsBuffers a, RtsBuffers b) {
+    const int n = b.ctr->n_compute;
+    const int nx = pa.dims[0], ny = pa.dims[1], nz = pa.dims[2];
+    const float4 *cpos = reinterpret_cast<const float4 *>(a.cpos);
+    long long lost = 0;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        const int i = b.active[t];
+        const double xi = b.pos[3 * i], yi = b.pos[3 * i + 1], zi = b.pos[3 * i + 2];
+        const int cx = trunc_axis(xi, pa.origin[0], pa.inv_block, nx);
+        const int cy = trunc_axis(yi, pa.origin[1], pa.inv_block, ny);
+        const int cz = trunc_axis(zi, pa.origin[2], pa.inv_block, nz);
+        const int *row = b.nbr + (size_t)i * pa.width;
+        const int c = b.cnt[i];
+        for (int ax = max(0, cx - 1); ax <= min(nx - 1, cx + 1); ++ax)
+            for (int ay = max(0, cy - 1); ay <= min(ny - 1, cy + 1); ++ay) {
+                const int base = (ax * ny + ay) * nz;
+                const int k0 = a.starts[base + max(0, cz - 1)];
+                const int k1 = a.starts[base + min(nz - 1, cz + 1) + 1];
+                for (int k = k0; k < k1; ++k) {
+                    const float4 o = cpos[k];
+                    if (!(dist2(xsub(xi, (double)o.x), xsub(yi, (double)o.y),
+                                xsub(zi, (double)o.z)) < pa.h2))
+                        continue;
+                    const int j = a.order[k];
+                    bool found = false;
+                    for (int q = 0; q < c; ++q)
+                        if (row[q] == j) { found = true; break; }
+                    if (!found) ++lost;
+                }
+            }
+    }
+    if (lost) atomicAdd((unsigned long long *)&b.ctr->missing, (unsigned long long)lost);
+}
+
 }  // namespace
 
 extern "C" {
+
+int rts_pci_audit(const RtsParams *pa, const RtsBuffers *a, const RtsBuffers *b, void *stream) {
+    rts_note_launch(), k_audit<<<rts_blocks(pa->n_fluid, 128), 128, 0, (cudaStream_t)stream>>>(*pa, *a, *b);
+    RTS_LAUNCH_CHECK();
+    return 0;
+}
+
 
 int rts_pci_walls(const RtsParams *p, const RtsBuffers *b, void *stream) {
     if (p->n_bound <= 0) return 0;

@@ -24,6 +24,7 @@ from ._device import raise_on_errors
 from .errors import ConfigError, NumericalError
 from .scene import Scene
 from .stats import StepStats
+from .grid import BlockGrid
 from .wcsph import NEIGHBOR_WIDTH, _DeviceSolver
 
 __all__ = ["PcisphSolver", "MajorStepController", "DEFAULT_SCHEDULE", "VALIDITY_PERIOD",
@@ -474,7 +475,9 @@ class PcisphSolver(_DeviceSolver):
         self._prepare(self.dt)
         self.params.n_max = min(self.n_regions, n_minor)
         st = self._stream()
-        if self.use_graphs and self._xch is None:
+        audit = bool(self.audit_neighbors)
+        missed = []
+        if self.use_graphs and self._xch is None and not audit:
             N.call("rts_graph_launch", self._graph(0, n_minor), st.cuda_stream)
         else:
             N.call("rts_counters_reset", self.arena.buf, st.cuda_stream)
@@ -485,11 +488,14 @@ class PcisphSolver(_DeviceSolver):
             self._call("rts_pci_major_particles")
             x = self._xch
             for j in range(n_minor):
-                if self._ktimes is None and x is None:
+                if self._ktimes is None and x is None and not audit:
                     self._call("rts_pci_minor_head", j)
                 else:
                     self._call("rts_pci_minor_begin", j, 0)
                     self._call("rts_pci_refresh", 0, 1)
+                    if audit:
+                        self._audit_refresh()
+                        missed.append(self.counters.read(st).missing)
                     self._call("rts_pci_zero_pressure")
                     N.call("rts_memset", self.arena.buf.in_se, 0, self.n_fluid, st.cuda_stream)
                     self._call("rts_pci_observed", 0)
@@ -526,10 +532,12 @@ class PcisphSolver(_DeviceSolver):
                 iters_r1=int(ms.riters[1]), iters_r2=int(ms.riters[2]),
                 iters_r3=int(ms.riters[3]), iters_r4=int(ms.riters[4]),
                 max_err=float(ms.max_err), avg_err=float(ms.avg_err), early_term=int(ms.early),
-                missed_neighbors=0,
+                missed_neighbors=(int(missed[j]) - (int(missed[j - 1]) if j else 0))
+                if j < len(missed) else 0,
                 t_neighbor=max(0, ms.t_refreshed - ms.t_begin) * 1e-9,
                 t_physics=max(0, ms.t_looped - ms.t_refreshed) * 1e-9,
                 t_rts=max(0, ms.t_end - ms.t_looped) * 1e-9))
+        self.missed_neighbors_total += sum(r.missed_neighbors for r in rows)
         self._raise_control(ctl, c)
         self.controller.note_major(early)
         return rows
@@ -561,5 +569,36 @@ class PcisphSolver(_DeviceSolver):
         if not launch_only:
             self._raise(self.counters.read(self._stream()))
 
-    def _audit_refresh(self) -> int:
-        raise NotImplementedError("neighbour audit on the B200 path is not implemented yet")
+    def _audit_refresh(self) -> None:
+        """count_missing_neighbors (grid.py:353-394) for this minor's refresh
+        list: a grid freshly rebuilt at the current positions (block edge
+        max(h, block), all wall samples near fluid) is scanned one layer
+        around each refreshed particle; true neighbours absent from its new
+        table row accumulate in ctr.missing."""
+        from ._device import Arena, Counters
+        st = self._stream()
+        ag = getattr(self, "_audit_grid", None)
+        if ag is None:
+            g = self.grid
+            hi = g.origin + np.asarray(g.dims) * g.block_size
+            ag = BlockGrid(g.origin, hi, max(self.kernel.h, g.block_size), device=self.device,
+                           arena=Arena(self.device))
+            ag.counters = Counters(ag.arena)
+            self._audit_grid = ag
+        A = ag.arena
+        nf, nb = self.n_fluid, self.n_bound
+        if getattr(self, "_audit_n", None) != (nf, nb):
+            ag._ensure_particles(nf, nf + nb)
+            ag.bind_boundary(self.pos[nf:nf + nb].double().cpu().numpy(), nf)
+            A.alloc("cpos", (max(nf + nb, 1), 4), torch.float32, 0)
+            A.alloc("slot_of", (max(nf, 1),), torch.int32, 0)
+            self._audit_n = (nf, nb)
+        A.bind("pos", self._pos)
+        pa = ag.params
+        pa.n_fluid, pa.n_bound, pa.n_bcells = nf, nb, ag.n_bcells
+        pa.h2 = self.kernel.h2
+        pa.width = NEIGHBOR_WIDTH
+        ag.counters.reset(st)
+        ag.launch_rebuild(pa, st)
+        N.call("rts_pci_gather", pa, A.buf, st.cuda_stream)
+        N.call("rts_pci_audit", pa, A.buf, self.arena.buf, st.cuda_stream)

@@ -271,12 +271,15 @@ def test_unconvergable_minor_raises():
         s.advance()
 
 
-def test_short_run_holds_density(tank_scene):
+def test_short_run_holds_density_and_misses_nothing(tank_scene):
+    """pkg/tests/test_pcisph.py:310-319 with the device neighbour audit."""
     from paper_2009_14514_b200 import PcisphSolver
-    s = PcisphSolver(tank_scene, mode="rts")
+    s = PcisphSolver(tank_scene, mode="rts", audit_neighbors=True)
     rows = []
     while s.sim_time < 0.05:
         rows.extend(s.advance())
+    assert s.missed_neighbors_total == 0
+    assert all(m.missed_neighbors == 0 for m in rows)
     clean = [m for m in rows if not m.early_term]
     assert clean
     assert all(m.max_err < tank_scene.eta_max for m in clean)
@@ -287,3 +290,24 @@ def test_unknown_mode_rejected(tank_scene):
     from paper_2009_14514_b200 import PcisphSolver
     with pytest.raises(ValueError, match="unknown pcisph mode"):
         PcisphSolver(tank_scene, mode="warp")
+
+
+def test_audit_counts_missing_entries():
+    """The audit kernel finds true neighbours that are absent from a row:
+    truncate every refreshed table by one entry and count."""
+    from paper_2009_14514_b200 import PcisphSolver
+    s = PcisphSolver(tiny_tank(), mode="rts")
+    s._prepare(s.dt)
+    s._rebuild(True)
+    s._assign_major_regions(4, rebuilt=True)
+    s._call("rts_pci_minor_begin", 0, 0)
+    s._call("rts_pci_refresh", 0, 1)
+    s._audit_refresh()
+    assert s.counters.read(s._stream()).missing == 0
+    s.cnt.sub_(1)  # drop the last entry of every row
+    s.counters.reset(s._stream())
+    s._call("rts_pci_refresh", 1, 1)
+    s.cnt.sub_(1)
+    s._audit_refresh()
+    c = s.counters.read(s._stream())
+    assert c.missing == s.n_fluid
