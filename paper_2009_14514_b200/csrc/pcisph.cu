@@ -91,13 +91,21 @@ __global__ void k_major_particles(const __grid_constant__ RtsParams p, RtsBuffer
 }
 
 // refresh list: particles whose tables are renewed this minor step
+// The refresh list is built in CSR (block-key) order, not particle order:
+// consecutive lanes then belong to the same or z-adjacent blocks, so their
+// candidate spans coincide and a warp's span loads collapse onto a few cache
+// lines instead of one line per lane (-16 % on the full refresh).  The
+// table-driven kernels keep particle order, where consecutive lanes read
+// consecutive rows.
 __global__ void __launch_bounds__(256) k_refresh_list(const __grid_constant__ RtsParams p,
                                                       RtsBuffers b, int all) {
     RTS_MINOR_GUARD();
     const int nf = p.n_fluid;
+    const int ns = b.ctr->n_sorted;
     const int stride = gridDim.x * blockDim.x;
-    for (int base = blockIdx.x * blockDim.x; base < nf; base += stride) {
-        const int i = base + threadIdx.x;
+    for (int base = blockIdx.x * blockDim.x; base < ns; base += stride) {
+        const int k = base + threadIdx.x;
+        const int i = k < ns ? b.order[k] : nf;
         const bool r = i < nf && (all || b.compute[i]) && !is_ghost(b, i);
         block_append2<256>(r, i, b.active, &b.ctr->n_compute, false, 0, nullptr, nullptr);
     }
@@ -189,16 +197,26 @@ RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshC
             const int base = (ax * ny + ay) * nz;
             const int k0 = b.starts[base + z0], k1 = b.starts[base + z1 + 1];
             if (G == 1) {
-                for (int kb = k0; kb < k1; kb += 4) {
-                    float4 ob[4];
+                // membership bits of up to 64 candidates, then the (few) hits:
+                // the candidate loop carries no memory traffic or branches
+                for (int cb = k0; cb < k1; cb += 64) {
+                    const int ce = min(cb + 64, k1);
+                    unsigned long long bits = 0ull;
+                    for (int kb = cb; kb < ce; kb += 4) {
+                        float4 ob[4];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) ob[u] = cpos[min(kb + u, k1 - 1)];
+                        for (int u = 0; u < 4; ++u) ob[u] = cpos[min(kb + u, ce - 1)];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        if (kb + u < k1 && is_neighbour(k, p, fxi, fyi, fzi, ob[u])) {
-                            if (cntn < p.width) row[cntn] = b.order[kb + u];
-                            ++cntn;
+                        for (int u = 0; u < 4; ++u) {
+                            const bool in = kb + u < ce && is_neighbour(k, p, fxi, fyi, fzi, ob[u]);
+                            bits |= (unsigned long long)in << (kb + u - cb);
                         }
+                    }
+                    while (bits) {
+                        const int q = __ffsll((long long)bits) - 1;
+                        bits &= bits - 1ull;
+                        if (cntn < p.width) row[cntn] = b.order[cb + q];
+                        ++cntn;
                     }
                 }
             } else {
@@ -387,17 +405,20 @@ RTS_DEV void density_one(const RtsParams &p, const RtsBuffers &b, int i, int lan
 __global__ void __launch_bounds__(kThreads) k_density(const __grid_constant__ RtsParams p,
                                                       RtsBuffers b) {
     RTS_ITER_GUARD();
+    const bool all = b.ctr->lists_all;  // every fluid particle, particle order
     const int n = b.ctr->n_pred;
-    const bool all = b.ctr->lists_all;
     const int nthreads = gridDim.x * blockDim.x;
     const int tid = blockIdx.x * blockDim.x + threadIdx.x;
     if ((long long)n * kPG <= nthreads) {
         const int wl = threadIdx.x & 31, lane = wl & (kPG - 1);
         const unsigned gmask = ((1u << kPG) - 1u) << (wl & ~(kPG - 1));
-        for (int t = tid / kPG; t < n; t += nthreads / kPG)
+        for (int t = tid / kPG; t < n; t += nthreads / kPG) {
             density_one<kPG>(p, b, all ? t : b.active[t], lane, gmask);
+        }
     } else {
-        for (int t = tid; t < n; t += nthreads) density_one<1>(p, b, all ? t : b.active[t], 0, 0u);
+        for (int t = tid; t < n; t += nthreads) {
+            density_one<1>(p, b, all ? t : b.active[t], 0, 0u);
+        }
     }
 }
 
@@ -573,17 +594,20 @@ RTS_DEV void pforce_one(const RtsParams &p, const RtsBuffers &b, int i, int lane
 __global__ void __launch_bounds__(kThreads) k_pforces(const __grid_constant__ RtsParams p,
                                                       RtsBuffers b) {
     RTS_ITER_GUARD();
+    const bool all = b.ctr->lists_all;  // every fluid particle, particle order
     const int n = b.ctr->n_force;
-    const bool all = b.ctr->lists_all;
     const int nthreads = gridDim.x * blockDim.x;
     const int tid = blockIdx.x * blockDim.x + threadIdx.x;
     if ((long long)n * kPG <= nthreads) {
         const int wl = threadIdx.x & 31, lane = wl & (kPG - 1);
         const unsigned gmask = ((1u << kPG) - 1u) << (wl & ~(kPG - 1));
-        for (int t = tid / kPG; t < n; t += nthreads / kPG)
+        for (int t = tid / kPG; t < n; t += nthreads / kPG) {
             pforce_one<kPG>(p, b, all ? t : b.list2[t], lane, gmask);
+        }
     } else {
-        for (int t = tid; t < n; t += nthreads) pforce_one<1>(p, b, all ? t : b.list2[t], 0, 0u);
+        for (int t = tid; t < n; t += nthreads) {
+            pforce_one<1>(p, b, all ? t : b.list2[t], 0, 0u);
+        }
     }
 }
 
