@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define RTS_ABI_VERSION 12
+#define RTS_ABI_VERSION 13
 
 /* err_flags bits */
 #define RTS_ERR_ESCAPED   0x1u  /* fluid left the padded grid or non-finite (grid.py:268-273) */
@@ -73,6 +73,9 @@ typedef struct RtsParams {
     int32_t n_sms;         /* grid sizing for persistent kernels */
     int32_t n_regions;     /* region ids 1..n_regions (pcisph.py:294) */
     int32_t n_global;      /* fluid count of the whole scene (x-slab ranks); 0 = n_fluid */
+    int32_t nbr_stride;    /* column stride of the neighbour table: entry q of particle i
+                            * is nbr[q * nbr_stride + i] (column-major, coalesced reads) */
+    int32_t pad2;
 } RtsParams;
 
 /* Device-side counters; copied to the host once per step. */
@@ -187,7 +190,8 @@ typedef struct RtsBuffers {
     int32_t *active;       /* (Nf) compacted CSR slots of active fluid particles */
     int32_t *list2;        /* (Nf) second compacted list */
     /* PCISPH neighbour tables */
-    int32_t *nbr;          /* (Nf, width) neighbour particle indices (grid.py:146-149) */
+    int32_t *nbr;          /* (width, nbr_stride) column-major neighbour particle indices
+                            * (grid.py:146-149 rows, transposed) */
     int32_t *cnt;          /* (Nf) */
     float   *xs4;          /* (Nf+Nb, 4) fluid: x* p ; wall: pos -1 */
     uint8_t *pflag;        /* (Nf) per-iteration set bits (1 = force set) */

@@ -191,7 +191,8 @@ RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshC
     const int z0 = max(0, cz - lay), z1 = min(nz - 1, cz + lay);
     const unsigned lt = (1u << lane) - 1u;
     int cntn = 0;
-    int *row = b.nbr + (size_t)i * p.width;
+    int *row = b.nbr + i;  // entry q at row[q * S]
+    const size_t S = p.nbr_stride;
     for (int ax = max(0, cx - lay); ax <= min(nx - 1, cx + lay); ++ax)
         for (int ay = max(0, cy - lay); ay <= min(ny - 1, cy + lay); ++ay) {
             const int base = (ax * ny + ay) * nz;
@@ -215,7 +216,7 @@ RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshC
                     while (bits) {
                         const int q = __ffsll((long long)bits) - 1;
                         bits &= bits - 1ull;
-                        if (cntn < p.width) row[cntn] = b.order[cb + q];
+                        if (cntn < p.width) row[cntn * S] = b.order[cb + q];
                         ++cntn;
                     }
                 }
@@ -227,7 +228,7 @@ RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshC
                         (__ballot_sync(gmask, in) >> gshift) & (G == 32 ? 0xffffffffu : ((1u << G) - 1u));
                     if (in) {
                         const int slot = cntn + __popc(m & lt);
-                        if (slot < p.width) row[slot] = b.order[kk];
+                        if (slot < p.width) row[slot * S] = b.order[kk];
                     }
                     cntn += __popc(m);
                 }
@@ -238,7 +239,7 @@ RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshC
     const double vxi = b.vel[3 * i], vyi = b.vel[3 * i + 1], vzi = b.vel[3 * i + 2];
     double fx = 0.0, fy = 0.0, fz = 0.0;
     for (int q = lane; q < nrow; q += G) {
-        const int j = row[q];
+        const int j = row[q * S];
         const float4 pj = make_float4(b.pos[3 * j], b.pos[3 * j + 1], b.pos[3 * j + 2], 0.f);
         visc_term(k, p, b, i, j, xi, yi, zi, pj, vxi, vyi, vzi, fx, fy, fz);
     }
@@ -358,14 +359,14 @@ RTS_DEV void density_one(const RtsParams &p, const RtsBuffers &b, int i, int lan
     const float4 a = xs4[i];
     const double xi = a.x, yi = a.y, zi = a.z;
     const int c = b.cnt[i];
-    const int *row = b.nbr + (size_t)i * p.width;
+    const int *row = b.nbr + i;  // entry q at row[q * S]: coalesced across lanes
+    const size_t S = p.nbr_stride;
     double acc = 0.0;
     if (LG == 1) {
-        const int4 *row4 = reinterpret_cast<const int4 *>(row);
         for (int q = 0; q < c; q += 8) {
-            const int4 ja = row4[q >> 2];
-            const int4 jb = row4[(q >> 2) + 1];
-            const int j8[8] = {ja.x, ja.y, ja.z, ja.w, jb.x, jb.y, jb.z, jb.w};
+            int j8[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) j8[u] = q + u < c ? row[(q + u) * S] : i;
             float4 o[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) o[u] = xs4[q + u < c ? j8[u] : i];
@@ -379,7 +380,7 @@ RTS_DEV void density_one(const RtsParams &p, const RtsBuffers &b, int i, int lan
         }
     } else {
         for (int q = lane; q < c; q += LG) {
-            const float4 o = xs4[row[q]];
+            const float4 o = xs4[row[q * S]];
             acc = xadd(acc, poly6(dist2(xsub(xi, (double)o.x), xsub(yi, (double)o.y),
                                         xsub(zi, (double)o.z)),
                                   p.h2, p.c_poly6));
@@ -556,13 +557,14 @@ RTS_DEV void pforce_one(const RtsParams &p, const RtsBuffers &b, int i, int lane
     const double term_i = xmul((double)a.w, inv_rho0_sq);
     const double wall = xadd(term_i, term_i);
     const int c = b.cnt[i];
-    const int *row = b.nbr + (size_t)i * p.width;
+    const int *row = b.nbr + i;  // entry q at row[q * S]: coalesced across lanes
+    const size_t S = p.nbr_stride;
     double fx = 0.0, fy = 0.0, fz = 0.0;
     if (LG == 1) {
-        const int4 *row4 = reinterpret_cast<const int4 *>(row);
         for (int q = 0; q < c; q += 4) {
-            const int4 jj = row4[q >> 2];
-            const int j4[4] = {jj.x, jj.y, jj.z, jj.w};
+            int j4[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) j4[u] = q + u < c ? row[(q + u) * S] : i;
             float4 o4[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) o4[u] = xs4[q + u < c ? j4[u] : i];
@@ -574,7 +576,7 @@ RTS_DEV void pforce_one(const RtsParams &p, const RtsBuffers &b, int i, int lane
         }
     } else {
         for (int q = lane; q < c; q += LG) {
-            const int j = row[q];
+            const int j = row[q * S];
             pforce_pair(p, xi, yi, zi, term_i, wall, m2, inv_rho0_sq, i, j, xs4[j], fx, fy, fz);
         }
 #pragma unroll
@@ -942,7 +944,8 @@ __global__ void k_audit(const __grid_constant__ RtsParams pa, RtsBuffers a, RtsB
         const int cx = trunc_axis(xi, pa.origin[0], pa.inv_block, nx);
         const int cy = trunc_axis(yi, pa.origin[1], pa.inv_block, ny);
         const int cz = trunc_axis(zi, pa.origin[2], pa.inv_block, nz);
-        const int *row = b.nbr + (size_t)i * pa.width;
+        const int *row = b.nbr + i;
+        const size_t S = pa.nbr_stride;
         const int c = b.cnt[i];
         for (int ax = max(0, cx - 1); ax <= min(nx - 1, cx + 1); ++ax)
             for (int ay = max(0, cy - 1); ay <= min(ny - 1, cy + 1); ++ay) {
@@ -957,7 +960,7 @@ __global__ void k_audit(const __grid_constant__ RtsParams pa, RtsBuffers a, RtsB
                     const int j = a.order[k];
                     bool found = false;
                     for (int q = 0; q < c; ++q)
-                        if (row[q] == j) { found = true; break; }
+                        if (row[q * S] == j) { found = true; break; }
                     if (!found) ++lost;
                 }
             }

@@ -146,7 +146,9 @@ class PcisphSolver(_DeviceSolver):
 
     def _realloc_extra(self, cap: int, nb: int) -> None:
         A = self.arena
-        self._nbr = A.alloc("nbr", (cap, NEIGHBOR_WIDTH), torch.int32, 0)
+        stride = -(-max(cap, 1) // 32) * 32
+        self._nbr = A.alloc("nbr", (NEIGHBOR_WIDTH, stride), torch.int32, 0)
+        self.params.nbr_stride = stride
         self._cnt_full = A.alloc("cnt", (cap,), torch.int32, 0)
         A.alloc("xs4", (cap + nb, 4), torch.float32, 0)
         A.alloc("pflag", (cap,), torch.uint8, 0)
@@ -209,7 +211,9 @@ class PcisphSolver(_DeviceSolver):
         self.compute = A.alloc("compute", (n1,), torch.bool, True)[:nf]
         self.in_se = A.alloc("in_se", (n1,), torch.bool, False)[:nf]
         self.in_sob = A.alloc("in_sob", (n1,), torch.bool, False)[:nf]
-        self._nbr = A.alloc("nbr", (n1, NEIGHBOR_WIDTH), torch.int32, 0)
+        stride = -(-n1 // 32) * 32  # column-major table: entry q of particle i at [q, i]
+        self._nbr = A.alloc("nbr", (NEIGHBOR_WIDTH, stride), torch.int32, 0)
+        self.params.nbr_stride = stride
         self.cnt = A.alloc("cnt", (n1,), torch.int32, 0)[:nf]
         A.alloc("xs4", (max(nf + self.n_bound, 1), 4), f32, 0)
         A.alloc("pflag", (n1,), torch.uint8, 0)
@@ -346,7 +350,9 @@ class PcisphSolver(_DeviceSolver):
 
     @property
     def nbr(self) -> torch.Tensor:
-        return self._nbr[: self.n_fluid]
+        """(n_fluid, 128) view of the column-major device table (rows as in
+        the reference, grid.py:146-149)."""
+        return self._nbr[:, : self.n_fluid].T
 
     def delta(self, dt: float) -> float:
         rho0 = self.scene.rest_density
@@ -598,6 +604,7 @@ class PcisphSolver(_DeviceSolver):
         pa.n_fluid, pa.n_bound, pa.n_bcells = nf, nb, ag.n_bcells
         pa.h2 = self.kernel.h2
         pa.width = NEIGHBOR_WIDTH
+        pa.nbr_stride = self.params.nbr_stride
         ag.counters.reset(st)
         ag.launch_rebuild(pa, st)
         N.call("rts_pci_gather", pa, A.buf, st.cuda_stream)
