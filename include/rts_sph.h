@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define RTS_ABI_VERSION 13
+#define RTS_ABI_VERSION 14
 
 /* err_flags bits */
 #define RTS_ERR_ESCAPED   0x1u  /* fluid left the padded grid or non-finite (grid.py:268-273) */
@@ -95,7 +95,9 @@ typedef struct RtsCounters {
     int32_t  any_se;           /* PCISPH: any particle in S_e */
     int32_t  lists_all;        /* PCISPH: this iteration's pred = force = all fluid (no lists) */
     int64_t  missing;          /* neighbour audit: true neighbours absent from tables */
-    double   reserved[7];
+    uint32_t blocks_done;      /* last-block-done counter of the S_e reduction */
+    int32_t  pad3;
+    double   reserved[6];
 } RtsCounters;
 
 /* Per-minor-step record written by the device loop control (StepStats,

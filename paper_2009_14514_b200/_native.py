@@ -12,7 +12,7 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "librtssph.so")
-ABI_VERSION = 13
+ABI_VERSION = 14
 
 _c = ctypes
 _D = _c.c_double
@@ -39,7 +39,8 @@ class RtsCounters(_c.Structure):
         ("err_flags", _c.c_uint32), ("n_escaped", _I), ("first_escaped", _I), ("n_compute", _I),
         ("overflow", _c.c_int64), ("n_sorted", _I), ("n_pred", _I), ("n_force", _I),
         ("n_list", _I), ("fmax_bits", _c.c_uint64), ("sum_rho", _D), ("max_err", _D),
-        ("any_se", _I), ("lists_all", _I), ("missing", _c.c_int64), ("reserved", _D * 7),
+        ("any_se", _I), ("lists_all", _I), ("missing", _c.c_int64),
+        ("blocks_done", _c.c_uint32), ("pad3", _I), ("reserved", _D * 6),
     ]
 
 

@@ -26,7 +26,7 @@ using namespace rts;
 namespace {
 
 constexpr int kThreads = 128;
-constexpr int kRedBlocks = 296;  // fixed partial count -> deterministic sums
+constexpr int kRedBlocks = 592;  // fixed partial count -> deterministic sums
 
 __constant__ int kValidity[5] = {0, 1, 2, 4, 4};  // pcisph.py:66
 
@@ -288,16 +288,60 @@ RTS_DEV void motion_one(const RtsParams &p, const RtsBuffers &b, int i, double d
     reinterpret_cast<float4 *>(b.xs4)[i] = make_float4(xs[0], xs[1], xs[2], b.pres[i]);
 }
 
-// all = 1: every fluid particle; 0: the previous force list; -1: ctl->motion_all
+// float3 rows of 4 consecutive particles as 3 float4 (16-byte aligned)
+RTS_DEV void load12(const float *a, int g, float v[12]) {
+    const float4 *q = reinterpret_cast<const float4 *>(a) + 3 * g;
+    const float4 x = q[0], y = q[1], z = q[2];
+    v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+    v[4] = y.x; v[5] = y.y; v[6] = y.z; v[7] = y.w;
+    v[8] = z.x; v[9] = z.y; v[10] = z.z; v[11] = z.w;
+}
+RTS_DEV void store12(float *a, int g, const float v[12]) {
+    float4 *q = reinterpret_cast<float4 *>(a) + 3 * g;
+    q[0] = make_float4(v[0], v[1], v[2], v[3]);
+    q[1] = make_float4(v[4], v[5], v[6], v[7]);
+    q[2] = make_float4(v[8], v[9], v[10], v[11]);
+}
+
+// all = 1: every fluid particle; 0: the previous force list; -1: ctl->motion_all.
+// The all-particle pass streams four particles per thread with float4 loads.
 __global__ void k_motion(const __grid_constant__ RtsParams p, RtsBuffers b, int all) {
     RTS_ITER_GUARD();
     if (all < 0) all = b.ctl->motion_all;
     const double dim = xmul(p.dt, p.inv_mass);
-    const int n = all ? p.n_fluid : b.ctl->prev_force;
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
-        const int i = all ? t : b.list2[t];
-        if (!is_ghost(b, i)) motion_one(p, b, i, dim);
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+    if (!all) {
+        const int n = b.ctl->prev_force;
+        for (int t = tid; t < n; t += nt) {
+            const int i = b.list2[t];
+            if (!is_ghost(b, i)) motion_one(p, b, i, dim);
+        }
+        return;
     }
+    const int nf = p.n_fluid, ng = nf / 4;
+    float4 *xs4 = reinterpret_cast<float4 *>(b.xs4);
+    for (int g = tid; g < ng; g += nt) {
+        float fe[12], fp[12], v[12], x[12];
+        load12(b.force, g, fe);
+        load12(b.f_p, g, fp);
+        load12(b.vel, g, v);
+        load12(b.pos, g, x);
+        const float4 pr = reinterpret_cast<const float4 *>(b.pres)[g];
+        const float prs[4] = {pr.x, pr.y, pr.z, pr.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            float xs[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const int c = 3 * q + a;
+                const double vv = xadd((double)v[c], xmul(dim, xadd((double)fe[c], (double)fp[c])));
+                xs[a] = (float)xadd((double)x[c], xmul(p.dt, vv));
+            }
+            if (!is_ghost(b, 4 * g + q)) xs4[4 * g + q] = make_float4(xs[0], xs[1], xs[2], prs[q]);
+        }
+    }
+    for (int i = 4 * ng + tid; i < nf; i += nt)
+        if (!is_ghost(b, i)) motion_one(p, b, i, dim);
 }
 
 // set membership for one iteration (pcisph.py:634-643); row_mask bit n set
@@ -423,40 +467,65 @@ __global__ void __launch_bounds__(kThreads) k_density(const __grid_constant__ Rt
     }
 }
 
-// S_e, S_e blocks, max err, sum rho* (deterministic), any S_e
+// S_e, S_e blocks, max err, sum rho* and any S_e over all fluid
+// (pcisph.py:662, 421-430, 682-683).  Each block owns a fixed contiguous
+// chunk (multiple of 4: double2/float4/uchar4 vector accesses) and sums it
+// in a fixed tree; the last block to finish adds the block partials in
+// index order -- the sum is deterministic and needs no further launch.
+RTS_DEV void se_one(const RtsParams &p, const RtsBuffers &b, int i, double e, float rho,
+                    int with_se, double thr, int gen, double &s, double &m, int &any,
+                    uint8_t &flag) {
+    const bool se = with_se && e > thr;
+    flag = se;
+    if (se) {
+        any = 1;
+        const int c = b.fluid_cells[i];
+        if (atomicExch(&b.se_stamp[c], gen) != gen) {  // first S_e particle of block c
+            const int nx = p.dims[0], ny = p.dims[1], nz = p.dims[2];
+            const int cz = c % nz, cy = (c / nz) % ny, cx = c / (ny * nz);
+            for (int ax = max(0, cx - 1); ax <= min(nx - 1, cx + 1); ++ax)
+                for (int ay = max(0, cy - 1); ay <= min(ny - 1, cy + 1); ++ay) {
+                    const int base = (ax * ny + ay) * nz;
+                    for (int az = max(0, cz - 1); az <= min(nz - 1, cz + 1); ++az)
+                        b.near_stamp[base + az] = gen;
+                }
+        }
+    }
+    if (is_ghost(b, i)) return;  // reductions over owned particles (all-reduced)
+    if (e > m) m = e;
+    s = xadd(s, (double)rho);
+}
+
 __global__ void __launch_bounds__(256) k_se_reduce(const __grid_constant__ RtsParams p,
                                                    RtsBuffers b, int with_se) {
     RTS_ITER_GUARD();
     __shared__ double ssum[8];
+    __shared__ bool last;
     const int nf = p.n_fluid;
     const double thr = xmul(0.5, p.eta_max);
-    // contiguous chunk per block, fixed tree inside -> order-independent of timing
-    const int chunk = (nf + gridDim.x - 1) / gridDim.x;
+    const int chunk = (((nf + gridDim.x - 1) / gridDim.x) + 3) & ~3;
     const int i0 = blockIdx.x * chunk, i1 = min(nf, i0 + chunk);
     const int gen = b.ctl ? b.ctl->stamp + 1 : 1;
-    const int nx = p.dims[0], ny = p.dims[1], nz = p.dims[2];
     double s = 0.0, m = 0.0;
     int any = 0;
-    for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
-        const double e = b.err[i];
-        const bool se = with_se && e > thr;
-        if (with_se) b.in_se[i] = se;
-        if (se) {
-            any = 1;
-            const int c = b.fluid_cells[i];
-            if (atomicExch(&b.se_stamp[c], gen) != gen) {  // first S_e particle of block c
-                const int cz = c % nz, cy = (c / nz) % ny, cx = c / (ny * nz);
-                for (int ax = max(0, cx - 1); ax <= min(nx - 1, cx + 1); ++ax)
-                    for (int ay = max(0, cy - 1); ay <= min(ny - 1, cy + 1); ++ay) {
-                        const int base = (ax * ny + ay) * nz;
-                        for (int az = max(0, cz - 1); az <= min(nz - 1, cz + 1); ++az)
-                            b.near_stamp[base + az] = gen;
-                    }
+    for (int g = i0 + 4 * threadIdx.x; g < i1; g += 4 * blockDim.x) {
+        if (g + 3 < i1) {
+            const double2 e01 = *reinterpret_cast<const double2 *>(b.err + g);
+            const double2 e23 = *reinterpret_cast<const double2 *>(b.err + g + 2);
+            const float4 r = *reinterpret_cast<const float4 *>(b.rho + g);
+            uchar4 f;
+            se_one(p, b, g, e01.x, r.x, with_se, thr, gen, s, m, any, f.x);
+            se_one(p, b, g + 1, e01.y, r.y, with_se, thr, gen, s, m, any, f.y);
+            se_one(p, b, g + 2, e23.x, r.z, with_se, thr, gen, s, m, any, f.z);
+            se_one(p, b, g + 3, e23.y, r.w, with_se, thr, gen, s, m, any, f.w);
+            if (with_se) *reinterpret_cast<uchar4 *>(b.in_se + g) = f;
+        } else {
+            for (int i = g; i < i1; ++i) {
+                uint8_t f;
+                se_one(p, b, i, b.err[i], b.rho[i], with_se, thr, gen, s, m, any, f);
+                if (with_se) b.in_se[i] = f;
             }
         }
-        if (is_ghost(b, i)) continue;  // reductions over owned particles (allreduced)
-        if (e > m) m = e;
-        s = xadd(s, (double)b.rho[i]);
     }
     for (int o = 16; o > 0; o >>= 1) {
         s = xadd(s, __shfl_down_sync(0xffffffffu, s, o));
@@ -476,23 +545,24 @@ __global__ void __launch_bounds__(256) k_se_reduce(const __grid_constant__ RtsPa
         double t = 0.0;
         for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t = xadd(t, ssum[w]);
         b.partial[blockIdx.x] = t;
+        __threadfence();
+        last = atomicAdd(&b.ctr->blocks_done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    double t = 0.0;  // fixed-order sum of the block partials
+    for (int q = threadIdx.x; q < (int)gridDim.x; q += blockDim.x) t = xadd(t, __ldcg(b.partial + q));
+    for (int o = 16; o > 0; o >>= 1) t = xadd(t, __shfl_down_sync(0xffffffffu, t, o));
+    if (lane == 0) ssum[warp] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double u = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) u = xadd(u, ssum[w]);
+        b.ctr->sum_rho = u;
+        b.ctr->blocks_done = 0;
     }
 }
 
-__global__ void k_sum_partials(RtsBuffers b, int n) {
-    if (loop_done(b)) return;
-    __shared__ double ssum[32];
-    double s = 0.0;
-    for (int q = threadIdx.x; q < n; q += blockDim.x) s = xadd(s, b.partial[q]);
-    for (int o = 16; o > 0; o >>= 1) s = xadd(s, __shfl_down_sync(0xffffffffu, s, o));
-    if ((threadIdx.x & 31) == 0) ssum[threadIdx.x >> 5] = s;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double t = 0.0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t = xadd(t, ssum[w]);
-        b.ctr->sum_rho = t;
-    }
-}
 
 // observed blocks (regions.py:110-125): occupied and (bordering a strictly
 // smaller region, or bordering an S_e block without being one); -> block_tmp
@@ -614,51 +684,119 @@ __global__ void __launch_bounds__(kThreads) k_pforces(const __grid_constant__ Rt
 }
 
 // _integrate (pcisph.py:759-768) + validity countdown (pcisph.py:580-584)
+RTS_DEV void integrate_one(const RtsParams &p, const RtsBuffers &b, int i, int countdown,
+                           int gen, double dim) {
+    // public x* = the last prediction; S_ob from the final S_e generation
+    const float4 xs = reinterpret_cast<const float4 *>(b.xs4)[i];
+    b.xstar[3 * i] = xs.x;
+    b.xstar[3 * i + 1] = xs.y;
+    b.xstar[3 * i + 2] = xs.z;
+    if (countdown) b.in_sob[i] = observed_block(b, b.fluid_cells[i], gen);
+    float nx[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double f = xadd((double)b.force[3 * i + a], (double)b.f_p[3 * i + a]);
+        double v = xadd((double)b.vel[3 * i + a], xmul(f, dim));
+        double x = xadd((double)b.pos[3 * i + a], xmul(v, p.dt));
+        if (x < p.clamp_lo[a]) {
+            x = p.clamp_lo[a];
+            v = 0.0;
+        } else if (x > p.clamp_hi[a]) {
+            x = p.clamp_hi[a];
+            v = 0.0;
+        }
+        b.pos[3 * i + a] = (float)x;
+        b.vel[3 * i + a] = (float)v;
+        nx[a] = (float)x;
+    }
+    if (countdown) {
+        reinterpret_cast<float4 *>(b.cpos)[b.slot_of[i]] = make_float4(nx[0], nx[1], nx[2], 0.f);
+        int v = b.validity[i] - 1;
+        const bool expired = v <= 0;
+        if (expired) {
+            const int8_t r = b.region[i];
+            v = kValidity[r < 0 ? 0 : (r > 4 ? 4 : r)];
+        }
+        b.validity[i] = v;
+        b.compute[i] = expired;
+    }
+}
+
+// _integrate (pcisph.py:759-768) + validity countdown (pcisph.py:580-584);
+// four particles per thread with vector loads/stores when no ghost rows exist
 __global__ void k_integrate(const __grid_constant__ RtsParams p, RtsBuffers b, int countdown) {
     RTS_MINOR_GUARD();
     const double dim = xmul(p.dt, p.inv_mass);
     const int gen = b.ctl ? b.ctl->stamp : 0;
     if (b.ctl && countdown && blockIdx.x == 0 && threadIdx.x == 0)
         b.ctl->stats[b.ctl->minor].t_looped = gtimer();
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.n_fluid;
-         i += gridDim.x * blockDim.x) {
-        if (is_ghost(b, i)) continue;
-        // public x* = the last prediction; S_ob from the final S_e generation
-        const float4 xs = reinterpret_cast<const float4 *>(b.xs4)[i];
-        b.xstar[3 * i] = xs.x;
-        b.xstar[3 * i + 1] = xs.y;
-        b.xstar[3 * i + 2] = xs.z;
-        if (countdown) b.in_sob[i] = observed_block(b, b.fluid_cells[i], gen);
-        float nx[3];
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+    const int nf = p.n_fluid;
+    if (b.ghost) {
+        for (int i = tid; i < nf; i += nt)
+            if (!is_ghost(b, i)) integrate_one(p, b, i, countdown, gen, dim);
+        return;
+    }
+    const int ng = nf / 4;
+    for (int g = tid; g < ng; g += nt) {
+        float fe[12], fp[12], v[12], x[12], xsv[12];
+        load12(b.force, g, fe);
+        load12(b.f_p, g, fp);
+        load12(b.vel, g, v);
+        load12(b.pos, g, x);
 #pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            const double f = xadd((double)b.force[3 * i + a], (double)b.f_p[3 * i + a]);
-            double v = xadd((double)b.vel[3 * i + a], xmul(f, dim));
-            double x = xadd((double)b.pos[3 * i + a], xmul(v, p.dt));
-            if (x < p.clamp_lo[a]) {
-                x = p.clamp_lo[a];
-                v = 0.0;
-            } else if (x > p.clamp_hi[a]) {
-                x = p.clamp_hi[a];
-                v = 0.0;
-            }
-            b.pos[3 * i + a] = (float)x;
-            b.vel[3 * i + a] = (float)v;
-            nx[a] = (float)x;
+        for (int q = 0; q < 4; ++q) {
+            const float4 xs = reinterpret_cast<const float4 *>(b.xs4)[4 * g + q];
+            xsv[3 * q] = xs.x;
+            xsv[3 * q + 1] = xs.y;
+            xsv[3 * q + 2] = xs.z;
         }
-        if (countdown)
-            reinterpret_cast<float4 *>(b.cpos)[b.slot_of[i]] = make_float4(nx[0], nx[1], nx[2], 0.f);
-        if (countdown) {
-            int v = b.validity[i] - 1;
-            const bool expired = v <= 0;
-            if (expired) {
-                const int8_t r = b.region[i];
-                v = kValidity[r < 0 ? 0 : (r > 4 ? 4 : r)];
+        store12(b.xstar, g, xsv);
+#pragma unroll
+        for (int c = 0; c < 12; ++c) {
+            const int a = c % 3;
+            const double f = xadd((double)fe[c], (double)fp[c]);
+            double vv = xadd((double)v[c], xmul(f, dim));
+            double xx = xadd((double)x[c], xmul(vv, p.dt));
+            if (xx < p.clamp_lo[a]) {
+                xx = p.clamp_lo[a];
+                vv = 0.0;
+            } else if (xx > p.clamp_hi[a]) {
+                xx = p.clamp_hi[a];
+                vv = 0.0;
             }
-            b.validity[i] = v;
-            b.compute[i] = expired;
+            x[c] = (float)xx;
+            v[c] = (float)vv;
+        }
+        store12(b.pos, g, x);
+        store12(b.vel, g, v);
+        if (countdown) {
+            const int4 cells = reinterpret_cast<const int4 *>(b.fluid_cells)[g];
+            const int4 slots = reinterpret_cast<const int4 *>(b.slot_of)[g];
+            int4 val = reinterpret_cast<const int4 *>(b.validity)[g];
+            const char4 reg = reinterpret_cast<const char4 *>(b.region)[g];
+            const int cl[4] = {cells.x, cells.y, cells.z, cells.w};
+            const int sl[4] = {slots.x, slots.y, slots.z, slots.w};
+            int vl[4] = {val.x, val.y, val.z, val.w};
+            const int rg[4] = {reg.x, reg.y, reg.z, reg.w};
+            uint8_t sob[4], cmp[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                sob[q] = observed_block(b, cl[q], gen);
+                reinterpret_cast<float4 *>(b.cpos)[sl[q]] =
+                    make_float4(x[3 * q], x[3 * q + 1], x[3 * q + 2], 0.f);
+                int vv = vl[q] - 1;
+                const bool expired = vv <= 0;
+                if (expired) vv = kValidity[rg[q] < 0 ? 0 : (rg[q] > 4 ? 4 : rg[q])];
+                vl[q] = vv;
+                cmp[q] = expired;
+            }
+            reinterpret_cast<int4 *>(b.validity)[g] = make_int4(vl[0], vl[1], vl[2], vl[3]);
+            reinterpret_cast<uchar4 *>(b.compute)[g] = make_uchar4(cmp[0], cmp[1], cmp[2], cmp[3]);
+            reinterpret_cast<uchar4 *>(b.in_sob)[g] = make_uchar4(sob[0], sob[1], sob[2], sob[3]);
         }
     }
+    for (int i = 4 * ng + tid; i < nf; i += nt) integrate_one(p, b, i, countdown, gen, dim);
 }
 
 // _mark_timestep_updates (pcisph.py:718-755), block part: block_raw holds the
@@ -823,16 +961,10 @@ __global__ void k_control(const __grid_constant__ RtsParams p, RtsBuffers b, int
     RtsControl *c = b.ctl;
     RtsCounters *ctr = b.ctr;
     int done = c->done;
-    // fixed-order sum of the per-block rho* partials (deterministic)
-    double part = 0.0;
-    if (!done)
-        for (int q = threadIdx.x; q < n_part; q += 32) part = xadd(part, b.partial[q]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) part = xadd(part, __shfl_xor_sync(0xffffffffu, part, o));
+    (void)n_part;  // sum_rho: completed by k_se_reduce's last block (and all-reduced on ranks)
     if (threadIdx.x != 0) return;
     const int n_all = p.n_global > 0 ? p.n_global : p.n_fluid;
     if (!done) {
-        if (n_part > 0) ctr->sum_rho = part;  // n_part == 0: sum_rho already reduced (ranks)
         c->snap_op = 0;
         c->it += 1;
         c->corrected += sync_mode ? n_all : ctr->n_pred;
@@ -1033,15 +1165,11 @@ int rts_pci_density(const RtsParams *p, const RtsBuffers *b, void *stream) {
 int rts_pci_se_reduce(const RtsParams *p, const RtsBuffers *b, int with_se, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
 
-    int blocks = (p->n_fluid + 255) / 256;
+    int blocks = (p->n_fluid + 1023) / 1024;
     if (blocks > kRedBlocks) blocks = kRedBlocks;
     if (blocks < 1) blocks = 1;
     rts_note_launch(), k_se_reduce<<<blocks, 256, 0, s>>>(*p, *b, with_se);
     RTS_LAUNCH_CHECK();
-    if (!b->ctl || p->n_global > 0) {  // outside the device loop / ranks: finish the sum here
-        rts_note_launch(), k_sum_partials<<<1, 1024, 0, s>>>(*b, blocks);
-        RTS_LAUNCH_CHECK();
-    }
     return 0;
 }
 
@@ -1145,10 +1273,7 @@ int rts_pci_control(const RtsParams *p, const RtsBuffers *b, int sync_mode,
                     unsigned long long cond_handle, int local_attempts, int iteration_cap,
                     void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
-    int n_part = (p->n_fluid + 255) / 256;
-    if (n_part > kRedBlocks) n_part = kRedBlocks;
-    if (n_part < 1) n_part = 1;
-    if (p->n_global > 0) n_part = 0;  // ranks: sum_rho was reduced across ranks already
+    const int n_part = 0;  // k_se_reduce's last block already summed the partials
     rts_note_launch(), k_control<<<1, 32, 0, s>>>(*p, *b, sync_mode, cond_handle, local_attempts,
                                                   iteration_cap, n_part);
     RTS_LAUNCH_CHECK();
