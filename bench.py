@@ -88,7 +88,8 @@ def make_device_solver(kind: str, device):
 
 # per-kernel algorithmic bytes (fp32 state, int32 indices, neighbour data
 # reused on chip) -- DESIGN.md "Kernels and their rooflines"
-def algo_bytes(name: str, solver, c_mean: float, rec: dict) -> float:
+def algo_bytes(name: str, solver, c_mean: float, rec: dict, launches: int = 1) -> float:
+    """Algorithmic bytes of all recorded launches of one entry point."""
     nf = solver.n_fluid
     if name == "rts_pci_density":
         return rec["pred"] * (40 + 4 * c_mean) + rec["force"] * 12
@@ -99,11 +100,11 @@ def algo_bytes(name: str, solver, c_mean: float, rec: dict) -> float:
     if name == "rts_pci_motion":
         return rec["motion"] * 84
     if name == "rts_pci_sets":
-        return nf * 9 + 4 * (rec["pred"] + rec["force"])
+        return launches * nf * 9 + 4 * (rec["pred"] + rec["force"])
     if name == "rts_pci_se_reduce":
-        return nf * 13
+        return launches * nf * 13
     if name == "rts_pci_integrate":
-        return nf * 82
+        return launches * nf * 82
     return 0.0
 
 
@@ -121,7 +122,7 @@ class ClockSampler:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={q}", "--format=csv,noheader",
-                 "-lms", "100"], stdout=self.fh, stderr=subprocess.DEVNULL)
+                 "-lms", "20"], stdout=self.fh, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
 
@@ -218,7 +219,7 @@ def run_reference_arm(args, rank: int, world: int) -> None:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=25)
+    ap.add_argument("--steps", type=int, default=125)  # 125 majors = configs[1]'s 500 steps
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -327,7 +328,7 @@ def main():
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    alg = algo_bytes(dom, solver, c_mean, rec)
+    alg = algo_bytes(dom, solver, c_mean, rec, counts[dom])
     achieved = alg / totals[dom] / 1e9 if totals[dom] > 0 else 0.0
     traffic = None
     tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -338,6 +339,11 @@ def main():
                 "launches": counts[dom], "kernel_s": round(totals[dom], 6),
                 "algorithmic_bytes": alg,
                 "share_of_step": round(totals[dom] / max(1e-12, sum(totals.values())), 3),
+                "kernels": {k: {"s": round(totals[k], 6), "launches": counts[k],
+                                "achieved_gbs": round(algo_bytes(k, solver, c_mean, rec,
+                                                                 counts[k]) /
+                                                      max(totals[k], 1e-12) / 1e9, 1)}
+                            for k in kernels if counts[k]},
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s"}
 
     # ---- e2e through the public API with host-owned state ----------------------

@@ -212,7 +212,8 @@ typedef struct RtsBuffers {
 int rts_abi_version(void);
 /* Query the current device; returns its SM count or a negative cudaError. */
 int rts_device_sms(void);
-/* Number of librtssph kernels launched by this process so far. */
+/* Number of librtssph kernels launched (or captured into graphs) by this
+ * process so far. */
 long long rts_launch_count(void);
 /* Zero-filled cudaMemsetAsync helper so hosts need not link cudart. */
 int rts_memset(void *dst, int value, int64_t bytes, void *stream);
@@ -320,6 +321,9 @@ void *rts_pci_graph_create(const RtsParams *p, const RtsBuffers *b, int mode, in
                            int local_attempts, int iteration_cap, int *err);
 int rts_graph_launch(void *graph, void *stream);
 void rts_graph_destroy(void *graph);
+/* Kernel nodes of a graph: run once per launch / once per correction
+ * iteration of each conditional while body (for launch accounting). */
+int rts_graph_kernel_counts(void *graph, long long *static_kernels, long long *body_kernels);
 
 /* ---- RTS-WCSPH (wcsph.py) -------------------------------------------- */
 /* Validity countdown / pre-emption (wcsph.py:262-266) fused with the sorted

@@ -160,6 +160,8 @@ def load(path: str = LIB_PATH):
     lib.rts_pci_graph_create.restype = _c.c_void_p
     lib.rts_wcsph_graph_create.argtypes = [_PP, _PB, _c.POINTER(_c.c_int)]
     lib.rts_wcsph_graph_create.restype = _c.c_void_p
+    lib.rts_graph_kernel_counts.argtypes = [_P, _c.POINTER(_c.c_longlong), _c.POINTER(_c.c_longlong)]
+    lib.rts_graph_kernel_counts.restype = _c.c_int
     lib.rts_graph_destroy.argtypes = [_P]
     lib.rts_graph_destroy.restype = None
     if lib.rts_abi_version() != ABI_VERSION:
@@ -168,8 +170,23 @@ def load(path: str = LIB_PATH):
     return lib
 
 
+_graph_launched = 0  # kernels executed inside graph launches (counted by the host)
+
+
 def launch_count() -> int:
-    return int(load().rts_launch_count())
+    """librtssph kernels launched directly plus those executed by graphs."""
+    return int(load().rts_launch_count()) + _graph_launched
+
+
+def graph_kernel_counts(graph) -> tuple[int, int]:
+    a, b = _c.c_longlong(0), _c.c_longlong(0)
+    load().rts_graph_kernel_counts(graph, _c.byref(a), _c.byref(b))
+    return int(a.value), int(b.value)
+
+
+def note_graph_kernels(n: int) -> None:
+    global _graph_launched
+    _graph_launched += int(n)
 
 
 def call(name: str, *args) -> None:

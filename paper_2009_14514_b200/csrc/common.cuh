@@ -177,11 +177,14 @@ RTS_DEV int warp_count_add(bool pred, int *count) {
 
 // kernel-launch counter (reported by bench.py as gpu_launches)
 extern "C" void rts_note_launch(void);
+extern "C" long long rts_launch_count(void);
 
 // owned CUDA graph (rts_pci_graph_create / rts_wcsph_graph_create)
 struct RtsGraph {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
+    long long static_kernels = 0;  // kernel nodes outside conditional bodies
+    long long body_kernels = 0;    // kernel nodes per conditional-body iteration
 };
 
 // launch helpers

@@ -1308,6 +1308,8 @@ int rts_pci_minor_tail(const RtsParams *p, const RtsBuffers *b, int minor, int l
 }
 
 // ---- CUDA graphs -----------------------------------------------------------
+static long long g_body_kernels = 0;
+
 static int add_while_loop(cudaStream_t cs, const RtsParams *p, const RtsBuffers *b, int sync_mode,
                           int local_attempts, int iteration_cap) {
     cudaStreamCaptureStatus st;
@@ -1332,8 +1334,10 @@ static int add_while_loop(cudaStream_t cs, const RtsParams *p, const RtsBuffers 
     cudaStreamCreateWithFlags(&bs, cudaStreamNonBlocking);
     e = cudaStreamBeginCaptureToGraph(bs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed);
     if (e != cudaSuccess) return (int)e;
+    const long long before = rts_launch_count();
     int rc = rts_pci_iteration(p, b, sync_mode, (unsigned long long)h, local_attempts,
                                iteration_cap, bs);
+    g_body_kernels = rts_launch_count() - before;
     cudaGraph_t out;
     e = cudaStreamEndCapture(bs, &out);
     cudaStreamDestroy(bs);
@@ -1359,6 +1363,8 @@ void *rts_pci_graph_create(const RtsParams *p, const RtsBuffers *b, int mode, in
     cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed);
     if (e != cudaSuccess) { *err = (int)e; cudaStreamDestroy(cs); return nullptr; }
     int rc = 0;
+    const long long count0 = rts_launch_count();
+    g_body_kernels = 0;
     do {
         if ((rc = reset_counters(b, cs))) break;
         if ((rc = rts_pci_major_begin(p, b, cs))) break;
@@ -1392,6 +1398,9 @@ void *rts_pci_graph_create(const RtsParams *p, const RtsBuffers *b, int mode, in
     }
     RtsGraph *rg = new RtsGraph;
     rg->graph = g;
+    const int loops = mode == 0 ? n_minor : 1;
+    rg->body_kernels = g_body_kernels;
+    rg->static_kernels = rts_launch_count() - count0 - loops * g_body_kernels;
     e = cudaGraphInstantiate(&rg->exec, g, 0);
     if (e != cudaSuccess) {
         *err = (int)e;
@@ -1400,6 +1409,15 @@ void *rts_pci_graph_create(const RtsParams *p, const RtsBuffers *b, int mode, in
         return nullptr;
     }
     return rg;
+}
+
+// kernel nodes of a graph: static ones (run once per launch) and those of one
+// conditional-body iteration (run once per correction iteration)
+int rts_graph_kernel_counts(void *graph, long long *static_kernels, long long *body_kernels) {
+    RtsGraph *rg = (RtsGraph *)graph;
+    *static_kernels = rg->static_kernels;
+    *body_kernels = rg->body_kernels;
+    return 0;
 }
 
 int rts_graph_launch(void *graph, void *stream) {

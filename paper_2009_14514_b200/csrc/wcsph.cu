@@ -348,6 +348,7 @@ void *rts_wcsph_graph_create(const RtsParams *p, const RtsBuffers *b, int *err) 
     cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed);
     if (e != cudaSuccess) { *err = (int)e; cudaStreamDestroy(cs); return nullptr; }
     int rc = 0;
+    const long long count0 = rts_launch_count();
     do {
         if ((rc = rts_counters_reset(b, cs))) break;
         if ((rc = rts_grid_keys(p, b, p->rts, 0, cs))) break;
@@ -368,6 +369,7 @@ void *rts_wcsph_graph_create(const RtsParams *p, const RtsBuffers *b, int *err) 
     }
     RtsGraph *rg = new RtsGraph;
     rg->graph = g;
+    rg->static_kernels = rts_launch_count() - count0;
     e = cudaGraphInstantiate(&rg->exec, g, 0);
     if (e != cudaSuccess) {
         *err = (int)e;

@@ -423,8 +423,10 @@ class PcisphSolver(_DeviceSolver):
         dt = self.dt
         self._prepare(dt)
         st = self._stream()
+        graph = None
         if self.use_graphs:
-            N.call("rts_graph_launch", self._graph(1, 1), st.cuda_stream)
+            graph = self._graph(1, 1)
+            N.call("rts_graph_launch", graph, st.cuda_stream)
         else:
             N.call("rts_counters_reset", self.arena.buf, st.cuda_stream)
             self._call("rts_pci_major_begin")
@@ -437,6 +439,9 @@ class PcisphSolver(_DeviceSolver):
             self._call("rts_pci_integrate", 0)
             self._call("rts_pci_minor_end", 0)
         ctl, c = self._read_control()
+        if graph is not None:
+            n_static, n_body = N.graph_kernel_counts(graph)
+            N.note_graph_kernels(n_static + n_body * max(0, ctl.stats[0].iterations))
         self._raise_control(ctl, c)
         ms = ctl.stats[0]
         it = int(ms.iterations)
@@ -483,8 +488,10 @@ class PcisphSolver(_DeviceSolver):
         st = self._stream()
         audit = bool(self.audit_neighbors)
         missed = []
+        graph = None
         if self.use_graphs and self._xch is None and not audit:
-            N.call("rts_graph_launch", self._graph(0, n_minor), st.cuda_stream)
+            graph = self._graph(0, n_minor)
+            N.call("rts_graph_launch", graph, st.cuda_stream)
         else:
             N.call("rts_counters_reset", self.arena.buf, st.cuda_stream)
             self._call("rts_pci_major_begin")
@@ -518,6 +525,10 @@ class PcisphSolver(_DeviceSolver):
                         self._call("rts_pci_mark_updates")
                     self._call("rts_pci_minor_end", j)
         ctl, c = self._read_control()
+        if graph is not None:  # launch accounting of the graph's kernel nodes
+            n_static, n_body = N.graph_kernel_counts(graph)
+            its = sum(max(0, ctl.stats[j].iterations) for j in range(n_minor))
+            N.note_graph_kernels(n_static + n_body * its)
         rows = []
         early = False
         nf = self.n_fluid

@@ -364,7 +364,9 @@ class WcsphSolver(_DeviceSolver):
         rts = self.mode == "rts"
         if self.use_graphs and rts and self._ktimes is None:  # baseline dt varies per step
             tm.start(stream)
-            N.call("rts_graph_launch", self._graph(), stream.cuda_stream)
+            graph = self._graph()
+            N.call("rts_graph_launch", graph, stream.cuda_stream)
+            N.note_graph_kernels(N.graph_kernel_counts(graph)[0])
             tm.mark("physics", stream)
             if not read:
                 return None
