@@ -338,6 +338,7 @@ def main():
                 "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": dom,
                 "launches": counts[dom], "kernel_s": round(totals[dom], 6),
                 "algorithmic_bytes": alg,
+                "algorithmic_bytes_per_launch": round(alg / max(1, counts[dom])),
                 "share_of_step": round(totals[dom] / max(1e-12, sum(totals.values())), 3),
                 "kernels": {k: {"s": round(totals[k], 6), "launches": counts[k],
                                 "achieved_gbs": round(algo_bytes(k, solver, c_mean, rec,
