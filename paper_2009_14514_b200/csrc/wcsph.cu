@@ -80,13 +80,17 @@ __device__ __forceinline__ int block_spans(const RtsParams &p, const int *starts
     return n;
 }
 
-// ---- pair kernels: two passes per active particle ----------------------
-// Pass 1 walks the nine CSR spans with four float4 candidates in flight and
-// collects the slots of true neighbours (exact reference membership, see
-// in_support) into a per-thread shared-memory list, in reference order.
-// Pass 2 evaluates the fp64 pair terms over that list without divergence
-// and sums them sequentially in that order, so rho / force equal the
-// reference's fp64 values from a common state (up to the fp32 store).
+// ---- pair kernels -------------------------------------------------------
+// The density pass walks the nine CSR spans with four float4 candidates in
+// flight and collects the slots of true neighbours (exact reference
+// membership, see in_support) into a per-thread shared-memory list, in
+// reference order; it then evaluates the fp64 pair terms over that list
+// without divergence and sums them sequentially in that order, so rho
+// equals the reference's fp64 value from a common state (up to the fp32
+// store).  The list is also kept in a column-major table (column = index in
+// the active list, nbr[q * nbr_stride + t], cnt[t]), so the force pass of
+// the same step reads its neighbours instead of searching again (positions
+// do not change in between).
 constexpr int kHitCap = 64;  // list entries per thread (overflow -> direct path)
 
 RTS_DEV int collect_hits(const RtsParams &p, const RtsBuffers &b, const float4 *cpos, int cell,
@@ -122,6 +126,7 @@ __global__ void __launch_bounds__(kThreads) k_density(const __grid_constant__ Rt
     const int n_act = b.ctr->n_compute;
     const float4 *cpos = reinterpret_cast<const float4 *>(b.cpos);
     const Band bd = make_band(p.h2);
+    const size_t S = p.nbr_stride;
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n_act; t += gridDim.x * blockDim.x) {
         const int k = b.active[t];
         const int j = b.order[k];
@@ -129,6 +134,9 @@ __global__ void __launch_bounds__(kThreads) k_density(const __grid_constant__ Rt
         const double xi = a.x, yi = a.y, zi = a.z;
         int n_all;
         const int nh = collect_hits(p, b, cpos, b.fluid_cells[j], a, bd, hits, &n_all);
+        b.cnt[t] = n_all;
+        int *col = b.nbr + t;
+        for (int q = 0; q < nh; ++q) col[q * S] = hits[q * kThreads];
         double acc = 0.0;
         if (n_all <= kHitCap) {
             for (int q = 0; q < nh; ++q) {
@@ -209,8 +217,7 @@ RTS_DEV void force_pair(const RtsParams &p, double xi, double yi, double zi, flo
 __global__ void __launch_bounds__(kThreads) k_forces(const __grid_constant__ RtsParams p,
                                                      RtsBuffers b) {
     if (fatal(b.ctr)) return;
-    __shared__ int s_hits[kHitCap * kThreads];
-    int *hits = s_hits + threadIdx.x;
+    const size_t S = p.nbr_stride;
     const int n_act = b.ctr->n_compute;
     const float4 *cpos = reinterpret_cast<const float4 *>(b.cpos);
     const float4 *cvel = reinterpret_cast<const float4 *>(b.cvel);
@@ -228,12 +235,12 @@ __global__ void __launch_bounds__(kThreads) k_forces(const __grid_constant__ Rts
         const double term_i = xdiv(p_i, xmul(rho_i, rho_i));
         const double inv_rho_i = xdiv(1.0, rho_i);
         const double wall_term = xadd(term_i, xmul(p_i, inv_rho0_sq));
-        int n_all;
-        const int nh = collect_hits(p, b, cpos, b.fluid_cells[j], a, bd, hits, &n_all);
+        const int n_all = b.cnt[t];  // the density pass's neighbour list of slot k
+        const int *col = b.nbr + t;
         double fx = 0.0, fy = 0.0, fz = 0.0;
         if (n_all <= kHitCap) {
-            for (int q = 0; q < nh; ++q) {
-                const int kq = hits[q * kThreads];
+            for (int q = 0; q < n_all; ++q) {
+                const int kq = col[q * S];
                 if (kq == k) continue;
                 force_pair(p, xi, yi, zi, va, inv_rho_i, term_i, wall_term, m2, mum2, cpos[kq],
                            cvel[kq], fx, fy, fz);

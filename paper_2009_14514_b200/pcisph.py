@@ -285,7 +285,8 @@ class PcisphSolver(_DeviceSolver):
         return int(ctl.local_reverted) if ctl is not None else 0
 
     def _graph(self, mode: int, n_minor: int):
-        key = (mode, n_minor, bytes(self.params), self.local_attempts, self.iteration_cap)
+        key = (mode, n_minor, bytes(self.params), bytes(self.arena.buf), self.local_attempts,
+               self.iteration_cap)
         g = self._graphs.get(key)
         if g is None:
             if len(self._graphs) >= 8:

@@ -36,6 +36,7 @@ from .stats import StepStats
 __all__ = ["WcsphSolver", "tait_pressure", "NEIGHBOR_WIDTH"]
 
 NEIGHBOR_WIDTH = 128
+HIT_CAP = 64  # wcsph.cu kHitCap: per-particle list of the density pass
 
 
 def tait_pressure(rho: float, rest_density: float, sound_speed: float) -> float:
@@ -232,6 +233,13 @@ class WcsphSolver(_DeviceSolver):
     """Weakly compressible SPH, ``mode`` "baseline" or "rts" (wcsph.py:108)."""
 
     mode_names = ("baseline", "rts")
+
+    def _realloc_extra(self, cap: int, nb: int) -> None:
+        # the density pass's neighbour lists (slots), reused by the force pass
+        stride = -(-max(cap, 1) // 32) * 32
+        self.arena.alloc("nbr", (HIT_CAP, stride), torch.int32, 0)
+        self.arena.alloc("cnt", (max(cap, 1),), torch.int32, 0)
+        self.params.nbr_stride = stride
     _FIELDS = (("vel", "vel", 3, torch.float32, 0.0), ("acc", "acc", 3, torch.float32, 0.0),
                ("acc_prev", "acc_prev", 3, torch.float32, 0.0),
                ("force", "force", 3, torch.float32, 0.0), ("rho", "rho", 1, torch.float32, None),
@@ -278,6 +286,7 @@ class WcsphSolver(_DeviceSolver):
         self.validity = A.alloc("validity", (max(nf, 1),), torch.int32, 0)[:nf]
         self.region = A.alloc("region", (max(nf, 1),), torch.int8, 1)[:nf]
         self.compute = A.alloc("compute", (max(nf, 1),), torch.bool, True)[:nf]
+        self._realloc_extra(max(nf, 1), self.n_bound)
         self._missed_last = 0
         self.use_graphs = use_graphs
         self._graphs: dict = {}
@@ -291,7 +300,7 @@ class WcsphSolver(_DeviceSolver):
 
     def _graph(self):
         import ctypes
-        key = bytes(self.params)
+        key = bytes(self.params) + bytes(self.arena.buf)  # values and buffer addresses
         g = self._graphs.get(key)
         if g is None:
             if len(self._graphs) >= 8:
