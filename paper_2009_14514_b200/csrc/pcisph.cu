@@ -394,6 +394,7 @@ __global__ void k_sob(const __grid_constant__ RtsParams p, RtsBuffers b) {
 // load); short lists (the later, S_e-driven iterations) run an 8-lane group
 // per particle so the launch still has enough independent loads in flight.
 constexpr int kPG = 8;
+constexpr int kPF = 4;  // pressure-force chunk (table entries + gathers in flight)
 
 template <int LG>
 RTS_DEV void density_one(const RtsParams &p, const RtsBuffers &b, int i, int lane,
@@ -407,13 +408,21 @@ RTS_DEV void density_one(const RtsParams &p, const RtsBuffers &b, int i, int lan
     const size_t S = p.nbr_stride;
     double acc = 0.0;
     if (LG == 1) {
+        // software-pipelined: the next chunk's table entries (mostly DRAM:
+        // the tables exceed L2) are requested before this chunk's gathers
+        int jn[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) jn[u] = u < c ? row[u * S] : i;
         for (int q = 0; q < c; q += 8) {
             int j8[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) j8[u] = q + u < c ? row[(q + u) * S] : i;
+            for (int u = 0; u < 8; ++u) {
+                j8[u] = jn[u];
+                jn[u] = q + 8 + u < c ? row[(q + 8 + u) * S] : i;
+            }
             float4 o[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) o[u] = xs4[q + u < c ? j8[u] : i];
+            for (int u = 0; u < 8; ++u) o[u] = xs4[j8[u]];
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 if (q + u < c)
@@ -631,15 +640,21 @@ RTS_DEV void pforce_one(const RtsParams &p, const RtsBuffers &b, int i, int lane
     const size_t S = p.nbr_stride;
     double fx = 0.0, fy = 0.0, fz = 0.0;
     if (LG == 1) {
-        for (int q = 0; q < c; q += 4) {
-            int j4[4];
+        int jn[kPF];  // software-pipelined table reads, as in density_one
 #pragma unroll
-            for (int u = 0; u < 4; ++u) j4[u] = q + u < c ? row[(q + u) * S] : i;
-            float4 o4[4];
+        for (int u = 0; u < kPF; ++u) jn[u] = u < c ? row[u * S] : i;
+        for (int q = 0; q < c; q += kPF) {
+            int j4[kPF];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) o4[u] = xs4[q + u < c ? j4[u] : i];
+            for (int u = 0; u < kPF; ++u) {
+                j4[u] = jn[u];
+                jn[u] = q + kPF + u < c ? row[(q + kPF + u) * S] : i;
+            }
+            float4 o4[kPF];
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
+            for (int u = 0; u < kPF; ++u) o4[u] = xs4[j4[u]];
+#pragma unroll
+            for (int u = 0; u < kPF; ++u)
                 if (q + u < c)
                     pforce_pair(p, xi, yi, zi, term_i, wall, m2, inv_rho0_sq, i, j4[u], o4[u],
                                 fx, fy, fz);
