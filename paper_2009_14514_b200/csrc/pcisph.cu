@@ -198,24 +198,44 @@ RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshC
             const int base = (ax * ny + ay) * nz;
             const int k0 = b.starts[base + z0], k1 = b.starts[base + z1 + 1];
             if (G == 1) {
-                // membership bits of up to 64 candidates, then the (few) hits:
-                // the candidate loop carries no memory traffic or branches
-                for (int cb = k0; cb < k1; cb += 64) {
-                    const int ce = min(cb + 64, k1);
-                    unsigned long long bits = 0ull;
-                    for (int kb = cb; kb < ce; kb += 4) {
+                // Branch-free classification of 32 candidates at a time: two
+                // 32-bit masks (r2 < h2_lo: member; r2 > h2_hi: not) built
+                // from the sign bits of r2 - bound with one funnel shift per
+                // candidate; the rare in-band candidates then take the exact
+                // fp64 test, and the members are emitted in candidate order.
+                // Reads run up to 3 slots past the span (cpos is padded).
+                for (int cb = k0; cb < k1; cb += 32) {
+                    const int n = min(32, k1 - cb);
+                    const float4 *cp = cpos + cb;
+                    unsigned mem = 0u, out = 0u;  // first candidate ends in the top bit
+                    for (int u = 0; u < n; u += 4) {
                         float4 ob[4];
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) ob[u] = cpos[min(kb + u, ce - 1)];
+                        for (int v = 0; v < 4; ++v) ob[v] = cp[u + v];
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const bool in = kb + u < ce && is_neighbour(k, p, fxi, fyi, fzi, ob[u]);
-                            bits |= (unsigned long long)in << (kb + u - cb);
+                        for (int v = 0; v < 4; ++v) {
+                            const float ex = __fsub_rn(fxi, ob[v].x), ey = __fsub_rn(fyi, ob[v].y),
+                                        ez = __fsub_rn(fzi, ob[v].z);
+                            const float r2f = __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, __fmul_rn(ez, ez)));
+                            mem = __funnelshift_l(__float_as_uint(__fsub_rn(r2f, k.h2_lo)), mem, 1);
+                            out = __funnelshift_l(__float_as_uint(__fsub_rn(k.h2_hi, r2f)), out, 1);
                         }
                     }
-                    while (bits) {
-                        const int q = __ffsll((long long)bits) - 1;
-                        bits &= bits - 1ull;
+                    const int nr = (n + 3) & ~3;  // candidates classified
+                    // bit (nr-1-u) <-> candidate u; reverse so bit u <-> candidate u
+                    const unsigned valid = n == 32 ? 0xffffffffu : ((1u << n) - 1u);
+                    mem = (__brev(mem) >> (32 - nr)) & valid;
+                    out = (__brev(out) >> (32 - nr)) & valid;
+                    unsigned amb = valid & ~mem & ~out;
+                    while (amb) {
+                        const int q = __ffs(amb) - 1;
+                        amb &= amb - 1u;
+                        const float4 o = cp[q];
+                        if (exact_neighbour(p.h2, fxi, fyi, fzi, o.x, o.y, o.z)) mem |= 1u << q;
+                    }
+                    while (mem) {
+                        const int q = __ffs(mem) - 1;
+                        mem &= mem - 1u;
                         if (cntn < p.width) row[cntn * S] = b.order[cb + q];
                         ++cntn;
                     }

@@ -608,7 +608,7 @@ class PcisphSolver(_DeviceSolver):
         if getattr(self, "_audit_n", None) != (nf, nb):
             ag._ensure_particles(nf, nf + nb)
             ag.bind_boundary(self.pos[nf:nf + nb].double().cpu().numpy(), nf)
-            A.alloc("cpos", (max(nf + nb, 1), 4), torch.float32, 0)
+            A.alloc("cpos", (nf + nb + 4, 4), torch.float32, 0)
             A.alloc("slot_of", (max(nf, 1),), torch.int32, 0)
             self._audit_n = (nf, nb)
         A.bind("pos", self._pos)

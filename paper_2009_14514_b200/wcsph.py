@@ -92,7 +92,7 @@ class _DeviceSolver:
         p.eta_max, p.eta_avg, p.rho_T = scene.eta_max, scene.eta_avg, scene.rho_T
         sms = N.load().rts_device_sms()
         p.n_sms = sms if sms > 0 else 148
-        A.alloc("cpos", (max(nf + self.n_bound, 1), 4), torch.float32, 0)
+        A.alloc("cpos", (nf + self.n_bound + 4, 4), torch.float32, 0)
         A.alloc("cvel", (max(nf + self.n_bound, 1), 4), torch.float32, 0)
         A.alloc("active", (max(nf, 1),), torch.int32, 0)
         A.alloc("list2", (max(nf, 1),), torch.int32, 0)
@@ -194,7 +194,7 @@ class _DeviceSolver:
                 fill = self.scene.rest_density if fill is None else fill
                 A.alloc(arena, (cap, w) if w > 1 else (cap,), dt, fill)
             for name in ("cpos", "cvel"):
-                A.alloc(name, (cap + nb, 4), torch.float32, 0)
+                A.alloc(name, (cap + nb + 4, 4), torch.float32, 0)  # +4: padded candidate reads
             for name in ("active", "list2"):
                 A.alloc(name, (cap,), torch.int32, 0)
             self._realloc_extra(cap, nb)
