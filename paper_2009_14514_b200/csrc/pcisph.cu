@@ -414,9 +414,8 @@ __global__ void k_sob(const __grid_constant__ RtsParams p, RtsBuffers b) {
 // load); short lists (the later, S_e-driven iterations) run an 8-lane group
 // per particle so the launch still has enough independent loads in flight.
 constexpr int kPG = 8;
-constexpr int kPF = 4;  // pressure-force chunk (table entries + gathers in flight)
 
-template <int LG>
+template <int LG, int CH = 8>
 RTS_DEV void density_one(const RtsParams &p, const RtsBuffers &b, int i, int lane,
                          unsigned gmask) {
     if (is_ghost(b, i)) return;
@@ -430,21 +429,21 @@ RTS_DEV void density_one(const RtsParams &p, const RtsBuffers &b, int i, int lan
     if (LG == 1) {
         // software-pipelined: the next chunk's table entries (mostly DRAM:
         // the tables exceed L2) are requested before this chunk's gathers
-        int jn[8];
+        int jn[CH];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) jn[u] = u < c ? row[u * S] : i;
-        for (int q = 0; q < c; q += 8) {
-            int j8[8];
+        for (int u = 0; u < CH; ++u) jn[u] = u < c ? row[u * S] : i;
+        for (int q = 0; q < c; q += CH) {
+            int j8[CH];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < CH; ++u) {
                 j8[u] = jn[u];
-                jn[u] = q + 8 + u < c ? row[(q + 8 + u) * S] : i;
+                jn[u] = q + CH + u < c ? row[(q + CH + u) * S] : i;
             }
-            float4 o[8];
+            float4 o[CH];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) o[u] = xs4[j8[u]];
+            for (int u = 0; u < CH; ++u) o[u] = xs4[j8[u]];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < CH; ++u) {
                 if (q + u < c)
                     acc = xadd(acc, poly6(dist2(xsub(xi, (double)o[u].x), xsub(yi, (double)o[u].y),
                                                 xsub(zi, (double)o[u].z)),
@@ -476,7 +475,8 @@ RTS_DEV void density_one(const RtsParams &p, const RtsBuffers &b, int i, int lan
     }
 }
 
-__global__ void __launch_bounds__(kThreads) k_density(const __grid_constant__ RtsParams p,
+template <int CH, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_density(const __grid_constant__ RtsParams p,
                                                       RtsBuffers b) {
     RTS_ITER_GUARD();
     const bool all = b.ctr->lists_all;  // every fluid particle, particle order
@@ -491,7 +491,7 @@ __global__ void __launch_bounds__(kThreads) k_density(const __grid_constant__ Rt
         }
     } else {
         for (int t = tid; t < n; t += nthreads) {
-            density_one<1>(p, b, all ? t : b.active[t], 0, 0u);
+            density_one<1, CH>(p, b, all ? t : b.active[t], 0, 0u);
         }
     }
 }
@@ -644,7 +644,7 @@ RTS_DEV void pforce_pair(const RtsParams &p, double xi, double yi, double zi, do
     fz = xsub(fz, xmul(s, dz));
 }
 
-template <int LG>
+template <int LG, int kPF = 4>
 RTS_DEV void pforce_one(const RtsParams &p, const RtsBuffers &b, int i, int lane,
                         unsigned gmask) {
     if (is_ghost(b, i)) return;
@@ -698,7 +698,8 @@ RTS_DEV void pforce_one(const RtsParams &p, const RtsBuffers &b, int i, int lane
     }
 }
 
-__global__ void __launch_bounds__(kThreads) k_pforces(const __grid_constant__ RtsParams p,
+template <int CH, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_pforces(const __grid_constant__ RtsParams p,
                                                       RtsBuffers b) {
     RTS_ITER_GUARD();
     const bool all = b.ctr->lists_all;  // every fluid particle, particle order
@@ -713,7 +714,7 @@ __global__ void __launch_bounds__(kThreads) k_pforces(const __grid_constant__ Rt
         }
     } else {
         for (int t = tid; t < n; t += nthreads) {
-            pforce_one<1>(p, b, all ? t : b.list2[t], 0, 0u);
+            pforce_one<1, CH>(p, b, all ? t : b.list2[t], 0, 0u);
         }
     }
 }
@@ -1192,7 +1193,10 @@ int rts_pci_sets(const RtsParams *p, const RtsBuffers *b, int row_mask, int all_
 }
 
 int rts_pci_density(const RtsParams *p, const RtsBuffers *b, void *stream) {
-    rts_note_launch(), k_density<<<rts_blocks(p->n_fluid, kThreads), kThreads, 0, (cudaStream_t)stream>>>(*p, *b);
+    const int nb = rts_blocks(p->n_fluid, kThreads);
+    cudaStream_t s = (cudaStream_t)stream;
+    // 4-deep chunks, <= 48 registers: 10 CTAs of 128 threads per SM
+    rts_note_launch(), k_density<4, 10><<<nb, kThreads, 0, s>>>(*p, *b);
     RTS_LAUNCH_CHECK();
     return 0;
 }
@@ -1221,7 +1225,9 @@ int rts_pci_sob(const RtsParams *p, const RtsBuffers *b, void *stream) {
 }
 
 int rts_pci_pforces(const RtsParams *p, const RtsBuffers *b, void *stream) {
-    rts_note_launch(), k_pforces<<<rts_blocks(p->n_fluid, kThreads), kThreads, 0, (cudaStream_t)stream>>>(*p, *b);
+    const int nb = rts_blocks(p->n_fluid, kThreads);
+    cudaStream_t s = (cudaStream_t)stream;
+    rts_note_launch(), k_pforces<4, 7><<<nb, kThreads, 0, s>>>(*p, *b);
     RTS_LAUNCH_CHECK();
     return 0;
 }
