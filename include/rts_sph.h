@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define RTS_ABI_VERSION 14
+#define RTS_ABI_VERSION 15
 
 /* err_flags bits */
 #define RTS_ERR_ESCAPED   0x1u  /* fluid left the padded grid or non-finite (grid.py:268-273) */
@@ -191,6 +191,9 @@ typedef struct RtsBuffers {
     float   *cvel;         /* (Nf+Nb, 4)  vx vy vz rho */
     int32_t *active;       /* (Nf) compacted CSR slots of active fluid particles */
     int32_t *list2;        /* (Nf) second compacted list */
+    int32_t *list3;        /* (Nf) PCISPH: force list of the previous iteration (motion
+                            * input; written by the pressure-force pass, so k_sets may
+                            * rebuild list2 concurrently with k_motion) */
     /* PCISPH neighbour tables */
     int32_t *nbr;          /* (width, nbr_stride) column-major neighbour particle indices
                             * (grid.py:146-149 rows, transposed) */

@@ -323,17 +323,29 @@ RTS_DEV void store12(float *a, int g, const float v[12]) {
     q[2] = make_float4(v[8], v[9], v[10], v[11]);
 }
 
+// restore p, f_p of particle i from the local-phase entry snapshot
+RTS_DEV void restore_one(const RtsBuffers &b, int i) {
+    b.pres[i] = b.snap_p[i];
+    b.f_p[3 * i] = b.snap_fp[3 * i];
+    b.f_p[3 * i + 1] = b.snap_fp[3 * i + 1];
+    b.f_p[3 * i + 2] = b.snap_fp[3 * i + 2];
+}
+
 // all = 1: every fluid particle; 0: the previous force list; -1: ctl->motion_all.
 // The all-particle pass streams four particles per thread with float4 loads.
+// A revert decided by the previous iteration's control (ctl->snap_op == 2,
+// which also sets motion_all) restores p, f_p here, before x* is formed.
 __global__ void k_motion(const __grid_constant__ RtsParams p, RtsBuffers b, int all) {
     RTS_ITER_GUARD();
+    const bool restore = b.ctl && b.ctl->snap_op == 2;
     if (all < 0) all = b.ctl->motion_all;
+    if (restore) all = 1;
     const double dim = xmul(p.dt, p.inv_mass);
     const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
     if (!all) {
         const int n = b.ctl->prev_force;
         for (int t = tid; t < n; t += nt) {
-            const int i = b.list2[t];
+            const int i = b.list3[t];
             if (!is_ghost(b, i)) motion_one(p, b, i, dim);
         }
         return;
@@ -343,10 +355,14 @@ __global__ void k_motion(const __grid_constant__ RtsParams p, RtsBuffers b, int 
     for (int g = tid; g < ng; g += nt) {
         float fe[12], fp[12], v[12], x[12];
         load12(b.force, g, fe);
-        load12(b.f_p, g, fp);
+        load12(restore ? b.snap_fp : b.f_p, g, fp);
         load12(b.vel, g, v);
         load12(b.pos, g, x);
-        const float4 pr = reinterpret_cast<const float4 *>(b.pres)[g];
+        const float4 pr = reinterpret_cast<const float4 *>(restore ? b.snap_p : b.pres)[g];
+        if (restore) {
+            store12(b.f_p, g, fp);
+            reinterpret_cast<float4 *>(b.pres)[g] = pr;
+        }
         const float prs[4] = {pr.x, pr.y, pr.z, pr.w};
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -360,8 +376,10 @@ __global__ void k_motion(const __grid_constant__ RtsParams p, RtsBuffers b, int 
             if (!is_ghost(b, 4 * g + q)) xs4[4 * g + q] = make_float4(xs[0], xs[1], xs[2], prs[q]);
         }
     }
-    for (int i = 4 * ng + tid; i < nf; i += nt)
+    for (int i = 4 * ng + tid; i < nf; i += nt) {
+        if (restore) restore_one(b, i);
         if (!is_ghost(b, i)) motion_one(p, b, i, dim);
+    }
 }
 
 // set membership for one iteration (pcisph.py:634-643); row_mask bit n set
@@ -374,6 +392,16 @@ __global__ void __launch_bounds__(256) k_sets(const __grid_constant__ RtsParams 
     const int nf = p.n_fluid;
     // every region scheduled (or a synchronous baseline): pred = force = all
     // fluid; the pair kernels then walk 0..nf-1 directly (no lists)
+    // a local-phase entry decided by the previous control (ctl->snap_op == 1)
+    // snapshots p, f_p of every fluid particle here (motion leaves them alone)
+    if (b.ctl && b.ctl->snap_op == 1) {
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nf; i += gridDim.x * blockDim.x) {
+            b.snap_p[i] = b.pres[i];
+            b.snap_fp[3 * i] = b.f_p[3 * i];
+            b.snap_fp[3 * i + 1] = b.f_p[3 * i + 1];
+            b.snap_fp[3 * i + 2] = b.f_p[3 * i + 2];
+        }
+    }
     const int all_mask = ((1 << (p.n_regions + 1)) - 1) & ~1;
     if (!b.ghost && (all_pred || (p.n_regions > 0 && (row_mask & all_mask) == all_mask))) {
         if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -710,11 +738,15 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pforces(const __grid_constan
         const int wl = threadIdx.x & 31, lane = wl & (kPG - 1);
         const unsigned gmask = ((1u << kPG) - 1u) << (wl & ~(kPG - 1));
         for (int t = tid / kPG; t < n; t += nthreads / kPG) {
-            pforce_one<kPG>(p, b, all ? t : b.list2[t], lane, gmask);
+            const int i = all ? t : b.list2[t];
+            if (!all && lane == 0) b.list3[t] = i;  // the next motion pass's list
+            pforce_one<kPG>(p, b, i, lane, gmask);
         }
     } else {
         for (int t = tid; t < n; t += nthreads) {
-            pforce_one<1, CH>(p, b, all ? t : b.list2[t], 0, 0u);
+            const int i = all ? t : b.list2[t];
+            if (!all) b.list3[t] = i;
+            pforce_one<1, CH>(p, b, i, 0, 0u);
         }
     }
 }
@@ -1299,14 +1331,30 @@ int rts_pci_control(const RtsParams *p, const RtsBuffers *b, int sync_mode,
 int rts_pci_iteration(const RtsParams *p, const RtsBuffers *b, int sync_mode,
                       unsigned long long cond_handle, int local_attempts, int iteration_cap,
                       void *stream) {
+    // DAG: {motion || sets} -> density -> {pforces || S_e reduction} -> control
+    // (independent kernels on a side stream; also inside a graph capture)
     cudaStream_t s = (cudaStream_t)stream;
+    static cudaStream_t side = nullptr;
+    static cudaEvent_t ev[2];
+    if (!side) {
+        cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking);
+        cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming);
+    }
     int rc;
+    cudaEventRecord(ev[0], s);
+    cudaStreamWaitEvent(side, ev[0], 0);
+    if ((rc = rts_pci_sets(p, b, -1, sync_mode, side))) return rc;
     if ((rc = rts_pci_motion(p, b, -1, stream))) return rc;
-    if ((rc = rts_pci_sets(p, b, -1, sync_mode, stream))) return rc;
+    cudaEventRecord(ev[1], side);
+    cudaStreamWaitEvent(s, ev[1], 0);
     if ((rc = rts_pci_density(p, b, stream))) return rc;
-    if ((rc = rts_pci_se_reduce(p, b, !sync_mode, stream))) return rc;
+    cudaEventRecord(ev[0], s);
+    cudaStreamWaitEvent(side, ev[0], 0);
+    if ((rc = rts_pci_se_reduce(p, b, !sync_mode, side))) return rc;
     if ((rc = rts_pci_pforces(p, b, stream))) return rc;
-    (void)s;
+    cudaEventRecord(ev[1], side);
+    cudaStreamWaitEvent(s, ev[1], 0);
     return rts_pci_control(p, b, sync_mode, cond_handle, local_attempts, iteration_cap, stream);
 }
 
@@ -1318,10 +1366,8 @@ int rts_pci_control(const RtsParams *p, const RtsBuffers *b, int sync_mode,
     rts_note_launch(), k_control<<<1, 32, 0, s>>>(*p, *b, sync_mode, cond_handle, local_attempts,
                                                   iteration_cap, n_part);
     RTS_LAUNCH_CHECK();
-    if (!sync_mode) {
-        rts_note_launch(), k_snapshot<<<rts_blocks(p->n_fluid, 256, 148 * 4), 256, 0, s>>>(*p, *b, -1);
-        RTS_LAUNCH_CHECK();
-    }
+    // the snapshot / revert it decides (ctl->snap_op) is applied by the next
+    // iteration's k_sets / k_motion
     return 0;
 }
 

@@ -97,6 +97,7 @@ class _DeviceSolver:
         A.alloc("cvel", (max(nf + self.n_bound, 1), 4), torch.float32, 0)
         A.alloc("active", (max(nf, 1),), torch.int32, 0)
         A.alloc("list2", (max(nf, 1),), torch.int32, 0)
+        A.alloc("list3", (max(nf, 1),), torch.int32, 0)
         self.step_index = 0
         self.sim_time = 0.0
         self.missed_neighbors_total = 0
@@ -196,7 +197,7 @@ class _DeviceSolver:
                 A.alloc(arena, (cap, w) if w > 1 else (cap,), dt, fill)
             for name in ("cpos", "cvel"):
                 A.alloc(name, (cap + nb + 4, 4), torch.float32, 0)  # +4: padded candidate reads
-            for name in ("active", "list2"):
+            for name in ("active", "list2", "list3"):
                 A.alloc(name, (cap,), torch.int32, 0)
             self._realloc_extra(cap, nb)
             self.grid._ensure_particles(cap, cap + nb)
