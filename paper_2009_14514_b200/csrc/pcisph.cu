@@ -258,10 +258,42 @@ RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshC
     const int nrow = min(cntn, p.width);
     const double vxi = b.vel[3 * i], vyi = b.vel[3 * i + 1], vzi = b.vel[3 * i + 2];
     double fx = 0.0, fy = 0.0, fz = 0.0;
-    for (int q = lane; q < nrow; q += G) {
-        const int j = row[q * S];
-        const float4 pj = make_float4(b.pos[3 * j], b.pos[3 * j + 1], b.pos[3 * j + 2], 0.f);
-        visc_term(k, p, b, i, j, xi, yi, zi, pj, vxi, vyi, vzi, fx, fy, fz);
+    if (G == 1) {
+        // four entries at a time, every load issued before the fp64 terms
+        // (which are summed in row order, as below)
+        for (int q = 0; q < nrow; q += 4) {
+            int jj[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) jj[u] = q + u < nrow ? row[(q + u) * S] : i;
+            float4 pj[4];
+            float vj[4][3];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int jc = jj[u] < p.n_fluid ? jj[u] : i;  // walls: no term, no vel row
+                pj[u] = make_float4(b.pos[3 * jc], b.pos[3 * jc + 1], b.pos[3 * jc + 2], 0.f);
+                vj[u][0] = b.vel[3 * jc];
+                vj[u][1] = b.vel[3 * jc + 1];
+                vj[u][2] = b.vel[3 * jc + 2];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int j = jj[u];
+                if (q + u >= nrow || j >= p.n_fluid || j == i) continue;
+                const double r = xsqrt(dist2(xsub(xi, (double)pj[u].x), xsub(yi, (double)pj[u].y),
+                                             xsub(zi, (double)pj[u].z)));
+                if (r >= p.h) continue;
+                const double lap = xmul(xmul(k.mum2, visc_lap(r, p.h, p.c_visc)), k.inv_rho0_sq);
+                fx = xadd(fx, xmul(lap, xsub((double)vj[u][0], vxi)));
+                fy = xadd(fy, xmul(lap, xsub((double)vj[u][1], vyi)));
+                fz = xadd(fz, xmul(lap, xsub((double)vj[u][2], vzi)));
+            }
+        }
+    } else {
+        for (int q = lane; q < nrow; q += G) {
+            const int j = row[q * S];
+            const float4 pj = make_float4(b.pos[3 * j], b.pos[3 * j + 1], b.pos[3 * j + 2], 0.f);
+            visc_term(k, p, b, i, j, xi, yi, zi, pj, vxi, vyi, vzi, fx, fy, fz);
+        }
     }
     if (G > 1) {
 #pragma unroll
