@@ -306,7 +306,7 @@ RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshC
     if (lane == 0) finish_refresh(p, b, i, cntn, fx, fy, fz);
 }
 
-__global__ void __launch_bounds__(kThreads) k_refresh(const __grid_constant__ RtsParams p,
+__global__ void __launch_bounds__(kThreads, 8) k_refresh(const __grid_constant__ RtsParams p,
                                                       RtsBuffers b, int two_layer_r1) {
     RTS_MINOR_GUARD();
     const int n = b.ctr->n_compute;
