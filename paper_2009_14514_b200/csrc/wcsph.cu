@@ -100,16 +100,43 @@ RTS_DEV int collect_hits(const RtsParams &p, const RtsBuffers &b, const float4 *
     int n = 0;
     for (int s = 0; s < ns; ++s) {
         const int k0 = sp[s].k0, k1 = sp[s].k1;
-        for (int kb = k0; kb < k1; kb += 4) {
-            float4 ob[4];
+        // branch-free classification of 32 candidates at a time (sign bits of
+        // r2 - bound collected with funnel shifts); in-band candidates take
+        // the exact fp64 test; reads run up to 3 slots past the span (cpos
+        // is padded)
+        for (int cb = k0; cb < k1; cb += 32) {
+            const int m = min(32, k1 - cb);
+            const float4 *cp = cpos + cb;
+            unsigned mem = 0u, out = 0u;
+            for (int u = 0; u < m; u += 4) {
+                float4 ob[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) ob[u] = cpos[min(kb + u, k1 - 1)];
+                for (int v = 0; v < 4; ++v) ob[v] = cp[u + v];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                if (kb + u < k1 && in_support(bd, a.x, a.y, a.z, ob[u])) {
-                    if (n < kHitCap) hits[n * kThreads] = kb + u;
-                    ++n;
+                for (int v = 0; v < 4; ++v) {
+                    const float ex = __fsub_rn(a.x, ob[v].x), ey = __fsub_rn(a.y, ob[v].y),
+                                ez = __fsub_rn(a.z, ob[v].z);
+                    const float r2f = __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, __fmul_rn(ez, ez)));
+                    mem = __funnelshift_l(__float_as_uint(__fsub_rn(r2f, bd.lo)), mem, 1);
+                    out = __funnelshift_l(__float_as_uint(__fsub_rn(bd.hi, r2f)), out, 1);
                 }
+            }
+            const int mr = (m + 3) & ~3;
+            const unsigned valid = m == 32 ? 0xffffffffu : ((1u << m) - 1u);
+            mem = (__brev(mem) >> (32 - mr)) & valid;
+            out = (__brev(out) >> (32 - mr)) & valid;
+            unsigned amb = valid & ~mem & ~out;
+            while (amb) {
+                const int q = __ffs(amb) - 1;
+                amb &= amb - 1u;
+                const float4 o = cp[q];
+                if (exact_neighbour(bd.h2, a.x, a.y, a.z, o.x, o.y, o.z)) mem |= 1u << q;
+            }
+            while (mem) {
+                const int q = __ffs(mem) - 1;
+                mem &= mem - 1u;
+                if (n < kHitCap) hits[n * kThreads] = cb + q;
+                ++n;
             }
         }
     }
