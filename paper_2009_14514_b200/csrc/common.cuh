@@ -166,6 +166,21 @@ RTS_DEV void block_append2(bool p0, int v0, int *list0, int *count0, bool p1, in
     __syncthreads();  // shared slots are reused by the next loop trip
 }
 
+// float3 rows of 4 consecutive particles as 3 float4 (16-byte aligned)
+RTS_DEV void load12(const float *a, int g, float v[12]) {
+    const float4 *q = reinterpret_cast<const float4 *>(a) + 3 * g;
+    const float4 x = q[0], y = q[1], z = q[2];
+    v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+    v[4] = y.x; v[5] = y.y; v[6] = y.z; v[7] = y.w;
+    v[8] = z.x; v[9] = z.y; v[10] = z.z; v[11] = z.w;
+}
+RTS_DEV void store12(float *a, int g, const float v[12]) {
+    float4 *q = reinterpret_cast<float4 *>(a) + 3 * g;
+    q[0] = make_float4(v[0], v[1], v[2], v[3]);
+    q[1] = make_float4(v[4], v[5], v[6], v[7]);
+    q[2] = make_float4(v[8], v[9], v[10], v[11]);
+}
+
 RTS_DEV int warp_count_add(bool pred, int *count) {
     const unsigned mask = __ballot_sync(0xffffffffu, pred);
     const int lane = threadIdx.x & 31;

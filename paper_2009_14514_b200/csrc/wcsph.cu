@@ -303,39 +303,78 @@ __global__ void __launch_bounds__(kThreads) k_forces(const __grid_constant__ Rts
 }
 
 // wcsph.py:299-319: predictor for all, corrector (after it) for active, clamp
+RTS_DEV void integrate_axis(const RtsParams &p, double dt, double half_dt2, bool correct,
+                            double corr_x, double corr_v, int a, float &xf, float &vf, float acf,
+                            float apf) {
+    double x = xf, v = vf;
+    const double ac = acf;
+    x = xadd(x, xadd(xmul(v, dt), xmul(ac, half_dt2)));
+    v = xadd(v, xmul(ac, dt));
+    if (correct) {
+        const double da = xsub(ac, (double)apf);
+        x = xadd(x, xmul(da, corr_x));
+        v = xadd(v, xmul(da, corr_v));
+    }
+    if (x < p.clamp_lo[a]) {
+        x = p.clamp_lo[a];
+        v = 0.0;
+    } else if (x > p.clamp_hi[a]) {
+        x = p.clamp_hi[a];
+        v = 0.0;
+    }
+    xf = (float)x;
+    vf = (float)v;
+}
+
+// four particles per thread with float4 / double2 vector accesses
 __global__ void k_integrate(const __grid_constant__ RtsParams p, RtsBuffers b) {
     if (fatal(b.ctr)) return;
     const double dt = p.dt;
     const double half_dt2 = xmul(xmul(0.5, dt), dt);
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.n_fluid;
-         i += gridDim.x * blockDim.x) {
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+    const int nf = p.n_fluid, ng = nf / 4;
+    for (int g = tid; g < ng; g += nt) {
+        float x[12], v[12], ac[12], ap[12];
+        load12(b.pos, g, x);
+        load12(b.vel, g, v);
+        load12(b.acc, g, ac);
+        load12(b.acc_prev, g, ap);
+        const double2 c01 = reinterpret_cast<const double2 *>(b.dt_corr)[2 * g];
+        const double2 c23 = reinterpret_cast<const double2 *>(b.dt_corr)[2 * g + 1];
+        double2 s01 = reinterpret_cast<const double2 *>(b.dt_since)[2 * g];
+        double2 s23 = reinterpret_cast<const double2 *>(b.dt_since)[2 * g + 1];
+        const uchar4 cm = reinterpret_cast<const uchar4 *>(b.compute)[g];
+        const double dtc[4] = {c01.x, c01.y, c23.x, c23.y};
+        const bool act[4] = {cm.x != 0, cm.y != 0, cm.z != 0, cm.w != 0};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const bool correct = p.apply_correction && (p.rts ? act[q] : true);
+            const double corr_x = xdiv(xmul(dtc[q], dtc[q]), 6.0);
+            const double corr_v = xdiv(dtc[q], 2.0);
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+                integrate_axis(p, dt, half_dt2, correct, corr_x, corr_v, a, x[3 * q + a],
+                               v[3 * q + a], ac[3 * q + a], ap[3 * q + a]);
+        }
+        store12(b.pos, g, x);
+        store12(b.vel, g, v);
+        s01.x = xadd(s01.x, dt);
+        s01.y = xadd(s01.y, dt);
+        s23.x = xadd(s23.x, dt);
+        s23.y = xadd(s23.y, dt);
+        reinterpret_cast<double2 *>(b.dt_since)[2 * g] = s01;
+        reinterpret_cast<double2 *>(b.dt_since)[2 * g + 1] = s23;
+    }
+    for (int i = 4 * ng + tid; i < nf; i += nt) {
         const bool act = p.rts ? (b.compute[i] != 0) : true;
         const double dtc = b.dt_corr[i];
         const double corr_x = xdiv(xmul(dtc, dtc), 6.0);
         const double corr_v = xdiv(dtc, 2.0);
         const bool correct = p.apply_correction && act;
 #pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            double x = b.pos[3 * i + a];
-            double v = b.vel[3 * i + a];
-            const double ac = b.acc[3 * i + a];
-            x = xadd(x, xadd(xmul(v, dt), xmul(ac, half_dt2)));
-            v = xadd(v, xmul(ac, dt));
-            if (correct) {
-                const double da = xsub(ac, (double)b.acc_prev[3 * i + a]);
-                x = xadd(x, xmul(da, corr_x));
-                v = xadd(v, xmul(da, corr_v));
-            }
-            if (x < p.clamp_lo[a]) {
-                x = p.clamp_lo[a];
-                v = 0.0;
-            } else if (x > p.clamp_hi[a]) {
-                x = p.clamp_hi[a];
-                v = 0.0;
-            }
-            b.pos[3 * i + a] = (float)x;
-            b.vel[3 * i + a] = (float)v;
-        }
+        for (int a = 0; a < 3; ++a)
+            integrate_axis(p, dt, half_dt2, correct, corr_x, corr_v, a, b.pos[3 * i + a],
+                           b.vel[3 * i + a], b.acc[3 * i + a], b.acc_prev[3 * i + a]);
         b.dt_since[i] = xadd(b.dt_since[i], dt);
     }
 }
