@@ -1343,6 +1343,23 @@ int rts_pci_control(const RtsParams *p, const RtsBuffers *b, int sync_mode,
                     unsigned long long cond_handle, int local_attempts, int iteration_cap,
                     void *stream);
 
+// Second streams (and events) for the fork/join parts of a correction
+// iteration (slot 0) and of a minor-step head (slot 1); they work inside a
+// stream capture as well.  Separate slots because a head's side stream stays
+// joined to the major graph's capture while the iterations are captured into
+// the conditional bodies.
+static void side_stream(int slot, cudaStream_t *side, cudaEvent_t **ev) {
+    static cudaStream_t st[2] = {nullptr, nullptr};
+    static cudaEvent_t e[2][2];
+    if (!st[slot]) {
+        cudaStreamCreateWithFlags(&st[slot], cudaStreamNonBlocking);
+        cudaEventCreateWithFlags(&e[slot][0], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&e[slot][1], cudaEventDisableTiming);
+    }
+    *side = st[slot];
+    *ev = e[slot];
+}
+
 // One correction iteration with device-side control (pcisph.py:633-715 or
 // 446-468): motion, sets, density + pressure, S_e/reductions, observed,
 // pressure forces, control, snapshot/revert.
@@ -1352,13 +1369,9 @@ int rts_pci_iteration(const RtsParams *p, const RtsBuffers *b, int sync_mode,
     // DAG: {motion || sets} -> density -> {pforces || S_e reduction} -> control
     // (independent kernels on a side stream; also inside a graph capture)
     cudaStream_t s = (cudaStream_t)stream;
-    static cudaStream_t side = nullptr;
-    static cudaEvent_t ev[2];
-    if (!side) {
-        cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking);
-        cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming);
-    }
+    cudaStream_t side;
+    cudaEvent_t *ev;
+    side_stream(0, &side, &ev);
     int rc;
     cudaEventRecord(ev[0], s);
     cudaStreamWaitEvent(side, ev[0], 0);
@@ -1393,11 +1406,20 @@ int rts_pci_control(const RtsParams *p, const RtsBuffers *b, int sync_mode,
 // and its tail after the loop.
 int rts_pci_minor_head(const RtsParams *p, const RtsBuffers *b, int minor, void *stream) {
     int rc;
+    cudaStream_t s = (cudaStream_t)stream, side;
+    cudaEvent_t *ev;
+    side_stream(1, &side, &ev);
     if ((rc = rts_pci_minor_begin(p, b, minor, 0, stream))) return rc;
+    // {refresh -> p, f_p = 0} || {S_e = empty, observed blocks}
+    cudaEventRecord(ev[0], s);
+    cudaStreamWaitEvent(side, ev[0], 0);
+    cudaMemsetAsync(b->in_se, 0, (size_t)p->n_fluid, side);
+    if ((rc = rts_pci_observed(p, b, 0, side))) return rc;
     if ((rc = rts_pci_refresh(p, b, 0, 1, stream))) return rc;
     if ((rc = rts_pci_zero_pressure(p, b, stream))) return rc;
-    cudaMemsetAsync(b->in_se, 0, (size_t)p->n_fluid, (cudaStream_t)stream);
-    return rts_pci_observed(p, b, 0, stream);
+    cudaEventRecord(ev[1], side);
+    cudaStreamWaitEvent(s, ev[1], 0);
+    return 0;
 }
 
 int rts_pci_minor_tail(const RtsParams *p, const RtsBuffers *b, int minor, int last,
