@@ -1,0 +1,14 @@
+"""The driver's round-end smoke check (__graft_entry__.smoke) as a GPU test."""
+
+import os
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def test_graft_entry_smoke():
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import __graft_entry__
+    __graft_entry__.smoke()
