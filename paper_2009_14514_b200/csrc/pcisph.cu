@@ -671,23 +671,23 @@ __global__ void k_observed(const __grid_constant__ RtsParams p, RtsBuffers b, in
 // pressure forces at x* over the force list (pcisph.py:238-271); same
 // adaptive granularity as k_density.
 RTS_DEV void pforce_pair(const RtsParams &p, double xi, double yi, double zi, double term_i,
-                         double wall, double m2, double inv_rho0_sq, int i, int j, float4 o,
+                         double wall, double m2c, double inv_rho0_sq, int i, int j, float4 o,
                          double &fx, double &fy, double &fz) {
+    // f_p is not a bit-exact quantity (parity bar 1e-4 per particle): the pair
+    // term uses fused multiply-adds and one fp64 rsqrt (1e-16-level deviation
+    // from the reference's sqrt / divide / unfused products)
     if (j == i) return;
     const double dx = xsub(xi, (double)o.x), dy = xsub(yi, (double)o.y),
                  dz = xsub(zi, (double)o.z);
-    const double term = j < p.n_fluid ? xadd(term_i, xmul((double)o.w, inv_rho0_sq)) : wall;
-    const double r2 = dist2(dx, dy, dz);
+    const double r2 = __fma_rn(dx, dx, __fma_rn(dy, dy, __dmul_rn(dz, dz)));
     if (!(r2 > 0.0) || !(r2 < p.h2)) return;  // r <= 0 or r >= h
-    // spiky factor c (h - r)^2 / r via one fp64 rsqrt (1e-16-level deviation
-    // from sqrt + divide; the f_p parity bar is 1e-4)
+    const double term = j < p.n_fluid ? __fma_rn((double)o.w, inv_rho0_sq, term_i) : wall;
     const double rinv = rsqrt(r2);
-    const double r = xmul(r2, rinv);
-    const double d = xsub(p.h, r);
-    const double s = xmul(xmul(xmul(m2, term), xmul(xmul(p.c_spiky, d), d)), rinv);
-    fx = xsub(fx, xmul(s, dx));
-    fy = xsub(fy, xmul(s, dy));
-    fz = xsub(fz, xmul(s, dz));
+    const double d = __fma_rn(-r2, rinv, p.h);  // h - r
+    const double s = __dmul_rn(__dmul_rn(__dmul_rn(m2c, term), __dmul_rn(d, d)), rinv);
+    fx = __fma_rn(-s, dx, fx);
+    fy = __fma_rn(-s, dy, fy);
+    fz = __fma_rn(-s, dz, fz);
 }
 
 template <int LG, int kPF = 4>
@@ -695,7 +695,7 @@ RTS_DEV void pforce_one(const RtsParams &p, const RtsBuffers &b, int i, int lane
                         unsigned gmask) {
     if (is_ghost(b, i)) return;
     const float4 *xs4 = reinterpret_cast<const float4 *>(b.xs4);
-    const double m2 = xmul(p.mass, p.mass);
+    const double m2 = xmul(xmul(p.mass, p.mass), p.c_spiky);  // m^2 c_spiky
     const double inv_rho0_sq = xdiv(1.0, xmul(p.rho0, p.rho0));
     const float4 a = xs4[i];
     const double xi = a.x, yi = a.y, zi = a.z;
