@@ -282,7 +282,10 @@ int rts_pci_observed(const RtsParams *p, const RtsBuffers *b, int with_se, void 
 int rts_pci_sob(const RtsParams *p, const RtsBuffers *b, void *stream);
 /* _pressure_forces over the force list (pcisph.py:238-271). */
 int rts_pci_pforces(const RtsParams *p, const RtsBuffers *b, void *stream);
-/* _integrate (pcisph.py:759-768) + validity countdown (pcisph.py:580-584). */
+/* _integrate (pcisph.py:759-768) + validity countdown (pcisph.py:580-584).
+ * countdown bit 0: RTS minor step (countdown, S_ob, candidate copies); bit 1:
+ * also the per-block maxima of rts_block_maxima(add_fp = 1) into vmax / fmax,
+ * which the caller zeroes first (no ghost rows). */
 int rts_pci_integrate(const RtsParams *p, const RtsBuffers *b, int countdown, void *stream);
 /* _mark_timestep_updates (pcisph.py:718-755); block_raw = required levels. */
 int rts_pci_mark_updates(const RtsParams *p, const RtsBuffers *b, void *stream);

@@ -770,6 +770,16 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pforces(const __grid_constan
 }
 
 // _integrate (pcisph.py:759-768) + validity countdown (pcisph.py:580-584)
+// per-block max |v| and |f_ext + f_p| of one particle (k_block_maxima with
+// add_fp, grid.cu), from the integrated velocity
+RTS_DEV void block_maxima_one(const RtsBuffers &b, int c, const float *v, const float *fe,
+                              const float *fp) {
+    atomic_max_pos(&b.vmax[c], norm3(v[0], v[1], v[2]));
+    const double fx = xadd((double)fe[0], (double)fp[0]), fy = xadd((double)fe[1], (double)fp[1]),
+                 fz = xadd((double)fe[2], (double)fp[2]);
+    atomic_max_pos(&b.fmax[c], xsqrt(dist2(fx, fy, fz)));
+}
+
 RTS_DEV void integrate_one(const RtsParams &p, const RtsBuffers &b, int i, int countdown,
                            int gen, double dim) {
     // public x* = the last prediction; S_ob from the final S_e generation
@@ -795,6 +805,8 @@ RTS_DEV void integrate_one(const RtsParams &p, const RtsBuffers &b, int i, int c
         b.vel[3 * i + a] = (float)v;
         nx[a] = (float)x;
     }
+    if (countdown & 2) block_maxima_one(b, b.fluid_cells[i], &b.vel[3 * i], &b.force[3 * i],
+                                        &b.f_p[3 * i]);
     if (countdown) {
         reinterpret_cast<float4 *>(b.cpos)[b.slot_of[i]] = make_float4(nx[0], nx[1], nx[2], 0.f);
         int v = b.validity[i] - 1;
@@ -809,7 +821,11 @@ RTS_DEV void integrate_one(const RtsParams &p, const RtsBuffers &b, int i, int c
 }
 
 // _integrate (pcisph.py:759-768) + validity countdown (pcisph.py:580-584);
-// four particles per thread with vector loads/stores when no ghost rows exist
+// four particles per thread with vector loads/stores when no ghost rows exist.
+// countdown bit 0: validity countdown / S_ob / candidate copies (RTS minor
+// steps); bit 1: also the per-block maxima of the mid-major marking
+// (vmax / fmax zeroed beforehand), saving the separate k_block_maxima pass.
+template <bool MAXIMA>
 __global__ void k_integrate(const __grid_constant__ RtsParams p, RtsBuffers b, int countdown) {
     RTS_MINOR_GUARD();
     const double dim = xmul(p.dt, p.inv_mass);
@@ -868,6 +884,7 @@ __global__ void k_integrate(const __grid_constant__ RtsParams p, RtsBuffers b, i
             uint8_t sob[4], cmp[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
+                if (MAXIMA) block_maxima_one(b, cl[q], &v[3 * q], &fe[3 * q], &fp[3 * q]);
                 sob[q] = observed_block(b, cl[q], gen);
                 reinterpret_cast<float4 *>(b.cpos)[sl[q]] =
                     make_float4(x[3 * q], x[3 * q + 1], x[3 * q + 2], 0.f);
@@ -1283,8 +1300,12 @@ int rts_pci_pforces(const RtsParams *p, const RtsBuffers *b, void *stream) {
 }
 
 int rts_pci_integrate(const RtsParams *p, const RtsBuffers *b, int countdown, void *stream) {
-    rts_note_launch(), k_integrate<<<rts_blocks(p->n_fluid, 256), 256, 0, (cudaStream_t)stream>>>(*p, *b,
-                                                                               countdown);
+    const int nb = rts_blocks(p->n_fluid, 256);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (countdown & 2)
+        rts_note_launch(), k_integrate<true><<<nb, 256, 0, s>>>(*p, *b, countdown);
+    else
+        rts_note_launch(), k_integrate<false><<<nb, 256, 0, s>>>(*p, *b, countdown);
     RTS_LAUNCH_CHECK();
     return 0;
 }
@@ -1425,11 +1446,15 @@ int rts_pci_minor_head(const RtsParams *p, const RtsBuffers *b, int minor, void 
 int rts_pci_minor_tail(const RtsParams *p, const RtsBuffers *b, int minor, int last,
                        void *stream) {
     int rc;
-    if ((rc = rts_pci_integrate(p, b, 1, stream))) return rc;  // includes S_ob / x* refresh
-    if (!last) {
-        if ((rc = rts_block_maxima(p, b, 1, stream))) return rc;
+    if (!last) {  // integrator + per-block maxima of the mid-major marking in one pass
+        cudaStream_t s = (cudaStream_t)stream;
+        cudaMemsetAsync(b->vmax, 0, sizeof(double) * (size_t)p->n_cells, s);
+        cudaMemsetAsync(b->fmax, 0, sizeof(double) * (size_t)p->n_cells, s);
+        if ((rc = rts_pci_integrate(p, b, 3, stream))) return rc;  // includes S_ob / x* refresh
         if ((rc = rts_block_levels(p, b, 2, stream))) return rc;
         if ((rc = rts_pci_mark_updates(p, b, stream))) return rc;
+    } else if ((rc = rts_pci_integrate(p, b, 1, stream))) {
+        return rc;
     }
     return rts_pci_minor_end(p, b, minor, stream);
 }
