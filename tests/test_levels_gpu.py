@@ -54,3 +54,50 @@ def test_levels_bit_exact_on_random_fields(mode):
             dev._launch("rts_pci_observed", 0)
             obs = A["block_tmp"].cpu().numpy().astype(bool)
             assert np.array_equal(obs, O.derive_observed(want, dims, np.zeros(len(want), bool)))
+
+
+@pytest.mark.parametrize("mode", ["wcsph", "pcisph"])
+def test_block_maxima_bit_exact(mode):
+    """Per-block max |v| and |F| (grid.py:347-351; PCISPH: |f_ext + f_p|,
+    pcisph.py:738-740) from a common state: fp64, bit-exact."""
+    from paper_2009_14514_b200 import PcisphSolver, WcsphSolver
+    from parity import apply_jitter
+    rng = np.random.default_rng(11)
+    if mode == "pcisph":
+        from oracle.sph import OraclePcisph
+        dev, orc = PcisphSolver(tiny_tank(), mode="rts"), OraclePcisph(tiny_tank(), mode="rts")
+    else:
+        from oracle.sph import OracleWcsph
+        dev, orc = WcsphSolver(tiny_tank(), mode="rts"), OracleWcsph(tiny_tank(), mode="rts")
+    apply_jitter(dev, orc, seed=9)
+    nf = dev.n_fluid
+    vel = rng.normal(0.0, 0.5, (nf, 3)).astype(np.float32)
+    fe = rng.normal(0.0, 0.1, (nf, 3)).astype(np.float32)
+    dev.vel.copy_(torch.as_tensor(vel))
+    orc.vel[:] = vel
+    if mode == "pcisph":
+        fp = rng.normal(0.0, 0.05, (nf, 3)).astype(np.float32)
+        dev.f_ext.copy_(torch.as_tensor(fe))
+        dev.f_p.copy_(torch.as_tensor(fp))
+        force = fe.astype(np.float64) + fp.astype(np.float64)
+    else:
+        dev.force.copy_(torch.as_tensor(fe))
+        force = fe.astype(np.float64)
+    st = torch.cuda.current_stream(dev.device)
+    dev._sync_params()
+    dev.grid.launch_rebuild(dev.params, st, want_maxima=True, add_fp=(mode == "pcisph"))
+    orc.grid.rebuild(orc.pos, orc.n_fluid)
+    v_ref = orc.grid.reduce_fluid_max(np.linalg.norm(vel.astype(np.float64), axis=1))
+    f_ref = orc.grid.reduce_fluid_max(np.linalg.norm(force, axis=1))
+    got_v = dev.arena["vmax"].cpu().numpy().reshape(-1)
+    got_f = dev.arena["fmax"].cpu().numpy().reshape(-1)
+    assert np.array_equal(got_v, np.asarray(v_ref).reshape(-1))
+    assert np.array_equal(got_f, np.asarray(f_ref).reshape(-1))
+    if mode == "pcisph":  # the mid-major pass (rts_block_maxima, add_fp)
+        dev.arena["vmax"].zero_()
+        dev.arena["fmax"].zero_()
+        dev._call("rts_block_maxima", 1)
+        assert np.array_equal(dev.arena["vmax"].cpu().numpy().reshape(-1),
+                              np.asarray(v_ref).reshape(-1))
+        assert np.array_equal(dev.arena["fmax"].cpu().numpy().reshape(-1),
+                              np.asarray(f_ref).reshape(-1))
