@@ -119,68 +119,84 @@ __device__ __forceinline__ int block_incl_scan(int v, int *warp_sums) {
     return v;
 }
 
-template <bool kFromCounts>
-__global__ void __launch_bounds__(kScanThreads) k_scan_tiles(const int *a, const int *a2, int n,
-                                                             int *out_excl, int *tile_sums) {
+// Single-pass exclusive scan of cell_count + cell_bcount into starts with
+// decoupled look-back: tiles take their index from an atomic counter (so a
+// tile only waits on tiles that have started), publish their aggregate, then
+// one warp walks back over the predecessors' status words (32 at a time)
+// until it meets an inclusive prefix.  One launch instead of tile scan +
+// recursive tile-sum scan + add + finish.
+constexpr int kLbThreads = 256;
+constexpr int kLbItems = 4;
+constexpr int kLbTile = kLbThreads * kLbItems;
+constexpr unsigned long long kFlagAgg = 1ull << 32, kFlagPre = 2ull << 32;
+
+__global__ void __launch_bounds__(kLbThreads) k_scan_lookback(const __grid_constant__ RtsParams p,
+                                                              RtsBuffers b) {
     __shared__ int warp_sums[32];
-    const int tile0 = blockIdx.x * kScanTile;
-    int v[kScanItems];
+    __shared__ int s_tile, s_excl;
+    unsigned long long *status = reinterpret_cast<unsigned long long *>(b.scan_tmp + 2);
+    int *counter = b.scan_tmp;
+    const int n = p.n_cells;
+    if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1);
+    __syncthreads();
+    const int tile = s_tile;
+    const int i0 = tile * kLbTile + threadIdx.x * kLbItems;
+    int v[kLbItems];
     int local = 0;
 #pragma unroll
-    for (int q = 0; q < kScanItems; ++q) {
-        const int idx = tile0 + threadIdx.x * kScanItems + q;
-        int x = 0;
-        if (idx < n) x = kFromCounts ? (a[idx] + a2[idx]) : a[idx];
-        v[q] = x;
-        local += x;
+    for (int q = 0; q < kLbItems; ++q) {
+        const int idx = i0 + q;
+        v[q] = idx < n ? b.cell_count[idx] + b.cell_bcount[idx] : 0;
+        local += v[q];
     }
     const int incl = block_incl_scan(local, warp_sums);
-    int run = incl - local;
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x == kLbThreads - 1) {  // the tile's aggregate
+        const unsigned long long word = (tile == 0 ? kFlagPre : kFlagAgg) | (unsigned)incl;
+        __threadfence();
+        atomicExch(status + tile, word);
+        if (tile == 0) s_excl = 0;
+    }
+    if (tile > 0 && threadIdx.x < 32) {
+        __syncwarp();
+        int excl = 0, base = tile - 1;
+        for (;;) {
+            const int j = base - lane;
+            unsigned long long w = kFlagPre;  // before tile 0: prefix 0
+            if (j >= 0) {
+                do {
+                    w = atomicAdd(status + j, 0ull);
+                } while ((w >> 32) == 0ull);
+            }
+            const bool pre = (w >> 32) == 2ull;
+            const unsigned pm = __ballot_sync(0xffffffffu, pre);
+            const int stop = pm ? __ffs(pm) - 1 : 31;  // nearest inclusive prefix
+            int x = lane <= stop ? (int)(unsigned)(w & 0xffffffffull) : 0;
 #pragma unroll
-    for (int q = 0; q < kScanItems; ++q) {
-        const int idx = tile0 + threadIdx.x * kScanItems + q;
-        if (idx < n) out_excl[idx] = run;
+            for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+            excl += x;
+            if (pm) break;
+            base -= 32;
+        }
+        if (lane == 0) s_excl = excl;
+    }
+    __syncthreads();
+    const int excl = s_excl;
+    if (tile > 0 && threadIdx.x == kLbThreads - 1) {
+        __threadfence();
+        atomicExch(status + tile, kFlagPre | (unsigned)(excl + incl));
+    }
+    int run = excl + incl - local;
+#pragma unroll
+    for (int q = 0; q < kLbItems; ++q) {
+        const int idx = i0 + q;
+        if (idx < n) b.starts[idx] = run;
         run += v[q];
     }
-    if (threadIdx.x == blockDim.x - 1) tile_sums[blockIdx.x] = incl;
-}
-
-__global__ void k_scan_add(int *out, int n, const int *tile_offsets) {
-    const int tile = blockIdx.x;
-    const int add = tile_offsets[tile];
-    if (add == 0) return;
-    for (int q = threadIdx.x; q < kScanTile; q += blockDim.x) {
-        const int idx = tile * kScanTile + q;
-        if (idx < n) out[idx] += add;
+    if (i0 < n && i0 + kLbItems >= n) {  // owner of the last cell: total members
+        b.starts[n] = run;
+        b.ctr->n_sorted = run;
     }
-}
-
-__global__ void k_scan_finish(const __grid_constant__ RtsParams p, RtsBuffers b) {
-    // starts[n_cells] = total members
-    const int nc = p.n_cells;
-    const int last = b.starts[nc - 1] + b.cell_count[nc - 1] + b.cell_bcount[nc - 1];
-    b.starts[nc] = last;
-    b.ctr->n_sorted = last;
-}
-
-// recursive tile scan: exclusive scan of a[0..n) into out (a2 added when kFromCounts)
-int scan_exclusive(const int *a, const int *a2, int n, int *out, int *tmp, cudaStream_t s,
-                   bool from_counts) {
-    const int tiles = (n + kScanTile - 1) / kScanTile;
-    int *sums = tmp;
-    int *offs = tmp + tiles;
-    if (from_counts)
-        rts_note_launch(), k_scan_tiles<true><<<tiles, kScanThreads, 0, s>>>(a, a2, n, out, sums);
-    else
-        rts_note_launch(), k_scan_tiles<false><<<tiles, kScanThreads, 0, s>>>(a, a2, n, out, sums);
-    RTS_LAUNCH_CHECK();
-    if (tiles > 1) {
-        int rc = scan_exclusive(sums, nullptr, tiles, offs, tmp + 2 * tiles, s, false);
-        if (rc) return rc;
-        rts_note_launch(), k_scan_add<<<tiles, 256, 0, s>>>(out, n, offs);
-        RTS_LAUNCH_CHECK();
-    }
-    return 0;
 }
 
 // stable scatter, step 1: atomic cursor per block
@@ -194,7 +210,16 @@ __global__ void k_scatter_fluid(const __grid_constant__ RtsParams p, RtsBuffers 
     }
 }
 
-// step 2: restore ascending index order inside each block's fluid run
+// step 2: restore ascending index order inside each block's fluid run.
+// Runs of up to 16 (the common case: ~8-11 particles per block) are sorted
+// in registers by a fully unrolled bitonic network (static indices, no local
+// memory); longer runs fall back to an insertion sort in place.
+RTS_DEV void cswap(int &a, int &b) {
+    const int lo = min(a, b), hi = max(a, b);
+    a = lo;
+    b = hi;
+}
+
 __global__ void k_sort_runs(const __grid_constant__ RtsParams p, RtsBuffers b) {
     if (fatal(b.ctr)) return;
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < p.n_cells;
@@ -202,16 +227,25 @@ __global__ void k_sort_runs(const __grid_constant__ RtsParams p, RtsBuffers b) {
         const int n = b.cell_count[c];
         if (n < 2) continue;
         int *run = b.order + b.starts[c];
-        if (n <= 32) {
-            int v[32];
-            for (int q = 0; q < n; ++q) v[q] = run[q];
-            for (int q = 1; q < n; ++q) {
-                const int key = v[q];
-                int r = q - 1;
-                while (r >= 0 && v[r] > key) { v[r + 1] = v[r]; --r; }
-                v[r + 1] = key;
-            }
-            for (int q = 0; q < n; ++q) run[q] = v[q];
+        if (n <= 16) {
+            int v[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) v[q] = q < n ? run[q] : 0x7fffffff;
+#pragma unroll
+            for (int k = 2; k <= 16; k <<= 1)
+#pragma unroll
+                for (int j = k >> 1; j > 0; j >>= 1)
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) {
+                        const int r = q ^ j;
+                        if (r > q) {
+                            if ((q & k) == 0) cswap(v[q], v[r]);
+                            else cswap(v[r], v[q]);
+                        }
+                    }
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+                if (q < n) run[q] = v[q];
         } else {
             for (int q = 1; q < n; ++q) {
                 const int key = run[q];
@@ -297,10 +331,9 @@ int rts_grid_sort(const RtsParams *p, const RtsBuffers *b, void *stream) {
         rts_note_launch(), k_boundary_active<<<rts_blocks(p->n_bcells, kThreads), kThreads, 0, s>>>(*p, *b);
         RTS_LAUNCH_CHECK();
     }
-    int rc = scan_exclusive(b->cell_count, b->cell_bcount, p->n_cells, b->starts, b->scan_tmp, s,
-                            true);
-    if (rc) return rc;
-    rts_note_launch(), k_scan_finish<<<1, 1, 0, s>>>(*p, *b);
+    const int tiles = (p->n_cells + kLbTile - 1) / kLbTile;
+    cudaMemsetAsync(b->scan_tmp, 0, sizeof(int) * (size_t)(2 + 2 * tiles), s);  // counter + status
+    rts_note_launch(), k_scan_lookback<<<tiles, kLbThreads, 0, s>>>(*p, *b);
     RTS_LAUNCH_CHECK();
     cudaMemsetAsync(b->fill, 0, sizeof(int) * (size_t)p->n_cells, s);
     rts_note_launch(), k_scatter_fluid<<<rts_blocks(p->n_fluid, kThreads), kThreads, 0, s>>>(*p, *b);

@@ -118,8 +118,8 @@ class BlockGrid:
         A.alloc("cell_bcount", (nc,), i32, 0)
         A.alloc("starts", (nc + 1,), i32, 0)
         A.alloc("fill", (nc,), i32, 0)
-        tiles = -(-nc // 4096)
-        A.alloc("scan_tmp", (4 * tiles + 64,), i32, 0)
+        tiles = -(-nc // 1024)  # grid.cu k_scan_lookback: counter + one 64-bit status per tile
+        A.alloc("scan_tmp", (2 * tiles + 64,), i32, 0)
         A.alloc("vmax", (nc,), torch.float64, 0)
         A.alloc("fmax", (nc,), torch.float64, 0)
         A.alloc("block_raw", (nc,), i8, 0)
