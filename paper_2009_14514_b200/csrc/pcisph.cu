@@ -1370,15 +1370,19 @@ int rts_pci_control(const RtsParams *p, const RtsBuffers *b, int sync_mode,
 // joined to the major graph's capture while the iterations are captured into
 // the conditional bodies.
 static void side_stream(int slot, cudaStream_t *side, cudaEvent_t **ev) {
-    static cudaStream_t st[2] = {nullptr, nullptr};
-    static cudaEvent_t e[2][2];
-    if (!st[slot]) {
-        cudaStreamCreateWithFlags(&st[slot], cudaStreamNonBlocking);
-        cudaEventCreateWithFlags(&e[slot][0], cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&e[slot][1], cudaEventDisableTiming);
+    constexpr int kMaxDev = 16;  // per device: streams / events belong to one context
+    static cudaStream_t st[kMaxDev][2] = {};
+    static cudaEvent_t e[kMaxDev][2][2];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    dev = dev < kMaxDev ? dev : kMaxDev - 1;
+    if (!st[dev][slot]) {
+        cudaStreamCreateWithFlags(&st[dev][slot], cudaStreamNonBlocking);
+        cudaEventCreateWithFlags(&e[dev][slot][0], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&e[dev][slot][1], cudaEventDisableTiming);
     }
-    *side = st[slot];
-    *ev = e[slot];
+    *side = st[dev][slot];
+    *ev = e[dev][slot];
 }
 
 // One correction iteration with device-side control (pcisph.py:633-715 or
