@@ -477,13 +477,13 @@ RTS_DEV void density_one(const RtsParams &p, const RtsBuffers &b, int i, int lan
         // the tables exceed L2) are requested before this chunk's gathers
         int jn[CH];
 #pragma unroll
-        for (int u = 0; u < CH; ++u) jn[u] = u < c ? row[u * S] : i;
+        for (int u = 0; u < CH; ++u) jn[u] = u < c ? __ldcs(row + u * S) : i;
         for (int q = 0; q < c; q += CH) {
             int j8[CH];
 #pragma unroll
             for (int u = 0; u < CH; ++u) {
                 j8[u] = jn[u];
-                jn[u] = q + CH + u < c ? row[(q + CH + u) * S] : i;
+                jn[u] = q + CH + u < c ? __ldcs(row + (q + CH + u) * S) : i;
             }
             float4 o[CH];
 #pragma unroll
@@ -708,13 +708,13 @@ RTS_DEV void pforce_one(const RtsParams &p, const RtsBuffers &b, int i, int lane
     if (LG == 1) {
         int jn[kPF];  // software-pipelined table reads, as in density_one
 #pragma unroll
-        for (int u = 0; u < kPF; ++u) jn[u] = u < c ? row[u * S] : i;
+        for (int u = 0; u < kPF; ++u) jn[u] = u < c ? __ldcs(row + u * S) : i;
         for (int q = 0; q < c; q += kPF) {
             int j4[kPF];
 #pragma unroll
             for (int u = 0; u < kPF; ++u) {
                 j4[u] = jn[u];
-                jn[u] = q + kPF + u < c ? row[(q + kPF + u) * S] : i;
+                jn[u] = q + kPF + u < c ? __ldcs(row + (q + kPF + u) * S) : i;
             }
             float4 o4[kPF];
 #pragma unroll
