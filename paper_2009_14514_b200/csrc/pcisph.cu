@@ -236,7 +236,7 @@ RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshC
                     while (mem) {
                         const int q = __ffs(mem) - 1;
                         mem &= mem - 1u;
-                        if (cntn < p.width) row[cntn * S] = b.order[cb + q];
+                        if (cntn < p.width) __stcs(row + cntn * S, b.order[cb + q]);
                         ++cntn;
                     }
                 }
@@ -248,7 +248,7 @@ RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshC
                         (__ballot_sync(gmask, in) >> gshift) & (G == 32 ? 0xffffffffu : ((1u << G) - 1u));
                     if (in) {
                         const int slot = cntn + __popc(m & lt);
-                        if (slot < p.width) row[slot * S] = b.order[kk];
+                        if (slot < p.width) __stcs(row + slot * S, b.order[kk]);
                     }
                     cntn += __popc(m);
                 }
