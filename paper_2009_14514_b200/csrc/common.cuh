@@ -68,6 +68,21 @@ RTS_DEV double norm3(float x, float y, float z) {
     return xsqrt(dist2((double)x, (double)y, (double)z));
 }
 
+// L2 residency hint for gathered rows (x*, p): loads tagged evict_last stay in
+// L2 while the streamed neighbour tables (loaded evict_first) pass through.
+RTS_DEV unsigned long long l2_keep_policy() {
+    unsigned long long pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+RTS_DEV float4 ldg_keep(const float4 *ptr, unsigned long long pol) {
+    float4 v;
+    asm volatile("ld.global.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+        : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+        : "l"(ptr), "l"(pol));
+    return v;
+}
+
 // ---- exact neighbour membership ------------------------------------------
 // The reference keeps j iff fp64 ((dx^2 + dy^2) + dz^2) < h^2 (grid.py:140-144).
 // Candidates are first classified in fp32 with a +-1e-5 relative band around

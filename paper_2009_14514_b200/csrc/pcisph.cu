@@ -698,6 +698,7 @@ RTS_DEV void pforce_one(const RtsParams &p, const RtsBuffers &b, int i, int lane
     const double m2 = xmul(xmul(p.mass, p.mass), p.c_spiky);  // m^2 c_spiky
     const double inv_rho0_sq = xdiv(1.0, xmul(p.rho0, p.rho0));
     const float4 a = xs4[i];
+    const unsigned long long pol = l2_keep_policy();
     const double xi = a.x, yi = a.y, zi = a.z;
     const double term_i = xmul((double)a.w, inv_rho0_sq);
     const double wall = xadd(term_i, term_i);
@@ -718,7 +719,7 @@ RTS_DEV void pforce_one(const RtsParams &p, const RtsBuffers &b, int i, int lane
             }
             float4 o4[kPF];
 #pragma unroll
-            for (int u = 0; u < kPF; ++u) o4[u] = xs4[j4[u]];
+            for (int u = 0; u < kPF; ++u) o4[u] = ldg_keep(xs4 + j4[u], pol);
 #pragma unroll
             for (int u = 0; u < kPF; ++u)
                 if (q + u < c)
