@@ -80,12 +80,6 @@ def make_device_solver(kind: str, device):
         s = WcsphSolver(scene_cfg3(), mode="rts", device=device)
     nf = s.n_fluid
     x = (s.host("pos")[:nf] + jitter_np(nf, s.scene.spacing)).astype(np.float32)
-    if os.environ.get("RTS_BENCH_SORTED"):  # experiment: number particles in block order
-        g = s.grid
-        cell = np.clip(np.floor((x.astype(np.float64) - g.origin) / g.block_size), 0,
-                       np.asarray(g.dims) - 1).astype(np.int64)
-        key = (cell[:, 0] * g.dims[1] + cell[:, 1]) * g.dims[2] + cell[:, 2]
-        x = x[np.argsort(key, kind="stable")]
     s.pos[:nf] = torch.as_tensor(x, device=s.device)
     if kind == "pcisph":
         s.xstar[:] = s.pos[:nf]
