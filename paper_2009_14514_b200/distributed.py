@@ -140,8 +140,9 @@ class Exchanger:
         for q in peers:
             ops.append(dist.P2POp(dist.isend, counts_out[q], q))
             ops.append(dist.P2POp(dist.irecv, counts_in[q], q))
-        for r in dist.batch_isend_irecv(ops):
-            r.wait()
+        if ops:  # no peers (a single slab): nothing to exchange
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
         bufs = {q: torch.empty((int(counts_in[q].item()), width), dtype=torch.float64,
                                device=self.device) for q in peers}
         ops = []
@@ -218,11 +219,22 @@ class SlabDriver:
         if bool(far.any()):
             raise RuntimeError("a particle crossed more than one slab in one step")
         recv = self.x._sendrecv(send, self.width)
-        kidx = torch.nonzero(keep).reshape(-1)
-        rows = [pack({k: v[kidx] for k, v in state.items()}, gid[kidx], self.fields)] + recv
-        rows = torch.cat(rows, 0)
-        rows = rows[torch.argsort(rows[:, 0])]
-        return unpack(rows, self.fields)
+        # kept rows stay in their dtypes and their (global-id) order; only
+        # arrivals force a merge by global id
+        leaving = not bool(keep.all())
+        if leaving:
+            kidx = torch.nonzero(keep).reshape(-1)
+            gid = gid[kidx]
+            state = {k: v[kidx] for k, v in state.items()}
+        rows = torch.cat(recv, 0) if recv else None
+        if rows is None or rows.shape[0] == 0:
+            return gid, state
+        rgid, rstate = unpack(rows, self.fields)
+        allg = torch.cat([gid, rgid.to(gid.dtype)])
+        order = torch.argsort(allg)
+        out = {k: torch.cat([v, rstate[k].to(v.dtype).reshape((-1,) + v.shape[1:])])[order]
+               for k, v in state.items()}
+        return allg[order], out
 
     def merged(self, gid, state, ggid, gstate):
         """Owned + ghosts sorted by global id (the single-domain order)."""
