@@ -211,9 +211,9 @@ __global__ void k_scatter_fluid(const __grid_constant__ RtsParams p, RtsBuffers 
 }
 
 // step 2: restore ascending index order inside each block's fluid run.
-// Runs of up to 16 (the common case: ~8-11 particles per block) are sorted
-// in registers by a fully unrolled bitonic network (static indices, no local
-// memory); longer runs fall back to an insertion sort in place.
+// Runs of up to 16 (most WCSPH blocks, many PCISPH ones) are sorted in
+// registers by a fully unrolled bitonic network (static indices, no local
+// memory); runs up to 32 by insertion in a local array, longer ones in place.
 RTS_DEV void cswap(int &a, int &b) {
     const int lo = min(a, b), hi = max(a, b);
     a = lo;
@@ -246,6 +246,16 @@ __global__ void k_sort_runs(const __grid_constant__ RtsParams p, RtsBuffers b) {
 #pragma unroll
             for (int q = 0; q < 16; ++q)
                 if (q < n) run[q] = v[q];
+        } else if (n <= 32) {  // 2.2-spacing blocks hold up to 27 lattice points
+            int v[32];
+            for (int q = 0; q < n; ++q) v[q] = run[q];
+            for (int q = 1; q < n; ++q) {
+                const int key = v[q];
+                int r = q - 1;
+                while (r >= 0 && v[r] > key) { v[r + 1] = v[r]; --r; }
+                v[r + 1] = key;
+            }
+            for (int q = 0; q < n; ++q) run[q] = v[q];
         } else {
             for (int q = 1; q < n; ++q) {
                 const int key = run[q];
