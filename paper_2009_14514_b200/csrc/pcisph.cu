@@ -356,8 +356,13 @@ RTS_DEV void restore_one(const RtsBuffers &b, int i) {
 __global__ void k_motion(const __grid_constant__ RtsParams p, RtsBuffers b, int all) {
     RTS_ITER_GUARD();
     const bool restore = b.ctl && b.ctl->snap_op == 2;
+    // first iteration of a minor step: p = 0, f_p = 0 for all fluid
+    // (pcisph.py:570-571) folded in here; the refresh phase ends now
+    const bool zero = b.ctl && b.ctl->it == 0;
+    if (zero && blockIdx.x == 0 && threadIdx.x == 0)
+        b.ctl->stats[b.ctl->minor].t_refreshed = gtimer();
     if (all < 0) all = b.ctl->motion_all;
-    if (restore) all = 1;
+    if (restore || zero) all = 1;
     const double dim = xmul(p.dt, p.inv_mass);
     const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
     if (!all) {
@@ -373,11 +378,18 @@ __global__ void k_motion(const __grid_constant__ RtsParams p, RtsBuffers b, int 
     for (int g = tid; g < ng; g += nt) {
         float fe[12], fp[12], v[12], x[12];
         load12(b.force, g, fe);
-        load12(restore ? b.snap_fp : b.f_p, g, fp);
         load12(b.vel, g, v);
         load12(b.pos, g, x);
-        const float4 pr = reinterpret_cast<const float4 *>(restore ? b.snap_p : b.pres)[g];
-        if (restore) {
+        float4 pr;
+        if (zero) {
+#pragma unroll
+            for (int c = 0; c < 12; ++c) fp[c] = 0.f;
+            pr = make_float4(0.f, 0.f, 0.f, 0.f);
+        } else {
+            load12(restore ? b.snap_fp : b.f_p, g, fp);
+            pr = reinterpret_cast<const float4 *>(restore ? b.snap_p : b.pres)[g];
+        }
+        if (restore || zero) {
             store12(b.f_p, g, fp);
             reinterpret_cast<float4 *>(b.pres)[g] = pr;
         }
@@ -396,6 +408,10 @@ __global__ void k_motion(const __grid_constant__ RtsParams p, RtsBuffers b, int 
     }
     for (int i = 4 * ng + tid; i < nf; i += nt) {
         if (restore) restore_one(b, i);
+        if (zero) {
+            b.pres[i] = 0.f;
+            b.f_p[3 * i] = b.f_p[3 * i + 1] = b.f_p[3 * i + 2] = 0.f;
+        }
         if (!is_ghost(b, i)) motion_one(p, b, i, dim);
     }
 }
@@ -1436,13 +1452,12 @@ int rts_pci_minor_head(const RtsParams *p, const RtsBuffers *b, int minor, void 
     cudaEvent_t *ev;
     side_stream(1, &side, &ev);
     if ((rc = rts_pci_minor_begin(p, b, minor, 0, stream))) return rc;
-    // {refresh -> p, f_p = 0} || {S_e = empty, observed blocks}
+    // {refresh} || {S_e = empty, observed blocks}; p, f_p = 0 is folded into the first motion
     cudaEventRecord(ev[0], s);
     cudaStreamWaitEvent(side, ev[0], 0);
     cudaMemsetAsync(b->in_se, 0, (size_t)p->n_fluid, side);
     if ((rc = rts_pci_observed(p, b, 0, side))) return rc;
-    if ((rc = rts_pci_refresh(p, b, 0, 1, stream))) return rc;
-    if ((rc = rts_pci_zero_pressure(p, b, stream))) return rc;
+    if ((rc = rts_pci_refresh(p, b, 0, 1, stream))) return rc;  // p, f_p = 0: first motion
     cudaEventRecord(ev[1], side);
     cudaStreamWaitEvent(s, ev[1], 0);
     return 0;
@@ -1538,8 +1553,7 @@ void *rts_pci_graph_create(const RtsParams *p, const RtsBuffers *b, int mode, in
             }
         } else {
             if ((rc = rts_pci_minor_begin(p, b, 0, 1, cs))) break;
-            if ((rc = rts_pci_refresh(p, b, 1, 0, cs))) break;
-            if ((rc = rts_pci_zero_pressure(p, b, cs))) break;
+            if ((rc = rts_pci_refresh(p, b, 1, 0, cs))) break;  // p, f_p = 0: first motion
             if ((rc = add_while_loop(cs, p, b, 1, local_attempts, iteration_cap))) break;
             if ((rc = rts_pci_integrate(p, b, 0, cs))) break;
             rc = rts_pci_minor_end(p, b, 0, cs);
