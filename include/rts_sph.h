@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define RTS_ABI_VERSION 15
+#define RTS_ABI_VERSION 16
 
 /* err_flags bits */
 #define RTS_ERR_ESCAPED   0x1u  /* fluid left the padded grid or non-finite (grid.py:268-273) */
@@ -97,7 +97,9 @@ typedef struct RtsCounters {
     int64_t  missing;          /* neighbour audit: true neighbours absent from tables */
     uint32_t blocks_done;      /* last-block-done counter of the S_e reduction */
     int32_t  pad3;
-    double   reserved[6];
+    int64_t  stamps[4];        /* RTS-WCSPH step graph: %globaltimer (ns) at the start, end of
+                                * the grid rebuild, start of the density pass, end */
+    double   reserved[2];
 } RtsCounters;
 
 /* Per-minor-step record written by the device loop control (StepStats,
@@ -223,6 +225,8 @@ int rts_memset(void *dst, int value, int64_t bytes, void *stream);
 
 /* Reset the counters block (err_flags = 0, first_escaped = INT32_MAX ...). */
 int rts_counters_reset(const RtsBuffers *b, void *stream);
+/* stamps[slot] = %globaltimer (one-thread kernel; phase timing inside graphs). */
+int rts_stamp(const RtsBuffers *b, int slot, void *stream);
 
 /* ---- block grid (grid.py) -------------------------------------------- */
 /* One-time static binning of the boundary shell: bcell_of, and

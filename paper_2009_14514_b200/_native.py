@@ -12,7 +12,7 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "librtssph.so")
-ABI_VERSION = 15
+ABI_VERSION = 16
 
 _c = ctypes
 _D = _c.c_double
@@ -40,7 +40,8 @@ class RtsCounters(_c.Structure):
         ("overflow", _c.c_int64), ("n_sorted", _I), ("n_pred", _I), ("n_force", _I),
         ("n_list", _I), ("fmax_bits", _c.c_uint64), ("sum_rho", _D), ("max_err", _D),
         ("any_se", _I), ("lists_all", _I), ("missing", _c.c_int64),
-        ("blocks_done", _c.c_uint32), ("pad3", _I), ("reserved", _D * 6),
+        ("blocks_done", _c.c_uint32), ("pad3", _I), ("stamps", _c.c_int64 * 4),
+        ("reserved", _D * 2),
     ]
 
 
@@ -117,6 +118,7 @@ SIGNATURES = {
     "rts_pci_snapshot": [_PP, _PB, _c.c_int, _P],
     "rts_vel_max": [_PP, _PB, _P],
     "rts_counters_reset": [_PB, _P],
+    "rts_stamp": [_PB, _c.c_int, _P],
     "rts_pci_zero_pressure": [_PP, _PB, _P],
     "rts_pci_major_begin": [_PP, _PB, _P],
     "rts_pci_minor_begin": [_PP, _PB, _c.c_int, _c.c_int, _P],

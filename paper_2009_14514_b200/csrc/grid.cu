@@ -298,12 +298,21 @@ __global__ void k_force_max(const __grid_constant__ RtsParams p, RtsBuffers b) {
 __global__ void k_counters_reset(RtsCounters *c) {
     RtsCounters z = {};
     z.first_escaped = 0x7fffffff;
+    z.stamps[0] = gtimer();
     *c = z;
 }
+
+__global__ void k_stamp(RtsCounters *c, int slot) { c->stamps[slot] = gtimer(); }
 
 }  // namespace
 
 extern "C" {
+
+int rts_stamp(const RtsBuffers *b, int slot, void *stream) {
+    rts_note_launch(), k_stamp<<<1, 1, 0, (cudaStream_t)stream>>>(b->ctr, slot);
+    RTS_LAUNCH_CHECK();
+    return 0;
+}
 
 int rts_counters_reset(const RtsBuffers *b, void *stream) {
     rts_note_launch(), k_counters_reset<<<1, 1, 0, (cudaStream_t)stream>>>(b->ctr);

@@ -16,6 +16,7 @@ constexpr int8_t kEmpty = 127;  // regions.py:35
 
 __global__ void k_assign(const __grid_constant__ RtsParams p, RtsBuffers b) {
     if (fatal(b.ctr)) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) b.ctr->stamps[1] = gtimer();  // grid rebuilt
     const double r = p.block_size;
     const double sound_bound = xdiv(xmul(p.lambda_v, r), p.sound_speed);
     const double rm = xmul(r, p.mass);

@@ -22,6 +22,7 @@ constexpr int kThreads = 128;
 __global__ void __launch_bounds__(256) k_propagate(const __grid_constant__ RtsParams p,
                                                    RtsBuffers b) {
     if (fatal(b.ctr)) return;
+    if (!p.rts && blockIdx.x == 0 && threadIdx.x == 0) b.ctr->stamps[1] = gtimer();
     const int n_sorted = b.ctr->n_sorted;
     const int stride = gridDim.x * blockDim.x;
     for (int base = blockIdx.x * blockDim.x; base < n_sorted; base += stride) {
@@ -148,6 +149,7 @@ RTS_DEV int collect_hits(const RtsParams &p, const RtsBuffers &b, const float4 *
 __global__ void __launch_bounds__(kThreads) k_density(const __grid_constant__ RtsParams p,
                                                       RtsBuffers b) {
     if (fatal(b.ctr)) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) b.ctr->stamps[2] = gtimer();  // physics begins
     __shared__ int s_hits[kHitCap * kThreads];
     int *hits = s_hits + threadIdx.x;
     const int n_act = b.ctr->n_compute;
@@ -430,7 +432,8 @@ void *rts_wcsph_graph_create(const RtsParams *p, const RtsBuffers *b, int *err) 
         if ((rc = rts_wcsph_propagate(p, b, cs))) break;
         if ((rc = rts_wcsph_density(p, b, cs))) break;
         if ((rc = rts_wcsph_forces(p, b, cs))) break;
-        rc = rts_wcsph_integrate(p, b, cs);
+        if ((rc = rts_wcsph_integrate(p, b, cs))) break;
+        rc = rts_stamp(b, 3, cs);
     } while (0);
     cudaGraph_t g = nullptr;
     e = cudaStreamEndCapture(cs, &g);

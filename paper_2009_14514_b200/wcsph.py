@@ -353,7 +353,12 @@ class WcsphSolver(_DeviceSolver):
         n_compute = int(c.n_compute)
         self.step_index += 1
         self.sim_time += dt
-        self._timers = self.timer.totals()
+        if self._graph_step:  # device %globaltimer stamps inside the step graph
+            t0, t1, t2, t3 = (int(x) for x in c.stamps)
+            self._timers = {"neighbor": max(0, t1 - t0) * 1e-9, "rts": max(0, t2 - t1) * 1e-9,
+                            "physics": max(0, t3 - t2) * 1e-9}
+        else:
+            self._timers = self.timer.totals()
         st = StepStats(step=self.step_index, time=self.sim_time, dt=dt, n_compute=n_compute,
                        frac_compute=n_compute / max(1, self.n_fluid),
                        missed_neighbors=self._missed_last,
@@ -373,7 +378,8 @@ class WcsphSolver(_DeviceSolver):
         stream = torch.cuda.current_stream(self.device)
         tm = self.timer
         rts = self.mode == "rts"
-        if self.use_graphs and rts and self._ktimes is None:  # baseline dt varies per step
+        self._graph_step = self.use_graphs and rts and self._ktimes is None
+        if self._graph_step:  # baseline dt varies per step
             tm.start(stream)
             graph = self._graph()
             N.call("rts_graph_launch", graph, stream.cuda_stream)
