@@ -250,6 +250,13 @@ int rts_block_maxima(const RtsParams *p, const RtsBuffers *b, int add_fp, void *
  * pin_region override (wcsph.py:258-259, pcisph.py:528-529).  expand=2:
  * assign_regions only (required levels of _mark_timestep_updates). */
 int rts_block_levels(const RtsParams *p, const RtsBuffers *b, int expand, void *stream);
+/* The public region-field functions on caller-provided fields (regions.py:
+ * smooth_regions, expand_fast_regions, derive_observed):
+ *   op 0: smooth    block_raw -> block_field
+ *   op 1: expand    block_tmp -> block_field over `arg` layers (scratch block_flag, block_raw)
+ *   op 2: observed  block_field + error-block mask in block_flag -> block_tmp (0/1)
+ *   op 3: neighbour minimum of block_raw, out-of-grid cells = arg -> block_field */
+int rts_region_op(const RtsParams *p, const RtsBuffers *b, int op, int arg, void *stream);
 
 /* ---- RTS-PCISPH (pcisph.py) ------------------------------------------- */
 /* Wall rows of xs4 (static positions, marker -1). */

@@ -33,12 +33,20 @@ def __getattr__(name):
     if name in ("make_solver", "SOLVER_NAMES"):
         from . import bench_api
         return getattr(bench_api, name)
+    if name in ("run_simulation", "compare"):
+        from . import run
+        return getattr(run, name)
+    if name in ("assign_regions", "smooth_regions", "expand_fast_regions", "derive_observed"):
+        from . import regions
+        return getattr(regions, name)
     raise AttributeError(name)
 
 
 __all__ = [
     "BlockGrid", "ConfigError", "DEFAULT_SCHEDULE", "KernelSet", "MajorStepController",
-    "NumericalError", "PRESET_NAMES", "PcisphSolver", "Scene", "StepStats", "WcsphSolver",
+    "NumericalError", "PRESET_NAMES", "PcisphSolver", "SOLVER_NAMES", "Scene", "StepStats",
+    "WcsphSolver", "assign_regions", "compare", "derive_observed", "expand_fast_regions",
     "load_scene", "make_solver", "parse_scene_text", "pci_delta", "preset_scene", "read_stats",
-    "seed_particles", "tait_pressure", "validate_schedule", "write_stats", "__version__",
+    "run_simulation", "seed_particles", "smooth_regions", "tait_pressure", "validate_schedule",
+    "write_stats", "__version__",
 ]

@@ -115,6 +115,56 @@ __global__ void k_expand_apply(const __grid_constant__ RtsParams p, const int8_t
     }
 }
 
+// derive_observed (regions.py:110-125) for a caller-provided error mask
+// (block_flag): occupied and (bordering a strictly smaller region, or
+// bordering an error block without being one); -> block_tmp
+__global__ void k_observed_mask(const __grid_constant__ RtsParams p, RtsBuffers b) {
+    const int nx = p.dims[0], ny = p.dims[1], nz = p.dims[2];
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < p.n_cells;
+         c += gridDim.x * blockDim.x) {
+        const int8_t f = b.block_field[c];
+        bool obs = false;
+        if (f > 0) {
+            const int cz = c % nz, cy = (c / nz) % ny, cx = c / (ny * nz);
+            int8_t m = kEmpty;
+            bool near_err = false;
+            for (int ax = max(0, cx - 1); ax <= min(nx - 1, cx + 1); ++ax)
+                for (int ay = max(0, cy - 1); ay <= min(ny - 1, cy + 1); ++ay) {
+                    const int base = (ax * ny + ay) * nz;
+                    for (int az = max(0, cz - 1); az <= min(nz - 1, cz + 1); ++az) {
+                        const int q = base + az;
+                        if (q == c) continue;
+                        const int8_t v = b.block_field[q];
+                        if (v > 0 && v < m) m = v;
+                        near_err = near_err || b.block_flag[q];
+                    }
+                }
+            obs = (m < f) || (near_err && !b.block_flag[c]);
+        }
+        b.block_tmp[c] = obs;
+    }
+}
+
+// neighbor_min (grid.py:33-45) of an int8 field in block_raw, out-of-grid
+// cells = pad; -> block_field
+__global__ void k_neighbor_min(const __grid_constant__ RtsParams p, RtsBuffers b, int pad) {
+    const int nx = p.dims[0], ny = p.dims[1], nz = p.dims[2];
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < p.n_cells;
+         c += gridDim.x * blockDim.x) {
+        const int cz = c % nz, cy = (c / nz) % ny, cx = c / (ny * nz);
+        int m = pad;
+        for (int ax = cx - 1; ax <= cx + 1; ++ax)
+            for (int ay = cy - 1; ay <= cy + 1; ++ay)
+                for (int az = cz - 1; az <= cz + 1; ++az) {
+                    if (ax == cx && ay == cy && az == cz) continue;
+                    const bool in = ax >= 0 && ax < nx && ay >= 0 && ay < ny && az >= 0 && az < nz;
+                    const int v = in ? (int)b.block_raw[(ax * ny + ay) * nz + az] : pad;
+                    m = v < m ? v : m;
+                }
+        b.block_field[c] = (int8_t)m;
+    }
+}
+
 }  // namespace
 
 extern "C" int rts_block_levels(const RtsParams *p, const RtsBuffers *b, int expand,
@@ -138,6 +188,36 @@ extern "C" int rts_block_levels(const RtsParams *p, const RtsBuffers *b, int exp
     rts_note_launch(), k_dilate_axis<<<blocks, kThreads, 0, s>>>(*p, nullptr, m0, m1, 1, 4, 0);
     rts_note_launch(), k_dilate_axis<<<blocks, kThreads, 0, s>>>(*p, nullptr, m1, m0, 0, 4, 0);
     rts_note_launch(), k_expand_apply<<<blocks, kThreads, 0, s>>>(*p, b->block_tmp, m0, b->block_field);
+    RTS_LAUNCH_CHECK();
+    return 0;
+}
+
+// The regions.py functions on caller-provided fields (the public API of the
+// reference: smooth_regions, expand_fast_regions, derive_observed).
+//   op 0: smooth   block_raw -> block_field
+//   op 1: expand   block_tmp -> block_field, `arg` layers (scratch: block_flag)
+//   op 2: observed block_field + error mask block_flag -> block_tmp
+//   op 3: neighbour minimum of block_raw (out-of-grid = arg) -> block_field
+extern "C" int rts_region_op(const RtsParams *p, const RtsBuffers *b, int op, int arg,
+                             void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    const int blocks = rts_blocks(p->n_cells, kThreads);
+    if (op == 0) {
+        rts_note_launch(), k_smooth<<<blocks, kThreads, 0, s>>>(*p, *b, b->block_field);
+    } else if (op == 1) {
+        uint8_t *m0 = b->block_flag;
+        uint8_t *m1 = reinterpret_cast<uint8_t *>(b->block_raw);  // scratch
+        rts_note_launch(), k_dilate_axis<<<blocks, kThreads, 0, s>>>(*p, b->block_tmp, nullptr, m0, 2, arg, 1);
+        rts_note_launch(), k_dilate_axis<<<blocks, kThreads, 0, s>>>(*p, nullptr, m0, m1, 1, arg, 0);
+        rts_note_launch(), k_dilate_axis<<<blocks, kThreads, 0, s>>>(*p, nullptr, m1, m0, 0, arg, 0);
+        rts_note_launch(), k_expand_apply<<<blocks, kThreads, 0, s>>>(*p, b->block_tmp, m0, b->block_field);
+    } else if (op == 2) {
+        rts_note_launch(), k_observed_mask<<<blocks, kThreads, 0, s>>>(*p, *b);
+    } else if (op == 3) {
+        rts_note_launch(), k_neighbor_min<<<blocks, kThreads, 0, s>>>(*p, *b, arg);
+    } else {
+        return (int)cudaErrorInvalidValue;
+    }
     RTS_LAUNCH_CHECK();
     return 0;
 }

@@ -26,36 +26,18 @@ from ._device import Arena, Counters, as_device_f32, raise_on_errors, require_cu
 __all__ = ["BlockGrid", "neighbor_min", "dilate_mask"]
 
 
-def neighbor_min(field: np.ndarray, pad_value) -> np.ndarray:
-    """Host helper kept for API parity (grid.py:33-45): min over the 26
-    adjacent cells, ``pad_value`` outside."""
-    f = np.asarray(field)
-    padded = np.pad(f, 1, constant_values=pad_value)
-    out = np.full_like(f, pad_value)
-    nx, ny, nz = f.shape
-    for dx in (-1, 0, 1):
-        for dy in (-1, 0, 1):
-            for dz in (-1, 0, 1):
-                if dx or dy or dz:
-                    np.minimum(out, padded[1 + dx:1 + dx + nx, 1 + dy:1 + dy + ny,
-                                           1 + dz:1 + dz + nz], out=out)
-    return out
+def neighbor_min(field, pad_value):
+    """grid.py:33-45 of the reference (26-neighbour minimum, ``pad_value``
+    outside), evaluated on the device: ``regions.neighbor_min``."""
+    from .regions import neighbor_min as _nm
+    return _nm(field, pad_value)
 
 
-def dilate_mask(mask: np.ndarray, layers: int = 1) -> np.ndarray:
-    """Host helper kept for API parity (grid.py:48-62): Chebyshev dilation."""
-    cur = np.asarray(mask, dtype=bool)
-    for _ in range(layers):
-        padded = np.pad(cur, 1, constant_values=False)
-        nxt = cur.copy()
-        nx, ny, nz = cur.shape
-        for dx in (-1, 0, 1):
-            for dy in (-1, 0, 1):
-                for dz in (-1, 0, 1):
-                    if dx or dy or dz:
-                        nxt |= padded[1 + dx:1 + dx + nx, 1 + dy:1 + dy + ny, 1 + dz:1 + dz + nz]
-        cur = nxt
-    return cur
+def dilate_mask(mask, layers: int = 1):
+    """grid.py:48-62 of the reference (Chebyshev dilation by ``layers``),
+    evaluated on the device: ``regions.dilate_mask``."""
+    from .regions import dilate_mask as _dm
+    return _dm(mask, layers)
 
 
 class BlockGrid:
