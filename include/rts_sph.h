@@ -273,6 +273,11 @@ int rts_pci_major_particles(const RtsParams *p, const RtsBuffers *b, void *strea
  * with _ext_forces (pcisph.py:174-199). */
 int rts_pci_refresh(const RtsParams *p, const RtsBuffers *b, int all, int two_layer_r1,
                     void *stream);
+/* BlockGrid.search_into (grid.py:297-331): rows nbr / cnt for the n particles
+ * listed in active, layers[t] block layers for entry t, candidates from cpos
+ * (rts_pci_gather of the positions searched). */
+int rts_grid_search(const RtsParams *p, const RtsBuffers *b, const int8_t *layers, int n,
+                    void *stream);
 /* _predict_motion (pcisph.py:202-213): all fluid, or the last force list. */
 int rts_pci_motion(const RtsParams *p, const RtsBuffers *b, int all, void *stream);
 /* turn | S_e | S_ob membership (pcisph.py:634-643) -> pred list (active),

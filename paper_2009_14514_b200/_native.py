@@ -120,6 +120,7 @@ SIGNATURES = {
     "rts_counters_reset": [_PB, _P],
     "rts_stamp": [_PB, _c.c_int, _P],
     "rts_region_op": [_PP, _PB, _c.c_int, _c.c_int, _P],
+    "rts_grid_search": [_PP, _PB, _P, _c.c_int, _P],
     "rts_pci_zero_pressure": [_PP, _PB, _P],
     "rts_pci_major_begin": [_PP, _PB, _P],
     "rts_pci_minor_begin": [_PP, _PB, _c.c_int, _c.c_int, _P],

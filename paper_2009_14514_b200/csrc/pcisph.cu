@@ -158,6 +158,15 @@ RTS_DEV void visc_term(const RefreshConsts &k, const RtsParams &p, const RtsBuff
     fz = xadd(fz, xmul(lap, xsub((double)b.vel[3 * j + 2], vzi)));
 }
 
+RTS_DEV void finish_search(const RtsParams &p, const RtsBuffers &b, int i, int cntn) {
+    if (cntn > p.width) {
+        atomicOr(&b.ctr->err_flags, RTS_ERR_OVERFLOW);
+        atomicAdd((unsigned long long *)&b.ctr->overflow, (unsigned long long)(cntn - p.width));
+        cntn = p.width;
+    }
+    b.cnt[i] = cntn;
+}
+
 RTS_DEV void finish_refresh(const RtsParams &p, const RtsBuffers &b, int i, int cntn, double fx,
                             double fy, double fz) {
     if (cntn > p.width) {
@@ -177,14 +186,16 @@ RTS_DEV void finish_refresh(const RtsParams &p, const RtsBuffers &b, int i, int 
 // load); the short later lists (regions 1-2) use 8- or 32-lane groups so the
 // launch still has enough independent loads in flight (region-1 particles
 // scan 125 blocks, ~1300 candidates).
-template <int G>
+// EXT = false: the bare search (BlockGrid.search_into, grid.py:297-331) --
+// rows and counts only, `lay_in` block layers for this particle.
+template <int G, bool EXT = true>
 RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshConsts &k, int i,
-                         int two_layer_r1, int lane, unsigned gmask, int gshift) {
+                         int two_layer_r1, int lane, unsigned gmask, int gshift, int lay_in = 0) {
     const float4 *cpos = reinterpret_cast<const float4 *>(b.cpos);
     const int nx = p.dims[0], ny = p.dims[1], nz = p.dims[2];
     const float fxi = b.pos[3 * i], fyi = b.pos[3 * i + 1], fzi = b.pos[3 * i + 2];
     const double xi = fxi, yi = fyi, zi = fzi;
-    const int lay = (two_layer_r1 && b.region[i] == 1) ? 2 : 1;
+    const int lay = lay_in > 0 ? lay_in : ((two_layer_r1 && b.region[i] == 1) ? 2 : 1);
     const int cx = trunc_axis(xi, p.origin[0], p.inv_block, nx);
     const int cy = trunc_axis(yi, p.origin[1], p.inv_block, ny);
     const int cz = trunc_axis(zi, p.origin[2], p.inv_block, nz);
@@ -255,6 +266,10 @@ RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshC
             }
         }
     if (G > 1) __syncwarp(gmask);
+    if (!EXT) {
+        if (lane == 0) finish_search(p, b, i, cntn);
+        return;
+    }
     const int nrow = min(cntn, p.width);
     const double vxi = b.vel[3 * i], vyi = b.vel[3 * i + 1], vzi = b.vel[3 * i + 2];
     double fx = 0.0, fy = 0.0, fz = 0.0;
@@ -326,6 +341,15 @@ __global__ void __launch_bounds__(kThreads, 8) k_refresh(const __grid_constant__
         for (int t = tid; t < n; t += nthreads)
             refresh_one<1>(p, b, k, b.active[t], two_layer_r1, 0, 0u, 0);
     }
+}
+
+// BlockGrid.search_into: rows for the refresh list in `active`, layers[t]
+// block layers for entry t (grid.py:88-152)
+__global__ void __launch_bounds__(kThreads) k_search(const __grid_constant__ RtsParams p,
+                                                     RtsBuffers b, const int8_t *layers, int n) {
+    const RefreshConsts k = refresh_consts(p);
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x)
+        refresh_one<1, false>(p, b, k, b.active[t], 0, 0, 0u, 0, layers[t]);
 }
 
 // x* = pos + dt * (vel + dt/m (f_ext + f_p)) (pcisph.py:202-213); xs4.w = p
@@ -1258,6 +1282,15 @@ int rts_pci_refresh(const RtsParams *p, const RtsBuffers *b, int all, int two_la
     rts_note_launch(), k_refresh_list<<<rts_blocks(p->n_fluid, 256, 148 * 4), 256, 0, s>>>(*p, *b, all);
     RTS_LAUNCH_CHECK();
     rts_note_launch(), k_refresh<<<rts_blocks(p->n_fluid, kThreads), kThreads, 0, s>>>(*p, *b, two_layer_r1);
+    RTS_LAUNCH_CHECK();
+    return 0;
+}
+
+int rts_grid_search(const RtsParams *p, const RtsBuffers *b, const int8_t *layers, int n,
+                    void *stream) {
+    if (n <= 0) return 0;
+    rts_note_launch(), k_search<<<rts_blocks(n, kThreads), kThreads, 0, (cudaStream_t)stream>>>(
+        *p, *b, layers, n);
     RTS_LAUNCH_CHECK();
     return 0;
 }

@@ -206,6 +206,129 @@ class BlockGrid:
             return torch.zeros(0, dtype=torch.bool, device=self.device)
         return self.arena["bcell_active"][self._bslot].bool()
 
+    def _table_buffers(self, n_total: int, width: int, n_refresh: int) -> None:
+        A = self.arena
+        stride = -(-max(n_total, 1) // 32) * 32
+        if getattr(self, "_tbl", None) != (n_total, width, n_refresh):
+            A.alloc("cpos", (n_total + 4, 4), torch.float32, 0)
+            A.alloc("slot_of", (max(self.n_fluid, 1),), torch.int32, 0)
+            A.alloc("nbr", (width, stride), torch.int32, 0)
+            A.alloc("cnt", (max(n_total, 1),), torch.int32, 0)
+            A.alloc("active", (max(n_refresh, 1),), torch.int32, 0)
+            self._tbl = (n_total, width, n_refresh)
+        self.params.nbr_stride = stride
+        self.params.width = width
+
+    def search_into(self, pos, refresh, layers, h: float, nbr, cnt) -> None:
+        """Neighbour tables of the particles in ``refresh`` at positions
+        ``pos`` on this (possibly stale) grid, ``layers[t]`` block layers
+        around refresh[t] (grid.py:297-331): rows nbr[i, :cnt[i]] in the
+        reference's fill order; NumericalError on table overflow.  ``nbr`` /
+        ``cnt`` are numpy arrays or tensors, written in place."""
+        from .errors import NumericalError
+        if getattr(self, "n_sorted", None) is None:
+            raise RuntimeError("grid not built; call rebuild() first")
+        ref = torch.as_tensor(np.asarray(refresh), device=self.device).to(torch.int32).reshape(-1)
+        n = int(ref.numel())
+        if n == 0:
+            return
+        x = as_device_f32(pos, self.device).reshape(-1, 3)
+        width = int(nbr.shape[1])
+        self._table_buffers(x.shape[0], width, n)
+        A, p = self.arena, self.params
+        A.bind("pos", x)
+        A["active"][:n].copy_(ref)
+        lay = torch.as_tensor(np.asarray(layers), device=self.device).to(torch.int8).reshape(-1)
+        p.h2 = float(h) * float(h)
+        p.n_fluid = self.n_fluid
+        stream = torch.cuda.current_stream(self.device)
+        self.counters.reset(stream)  # clears the overflow count; restore the CSR size
+        off = N.RtsCounters.n_sorted.offset
+        self.counters.dev[off:off + 4].view(torch.int32).fill_(int(self.n_sorted))
+        N.call("rts_pci_gather", p, A.buf, stream.cuda_stream)  # candidates at `pos`
+        N.call("rts_grid_search", p, A.buf, lay.data_ptr(), n, stream.cuda_stream)
+        c = self.counters.read(stream)
+        idx = ref.long()
+        rows = A["nbr"][:, idx].T.contiguous()  # (n, width)
+        counts = A["cnt"][idx]
+        self._write_rows(nbr, cnt, idx, rows, counts)
+        if c.overflow:
+            raise NumericalError(
+                f"neighbor table overflow: {int(c.overflow)} entries dropped "
+                f"(table width {width}); the particle distribution has collapsed")
+
+    @staticmethod
+    def _write_rows(nbr, cnt, idx, rows, counts) -> None:
+        q = torch.arange(rows.shape[1], device=rows.device)
+        keep = q[None, :] < counts[:, None].long()
+        if isinstance(nbr, torch.Tensor):
+            i = idx.to(nbr.device)
+            cur = nbr[i]
+            nbr[i] = torch.where(keep.to(nbr.device), rows.to(nbr.device, nbr.dtype), cur)
+            cnt[i] = counts.to(cnt.device, cnt.dtype)
+        else:
+            i = idx.cpu().numpy()
+            r, k = rows.cpu().numpy(), keep.cpu().numpy()
+            cur = nbr[i]
+            nbr[i] = np.where(k, r.astype(nbr.dtype), cur)
+            cnt[i] = counts.cpu().numpy().astype(cnt.dtype)
+
+    def neighbors(self, pos, point_index: int, layers: int = 1) -> np.ndarray:
+        """Candidate indices around one particle: every member of the
+        (2 layers + 1)^3 blocks around its current block (grid.py:333-345)."""
+        if getattr(self, "n_sorted", None) is None:
+            raise RuntimeError("grid not built; call rebuild() first")
+        x = np.asarray(pos if not isinstance(pos, torch.Tensor) else pos.cpu().numpy())
+        cx, cy, cz = self.cell_coords(x[point_index:point_index + 1])[0]
+        nx, ny, nz = self.dims
+        starts = self.arena["starts"].cpu().numpy()
+        order = self.order.cpu().numpy()
+        out = []
+        for ax in range(max(0, cx - layers), min(nx, cx + layers + 1)):
+            for ay in range(max(0, cy - layers), min(ny, cy + layers + 1)):
+                base = (ax * ny + ay) * nz
+                z0, z1 = max(0, cz - layers), min(nz, cz + layers + 1)
+                out.append(order[starts[base + z0]:starts[base + z1]])
+        return np.concatenate(out).astype(np.int64) if out else np.zeros(0, dtype=np.int64)
+
+    def count_missing_neighbors(self, pos, n_fluid: int, refresh, h: float, nbr, cnt) -> int:
+        """True neighbours (fresh exhaustive search) absent from the tables of
+        ``refresh`` (grid.py:353-394)."""
+        ref = torch.as_tensor(np.asarray(refresh), device=self.device).to(torch.int32).reshape(-1)
+        n = int(ref.numel())
+        if n == 0:
+            return 0
+        x = as_device_f32(pos, self.device).reshape(-1, 3)
+        audit = BlockGrid(self.origin, self.origin + np.asarray(self.dims) * self.block_size,
+                          max(float(h), self.block_size), device=self.device)
+        audit.rebuild(x, n_fluid)
+        audit._table_buffers(x.shape[0], int(nbr.shape[1]), 1)
+        pa = audit.params
+        pa.h2 = float(h) * float(h)
+        stream = torch.cuda.current_stream(self.device)
+        N.call("rts_pci_gather", pa, audit.arena.buf, stream.cuda_stream)
+        # the tables under audit, column-major, with the refresh list
+        tb = Arena(self.device)
+        width = int(nbr.shape[1])
+        stride = -(-max(x.shape[0], 1) // 32) * 32
+        t_nbr = torch.as_tensor(np.asarray(nbr) if not isinstance(nbr, torch.Tensor) else nbr,
+                                device=self.device).to(torch.int32)
+        tb.alloc("nbr", (width, stride), torch.int32, 0)
+        tb["nbr"][:, : t_nbr.shape[0]].copy_(t_nbr.T)
+        t_cnt = torch.as_tensor(np.asarray(cnt) if not isinstance(cnt, torch.Tensor) else cnt,
+                                device=self.device).to(torch.int32).reshape(-1)
+        tb.bind("cnt", t_cnt.contiguous())
+        tb.alloc("active", (n,), torch.int32, 0)
+        tb["active"].copy_(ref)
+        tb.bind("pos", x)
+        ctr = Counters(tb)
+        ctr.reset(stream)
+        n_view = ctr.dev[N.RtsCounters.n_compute.offset:N.RtsCounters.n_compute.offset + 4]
+        n_view.view(torch.int32).fill_(n)
+        pa.nbr_stride = stride
+        N.call("rts_pci_audit", pa, audit.arena.buf, tb.buf, stream.cuda_stream)
+        return int(ctr.read(stream).missing)
+
     def reduce_fluid_max(self, values) -> torch.Tensor:
         """Per-block max of a fluid scalar, zeros in empty blocks (grid.py:347-351)."""
         v = torch.as_tensor(values, device=self.device).to(torch.float64).reshape(-1)
