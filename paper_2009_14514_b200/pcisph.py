@@ -350,6 +350,14 @@ class PcisphSolver(_DeviceSolver):
         return self.arena["block_field"]
 
     @property
+    def vstar(self) -> torch.Tensor:
+        """Predicted velocities of the last prediction (pcisph.py:202-213),
+        recovered as (x* - pos) / dt from the stored fp32 x* (the kernels keep
+        x* only)."""
+        nf = self.n_fluid
+        return (self.xstar.double() - self.pos[:nf].double()).div_(self.dt).float()
+
+    @property
     def nbr(self) -> torch.Tensor:
         """(n_fluid, 128) view of the column-major device table (rows as in
         the reference, grid.py:146-149)."""
