@@ -357,7 +357,7 @@ def main():
         "achieved_gbs": round(alg_live / max(t_live, 1e-12) / 1e9, 1),
         "frac": round(alg_live / max(t_live, 1e-12) / 1e9 / peak, 4),
         "share_of_step": round(t_live / max(t, 1e-12), 3),
-        "how": "globaltimer stamps in the major-step graph (minor begin -> pressure reset)"}
+        "how": "globaltimer stamps in the major-step graph (minor begin -> first prediction)"}
 
     # ---- e2e through the public API with host-owned state ----------------------
     e2e = None
@@ -419,10 +419,35 @@ def main():
         b.record(stream)
         b.synchronize()
         tw = a.elapsed_time(b) * 1e-3
+        sim_rts = n_w * ws.dt_base
         wc = {"metric": "particle-updates/s (RTS-WCSPH, 1M, base steps)",
               "value": ws.n_fluid * n_w / tw, "ms_per_step": 1e3 * tw / n_w,
-              "mean_active_fraction": fr / n_w, "steps": n_w}
+              "mean_active_fraction": fr / n_w, "steps": n_w,
+              "wall_s_per_simulated_ms": tw / (1e3 * sim_rts)}
         del ws
+        # configs[2]'s comparison: the global adaptive baseline (CFL step,
+        # dt_cap = 4 dt_base) on the same scene
+        from paper_2009_14514_b200 import WcsphSolver
+        wb = WcsphSolver(scene_cfg3(), mode="baseline", device=device)
+        wb.dt_cap = 4 * wb.dt_base
+        nfb = wb.n_fluid
+        xb = (wb.host("pos")[:nfb] + jitter_np(nfb, wb.scene.spacing)).astype("float32")
+        wb.pos[:nfb] = torch.as_tensor(xb, device=wb.device)
+        for _ in range(4):
+            wb.step()
+        torch.cuda.synchronize()
+        sim_b = 0.0
+        a.record(stream)
+        for _ in range(n_w // 2):
+            sim_b += wb.step().dt
+        b.record(stream)
+        b.synchronize()
+        tb = a.elapsed_time(b) * 1e-3
+        wc["baseline_adaptive"] = {
+            "ms_per_step": 1e3 * tb / (n_w // 2), "mean_dt": sim_b / (n_w // 2),
+            "wall_s_per_simulated_ms": tb / (1e3 * sim_b),
+            "rts_speedup_per_simulated_time": (tb / sim_b) / (tw / sim_rts)}
+        del wb
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
