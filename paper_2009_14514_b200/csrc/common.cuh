@@ -196,6 +196,53 @@ RTS_DEV void store12(float *a, int g, const float v[12]) {
     q[2] = make_float4(v[8], v[9], v[10], v[11]);
 }
 
+// Block-aggregated append of up to four items per thread to each of two
+// lists: bit q of m0 / m1 appends base + q.  Output order is thread order,
+// then bit order (ascending indices for contiguous groups); one global
+// atomic per block and list.  The loop around it must be block-uniform.
+template <int NT>
+RTS_DEV void block_append4x2(unsigned m0, unsigned m1, int base, int *list0, int *count0,
+                             int *list1, int *count1) {
+    constexpr int NW = NT / 32;
+    __shared__ int s_w0[NW], s_w1[NW], s_base[2];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int c0 = __popc(m0), c1 = __popc(m1);
+    int x0 = c0, x1 = c1;  // inclusive warp scans
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y0 = __shfl_up_sync(0xffffffffu, x0, o), y1 = __shfl_up_sync(0xffffffffu, x1, o);
+        if (lane >= o) {
+            x0 += y0;
+            x1 += y1;
+        }
+    }
+    if (lane == 31) {
+        s_w0[warp] = x0;
+        s_w1[warp] = x1;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int a = 0, c = 0;
+        for (int w = 0; w < NW; ++w) {
+            const int u = s_w0[w], v = s_w1[w];
+            s_w0[w] = a;
+            s_w1[w] = c;
+            a += u;
+            c += v;
+        }
+        s_base[0] = a ? atomicAdd(count0, a) : 0;
+        s_base[1] = c ? atomicAdd(count1, c) : 0;
+    }
+    __syncthreads();
+    int o0 = s_base[0] + s_w0[warp] + x0 - c0, o1 = s_base[1] + s_w1[warp] + x1 - c1;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        if ((m0 >> q) & 1u) list0[o0++] = base + q;
+        if ((m1 >> q) & 1u) list1[o1++] = base + q;
+    }
+    __syncthreads();  // shared slots are reused by the next loop trip
+}
+
 RTS_DEV int warp_count_add(bool pred, int *count) {
     const unsigned mask = __ballot_sync(0xffffffffu, pred);
     const int lane = threadIdx.x & 31;

@@ -470,18 +470,68 @@ __global__ void __launch_bounds__(256) k_sets(const __grid_constant__ RtsParams 
         return;
     }
     const int stride = gridDim.x * blockDim.x;
-    for (int base = blockIdx.x * blockDim.x; base < nf; base += stride) {
-        const int i = base + threadIdx.x;
-        bool pred = false, force = false;
-        if (i < nf && !is_ghost(b, i)) {
-            const bool sob = observed_block(b, b.fluid_cells[i], gen);
-            const bool turn = all_pred || ((row_mask >> b.region[i]) & 1);
-            const bool se = b.in_se[i] != 0;
-            pred = turn || se || sob;
-            force = turn || se;
-            b.pflag[i] = force;
+    if (b.ghost) {
+        for (int base = blockIdx.x * blockDim.x; base < nf; base += stride) {
+            const int i = base + threadIdx.x;
+            bool pred = false, force = false;
+            if (i < nf && !is_ghost(b, i)) {
+                const bool sob = observed_block(b, b.fluid_cells[i], gen);
+                const bool turn = all_pred || ((row_mask >> b.region[i]) & 1);
+                const bool se = b.in_se[i] != 0;
+                pred = turn || se || sob;
+                force = turn || se;
+                b.pflag[i] = force;
+            }
+            block_append2<256>(pred, i, b.active, &b.ctr->n_pred, force, i, b.list2,
+                               &b.ctr->n_force);
         }
-        block_append2<256>(pred, i, b.active, &b.ctr->n_pred, force, i, b.list2, &b.ctr->n_force);
+        return;
+    }
+    // four particles per thread (vector loads of cells / regions / S_e bits)
+    const int ng = (nf + 3) / 4;
+    for (int gb = blockIdx.x * blockDim.x; gb < ng; gb += stride) {
+        const int g = gb + threadIdx.x;
+        unsigned mp = 0u, mf = 0u;
+        if (g < ng) {
+            const int i0 = 4 * g;
+            int cl[4];
+            int8_t rg[4];
+            uint8_t se[4];
+            if (i0 + 3 < nf) {
+                const int4 c4 = reinterpret_cast<const int4 *>(b.fluid_cells)[g];
+                const char4 r4 = reinterpret_cast<const char4 *>(b.region)[g];
+                const uchar4 s4 = reinterpret_cast<const uchar4 *>(b.in_se)[g];
+                cl[0] = c4.x; cl[1] = c4.y; cl[2] = c4.z; cl[3] = c4.w;
+                rg[0] = r4.x; rg[1] = r4.y; rg[2] = r4.z; rg[3] = r4.w;
+                se[0] = s4.x; se[1] = s4.y; se[2] = s4.z; se[3] = s4.w;
+            } else {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const bool in = i0 + q < nf;
+                    cl[q] = in ? b.fluid_cells[i0 + q] : 0;
+                    rg[q] = in ? b.region[i0 + q] : 0;
+                    se[q] = in ? b.in_se[i0 + q] : 0;
+                }
+            }
+            uint8_t pf[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const bool in = i0 + q < nf;
+                const bool turn = all_pred || ((row_mask >> rg[q]) & 1);
+                const bool s = se[q] != 0;
+                const bool pred = in && (turn || s || observed_block(b, cl[q], gen));
+                const bool force = in && (turn || s);
+                pf[q] = force;
+                mp |= (unsigned)pred << q;
+                mf |= (unsigned)force << q;
+            }
+            if (i0 + 3 < nf) {
+                reinterpret_cast<uchar4 *>(b.pflag)[g] = make_uchar4(pf[0], pf[1], pf[2], pf[3]);
+            } else {
+                for (int q = 0; q < 4 && i0 + q < nf; ++q) b.pflag[i0 + q] = pf[q];
+            }
+        }
+        block_append4x2<256>(mp, mf, 4 * g, b.active, &b.ctr->n_pred, b.list2, &b.ctr->n_force);
     }
 }
 
