@@ -303,8 +303,14 @@ class PcisphSolver(_DeviceSolver):
         return g
 
     def _run_loop_host(self, sync_mode: int) -> None:
-        """Correction loop without a graph: enqueue iterations, read `done`."""
+        """Correction loop without a graph: enqueue iterations, read `done`.
+        With ghost exchanges (x-slab ranks) the first three iterations -- the
+        minimum of every minor step (pcisph.py:681) -- are enqueued before the
+        first read of `done`, so the exchanges of consecutive iterations are
+        queued without a host round trip (iterations after `done` are no-ops
+        in every kernel)."""
         x = self._xch
+        ahead = 3 if x is not None else 1
         while True:
             if self._ktimes is None and x is None:
                 self._call("rts_pci_iteration", sync_mode, 0, self.local_attempts,
@@ -323,6 +329,10 @@ class PcisphSolver(_DeviceSolver):
                 self._call("rts_pci_pforces")
                 self._call("rts_pci_control", sync_mode, 0, self.local_attempts,
                            self.iteration_cap)
+            ahead -= 1
+            if ahead > 0:
+                continue
+            ahead = 1
             self._ctl_host[24:28].copy_(self._ctl[24:28], non_blocking=True)  # ctl.done
             self._stream().synchronize()
             if int(self._ctl_host[24:28].view(torch.int32)[0]):
