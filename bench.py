@@ -91,12 +91,17 @@ def make_device_solver(kind: str, device):
 def algo_bytes(name: str, solver, c_mean: float, rec: dict, launches: int = 1) -> float:
     """Algorithmic bytes of all recorded launches of one entry point."""
     nf = solver.n_fluid
+    # SURVEY.md section 8(d): density 24 + 4c per predicted particle plus the
+    # pressure accumulation (8 B) of the force set; refresh 56 + 8c per
+    # refreshed particle (list build 16 + 4c, external forces 40 + 4c).  The
+    # pressure-force pass is the survey's fused force/predict (80 + 4c)
+    # without the prediction, which k_motion does (84 B per particle).
     if name == "rts_pci_density":
-        return rec["pred"] * (40 + 4 * c_mean) + rec["force"] * 12
+        return rec["pred"] * (24 + 4 * c_mean) + rec["force"] * 8
     if name == "rts_pci_pforces":
         return rec["force"] * (40 + 4 * c_mean)
     if name == "rts_pci_refresh":
-        return rec["refresh"] * (48 + 4 * c_mean) + nf * 1
+        return rec["refresh"] * (56 + 8 * c_mean) + nf * 1
     if name == "rts_pci_motion":
         return rec["motion"] * 84
     if name == "rts_pci_sets":
@@ -350,7 +355,7 @@ def main():
     # stamps around each minor step's refresh (StepStats.t_neighbor: refresh
     # list + search + f_ext on the launching stream) over the K timed majors
     t_live = sum(r.t_neighbor for r in rows)
-    alg_live = sum(r.n_compute for r in rows) * solver.n_fluid // max(1, nf) * (48 + 4 * c_mean) \
+    alg_live = sum(r.n_compute for r in rows) * solver.n_fluid // max(1, nf) * (56 + 8 * c_mean) \
         + solver.n_fluid * len(rows)
     roofline["live_timed_region"] = {
         "kernel": "rts_pci_refresh", "s": round(t_live, 6), "launches": len(rows),
