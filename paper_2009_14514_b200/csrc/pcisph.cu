@@ -123,6 +123,7 @@ __global__ void __launch_bounds__(256) k_refresh_list(const __grid_constant__ Rt
 struct RefreshConsts {
     float h2_lo, h2_hi;
     double m2, inv_rho0_sq, mum2;
+    float hf, visc_f;  // h and mu m^2 c_visc / rho0^2 for the fp32 viscosity terms
 };
 
 RTS_DEV RefreshConsts refresh_consts(const RtsParams &p) {
@@ -132,6 +133,8 @@ RTS_DEV RefreshConsts refresh_consts(const RtsParams &p) {
     k.m2 = xmul(p.mass, p.mass);
     k.inv_rho0_sq = xdiv(1.0, xmul(p.rho0, p.rho0));
     k.mum2 = xmul(p.mu, k.m2);
+    k.hf = (float)p.h;
+    k.visc_f = (float)xmul(xmul(k.mum2, p.c_visc), k.inv_rho0_sq);
     return k;
 }
 
@@ -144,18 +147,19 @@ RTS_DEV bool is_neighbour(const RefreshConsts &k, const RtsParams &p, float fxi,
     return exact_neighbour(p.h2, fxi, fyi, fzi, o.x, o.y, o.z);
 }
 
-// viscosity term of one table entry j for particle i (pcisph.py:183-196)
+// viscosity term of one table entry j for particle i (pcisph.py:183-196), in
+// fp32 like the thread path of refresh_one, accumulated in fp64
 RTS_DEV void visc_term(const RefreshConsts &k, const RtsParams &p, const RtsBuffers &b, int i,
                        int j, double xi, double yi, double zi, float4 pj, double vxi, double vyi,
                        double vzi, double &fx, double &fy, double &fz) {
     if (j >= p.n_fluid || j == i) return;
-    const double r = xsqrt(dist2(xsub(xi, (double)pj.x), xsub(yi, (double)pj.y),
-                                 xsub(zi, (double)pj.z)));
-    if (r >= p.h) return;
-    const double lap = xmul(xmul(k.mum2, visc_lap(r, p.h, p.c_visc)), k.inv_rho0_sq);
-    fx = xadd(fx, xmul(lap, xsub((double)b.vel[3 * j], vxi)));
-    fy = xadd(fy, xmul(lap, xsub((double)b.vel[3 * j + 1], vyi)));
-    fz = xadd(fz, xmul(lap, xsub((double)b.vel[3 * j + 2], vzi)));
+    const float dx = (float)xi - pj.x, dy = (float)yi - pj.y, dz = (float)zi - pj.z;
+    const float r = sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
+    if (r >= k.hf) return;
+    const float lap = k.visc_f * (k.hf - r);
+    fx += (double)(lap * (b.vel[3 * j] - (float)vxi));
+    fy += (double)(lap * (b.vel[3 * j + 1] - (float)vyi));
+    fz += (double)(lap * (b.vel[3 * j + 2] - (float)vzi));
 }
 
 RTS_DEV void finish_search(const RtsParams &p, const RtsBuffers &b, int i, int cntn) {
@@ -290,17 +294,20 @@ RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshC
                 vj[u][1] = b.vel[3 * jc + 1];
                 vj[u][2] = b.vel[3 * jc + 2];
             }
+            // viscosity terms in fp32 (f_ext = m g + a small viscous part:
+            // ~1e-7 relative deviation, bar 1e-4), summed in fp64 in row order
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int j = jj[u];
                 if (q + u >= nrow || j >= p.n_fluid || j == i) continue;
-                const double r = xsqrt(dist2(xsub(xi, (double)pj[u].x), xsub(yi, (double)pj[u].y),
-                                             xsub(zi, (double)pj[u].z)));
-                if (r >= p.h) continue;
-                const double lap = xmul(xmul(k.mum2, visc_lap(r, p.h, p.c_visc)), k.inv_rho0_sq);
-                fx = xadd(fx, xmul(lap, xsub((double)vj[u][0], vxi)));
-                fy = xadd(fy, xmul(lap, xsub((double)vj[u][1], vyi)));
-                fz = xadd(fz, xmul(lap, xsub((double)vj[u][2], vzi)));
+                const float dx = (float)xi - pj[u].x, dy = (float)yi - pj[u].y,
+                            dz = (float)zi - pj[u].z;
+                const float r = sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
+                if (r >= k.hf) continue;
+                const float lap = k.visc_f * (k.hf - r);
+                fx += (double)(lap * (vj[u][0] - (float)vxi));
+                fy += (double)(lap * (vj[u][1] - (float)vyi));
+                fz += (double)(lap * (vj[u][2] - (float)vzi));
             }
         }
     } else {
