@@ -770,21 +770,20 @@ __global__ void k_observed(const __grid_constant__ RtsParams p, RtsBuffers b, in
 RTS_DEV void pforce_pair(const RtsParams &p, double xi, double yi, double zi, double term_i,
                          double wall, double m2c, double inv_rho0_sq, int i, int j, float4 o,
                          double &fx, double &fy, double &fz) {
-    // f_p is not a bit-exact quantity (parity bar 1e-4 per particle): the pair
-    // term uses fused multiply-adds and one fp64 rsqrt (1e-16-level deviation
-    // from the reference's sqrt / divide / unfused products)
+    // f_p is a 1e-4-parity quantity: each pair term in fp32 (differences of
+    // the fp32 positions, rsqrt for 1/r; ~1e-7 relative per term, below the
+    // fp32 state's own rounding of x* and p), summed in fp64 in row order
     if (j == i) return;
-    const double dx = xsub(xi, (double)o.x), dy = xsub(yi, (double)o.y),
-                 dz = xsub(zi, (double)o.z);
-    const double r2 = __fma_rn(dx, dx, __fma_rn(dy, dy, __dmul_rn(dz, dz)));
-    if (!(r2 > 0.0) || !(r2 < p.h2)) return;  // r <= 0 or r >= h
-    const double term = j < p.n_fluid ? __fma_rn((double)o.w, inv_rho0_sq, term_i) : wall;
-    const double rinv = rsqrt(r2);
-    const double d = __fma_rn(-r2, rinv, p.h);  // h - r
-    const double s = __dmul_rn(__dmul_rn(__dmul_rn(m2c, term), __dmul_rn(d, d)), rinv);
-    fx = __fma_rn(-s, dx, fx);
-    fy = __fma_rn(-s, dy, fy);
-    fz = __fma_rn(-s, dz, fz);
+    const float dx = (float)xi - o.x, dy = (float)yi - o.y, dz = (float)zi - o.z;
+    const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+    if (!(r2 > 0.f) || !(r2 < (float)p.h2)) return;  // r <= 0 or r >= h
+    const float term = j < p.n_fluid ? fmaf(o.w, (float)inv_rho0_sq, (float)term_i) : (float)wall;
+    const float rinv = rsqrtf(r2);
+    const float d = fmaf(-r2, rinv, (float)p.h);  // h - r
+    const float s = (float)m2c * term * d * d * rinv;
+    fx -= (double)(s * dx);
+    fy -= (double)(s * dy);
+    fz -= (double)(s * dz);
 }
 
 template <int LG, int kPF = 4>
