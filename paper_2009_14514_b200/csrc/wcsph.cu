@@ -216,29 +216,27 @@ __global__ void __launch_bounds__(kThreads) k_density(const __grid_constant__ Rt
 RTS_DEV void force_pair(const RtsParams &p, double xi, double yi, double zi, float4 va,
                         double inv_rho_i, double term_i, double wall_term, double m2, double mum2,
                         float4 o, float4 vo, double &fx, double &fy, double &fz) {
-    const double dx = xsub(xi, (double)o.x), dy = xsub(yi, (double)o.y),
-                 dz = xsub(zi, (double)o.z);
-    const double r2 = dist2(dx, dy, dz);
-    const double rinv = r2 > 0.0 ? rsqrt(r2) : 0.0;  // r = 0: spiky 0, viscosity kept
-    const double r = xmul(r2, rinv);
-    if (r >= p.h) return;
-    const double d = xsub(p.h, r);
-    const double spk = xmul(xmul(xmul(p.c_spiky, d), d), rinv);
+    // one pair term in fp32 (force / acc are 1e-4-parity quantities: ~1e-7
+    // relative per term), accumulated in fp64 in the reference's order
+    const float dx = (float)xi - o.x, dy = (float)yi - o.y, dz = (float)zi - o.z;
+    const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+    const float rinv = r2 > 0.f ? rsqrtf(r2) : 0.f;  // r = 0: spiky 0, viscosity kept
+    const float r = r2 * rinv;
+    const float hf = (float)p.h;
+    if (r >= hf) return;
+    const float d = hf - r;
+    const float spk = (float)p.c_spiky * d * d * rinv;
     if (o.w >= 0.0f) {  // fluid neighbour: o.w = p_j / rho_j^2, vo.w = 1 / rho_j
-        const double term = xadd(term_i, (double)o.w);
-        const double sc = xmul(xmul(m2, term), spk);
-        fx = xsub(fx, xmul(sc, dx));
-        fy = xsub(fy, xmul(sc, dy));
-        fz = xsub(fz, xmul(sc, dz));
-        const double lap = xmul(xmul(xmul(mum2, xmul(p.c_visc, d)), inv_rho_i), (double)vo.w);
-        fx = xadd(fx, xmul(lap, xsub((double)vo.x, (double)va.x)));
-        fy = xadd(fy, xmul(lap, xsub((double)vo.y, (double)va.y)));
-        fz = xadd(fz, xmul(lap, xsub((double)vo.z, (double)va.z)));
+        const float sc = (float)m2 * ((float)term_i + o.w) * spk;
+        const float lap = (float)xmul(mum2, p.c_visc) * d * (float)inv_rho_i * vo.w;
+        fx += (double)(lap * (vo.x - va.x) - sc * dx);
+        fy += (double)(lap * (vo.y - va.y) - sc * dy);
+        fz += (double)(lap * (vo.z - va.z) - sc * dz);
     } else {  // static wall sample, mirrored pressure
-        const double sc = xmul(xmul(m2, wall_term), spk);
-        fx = xsub(fx, xmul(sc, dx));
-        fy = xsub(fy, xmul(sc, dy));
-        fz = xsub(fz, xmul(sc, dz));
+        const float sc = (float)m2 * (float)wall_term * spk;
+        fx -= (double)(sc * dx);
+        fy -= (double)(sc * dy);
+        fz -= (double)(sc * dz);
     }
 }
 
