@@ -767,9 +767,10 @@ __global__ void k_observed(const __grid_constant__ RtsParams p, RtsBuffers b, in
 
 // pressure forces at x* over the force list (pcisph.py:238-271); same
 // adaptive granularity as k_density.
+template <class T>
 RTS_DEV void pforce_pair(const RtsParams &p, double xi, double yi, double zi, double term_i,
                          double wall, double m2c, double inv_rho0_sq, int i, int j, float4 o,
-                         double &fx, double &fy, double &fz) {
+                         T &fx, T &fy, T &fz) {
     // f_p is a 1e-4-parity quantity: each pair term in fp32 (differences of
     // the fp32 positions, rsqrt for 1/r; ~1e-7 relative per term, below the
     // fp32 state's own rounding of x* and p), summed in fp64 in row order
@@ -781,9 +782,9 @@ RTS_DEV void pforce_pair(const RtsParams &p, double xi, double yi, double zi, do
     const float rinv = rsqrtf(r2);
     const float d = fmaf(-r2, rinv, (float)p.h);  // h - r
     const float s = (float)m2c * term * d * d * rinv;
-    fx -= (double)(s * dx);
-    fy -= (double)(s * dy);
-    fz -= (double)(s * dz);
+    fx -= (T)(s * dx);
+    fy -= (T)(s * dy);
+    fz -= (T)(s * dz);
 }
 
 template <int LG, int kPF = 4>
@@ -816,11 +817,16 @@ RTS_DEV void pforce_one(const RtsParams &p, const RtsBuffers &b, int i, int lane
             float4 o4[kPF];
 #pragma unroll
             for (int u = 0; u < kPF; ++u) o4[u] = ldg_keep(xs4 + j4[u], pol);
+            // the chunk's terms summed in fp32, the chunk sums in fp64
+            float gx = 0.f, gy = 0.f, gz = 0.f;
 #pragma unroll
             for (int u = 0; u < kPF; ++u)
                 if (q + u < c)
                     pforce_pair(p, xi, yi, zi, term_i, wall, m2, inv_rho0_sq, i, j4[u], o4[u],
-                                fx, fy, fz);
+                                gx, gy, gz);
+            fx += (double)gx;
+            fy += (double)gy;
+            fz += (double)gz;
         }
     } else {
         for (int q = lane; q < c; q += LG) {
