@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define RTS_ABI_VERSION 16
+#define RTS_ABI_VERSION 17
 
 /* err_flags bits */
 #define RTS_ERR_ESCAPED   0x1u  /* fluid left the padded grid or non-finite (grid.py:268-273) */
@@ -75,7 +75,7 @@ typedef struct RtsParams {
     int32_t n_global;      /* fluid count of the whole scene (x-slab ranks); 0 = n_fluid */
     int32_t nbr_stride;    /* column stride of the neighbour table: entry q of particle i
                             * is nbr[q * nbr_stride + i] (column-major, coalesced reads) */
-    int32_t pad2;
+    int32_t n_ghost;       /* ghost rows among the n_fluid (x-slab ranks; 0 otherwise) */
 } RtsParams;
 
 /* Device-side counters; copied to the host once per step. */

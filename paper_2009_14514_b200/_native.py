@@ -12,7 +12,7 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "librtssph.so")
-ABI_VERSION = 16
+ABI_VERSION = 17
 
 _c = ctypes
 _D = _c.c_double
@@ -30,7 +30,7 @@ class RtsParams(_c.Structure):
         ("betas", _D * 8), ("eta_max", _D), ("eta_avg", _D), ("rho_T", _D), ("delta", _D),
         ("dims", _I * 3), ("n_cells", _I), ("n_fluid", _I), ("n_bound", _I), ("n_bcells", _I),
         ("width", _I), ("n_max", _I), ("use_sound", _I), ("pin_region", _I),
-        ("apply_correction", _I), ("rts", _I), ("n_sms", _I), ("n_regions", _I), ("n_global", _I), ("nbr_stride", _I), ("pad2", _I),
+        ("apply_correction", _I), ("rts", _I), ("n_sms", _I), ("n_regions", _I), ("n_global", _I), ("nbr_stride", _I), ("n_ghost", _I),
     ]
 
 

@@ -468,10 +468,11 @@ __global__ void __launch_bounds__(256) k_sets(const __grid_constant__ RtsParams 
         }
     }
     const int all_mask = ((1 << (p.n_regions + 1)) - 1) & ~1;
-    if (!b.ghost && (all_pred || (p.n_regions > 0 && (row_mask & all_mask) == all_mask))) {
+    if (all_pred || (p.n_regions > 0 && (row_mask & all_mask) == all_mask)) {
+        // (ghost rows are skipped by every pass and not counted)
         if (blockIdx.x == 0 && threadIdx.x == 0) {
-            b.ctr->n_pred = nf;
-            b.ctr->n_force = nf;
+            b.ctr->n_pred = nf - p.n_ghost;
+            b.ctr->n_force = nf - p.n_ghost;
             b.ctr->lists_all = 1;
         }
         return;
@@ -623,7 +624,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_density(const __grid_constan
                                                       RtsBuffers b) {
     RTS_ITER_GUARD();
     const bool all = b.ctr->lists_all;  // every fluid particle, particle order
-    const int n = b.ctr->n_pred;
+    const int n = all ? p.n_fluid : b.ctr->n_pred;  // (all: ghost rows skipped inside)
     const int nthreads = gridDim.x * blockDim.x;
     const int tid = blockIdx.x * blockDim.x + threadIdx.x;
     if ((long long)n * kPG <= nthreads) {
@@ -852,7 +853,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pforces(const __grid_constan
                                                       RtsBuffers b) {
     RTS_ITER_GUARD();
     const bool all = b.ctr->lists_all;  // every fluid particle, particle order
-    const int n = b.ctr->n_force;
+    const int n = all ? p.n_fluid : b.ctr->n_force;  // (all: ghost rows skipped inside)
     const int nthreads = gridDim.x * blockDim.x;
     const int tid = blockIdx.x * blockDim.x + threadIdx.x;
     if ((long long)n * kPG <= nthreads) {

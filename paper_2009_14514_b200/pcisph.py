@@ -163,8 +163,10 @@ class PcisphSolver(_DeviceSolver):
         self.cnt = self.arena["cnt"][:nf]
         g = self.arena["ghost"]
         g.zero_()
+        self.params.n_ghost = 0
         if ghost is not None and nf:
             g[:nf].copy_(ghost.to(torch.uint8))
+            self.params.n_ghost = int(ghost.sum())
         self.params.n_fluid = nf
         N.call("rts_pci_walls", self.params, self.arena.buf, self._stream().cuda_stream)
 
