@@ -28,6 +28,20 @@ def _jitter(n, s=0.02):
     return np.random.default_rng(1234).uniform(-0.01 * s, 0.01 * s, (n, 3))
 
 
+def _collect(q, procs, n=2):
+    """Results of the n rank processes; a rank's exception fails the test at
+    once (the other rank is then stuck in a collective and is terminated)."""
+    res = []
+    for _ in range(n):
+        r = q.get(timeout=600)
+        if r[0] == "error":
+            for p in procs:
+                p.kill()
+            pytest.fail(f"rank {r[1]} raised:\n{r[2]}")
+        res.append(r)
+    return res
+
+
 def _worker(rank, world, port, steps, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -44,6 +58,10 @@ def _worker(rank, world, port, steps, q):
             d.step()
         q.put((rank, d.gid.cpu().numpy(), d.state["pos"].cpu().numpy(),
                d.state["vel"].cpu().numpy(), d.state["rho"].cpu().numpy()))
+    except Exception:  # report instead of leaving the parent waiting
+        import traceback
+        q.put(("error", rank, traceback.format_exc()))
+        os._exit(1)
     finally:
         dist.destroy_process_group()
 
@@ -68,7 +86,7 @@ def test_two_ranks_on_one_gpu_match_single_gpu_bitwise():
     procs = [ctx.Process(target=_worker, args=(r, 2, port, steps, q)) for r in range(2)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=600) for _ in range(2)]
+    res = _collect(q, procs)
     for p in procs:
         p.join(timeout=60)
     gid = np.concatenate([r[1] for r in res])
@@ -96,6 +114,10 @@ def _pworker(rank, world, port, majors, q):
             stats += [(r.n_compute, r.iterations, r.corrected, r.early_term) for r in d.advance()]
         q.put((rank, d.gid.cpu().numpy(), d.state["pos"].cpu().numpy(),
                d.state["rho_star"].cpu().numpy(), stats))
+    except Exception:  # report instead of leaving the parent waiting
+        import traceback
+        q.put(("error", rank, traceback.format_exc()))
+        os._exit(1)
     finally:
         dist.destroy_process_group()
 
@@ -126,7 +148,7 @@ def test_pcisph_two_ranks_on_one_gpu_match_single_gpu():
     procs = [ctx.Process(target=_pworker, args=(r, 2, port, majors, q)) for r in range(2)]
     for p in procs:
         p.start()
-    res = sorted([q.get(timeout=600) for _ in range(2)], key=lambda r: r[0])
+    res = sorted(_collect(q, procs), key=lambda r: r[0])
     for p in procs:
         p.join(timeout=60)
     assert res[0][4] == rstats and res[1][4] == rstats
