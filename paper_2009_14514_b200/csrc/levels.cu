@@ -14,31 +14,92 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int8_t kEmpty = 127;  // regions.py:35
 
+// region id of block c from its maxima (regions.py:38-75)
+RTS_DEV int8_t assign_cell(const RtsParams &p, const RtsBuffers &b, int c, double sound_bound,
+                           double rm) {
+    if (b.cell_count[c] <= 0) return 0;
+    const double r = p.block_size;
+    const double vmax = b.vmax[c], fmax = b.fmax[c];
+    // lambda_f * sqrt(r*m / f_max); f_max == 0 -> inf (numpy divide)
+    const double fb = xmul(p.lambda_f, xsqrt(xdiv(rm, fmax)));
+    int8_t region = 1;
+    for (int n = 2; n <= p.n_max; ++n) {
+        const double dt_n = xmul((double)n, p.dt_base);
+        if (p.use_sound && !(dt_n <= sound_bound)) break;
+        bool ok = (region == n - 1);
+        ok = ok && ((fmax == 0.0) || (dt_n <= fb));
+        const double beta = p.betas[n];
+        if (isfinite(beta)) ok = ok && (xdiv(xmul(dt_n, vmax), r) <= xmul(p.alpha, beta));
+        if (ok) region = (int8_t)n;
+    }
+    return region;
+}
+
 __global__ void k_assign(const __grid_constant__ RtsParams p, RtsBuffers b) {
     if (fatal(b.ctr)) return;
     if (blockIdx.x == 0 && threadIdx.x == 0) b.ctr->stamps[1] = gtimer();  // grid rebuilt
-    const double r = p.block_size;
-    const double sound_bound = xdiv(xmul(p.lambda_v, r), p.sound_speed);
-    const double rm = xmul(r, p.mass);
+    const double sound_bound = xdiv(xmul(p.lambda_v, p.block_size), p.sound_speed);
+    const double rm = xmul(p.block_size, p.mass);
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < p.n_cells;
-         c += gridDim.x * blockDim.x) {
-        const bool occ = b.cell_count[c] > 0;
-        int8_t region = occ ? 1 : 0;
-        if (occ) {
-            const double vmax = b.vmax[c], fmax = b.fmax[c];
-            // lambda_f * sqrt(r*m / f_max); f_max == 0 -> inf (numpy divide)
-            const double fb = xmul(p.lambda_f, xsqrt(xdiv(rm, fmax)));
-            for (int n = 2; n <= p.n_max; ++n) {
-                const double dt_n = xmul((double)n, p.dt_base);
-                if (p.use_sound && !(dt_n <= sound_bound)) break;
-                bool ok = (region == n - 1);
-                ok = ok && ((fmax == 0.0) || (dt_n <= fb));
-                const double beta = p.betas[n];
-                if (isfinite(beta)) ok = ok && (xdiv(xmul(dt_n, vmax), r) <= xmul(p.alpha, beta));
-                if (ok) region = (int8_t)n;
+         c += gridDim.x * blockDim.x)
+        b.block_raw[c] = assign_cell(p, b, c, sound_bound, rm);
+}
+
+// assign + smooth in one pass: each CTA assigns a tile of blocks plus a
+// one-block halo into shared memory, then smooths the tile from there
+// (WCSPH's level field, rts_block_levels expand = 0)
+constexpr int kTX = 4, kTY = 8, kTZ = 32;
+constexpr int kHX = kTX + 2, kHY = kTY + 2, kHZ = kTZ + 2;
+
+__global__ void __launch_bounds__(256) k_assign_smooth(const __grid_constant__ RtsParams p,
+                                                       RtsBuffers b, int8_t *out) {
+    if (fatal(b.ctr)) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) b.ctr->stamps[1] = gtimer();  // grid rebuilt
+    __shared__ int8_t s_reg[kHX * kHY * kHZ];
+    const int nx = p.dims[0], ny = p.dims[1], nz = p.dims[2];
+    const int tx = (nx + kTX - 1) / kTX, ty = (ny + kTY - 1) / kTY, tz = (nz + kTZ - 1) / kTZ;
+    const double sound_bound = xdiv(xmul(p.lambda_v, p.block_size), p.sound_speed);
+    const double rm = xmul(p.block_size, p.mass);
+    for (int t = blockIdx.x; t < tx * ty * tz; t += gridDim.x) {
+        const int bz = (t % tz) * kTZ, by = ((t / tz) % ty) * kTY, bx = (t / (tz * ty)) * kTX;
+        for (int h = threadIdx.x; h < kHX * kHY * kHZ; h += blockDim.x) {
+            const int hz = h % kHZ, hy = (h / kHZ) % kHY, hx = h / (kHZ * kHY);
+            const int cx = bx + hx - 1, cy = by + hy - 1, cz = bz + hz - 1;
+            int8_t r = 0;  // outside the grid: empty
+            if (cx >= 0 && cx < nx && cy >= 0 && cy < ny && cz >= 0 && cz < nz) {
+                const int c = (cx * ny + cy) * nz + cz;
+                r = assign_cell(p, b, c, sound_bound, rm);
+                const bool interior = hx >= 1 && hx <= kTX && hy >= 1 && hy <= kTY && hz >= 1 &&
+                                      hz <= kTZ;
+                if (interior) b.block_raw[c] = r;
             }
+            s_reg[h] = r;
         }
-        b.block_raw[c] = region;
+        __syncthreads();
+        for (int q = threadIdx.x; q < kTX * kTY * kTZ; q += blockDim.x) {
+            const int iz = q % kTZ, iy = (q / kTZ) % kTY, ix = q / (kTZ * kTY);
+            const int cx = bx + ix, cy = by + iy, cz = bz + iz;
+            if (cx >= nx || cy >= ny || cz >= nz) continue;
+            const int8_t f = s_reg[((ix + 1) * kHY + iy + 1) * kHZ + iz + 1];
+            int8_t res = 0;
+            if (f > 0) {
+                if (p.pin_region) {
+                    res = (int8_t)p.pin_region;
+                } else {
+                    int8_t m = kEmpty;
+                    for (int dx = 0; dx < 3; ++dx)
+                        for (int dy = 0; dy < 3; ++dy)
+                            for (int dz = 0; dz < 3; ++dz) {
+                                if (dx == 1 && dy == 1 && dz == 1) continue;
+                                const int8_t v = s_reg[((ix + dx) * kHY + iy + dy) * kHZ + iz + dz];
+                                if (v > 0 && v < m) m = v;
+                            }
+                    res = f < m ? f : m;
+                }
+            }
+            out[(cx * ny + cy) * nz + cz] = res;
+        }
+        __syncthreads();
     }
 }
 
@@ -171,16 +232,21 @@ extern "C" int rts_block_levels(const RtsParams *p, const RtsBuffers *b, int exp
                                 void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
     const int blocks = rts_blocks(p->n_cells, kThreads);
-    rts_note_launch(), k_assign<<<blocks, kThreads, 0, s>>>(*p, *b);
-    RTS_LAUNCH_CHECK();
-    if (expand == 2) return 0;  // assign only (required levels, pcisph.py:726-740)
-    if (!expand || p->pin_region) {
-        rts_note_launch(), k_smooth<<<blocks, kThreads, 0, s>>>(*p, *b, b->block_field);
+    if (expand == 2) {  // assign only (required levels, pcisph.py:726-740)
+        rts_note_launch(), k_assign<<<blocks, kThreads, 0, s>>>(*p, *b);
         RTS_LAUNCH_CHECK();
         return 0;
     }
-    // smoothed field into block_tmp, then expansion into block_field
-    rts_note_launch(), k_smooth<<<blocks, kThreads, 0, s>>>(*p, *b, b->block_tmp);
+    const long long tiles = (long long)((p->dims[0] + kTX - 1) / kTX) *
+                            ((p->dims[1] + kTY - 1) / kTY) * ((p->dims[2] + kTZ - 1) / kTZ);
+    const int tb = (int)(tiles < 148 * 8 ? tiles : 148 * 8);
+    if (!expand || p->pin_region) {  // assign + smooth -> block_field
+        rts_note_launch(), k_assign_smooth<<<tb, 256, 0, s>>>(*p, *b, b->block_field);
+        RTS_LAUNCH_CHECK();
+        return 0;
+    }
+    // assign + smooth into block_tmp, then the expansion into block_field
+    rts_note_launch(), k_assign_smooth<<<tb, 256, 0, s>>>(*p, *b, b->block_tmp);
     RTS_LAUNCH_CHECK();
     uint8_t *m0 = b->block_flag;
     uint8_t *m1 = reinterpret_cast<uint8_t *>(b->block_field);  // scratch until final write
