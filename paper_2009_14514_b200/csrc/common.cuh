@@ -35,19 +35,6 @@ RTS_DEV double poly6(double r2, double h2, double c) {
     if (d <= 0.0) return 0.0;
     return xmul(xmul(xmul(c, d), d), d);
 }
-// spiky gradient factor ((c*d)*d)/r, d = h - r (kernels.py:35-46)
-RTS_DEV double spiky(double r, double h, double c) {
-    if (r <= 0.0 || r >= h) return 0.0;
-    const double d = xsub(h, r);
-    return xdiv(xmul(xmul(c, d), d), r);
-}
-// viscosity Laplacian c*(h - r) (kernels.py:49-55)
-RTS_DEV double visc_lap(double r, double h, double c) {
-    const double d = xsub(h, r);
-    if (d <= 0.0) return 0.0;
-    return xmul(c, d);
-}
-
 // np.floor((x - origin) * inv_block), clipped to [0, n-1] (grid.py:248-250)
 RTS_DEV int cell_axis(double x, double o, double inv, int n) {
     const double v = floor(xmul(xsub(x, o), inv));

@@ -122,7 +122,6 @@ __global__ void __launch_bounds__(256) k_refresh_list(const __grid_constant__ Rt
 // (deterministic; f_ext parity bar 1e-4).
 struct RefreshConsts {
     float h2_lo, h2_hi;
-    double m2, inv_rho0_sq, mum2;
     float hf, visc_f;  // h and mu m^2 c_visc / rho0^2 for the fp32 viscosity terms
 };
 
@@ -130,11 +129,10 @@ RTS_DEV RefreshConsts refresh_consts(const RtsParams &p) {
     RefreshConsts k;
     k.h2_lo = (float)(p.h2 * (1.0 - 1e-5));
     k.h2_hi = (float)(p.h2 * (1.0 + 1e-5));
-    k.m2 = xmul(p.mass, p.mass);
-    k.inv_rho0_sq = xdiv(1.0, xmul(p.rho0, p.rho0));
-    k.mum2 = xmul(p.mu, k.m2);
     k.hf = (float)p.h;
-    k.visc_f = (float)xmul(xmul(k.mum2, p.c_visc), k.inv_rho0_sq);
+    // mu m^2 c_visc / rho0^2 (pcisph.py:183-196)
+    k.visc_f = (float)xmul(xmul(xmul(p.mu, xmul(p.mass, p.mass)), p.c_visc),
+                           xdiv(1.0, xmul(p.rho0, p.rho0)));
     return k;
 }
 
