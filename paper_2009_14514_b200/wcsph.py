@@ -22,7 +22,6 @@ tensors in the reference's particle order, writable in place
 from __future__ import annotations
 
 import math
-import os
 
 import numpy as np
 import torch
