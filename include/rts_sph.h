@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define RTS_ABI_VERSION 17
+#define RTS_ABI_VERSION 18
 
 /* err_flags bits */
 #define RTS_ERR_ESCAPED   0x1u  /* fluid left the padded grid or non-finite (grid.py:268-273) */
@@ -179,7 +179,7 @@ typedef struct RtsBuffers {
     int32_t *bcell_ids;    /* (Bc) sorted block ids holding boundary particles */
     int32_t *bcell_start;  /* (Bc+1) CSR into bidx */
     int32_t *bidx;         /* (Nb) boundary particle indices (Nf + b), grouped by block */
-    int32_t *bcell_of;     /* (Nb) block id of each boundary particle */
+    int32_t *bcell_of;     /* (Nb) index into bcell_ids of the block of bidx[q] */
     uint8_t *bcell_active; /* (Bc) */
     /* block fields */
     double  *vmax;         /* (Nc) per-block max |v| (grid.py:347) */

@@ -199,14 +199,24 @@ __global__ void __launch_bounds__(kLbThreads) k_scan_lookback(const __grid_const
     }
 }
 
-// stable scatter, step 1: atomic cursor per block
-__global__ void k_scatter_fluid(const __grid_constant__ RtsParams p, RtsBuffers b) {
+// stable scatter, step 1: fluid rows take an atomic cursor in their block's
+// run; the members of active wall blocks (threads past n_fluid) go straight
+// to their static rank behind the fluid run (the wall CSR is sorted)
+__global__ void k_scatter(const __grid_constant__ RtsParams p, RtsBuffers b) {
     if (fatal(b.ctr)) return;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.n_fluid;
-         i += gridDim.x * blockDim.x) {
-        const int c = b.fluid_cells[i];
-        const int slot = b.starts[c] + atomicAdd(&b.fill[c], 1);
-        b.order[slot] = i;
+    const int nf = p.n_fluid, nw = p.n_bcells > 0 ? p.n_bound : 0;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nf + nw;
+         k += gridDim.x * blockDim.x) {
+        if (k < nf) {
+            const int c = b.fluid_cells[k];
+            b.order[b.starts[c] + atomicAdd(&b.fill[c], 1)] = k;
+        } else {
+            const int q = k - nf;
+            const int t = b.bcell_of[q];
+            if (!b.bcell_active[t]) continue;
+            const int c = b.bcell_ids[t];
+            b.order[b.starts[c] + b.cell_count[c] + (q - b.bcell_start[t])] = b.bidx[q];
+        }
     }
 }
 
@@ -264,21 +274,6 @@ __global__ void k_sort_runs(const __grid_constant__ RtsParams p, RtsBuffers b) {
                 run[r + 1] = key;
             }
         }
-    }
-}
-
-// step 3: active wall blocks append their (statically sorted) boundary rows
-__global__ void k_scatter_boundary(const __grid_constant__ RtsParams p, RtsBuffers b) {
-    if (fatal(b.ctr)) return;
-    // one warp per wall block
-    const int lane = threadIdx.x & 31;
-    const int warps = (gridDim.x * blockDim.x) >> 5;
-    for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < p.n_bcells; t += warps) {
-        if (!b.bcell_active[t]) continue;
-        const int c = b.bcell_ids[t];
-        const int dst = b.starts[c] + b.cell_count[c];
-        const int s0 = b.bcell_start[t], s1 = b.bcell_start[t + 1];
-        for (int q = s0 + lane; q < s1; q += 32) b.order[dst + (q - s0)] = b.bidx[q];
     }
 }
 
@@ -355,15 +350,11 @@ int rts_grid_sort(const RtsParams *p, const RtsBuffers *b, void *stream) {
     rts_note_launch(), k_scan_lookback<<<tiles, kLbThreads, 0, s>>>(*p, *b);
     RTS_LAUNCH_CHECK();
     cudaMemsetAsync(b->fill, 0, sizeof(int) * (size_t)p->n_cells, s);
-    rts_note_launch(), k_scatter_fluid<<<rts_blocks(p->n_fluid, kThreads), kThreads, 0, s>>>(*p, *b);
+    rts_note_launch(), k_scatter<<<rts_blocks((long long)p->n_fluid + p->n_bound, kThreads), kThreads, 0, s>>>(
+        *p, *b);
     RTS_LAUNCH_CHECK();
     rts_note_launch(), k_sort_runs<<<rts_blocks(p->n_cells, kThreads), kThreads, 0, s>>>(*p, *b);
     RTS_LAUNCH_CHECK();
-    if (p->n_bcells > 0) {
-        rts_note_launch(), k_scatter_boundary<<<rts_blocks((long long)p->n_bcells * 32, kThreads), kThreads, 0, s>>>(
-            *p, *b);
-        RTS_LAUNCH_CHECK();
-    }
     return 0;
 }
 

@@ -144,7 +144,10 @@ class BlockGrid:
         self._bsrt = torch.as_tensor(srt.astype(np.int32), device=dev)
         self._bidx_base = n_fluid
         A.bind("bidx", self._bsrt + n_fluid)
-        A.bind("bcell_of", torch.as_tensor(cells.astype(np.int32), device=dev))
+        # block index (into bcell_ids) of every member of the wall CSR, for the
+        # member-parallel scatter (grid.cu k_scatter)
+        member_t = np.repeat(np.arange(len(ids), dtype=np.int32), np.diff(starts))
+        A.bind("bcell_of", torch.as_tensor(member_t, device=dev))
         A.alloc("bcell_active", (self.n_bcells,), torch.uint8, 0)
         self._bslot = torch.as_tensor(slot.astype(np.int64), device=dev)
 
