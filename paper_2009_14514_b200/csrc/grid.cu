@@ -147,6 +147,7 @@ __global__ void __launch_bounds__(kLbThreads) k_scan_lookback(const __grid_const
     for (int q = 0; q < kLbItems; ++q) {
         const int idx = i0 + q;
         v[q] = idx < n ? b.cell_count[idx] + b.cell_bcount[idx] : 0;
+        if (idx < n) b.fill[idx] = 0;  // the scatter's cursors
         local += v[q];
     }
     const int incl = block_incl_scan(local, warp_sums);
@@ -349,7 +350,6 @@ int rts_grid_sort(const RtsParams *p, const RtsBuffers *b, void *stream) {
     cudaMemsetAsync(b->scan_tmp, 0, sizeof(int) * (size_t)(2 + 2 * tiles), s);  // counter + status
     rts_note_launch(), k_scan_lookback<<<tiles, kLbThreads, 0, s>>>(*p, *b);
     RTS_LAUNCH_CHECK();
-    cudaMemsetAsync(b->fill, 0, sizeof(int) * (size_t)p->n_cells, s);
     rts_note_launch(), k_scatter<<<rts_blocks((long long)p->n_fluid + p->n_bound, kThreads), kThreads, 0, s>>>(
         *p, *b);
     RTS_LAUNCH_CHECK();
