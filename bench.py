@@ -64,23 +64,96 @@ def scene_cfg3():
                  sound_speed=10.0 * math.sqrt(2.0 * 9.81 * 1.0))
 
 
+def scene_cfg4():
+    """configs[3]: mixed-dynamics tank, z up.  A 4 x 2 x 2 m box; the pool
+    (80 %, ~6.4 M) fills z in [0, 2/3]; the falling block (20 %, ~1.6 M) has
+    its bottom at z = 5/3 (1 m above the pool), spans x in [1, 3] and the
+    full y width and is flattened to 35 layers (0.33 m) so it fits under
+    z = 2; spacing (V_pool / 6.4e6)^(1/3)."""
+    from paper_2009_14514_b200 import Scene
+    s = (4.0 * 2.0 * (2.0 / 3.0) / 6.4e6) ** (1.0 / 3.0)
+    z0 = 5.0 / 3.0
+    return Scene(domain_min=(0.0, 0.0, 0.0), domain_max=(4.0, 2.0, 2.0),
+                 fluid_boxes=(((0.0, 0.0, 0.0), (4.0, 2.0, 2.0 / 3.0)),
+                              ((1.0, 0.0, z0), (3.0, 2.0, z0 + 35 * s))),
+                 spacing=s, gravity=(0.0, 0.0, -9.81), eta_max=0.03, eta_avg=0.015,
+                 name="cfg4_mixed_tank")
+
+
+def scene_cfg5(world: int = 1, kind: str = "pcisph"):
+    """configs[4]: weak-scaling elongated dam-break tank, 4 M fluid particles
+    per GPU: an 8 m x 0.5 m x 1 m column per rank (5,000 per lattice layer
+    at s = 0.01) in a (8 N + 1) x 1 x 1 m tank."""
+    import math
+
+    from paper_2009_14514_b200 import Scene
+    kw = {"eta_max": 0.03, "eta_avg": 0.015} if kind == "pcisph" else {
+        "sound_speed": 10.0 * math.sqrt(2.0 * 9.81 * 0.5)}
+    return Scene(domain_min=(0.0, 0.0, 0.0), domain_max=(8.0 * world + 1.0, 1.0, 1.0),
+                 fluid_boxes=(((0.0, 0.0, 0.0), (8.0 * world, 0.5, 1.0)),), spacing=0.01,
+                 name=f"cfg5_weak_{kind}", **kw)
+
+
+WORKLOADS = {
+    "cfg2": ("pcisph", "cfg2: 1M dam break RTS-PCISPH (eta 3%/1.5%, cap 50, dt 1.75e-4, "
+                       "4 levels)", "weak"),
+    "cfg4": ("pcisph", "cfg4: 8M mixed-dynamics tank RTS-PCISPH (z up, pool 80% + block 20% "
+                       "at v0 = (0,0,-2), eta 3%/1.5%, cap 50)", "strong"),
+    "cfg5-pcisph": ("pcisph", "cfg5: weak scaling, 4M/GPU elongated tank RTS-PCISPH, "
+                              "v0 ~ N(0, 0.1 m/s), eta 3%/1.5%, cap 50", "weak"),
+    "cfg5-wcsph": ("wcsph", "cfg5: weak scaling, 4M/GPU elongated tank RTS-WCSPH, "
+                            "v0 ~ N(0, 0.1 m/s)", "weak"),
+}
+
+
+def workload_scene(workload: str, world: int = 1):
+    if workload == "cfg2":
+        return scene_cfg2(world)
+    if workload == "cfg4":
+        return scene_cfg4()
+    return scene_cfg5(world, WORKLOADS[workload][0])
+
+
+def initial_velocity(workload: str, fluid):
+    """(n, 3) float32 initial velocities for the seeded fluid, or None."""
+    import numpy as np
+    if workload == "cfg4":
+        v = np.zeros((len(fluid), 3), dtype=np.float32)
+        v[fluid[:, 2] > 1.0, 2] = -2.0  # the falling block
+        return v
+    if workload.startswith("cfg5"):
+        return np.random.default_rng(SEED + 1).normal(0.0, 0.1, (len(fluid), 3)).astype(
+            np.float32)
+    return None
+
+
 def jitter_np(n, spacing):
     import numpy as np
     return np.random.default_rng(SEED).uniform(-0.01 * spacing, 0.01 * spacing, (n, 3))
 
 
-def make_device_solver(kind: str, device):
+def make_device_solver(kind: str, device, workload: str | None = None):
+    """One-GPU solver for ``workload`` (default: cfg2 for "pcisph", cfg3 for
+    "wcsph"), seeded lattice + jitter (+ the workload's initial velocities)."""
     import numpy as np
     import torch
 
     from paper_2009_14514_b200 import PcisphSolver, WcsphSolver
-    if kind == "pcisph":
-        s = PcisphSolver(scene_cfg2(), mode="rts", iteration_cap=50, device=device)
+    if workload is None:
+        sc = scene_cfg2() if kind == "pcisph" else scene_cfg3()
     else:
-        s = WcsphSolver(scene_cfg3(), mode="rts", device=device)
+        sc = workload_scene(workload, 1)
+    if kind == "pcisph":
+        s = PcisphSolver(sc, mode="rts", iteration_cap=50, device=device)
+    else:
+        s = WcsphSolver(sc, mode="rts", device=device)
     nf = s.n_fluid
-    x = (s.host("pos")[:nf] + jitter_np(nf, s.scene.spacing)).astype(np.float32)
+    lattice = s.host("pos")[:nf]
+    x = (lattice + jitter_np(nf, s.scene.spacing)).astype(np.float32)
     s.pos[:nf] = torch.as_tensor(x, device=s.device)
+    v0 = initial_velocity(workload, lattice) if workload else None
+    if v0 is not None:
+        s.vel[:nf] = torch.as_tensor(v0, device=s.device)
     if kind == "pcisph":
         s.xstar[:] = s.pos[:nf]
     return s
@@ -159,66 +232,252 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_oracle_sample(majors: int = 2, warm: int = 1) -> dict:
-    """Time the CPU oracle (fp64 C + numpy restatement of the reference) on
-    the same scene: ``warm`` untimed majors, then ``majors`` timed."""
+METRICS = {
+    "cfg2": METRIC,
+    "cfg4": "particle-updates/s (RTS-PCISPH, 8M mixed tank, minor steps)",
+    "cfg5-pcisph": "particle-updates/s (RTS-PCISPH, 4M/GPU elongated tank, minor steps)",
+    "cfg5-wcsph": "particle-updates/s (RTS-WCSPH, 4M/GPU elongated tank, base steps)",
+}
+
+
+def _oracle_for(workload: str):
+    """The CPU oracle on the workload's one-GPU scene, jittered (and with the
+    workload's initial velocities) exactly as the device solver."""
     import numpy as np
 
     from oracle import sph as O
-    sc = scene_cfg2()
-    t_setup = time.perf_counter()
-    o = O.OraclePcisph(sc, mode="rts", iteration_cap=50)
+    kind = WORKLOADS[workload][0]
+    sc = workload_scene(workload, 1)
+    if kind == "pcisph":
+        o = O.OraclePcisph(sc, mode="rts", iteration_cap=50)
+    else:
+        o = O.OracleWcsph(sc, mode="rts")
     nf = o.n_fluid
-    x = (o.pos[:nf] + jitter_np(nf, sc.spacing)).astype(np.float32).astype(np.float64)
+    lattice = o.pos[:nf].copy()
+    x = (lattice + jitter_np(nf, sc.spacing)).astype(np.float32).astype(np.float64)
     o.pos[:nf] = x
-    o.xstar[:] = x
+    v0 = initial_velocity(workload, lattice) if workload != "cfg2" else None
+    if v0 is not None:
+        o.vel[:nf] = v0.astype(np.float64)
+    if kind == "pcisph":
+        o.xstar[:] = x
+    return o, O
+
+
+def _oracle_steps(o, budget_s: float, max_steps: int):
+    """Timed steps (advance() = one major for PCISPH, one base step for
+    WCSPH) until ``budget_s`` seconds or ``max_steps`` steps."""
+    import time as _t
+    units, steps = 0, 0
+    t0 = _t.perf_counter()
+    while steps < max_steps:
+        units += len(o.advance())
+        steps += 1
+        if _t.perf_counter() - t0 > budget_s:
+            break
+    return units, steps, _t.perf_counter() - t0
+
+
+def cpu_oracle_sample(majors: int = 2, warm: int = 1, workload: str = "cfg2") -> dict:
+    """Time the CPU oracle (fp64 C + numpy restatement of the reference) on
+    the same scene: ``warm`` untimed steps, then up to ``majors`` timed
+    (bounded to ~20 s of CPU work)."""
+    t_setup = time.perf_counter()
+    o, O = _oracle_for(workload)
+    nf = o.n_fluid
     for _ in range(warm):
         o.advance()
-    minors = 0
     t0 = time.perf_counter()
-    for _ in range(majors):
-        minors += len(o.advance())
-    dt = time.perf_counter() - t0
-    return {"value": nf * minors / dt, "unit": UNIT, "cores": O.num_threads(), "kind": "port",
-            "sample": f"{majors} major steps ({minors} minor steps) of the 1M cfg2 scene after "
-                      f"{warm} untimed major(s); oracle = fp64 C/OpenMP + numpy restatement",
+    units, steps, dt = _oracle_steps(o, 20.0, majors)
+    what = "major steps" if WORKLOADS[workload][0] == "pcisph" else "base steps"
+    return {"value": nf * units / dt, "unit": UNIT, "cores": O.num_threads(), "kind": "port",
+            "sample": f"{steps} {what} ({units} updates of every particle) of the "
+                      f"{workload} one-GPU scene ({nf} fluid) after {warm} untimed; "
+                      "oracle = fp64 C/OpenMP + numpy restatement",
             "seconds": round(dt, 3), "setup_s": round(t0 - t_setup, 1)}
 
 
 def run_reference_arm(args, rank: int, world: int) -> None:
     if rank != 0:
         return
-    from oracle import sph as O
-    import numpy as np
-    sc = scene_cfg2()
-    o = O.OraclePcisph(sc, mode="rts", iteration_cap=50)
+    kind, wl_name, scaling = WORKLOADS[args.workload]
+    o, O = _oracle_for(args.workload)
     nf = o.n_fluid
-    x = (o.pos[:nf] + jitter_np(nf, sc.spacing)).astype(np.float32).astype(np.float64)
-    o.pos[:nf] = x
-    o.xstar[:] = x
     warm = min(args.warmup, 1)
-    steps = max(1, min(args.steps, 6))  # bounded sample: ~3 s CPU per major here
     for _ in range(warm):
         o.advance()
-    minors = 0
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        minors += len(o.advance())
-    dt = time.perf_counter() - t0
-    v = nf * minors / dt
+    # bounded sample: ~3 s CPU per 1M major here; stop after ~60 s
+    units, steps, dt = _oracle_steps(o, 60.0, max(1, min(args.steps, 6)))
+    v = nf * units / dt
     line = {
-        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
-        "steps": steps, "warmup": warm, "ms_per_step": 1e3 * dt / steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "impl": "reference", "metric": METRICS[args.workload], "value": v, "unit": UNIT,
+        "n_gpus": world, "steps": steps, "warmup": warm, "ms_per_step": 1e3 * dt / steps,
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": "cfg2: 1M dam break RTS-PCISPH (eta 3%/1.5%, cap 50)",
-                   "n_fluid": nf, "minor_steps": minors, "host_threads": O.num_threads()},
+        "config": {"workload": wl_name, "n_fluid": nf, "updates_per_particle": units,
+                   "host_threads": O.num_threads(),
+                   "scene": "the one-GPU scene of the workload (host-sized sample)"},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": O.num_threads(), "kind": "port",
-                         "sample": f"{steps} major steps ({minors} minor steps) after {warm} "
-                                   "untimed; CPU oracle restating the reference"},
+                         "sample": f"{steps} steps ({units} updates per particle) after "
+                                   f"{warm} untimed; CPU oracle restating the reference"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def wcsph_algo_bytes(name: str, nf: int, active: int, launches: int) -> float:
+    """SURVEY.md section 8(d) RTS-WCSPH bytes: density + Tait 20 per active
+    particle, forces + bookkeeping 88 per active, predictor 68 per particle
+    + corrector 16 per active, level propagation 15 per particle."""
+    if name == "rts_wcsph_density":
+        return 20.0 * active
+    if name == "rts_wcsph_forces":
+        return 88.0 * active
+    if name == "rts_wcsph_integrate":
+        return 68.0 * nf * launches + 16.0 * active
+    if name == "rts_wcsph_propagate":
+        return 15.0 * nf * launches
+    return 0.0
+
+
+def run_wcsph_workload(args, rank: int, world: int, device, barrier) -> None:
+    """RTS-WCSPH bench line (cfg5-wcsph): K base steps, device time, max over
+    ranks; roofline of the dominant kernel from an instrumented pass."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2009_14514_b200 import _native
+    _, wl_name, scaling = WORKLOADS[args.workload]
+    if world == 1:
+        solver = make_device_solver("wcsph", device, args.workload)
+        driver = solver
+        n_total = solver.n_fluid
+    else:
+        from paper_2009_14514_b200.distributed import DistributedWcsph
+        from paper_2009_14514_b200.scene import seed_particles
+        sc = workload_scene(args.workload, world)
+        lattice = seed_particles(sc)[0]
+        n_total = len(lattice)
+        driver = DistributedWcsph(sc, device=device, jitter=jitter_np(n_total, sc.spacing),
+                                  velocity=initial_velocity(args.workload, lattice))
+        solver = driver.solver
+    stream = torch.cuda.current_stream(device)
+    steps = args.steps * 4  # one bench step = 4 base steps (a major's worth)
+    for _ in range(args.warmup * 4):
+        driver.step()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(device.index or 0)
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    launches0 = _native.launch_count()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    rows = [driver.step() for _ in range(steps)]
+    ev1.record(stream)
+    ev1.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    launches = _native.launch_count() - launches0
+    clk = clocks.stop()
+    t = ev0.elapsed_time(ev1) * 1e-3
+    if world > 1:
+        tt = torch.tensor([t], device=device, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt[0])
+    value = n_total * steps / t
+
+    kernels = ["rts_wcsph_propagate", "rts_wcsph_density", "rts_wcsph_forces",
+               "rts_wcsph_integrate", "rts_block_levels"]
+    solver.time_kernels(kernels)
+    prof = [driver.step() for _ in range(8)]
+    torch.cuda.synchronize()
+    totals = {k: sum(solver.kernel_times(k)) for k in kernels}
+    counts = {k: len(solver.kernel_times(k)) for k in kernels}
+    solver._ktimes = None
+    nf_local = solver.n_fluid
+    active = sum(int(r.n_compute) for r in prof)
+    dom = max(totals, key=totals.get)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    alg = wcsph_algo_bytes(dom, nf_local, active, counts[dom])
+    ach = alg / max(totals[dom], 1e-12) / 1e9
+    roofline = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(ach / peak, 4), "traffic": None, "kernel": dom,
+                "launches": counts[dom], "kernel_s": round(totals[dom], 6),
+                "algorithmic_bytes": alg,
+                "share_of_step": round(totals[dom] / max(1e-12, sum(totals.values())), 3),
+                "kernels": {k: {"s": round(totals[k], 6), "launches": counts[k],
+                                "achieved_gbs": round(wcsph_algo_bytes(k, nf_local, active,
+                                                                       counts[k]) /
+                                                      max(totals[k], 1e-12) / 1e9, 1)}
+                            for k in kernels if counts[k]},
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s"}
+
+    e2e = None
+    if not args.no_e2e:
+        def dev_state():
+            if world == 1:
+                return solver.pos[:solver.n_fluid], solver.vel
+            return driver.state["pos"], driver.state["vel"]
+        k_e2e = 16
+        cap = 2 * dev_state()[0].shape[0] + 1024
+        hp = torch.empty((cap, 3), dtype=torch.float32).pin_memory()
+        hv = torch.empty((cap, 3), dtype=torch.float32).pin_memory()
+        dp, dv = dev_state()
+        hp[:dp.shape[0]].copy_(dp)
+        hv[:dv.shape[0]].copy_(dv)
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        nbytes = 0
+        for _ in range(k_e2e):
+            dp, dv = dev_state()
+            n = dp.shape[0]
+            dp.copy_(hp[:n], non_blocking=True)
+            dv.copy_(hv[:n], non_blocking=True)
+            driver.step()
+            dp, dv = dev_state()
+            n2 = dp.shape[0]
+            hp[:n2].copy_(dp, non_blocking=True)
+            hv[:n2].copy_(dv, non_blocking=True)
+            nbytes = (n + n2) * 24
+        torch.cuda.synchronize()
+        te = time.perf_counter() - t0
+        if world > 1:
+            tt = torch.tensor([te], device=device, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            te = float(tt[0])
+        e2e = {"value": n_total * k_e2e / te, "unit": UNIT,
+               "h2d_bytes_per_step": nbytes // 2, "d2h_bytes_per_step": nbytes // 2,
+               "steps": k_e2e, "note": "pinned host pos+vel uploaded before and downloaded "
+                                       "after every step(); wall clock"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_oracle_sample(majors=8, warm=1, workload=args.workload)
+        except Exception as exc:  # pragma: no cover
+            cpu = {"value": None, "error": repr(exc)}
+    if rank == 0:
+        line = {
+            "metric": METRICS[args.workload], "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": wl_name, "n_fluid": n_total, "n_boundary": solver.n_bound,
+                       "base_steps": steps, "bench_step": "4 base steps",
+                       "mean_active_fraction": round(sum(r.frac_compute for r in rows) /
+                                                     max(1, len(rows)), 4),
+                       "l2": "working set > L2 (state + hit tables)",
+                       "parallelism": ("single GPU" if world == 1 else
+                                       f"x-slabs x{world} (ghost exchange + migration)"),
+                       "arithmetic": "fp32 state, fp64 density sums"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
 
 
 def main():
@@ -230,7 +489,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-wcsph", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS),
+                    help="cfg2 (default, the headline) or the BASELINE configs[3..4] "
+                         "workloads")
     args = ap.parse_args()
+    kind, wl_name, scaling = WORKLOADS[args.workload]
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -259,16 +522,24 @@ def main():
         if world > 1:
             dist.barrier()
 
+    if kind == "wcsph":
+        run_wcsph_workload(args, rank, world, device, barrier)
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
     if world == 1:
-        solver = make_device_solver("pcisph", device)
+        solver = make_device_solver("pcisph", device, args.workload)
         driver = solver
         n_total = solver.n_fluid
     else:  # x-slab decomposition (paper_2009_14514_b200/distributed.py)
         from paper_2009_14514_b200.distributed import DistributedPcisph
         from paper_2009_14514_b200.scene import seed_particles
-        sc = scene_cfg2(world)
-        n_total = len(seed_particles(sc)[0])
+        sc = workload_scene(args.workload, world)
+        lattice = seed_particles(sc)[0]
+        n_total = len(lattice)
         driver = DistributedPcisph(sc, device=device, jitter=jitter_np(n_total, sc.spacing),
+                                   velocity=initial_velocity(args.workload, lattice),
                                    iteration_cap=50)
         solver = driver.solver
     nf = n_total
@@ -409,7 +680,7 @@ def main():
 
     # ---- WCSPH extra (configs[2] geometry, 1M RTS-WCSPH) ----------------------
     wc = None
-    if not args.no_wcsph and world == 1:
+    if not args.no_wcsph and world == 1 and args.workload == "cfg2":
         ws = make_device_solver("wcsph", device)
         for _ in range(8):
             ws.step()
@@ -457,24 +728,24 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_oracle_sample()
+            cpu = cpu_oracle_sample(workload=args.workload)
         except Exception as exc:  # pragma: no cover
             cpu = {"value": None, "error": repr(exc)}
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": METRICS[args.workload], "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic",
-            "config": {"workload": "cfg2: 1M dam break RTS-PCISPH (eta 3%/1.5%, cap 50, "
-                                   "dt 1.75e-4, 4 levels)", "n_fluid": nf,
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": wl_name, "n_fluid": nf,
                        "n_boundary": solver.n_bound, "minor_steps": minors,
                        "iterations_per_minor": round(sum(r.iterations for r in rows) /
                                                      max(1, minors), 3),
                        "corrected_per_minor_over_nf": round(sum(r.corrected for r in rows) /
                                                            max(1, minors) / nf, 3),
-                       "l2": "working set > L2 (neighbour tables 512 MB + state)",
+                       "l2": "working set > L2 (neighbour tables >= 512 MB + state)",
                        "parallelism": ("single GPU" if world == 1 else
                                        f"x-slabs x{world} (ghost exchange + allreduce)"),
                        "arithmetic": "fp32 state, fp64 pair sums"},

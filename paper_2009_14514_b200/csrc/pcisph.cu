@@ -65,14 +65,15 @@ __global__ void k_xs4_walls(const __grid_constant__ RtsParams p, RtsBuffers b) {
     }
 }
 
-// candidate copies of the major grid: cpos[k] = pos[order[k]], slot_of
+// candidate copies of the major grid: cpos[k] = (pos[order[k]], bits of
+// order[k]), slot_of
 __global__ void k_gather(const __grid_constant__ RtsParams p, RtsBuffers b) {
     if (fatal(b.ctr)) return;
     const int n = b.ctr->n_sorted;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
         const int j = b.order[k];
         reinterpret_cast<float4 *>(b.cpos)[k] =
-            make_float4(b.pos[3 * j], b.pos[3 * j + 1], b.pos[3 * j + 2], 0.0f);
+            make_float4(b.pos[3 * j], b.pos[3 * j + 1], b.pos[3 * j + 2], __int_as_float(j));
         if (j < p.n_fluid) b.slot_of[j] = k;
     }
 }
@@ -183,11 +184,14 @@ RTS_DEV void finish_refresh(const RtsParams &p, const RtsBuffers &b, int i, int 
 }
 
 // One thread (G = 1) or one G-lane group per refreshed particle, chosen from
-// the list length: the full refresh at a major-step start keeps one thread
-// per particle (adjacent lanes share candidate spans -> few L1 lines per
-// load); the short later lists (regions 1-2) use 8- or 32-lane groups so the
-// launch still has enough independent loads in flight (region-1 particles
-// scan 125 blocks, ~1300 candidates).
+// the list length against the grid (pass_blocks): on large scenes the full
+// refresh at a major-step start keeps one thread per particle (adjacent lanes
+// share candidate spans -> few L1 lines per load) and, with G = 1 and EXT,
+// forms the viscosity sum while it emits the row (ids and positions come
+// from the candidate copy, so the row is never re-read); the short later
+// lists (regions 1-2) and every list of a small scene use 8- or 32-lane
+// groups so the launch still has enough independent loads in flight
+// (region-1 particles scan 125 blocks, ~1300 candidates).
 // EXT = false: the bare search (BlockGrid.search_into, grid.py:297-331) --
 // rows and counts only, `lay_in` block layers for this particle.
 template <int G, bool EXT = true>
@@ -204,6 +208,10 @@ RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshC
     const int z0 = max(0, cz - lay), z1 = min(nz - 1, cz + lay);
     const unsigned lt = (1u << lane) - 1u;
     int cntn = 0;
+    // G == 1 && EXT: the viscosity sum is formed while the row is emitted
+    const double vxi = EXT ? b.vel[3 * i] : 0.0, vyi = EXT ? b.vel[3 * i + 1] : 0.0,
+                 vzi = EXT ? b.vel[3 * i + 2] : 0.0;
+    double vfx = 0.0, vfy = 0.0, vfz = 0.0;
     int *row = b.nbr + i;  // entry q at row[q * S]
     const size_t S = p.nbr_stride;
     for (int ax = max(0, cx - lay); ax <= min(nx - 1, cx + lay); ++ax)
@@ -246,22 +254,72 @@ RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshC
                         const float4 o = cp[q];
                         if (exact_neighbour(p.h2, fxi, fyi, fzi, o.x, o.y, o.z)) mem |= 1u << q;
                     }
+                    if (!EXT) {
+                        while (mem) {
+                            const int q = __ffs(mem) - 1;
+                            mem &= mem - 1u;
+                            if (cntn < p.width) __stcs(row + cntn * S, __float_as_int(cp[q].w));
+                            ++cntn;
+                        }
+                        continue;
+                    }
+                    // members in candidate (= row) order, four at a time: the
+                    // candidate copy (L1-hot) gives j and pos_j, so the row is
+                    // written and its viscosity term (fp32, fp64 row-order sum;
+                    // pcisph.py:183-196) taken without re-reading the row
                     while (mem) {
-                        const int q = __ffs(mem) - 1;
-                        mem &= mem - 1u;
-                        if (cntn < p.width) __stcs(row + cntn * S, b.order[cb + q]);
-                        ++cntn;
+                        float4 o[4];
+                        float vj[4][3];
+                        int nq = 0;
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            o[u] = make_float4(fxi, fyi, fzi, __int_as_float(i));
+                            if (mem) {
+                                o[u] = cp[__ffs(mem) - 1];
+                                mem &= mem - 1u;
+                                nq = u + 1;
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int j = __float_as_int(o[u].w);
+                            const int jc = j < p.n_fluid ? j : i;
+                            vj[u][0] = b.vel[3 * jc];
+                            vj[u][1] = b.vel[3 * jc + 1];
+                            vj[u][2] = b.vel[3 * jc + 2];
+                        }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            if (u >= nq) break;
+                            const int j = __float_as_int(o[u].w);
+                            if (cntn < p.width) {
+                                __stcs(row + cntn * S, j);
+                                if (j < p.n_fluid && j != i) {
+                                    const float dx = fxi - o[u].x, dy = fyi - o[u].y,
+                                                dz = fzi - o[u].z;
+                                    const float r = sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
+                                    if (r < k.hf) {
+                                        const float lap = k.visc_f * (k.hf - r);
+                                        vfx += (double)(lap * (vj[u][0] - (float)vxi));
+                                        vfy += (double)(lap * (vj[u][1] - (float)vyi));
+                                        vfz += (double)(lap * (vj[u][2] - (float)vzi));
+                                    }
+                                }
+                            }
+                            ++cntn;
+                        }
                     }
                 }
             } else {
                 for (int kb = k0; kb < k1; kb += G) {
                     const int kk = kb + lane;
-                    const bool in = kk < k1 && is_neighbour(k, p, fxi, fyi, fzi, cpos[kk]);
+                    const float4 o = kk < k1 ? cpos[kk] : make_float4(0.f, 0.f, 0.f, 0.f);
+                    const bool in = kk < k1 && is_neighbour(k, p, fxi, fyi, fzi, o);
                     const unsigned m =
                         (__ballot_sync(gmask, in) >> gshift) & (G == 32 ? 0xffffffffu : ((1u << G) - 1u));
                     if (in) {
                         const int slot = cntn + __popc(m & lt);
-                        if (slot < p.width) __stcs(row + slot * S, b.order[kk]);
+                        if (slot < p.width) __stcs(row + slot * S, __float_as_int(o.w));
                     }
                     cntn += __popc(m);
                 }
@@ -273,42 +331,8 @@ RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshC
         return;
     }
     const int nrow = min(cntn, p.width);
-    const double vxi = b.vel[3 * i], vyi = b.vel[3 * i + 1], vzi = b.vel[3 * i + 2];
-    double fx = 0.0, fy = 0.0, fz = 0.0;
-    if (G == 1) {
-        // four entries at a time, every load issued before the fp64 terms
-        // (which are summed in row order, as below)
-        for (int q = 0; q < nrow; q += 4) {
-            int jj[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) jj[u] = q + u < nrow ? row[(q + u) * S] : i;
-            float4 pj[4];
-            float vj[4][3];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int jc = jj[u] < p.n_fluid ? jj[u] : i;  // walls: no term, no vel row
-                pj[u] = make_float4(b.pos[3 * jc], b.pos[3 * jc + 1], b.pos[3 * jc + 2], 0.f);
-                vj[u][0] = b.vel[3 * jc];
-                vj[u][1] = b.vel[3 * jc + 1];
-                vj[u][2] = b.vel[3 * jc + 2];
-            }
-            // viscosity terms in fp32 (f_ext = m g + a small viscous part:
-            // ~1e-7 relative deviation, bar 1e-4), summed in fp64 in row order
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int j = jj[u];
-                if (q + u >= nrow || j >= p.n_fluid || j == i) continue;
-                const float dx = (float)xi - pj[u].x, dy = (float)yi - pj[u].y,
-                            dz = (float)zi - pj[u].z;
-                const float r = sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
-                if (r >= k.hf) continue;
-                const float lap = k.visc_f * (k.hf - r);
-                fx += (double)(lap * (vj[u][0] - (float)vxi));
-                fy += (double)(lap * (vj[u][1] - (float)vyi));
-                fz += (double)(lap * (vj[u][2] - (float)vzi));
-            }
-        }
-    } else {
+    double fx = vfx, fy = vfy, fz = vfz;
+    if (G > 1) {  // (G == 1: summed above, while the row was emitted)
         for (int q = lane; q < nrow; q += G) {
             const int j = row[q * S];
             const float4 pj = make_float4(b.pos[3 * j], b.pos[3 * j + 1], b.pos[3 * j + 2], 0.f);
@@ -557,6 +581,16 @@ __global__ void k_sob(const __grid_constant__ RtsParams p, RtsBuffers b) {
 // per particle so the launch still has enough independent loads in flight.
 constexpr int kPG = 8;
 
+// Grid of the per-particle passes: one thread per particle, or -- on scenes
+// small enough that kPG lanes per particle fit the default grid cap -- kPG
+// threads per particle, so the kernels' group paths (shorter dependent load
+// chains per thread) serve latency-bound desk-scale runs.  Large scenes are
+// unaffected (the cap binds).
+static inline int pass_blocks(const RtsParams *p) {
+    return rts_blocks((long long)p->n_fluid * kPG, kThreads);
+}
+
+
 template <int LG, int CH = 8>
 RTS_DEV void density_one(const RtsParams &p, const RtsBuffers &b, int i, int lane,
                          unsigned gmask) {
@@ -670,7 +704,8 @@ RTS_DEV void se_one(const RtsParams &p, const RtsBuffers &b, int i, double e, fl
 __global__ void __launch_bounds__(256) k_se_reduce(const __grid_constant__ RtsParams p,
                                                    RtsBuffers b, int with_se) {
     RTS_ITER_GUARD();
-    __shared__ double ssum[8];
+    __shared__ double ssum[8], smax[8];
+    __shared__ int sany[8];
     __shared__ bool last;
     const int nf = p.n_fluid;
     const double thr = xmul(0.5, p.eta_max);
@@ -706,15 +741,22 @@ __global__ void __launch_bounds__(256) k_se_reduce(const __grid_constant__ RtsPa
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (lane == 0) {
         ssum[warp] = s;
-        if (m > 0.0)
-            atomicMax(reinterpret_cast<unsigned long long *>(&b.ctr->max_err),
-                      (unsigned long long)__double_as_longlong(m));
-        if (any) atomicOr(&b.ctr->any_se, 1);
+        smax[warp] = m;
+        sany[warp] = any;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        double t = 0.0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t = xadd(t, ssum[w]);
+    if (threadIdx.x == 0) {  // one atomic per block: same-address atomics serialise in L2
+        double t = 0.0, bm = 0.0;
+        int ba = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            t = xadd(t, ssum[w]);
+            bm = fmax(bm, smax[w]);
+            ba |= sany[w];
+        }
+        if (bm > 0.0)
+            atomicMax(reinterpret_cast<unsigned long long *>(&b.ctr->max_err),
+                      (unsigned long long)__double_as_longlong(bm));
+        if (ba) atomicOr(&b.ctr->any_se, 1);
         b.partial[blockIdx.x] = t;
         __threadfence();
         last = atomicAdd(&b.ctr->blocks_done, 1u) == gridDim.x - 1;
@@ -910,7 +952,8 @@ RTS_DEV void integrate_one(const RtsParams &p, const RtsBuffers &b, int i, int c
     if (countdown & 2) block_maxima_one(b, b.fluid_cells[i], &b.vel[3 * i], &b.force[3 * i],
                                         &b.f_p[3 * i]);
     if (countdown) {
-        reinterpret_cast<float4 *>(b.cpos)[b.slot_of[i]] = make_float4(nx[0], nx[1], nx[2], 0.f);
+        reinterpret_cast<float4 *>(b.cpos)[b.slot_of[i]] =
+            make_float4(nx[0], nx[1], nx[2], __int_as_float(i));
         int v = b.validity[i] - 1;
         const bool expired = v <= 0;
         if (expired) {
@@ -989,7 +1032,7 @@ __global__ void k_integrate(const __grid_constant__ RtsParams p, RtsBuffers b, i
                 if (MAXIMA) block_maxima_one(b, cl[q], &v[3 * q], &fe[3 * q], &fp[3 * q]);
                 sob[q] = observed_block(b, cl[q], gen);
                 reinterpret_cast<float4 *>(b.cpos)[sl[q]] =
-                    make_float4(x[3 * q], x[3 * q + 1], x[3 * q + 2], 0.f);
+                    make_float4(x[3 * q], x[3 * q + 1], x[3 * q + 2], __int_as_float(4 * g + q));
                 int vv = vl[q] - 1;
                 const bool expired = vv <= 0;
                 if (expired) vv = kValidity[rg[q] < 0 ? 0 : (rg[q] > 4 ? 4 : rg[q])];
@@ -1342,7 +1385,7 @@ int rts_pci_refresh(const RtsParams *p, const RtsBuffers *b, int all, int two_la
     cudaMemsetAsync(&b->ctr->n_compute, 0, sizeof(int), s);
     rts_note_launch(), k_refresh_list<<<rts_blocks(p->n_fluid, 256, 148 * 4), 256, 0, s>>>(*p, *b, all);
     RTS_LAUNCH_CHECK();
-    rts_note_launch(), k_refresh<<<rts_blocks(p->n_fluid, kThreads), kThreads, 0, s>>>(*p, *b, two_layer_r1);
+    rts_note_launch(), k_refresh<<<pass_blocks(p), kThreads, 0, s>>>(*p, *b, two_layer_r1);
     RTS_LAUNCH_CHECK();
     return 0;
 }
@@ -1371,7 +1414,7 @@ int rts_pci_sets(const RtsParams *p, const RtsBuffers *b, int row_mask, int all_
 }
 
 int rts_pci_density(const RtsParams *p, const RtsBuffers *b, void *stream) {
-    const int nb = rts_blocks(p->n_fluid, kThreads);
+    const int nb = pass_blocks(p);
     cudaStream_t s = (cudaStream_t)stream;
     // 4-deep chunks, <= 48 registers: 10 CTAs of 128 threads per SM
     rts_note_launch(), k_density<4, 10><<<nb, kThreads, 0, s>>>(*p, *b);
@@ -1403,7 +1446,7 @@ int rts_pci_sob(const RtsParams *p, const RtsBuffers *b, void *stream) {
 }
 
 int rts_pci_pforces(const RtsParams *p, const RtsBuffers *b, void *stream) {
-    const int nb = rts_blocks(p->n_fluid, kThreads);
+    const int nb = pass_blocks(p);
     cudaStream_t s = (cudaStream_t)stream;
     rts_note_launch(), k_pforces<4, 7><<<nb, kThreads, 0, s>>>(*p, *b);
     RTS_LAUNCH_CHECK();

@@ -263,7 +263,7 @@ class DistributedWcsph:
     owned + ghosts, extraction of the owned rows, migration."""
 
     def __init__(self, scene: Scene, mode: str = "rts", device=None, halo: int = 2,
-                 jitter=None, local=None, comm_device=None, **kw):
+                 jitter=None, local=None, comm_device=None, velocity=None, **kw):
         self.rank = dist.get_rank()
         self.world = dist.get_world_size()
         self.device = torch.device(device) if device is not None else torch.device("cuda")
@@ -283,6 +283,9 @@ class DistributedWcsph:
         self.gid = torch.as_tensor(gid, device=self.device)
         fl = torch.as_tensor(fluid[gid].astype(np.float32), device=self.device)
         self.state = self.solver._fresh_state(fl)
+        if velocity is not None:  # (n_global, 3) initial velocities by global id
+            self.state["vel"] = torch.as_tensor(np.asarray(velocity)[gid], device=self.device,
+                                                dtype=self.state["vel"].dtype)
         self.sim_time = 0.0
         self.step_index = 0
 
@@ -405,7 +408,7 @@ class DistributedPcisph:
     scalars every iteration."""
 
     def __init__(self, scene: Scene, device=None, halo: int = 6, inner: int = 2, jitter=None,
-                 comm_device=None, **kw):
+                 comm_device=None, velocity=None, **kw):
         from .pcisph import PcisphSolver
         self.rank = dist.get_rank()
         self.world = dist.get_world_size()
@@ -427,6 +430,9 @@ class DistributedPcisph:
         fl = torch.as_tensor(fluid[gid].astype(np.float32), device=self.device)
         st = self.solver._fresh_state(fl)
         st["xstar"] = fl.clone()
+        if velocity is not None:  # (n_global, 3) initial velocities by global id
+            st["vel"] = torch.as_tensor(np.asarray(velocity)[gid], device=self.device,
+                                        dtype=st["vel"].dtype)
         self.state = st
         self.sim_time = 0.0
         self.step_index = 0

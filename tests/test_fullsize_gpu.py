@@ -7,7 +7,9 @@ its bit-level checks run at the small sizes of the other test files):
   early-terminated one), particles are conserved, two solvers started from
   the same state agree bit for bit (deterministic reductions);
 * cfg3 (1 M RTS-WCSPH): deterministic, finite, densities near rest;
-* cfg4-scale (8 M, one GPU): a major step runs without index overflow.
+* cfg4 (8 M mixed tank, z up, one GPU): a major step runs without index
+  overflow, with mixed levels and the block falling;
+* cfg5 at one GPU (4 M, N(0, 0.1) velocities): both solvers stay sound.
 """
 
 import pytest
@@ -72,20 +74,51 @@ def test_cfg3_1m_wcsph_properties():
     assert float(e.mean()) < 0.02
 
 
-def test_cfg4_scale_8m_major_step():
-    from paper_2009_14514_b200 import PcisphSolver, Scene
-    # 8 M fluid particles at s = 0.01: a 2 x 2 x 2 m column in a 4 x 2.5 x 2.5 m tank
-    scene = Scene(domain_min=(0.0, 0.0, 0.0), domain_max=(4.0, 2.5, 2.5),
-                  fluid_boxes=(((0.0, 0.0, 0.0), (2.0, 2.0, 2.0)),), spacing=0.01,
-                  eta_max=0.03, eta_avg=0.015)
-    s = PcisphSolver(scene, mode="rts", iteration_cap=50, device="cuda:0")
-    assert s.n_fluid == 8_000_000
+def test_cfg4_mixed_tank_8m():
+    """configs[3] on one GPU: z-up gravity, 8 M fluid, the falling block
+    starts at (0, 0, -2) m/s.  Mixed dynamics must give several levels."""
+    b = _bench()
+    dev = torch.device("cuda", 0)
+    s = b.make_device_solver("pcisph", dev, "cfg4")
+    assert s.n_fluid == 8_015_190
+    s.audit_neighbors = True
     rows = s.advance()
     assert len(rows) == 4
+    assert sum(r.missed_neighbors for r in rows) == 0
     assert all(r.iterations >= 3 for r in rows)
+    for r in rows:
+        assert r.early_term or r.max_err < s.scene.eta_max, r
     assert int(s.cnt.max()) <= 128
     assert torch.isfinite(s.pos).all()
     n = s.cnt[: s.n_fluid].double()
     assert 20.0 < float(n.mean()) < 40.0
+    lv = torch.bincount(s.particle_regions().long().reshape(-1), minlength=5)
+    assert int((lv[1:] > 0).sum()) >= 2, lv  # fast block and slow pool differ
+    z = s.pos[: s.n_fluid, 2]
+    vz = s.vel[:, 2]
+    blk = z > 1.0
+    assert float(vz[blk].mean()) < -2.0  # still falling, accelerated by -z gravity
+    # the pool only settles (jitter + the first pressure build-up)
+    assert float(vz[~blk].abs().mean()) < 0.5
+    del s
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("kind", ["pcisph", "wcsph"])
+def test_cfg5_weak_4m_single_gpu(kind):
+    """configs[4] at one GPU: 4 M particles with N(0, 0.1) initial velocities."""
+    b = _bench()
+    dev = torch.device("cuda", 0)
+    s = b.make_device_solver(kind, dev, f"cfg5-{kind}")
+    assert s.n_fluid == 4_000_000
+    s.audit_neighbors = True
+    rows = []
+    for _ in range(2 if kind == "pcisph" else 8):
+        rows += s.advance()
+    assert sum(r.missed_neighbors for r in rows) == 0
+    if kind == "pcisph":
+        for r in rows:
+            assert r.early_term or r.max_err < s.scene.eta_max, r
+    assert torch.isfinite(s.pos).all() and torch.isfinite(s.vel).all()
     del s
     torch.cuda.empty_cache()
