@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define RTS_ABI_VERSION 18
+#define RTS_ABI_VERSION 19
 
 /* err_flags bits */
 #define RTS_ERR_ESCAPED   0x1u  /* fluid left the padded grid or non-finite (grid.py:268-273) */
@@ -364,6 +364,39 @@ int rts_wcsph_integrate(const RtsParams *p, const RtsBuffers *b, void *stream);
 void *rts_wcsph_graph_create(const RtsParams *p, const RtsBuffers *b, int *err);
 /* max |F| over fluid into ctr->fmax_bits (cfl_bound, wcsph.py:182-189). */
 int rts_force_max(const RtsParams *p, const RtsBuffers *b, void *stream);
+
+/* ---- x-slab ranks (no reference counterpart: the
+ * reference correction loop pcisph.py:612-716 runs in one process) ------- */
+#define RTS_HALO_MAX_FIELDS 8
+typedef struct {
+    void *ptr;              /* storage row 0 of the field */
+    const int32_t *remap;   /* row -> storage row (e.g. slot_of), or NULL */
+    int32_t words;          /* 32-bit words exchanged per row (fp64 = 2) */
+    int32_t stride;         /* 32-bit words between consecutive storage rows */
+    int32_t msg_off;        /* first word of the field inside a message row */
+    int32_t pad;
+} RtsHaloField;
+typedef struct {
+    int32_t n_fields;       /* 1 .. RTS_HALO_MAX_FIELDS */
+    int32_t row_words;      /* sum of f[].words (words moved per row) */
+    int32_t msg_words;      /* message row width; fields may share words on unpack
+                             * (one received word stored in two places) */
+    int32_t pad;
+    RtsHaloField f[RTS_HALO_MAX_FIELDS];
+} RtsHaloSpec;
+/* out[r * msg_words + f.msg_off + w] = word w of field f of row rows[r]
+ * (r < n), bit copies (fp64 fields travel as two words). */
+int rts_halo_pack(const RtsHaloSpec *s, const int32_t *rows, int64_t n, uint32_t *out,
+                  void *stream);
+/* Inverse of rts_halo_pack: word w of field f of row rows[r] =
+ * in[r * msg_words + f.msg_off + w]. */
+int rts_halo_unpack(const RtsHaloSpec *s, const int32_t *rows, int64_t n, const uint32_t *in,
+                    void *stream);
+/* out[0..3] = (max_err, any_se, sum_rho, n_pred) of ctr, as fp64. */
+int rts_ctl_publish(const RtsBuffers *b, double *out, void *stream);
+/* ctr = fold of the all-gathered (world, 4) publish rows: MAX of max_err /
+ * any_se, rank-order SUM of sum_rho / n_pred (before rts_pci_control). */
+int rts_ctl_fold(const RtsBuffers *b, const double *gathered, int world, void *stream);
 
 #ifdef __cplusplus
 }

@@ -12,7 +12,7 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "librtssph.so")
-ABI_VERSION = 18
+ABI_VERSION = 19
 
 _c = ctypes
 _D = _c.c_double
@@ -87,6 +87,19 @@ class RtsBuffers(_c.Structure):
     _fields_ = [(name, _P) for name in BUFFER_FIELDS]
 
 
+HALO_MAX_FIELDS = 8
+
+
+class RtsHaloField(_c.Structure):
+    _fields_ = [("ptr", _P), ("remap", _P), ("words", _I), ("stride", _I), ("msg_off", _I),
+                ("pad", _I)]
+
+
+class RtsHaloSpec(_c.Structure):
+    _fields_ = [("n_fields", _I), ("row_words", _I), ("msg_words", _I), ("pad", _I),
+                ("f", RtsHaloField * HALO_MAX_FIELDS)]
+
+
 ERR_ESCAPED, ERR_OVERFLOW, ERR_NONFINITE, ERR_ITERCAP = 0x1, 0x2, 0x4, 0x8
 
 # entry points: name -> argtypes (all return int)
@@ -134,6 +147,10 @@ SIGNATURES = {
     "rts_wcsph_density": [_PP, _PB, _P],
     "rts_wcsph_forces": [_PP, _PB, _P],
     "rts_wcsph_integrate": [_PP, _PB, _P],
+    "rts_halo_pack": [_c.POINTER(RtsHaloSpec), _P, _c.c_int64, _P, _P],
+    "rts_halo_unpack": [_c.POINTER(RtsHaloSpec), _P, _c.c_int64, _P, _P],
+    "rts_ctl_publish": [_PB, _P, _P],
+    "rts_ctl_fold": [_PB, _P, _c.c_int, _P],
 }
 
 _lib = None

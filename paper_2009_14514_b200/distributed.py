@@ -26,6 +26,7 @@ CFL bound is an all-reduce MAX of |F|.
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass
 
@@ -332,72 +333,129 @@ def _ctr_views(ctr: torch.Tensor) -> dict:
             "n_pred": ctr[off["n_pred"]:off["n_pred"] + 4].view(torch.int32)}
 
 
+class HaloChannel:
+    """One fixed-row exchange phase of a major step, native end to end:
+    ``rts_halo_pack`` of every peer's send rows into one word buffer, a
+    grouped send/recv of the per-peer slices (NCCL: stream-ordered, no host
+    synchronisation), ``rts_halo_unpack`` of the received rows.
+
+    ``pack`` / ``unpack``: ``(tensor, words, stride, remap, msg_off)`` in
+    32-bit words (fp64 = 2 words, bit copies).  Unpack fields may share
+    message words, so one received word can be stored in two places."""
+
+    def __init__(self, xch: "Exchanger", send_idx: dict, recv_idx: dict, pack, unpack=None):
+        from . import _native as N
+        self.N, self.x = N, xch
+        self.peers = sorted(send_idx)
+        dev = xch.compute_device
+
+        def rows(d):
+            if not self.peers:
+                return torch.zeros(0, dtype=torch.int32, device=dev)
+            return torch.cat([d[q].reshape(-1) for q in self.peers]).to(torch.int32).contiguous()
+
+        self.send_rows, self.recv_rows = rows(send_idx), rows(recv_idx)
+        self.n_send = [int(send_idx[q].numel()) for q in self.peers]
+        self.n_recv = [int(recv_idx[q].numel()) for q in self.peers]
+        self.msg_words = max(f[4] + f[1] for f in pack)
+        self.pack_spec = self._spec(pack)
+        self.unpack_spec = self._spec(unpack or pack)
+        self.send_buf = torch.empty((sum(self.n_send), self.msg_words), dtype=torch.int32,
+                                    device=dev)
+
+    def _spec(self, fields):
+        N = self.N
+        if not 1 <= len(fields) <= N.HALO_MAX_FIELDS:
+            raise ValueError(f"{len(fields)} halo fields (1..{N.HALO_MAX_FIELDS})")
+        spec = N.RtsHaloSpec()
+        spec.n_fields, spec.msg_words = len(fields), self.msg_words
+        spec.row_words = sum(f[1] for f in fields)
+        for k, (t, words, stride, remap, off) in enumerate(fields):
+            f = spec.f[k]
+            f.ptr = t.data_ptr()
+            f.remap = remap.data_ptr() if remap is not None else None
+            f.words, f.stride, f.msg_off = words, stride, off
+        return spec
+
+    def run(self) -> None:
+        if not self.peers:
+            return
+        N = self.N
+        st = torch.cuda.current_stream(self.x.compute_device).cuda_stream
+        N.call("rts_halo_pack", ctypes.byref(self.pack_spec), self.send_rows.data_ptr(),
+               self.send_rows.numel(), self.send_buf.data_ptr(), st)
+        send, a = {}, 0
+        for q, ns in zip(self.peers, self.n_send):
+            send[q] = self.send_buf[a:a + ns]
+            a += ns
+        got = self.x.swap(send, dict(zip(self.peers, self.n_recv)), self.msg_words, torch.int32)
+        parts = [got[q] for q in self.peers if got[q].shape[0]]
+        if not parts:
+            return
+        recv = torch.cat(parts) if len(parts) > 1 else parts[0].contiguous()
+        N.call("rts_halo_unpack", ctypes.byref(self.unpack_spec), self.recv_rows.data_ptr(),
+               self.recv_rows.numel(), recv.data_ptr(), st)
+
+
 class PcisphExchange:
     """Ghost refreshes inside a major step (hooks called by PcisphSolver's
     host-driven loop).  Only the two inner ghost columns on each side are
     neighbours of owned particles (two layers of 2.2s blocks cover the
     region-1 two-layer search); deeper ghosts exist for the major-start
     level fields only.  Per correction iteration: x* after the motion pass,
-    p / err / rho* after the density pass, then an all-reduce of the
-    convergence scalars (max err, sum rho*, any S_e, |pred|) -- the exchange
-    steps of SURVEY.md section 8e.  Per minor step: pos / vel / f_ext / f_p
-    after the integrator (next refresh, mid-major marking)."""
+    p / err / rho* after the density pass, then the convergence scalars
+    (max err, sum rho*, any S_e, |pred|) of every rank all-gathered and
+    folded on the device in rank order -- the exchange steps of SURVEY.md
+    section 8e.  Per minor step: pos / vel / f_ext / f_p after the
+    integrator (next refresh, mid-major marking).  Every phase is one native
+    pack, one grouped send/recv and one native unpack (``HaloChannel``)."""
 
     def __init__(self, driver: "SlabDriver", send_idx: dict, recv_idx: dict):
         self.x = driver.x
         self.send_idx, self.recv_idx = send_idx, recv_idx
         self.peers = sorted(send_idx)
+        self._ch = None
 
-    def _swap(self, columns_out, width: int, dtype=torch.float64) -> dict:
-        # the row sets are fixed for the whole major step and matched on both
-        # sides (same columns, global-id order), so no count round is needed
-        send = {q: columns_out(self.send_idx[q]) for q in self.peers}
-        recv = {q: int(self.recv_idx[q].numel()) for q in self.peers}
-        return self.x.swap(send, recv, width, dtype)
+    def _channels(self, s) -> dict:
+        if self._ch is None:
+            A = s.arena
+            xs4, pres, err, rho = A["xs4"], A["pres"], A["err"], A["rho"]
+            pos, vel, fe, fp = A["pos"], A["vel"], A["force"], A["f_p"]
+            ch = lambda pk, up=None: HaloChannel(self.x, self.send_idx, self.recv_idx, pk, up)
+            dens = [(pres, 1, 1, None, 0), (err, 2, 2, None, 1), (rho, 1, 1, None, 3)]
+            move = [(pos, 3, 3, None, 0), (vel, 3, 3, None, 3), (fe, 3, 3, None, 6),
+                    (fp, 3, 3, None, 9)]
+            self._ch = {
+                "motion": ch([(xs4, 4, 4, None, 0)]),
+                # p lands in pres and in xs4.w
+                "density": ch(dens, dens + [(xs4[:, 3:], 1, 4, None, 0)]),
+                # pos also refreshes the candidate copy at the row's CSR slot
+                "integrate": ch(move, move + [(A["cpos"], 3, 4, A["slot_of"], 0)]),
+            }
+            dev = self.x.compute_device
+            self._pub = torch.zeros(4, dtype=torch.float64, device=dev)
+            self._gath = torch.zeros((self.x.world, 4), dtype=torch.float64, device=dev)
+        return self._ch
 
     def after_motion(self, s) -> None:
-        xs4 = s.arena["xs4"]
-        got = self._swap(lambda idx: xs4[idx], 4, torch.float32)
-        for q, rows in got.items():
-            xs4[self.recv_idx[q]] = rows.float()
+        self._channels(s)["motion"].run()
 
     def after_density(self, s) -> None:
-        A = s.arena
-        xs4, pres, err, rho = A["xs4"], A["pres"], A["err"], A["rho"]
-        got = self._swap(lambda idx: torch.stack([pres[idx].double(), err[idx],
-                                                  rho[idx].double()], 1), 3)
-        for q, rows in got.items():
-            r = self.recv_idx[q]
-            pres[r] = rows[:, 0].float()
-            xs4[r, 3] = rows[:, 0].float()
-            err[r] = rows[:, 1]
-            rho[r] = rows[:, 2].float()
+        self._channels(s)["density"].run()
 
     def reduce(self, s) -> None:
-        v = _ctr_views(s.arena["ctr"])
-        dev = self.x.device
-        m = torch.cat([v["max_err"], v["any_se"].double()]).to(dev)
-        a = torch.cat([v["sum_rho"], v["n_pred"].double()]).to(dev)
-        dist.all_reduce(m, op=dist.ReduceOp.MAX)
-        dist.all_reduce(a, op=dist.ReduceOp.SUM)
-        m, a = m.to(v["max_err"].device), a.to(v["max_err"].device)
-        v["max_err"].copy_(m[:1])
-        v["any_se"].copy_(m[1:2].to(torch.int32))
-        v["sum_rho"].copy_(a[:1])
-        v["n_pred"].copy_(a[1:2].to(torch.int32))
+        from . import _native as N
+        self._channels(s)
+        st = torch.cuda.current_stream(self.x.compute_device).cuda_stream
+        N.call("rts_ctl_publish", s.arena.buf, self._pub.data_ptr(), st)
+        pub = self._pub.to(self.x.device)
+        parts = [torch.empty_like(pub) for _ in range(self.x.world)]
+        dist.all_gather(parts, pub)
+        self._gath.copy_(torch.stack(parts))
+        N.call("rts_ctl_fold", s.arena.buf, self._gath.data_ptr(), self.x.world, st)
 
     def after_integrate(self, s) -> None:
-        A = s.arena
-        pos, vel, fe, fp = A["pos"], A["vel"], A["force"], A["f_p"]
-        got = self._swap(lambda idx: torch.cat([pos[idx], vel[idx], fe[idx], fp[idx]], 1), 12,
-                         torch.float32)
-        cpos, slot = A["cpos"], A["slot_of"]
-        for q, rows in got.items():
-            r = self.recv_idx[q]
-            rows = rows.float()
-            pos[r], vel[r], fe[r], fp[r] = rows[:, 0:3], rows[:, 3:6], rows[:, 6:9], rows[:, 9:12]
-            sl = slot[r].long()
-            cpos[sl, 0:3] = rows[:, 0:3]
+        self._channels(s)["integrate"].run()
 
 
 class DistributedPcisph:

@@ -9,7 +9,8 @@ from paper_2009_14514_b200.distributed import DistributedPcisph
 from paper_2009_14514_b200.scene import seed_particles
 os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
 os.environ.setdefault("MASTER_PORT", "29555")
-dist.init_process_group("gloo", rank=0, world_size=1)
+print("backend", os.environ.get("RTS_DIST_BACKEND", "nccl"))
+dist.init_process_group(os.environ.get("RTS_DIST_BACKEND", "nccl"), rank=0, world_size=1)
 sc = bench.scene_cfg2(1)
 n = len(seed_particles(sc)[0])
 d = DistributedPcisph(sc, device=torch.device("cuda", 0), jitter=bench.jitter_np(n, sc.spacing),
