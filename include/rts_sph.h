@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define RTS_ABI_VERSION 19
+#define RTS_ABI_VERSION 20
 
 /* err_flags bits */
 #define RTS_ERR_ESCAPED   0x1u  /* fluid left the padded grid or non-finite (grid.py:268-273) */
@@ -210,6 +210,8 @@ typedef struct RtsBuffers {
     int32_t *se_stamp;     /* (Nc) S_e generation that last marked the block */
     int32_t *near_stamp;   /* (Nc) S_e generation that last marked a 26-neighbour */
     uint8_t *ghost;        /* (Nf) 1 = ghost row owned by another rank (or NULL) */
+    int32_t *sort_key;     /* (Nf) global ids of the fluid rows: within-block CSR order by key
+                            * instead of by row (x-slab ranks; NULL = by row) */
     RtsCounters *ctr;
 } RtsBuffers;
 
@@ -367,14 +369,16 @@ int rts_force_max(const RtsParams *p, const RtsBuffers *b, void *stream);
 
 /* ---- x-slab ranks (no reference counterpart: the
  * reference correction loop pcisph.py:612-716 runs in one process) ------- */
-#define RTS_HALO_MAX_FIELDS 8
+#define RTS_HALO_MAX_FIELDS 16
 typedef struct {
     void *ptr;              /* storage row 0 of the field */
     const int32_t *remap;   /* row -> storage row (e.g. slot_of), or NULL */
-    int32_t words;          /* 32-bit words exchanged per row (fp64 = 2) */
-    int32_t stride;         /* 32-bit words between consecutive storage rows */
+    int32_t words;          /* elements exchanged per row, one message word each
+                             * (4-byte elements; fp64 = 2) */
+    int32_t stride;         /* elements between consecutive storage rows */
     int32_t msg_off;        /* first word of the field inside a message row */
-    int32_t pad;
+    int32_t esize;          /* element bytes: 4 (or 0), or 1 for int8 / bool fields
+                             * (zero-extended into their message word) */
 } RtsHaloField;
 typedef struct {
     int32_t n_fields;       /* 1 .. RTS_HALO_MAX_FIELDS */

@@ -12,7 +12,7 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "librtssph.so")
-ABI_VERSION = 19
+ABI_VERSION = 20
 
 _c = ctypes
 _D = _c.c_double
@@ -79,7 +79,7 @@ BUFFER_FIELDS = (
     "cell_bcount", "starts", "order", "fill", "scan_tmp", "bcell_ids", "bcell_start", "bidx",
     "bcell_of", "bcell_active", "vmax", "fmax", "block_raw", "block_field", "block_tmp",
     "block_flag", "cpos", "cvel", "active", "list2", "list3", "nbr", "cnt", "xs4", "pflag", "partial",
-    "snap_p", "snap_fp", "slot_of", "ctl", "se_stamp", "near_stamp", "ghost", "ctr",
+    "snap_p", "snap_fp", "slot_of", "ctl", "se_stamp", "near_stamp", "ghost", "sort_key", "ctr",
 )
 
 
@@ -87,12 +87,12 @@ class RtsBuffers(_c.Structure):
     _fields_ = [(name, _P) for name in BUFFER_FIELDS]
 
 
-HALO_MAX_FIELDS = 8
+HALO_MAX_FIELDS = 16
 
 
 class RtsHaloField(_c.Structure):
     _fields_ = [("ptr", _P), ("remap", _P), ("words", _I), ("stride", _I), ("msg_off", _I),
-                ("pad", _I)]
+                ("esize", _I)]
 
 
 class RtsHaloSpec(_c.Structure):

@@ -278,6 +278,41 @@ __global__ void k_sort_runs(const __grid_constant__ RtsParams p, RtsBuffers b) {
     }
 }
 
+// x-slab ranks: fluid runs ordered by the rows' global ids (b.sort_key), so
+// a rank's local row order is free while every within-block order -- and so
+// every neighbour row and pair sum -- stays the single-domain one.
+__global__ void k_sort_runs_keyed(const __grid_constant__ RtsParams p, RtsBuffers b) {
+    if (fatal(b.ctr)) return;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < p.n_cells;
+         c += gridDim.x * blockDim.x) {
+        const int n = b.cell_count[c];
+        if (n < 2) continue;
+        int *run = b.order + b.starts[c];
+        auto key = [&](int i) {
+            return ((long long)b.sort_key[i] << 32) | (unsigned)i;
+        };
+        if (n <= 32) {
+            long long v[32];
+            for (int q = 0; q < n; ++q) v[q] = key(run[q]);
+            for (int q = 1; q < n; ++q) {
+                const long long k = v[q];
+                int r = q - 1;
+                while (r >= 0 && v[r] > k) { v[r + 1] = v[r]; --r; }
+                v[r + 1] = k;
+            }
+            for (int q = 0; q < n; ++q) run[q] = (int)(v[q] & 0xffffffffll);
+        } else {
+            for (int q = 1; q < n; ++q) {
+                const int x = run[q];
+                const long long k = key(x);
+                int r = q - 1;
+                while (r >= 0 && key(run[r]) > k) { run[r + 1] = run[r]; --r; }
+                run[r + 1] = x;
+            }
+        }
+    }
+}
+
 __global__ void k_force_max(const __grid_constant__ RtsParams p, RtsBuffers b) {
     double m = 0.0;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.n_fluid;
@@ -353,7 +388,10 @@ int rts_grid_sort(const RtsParams *p, const RtsBuffers *b, void *stream) {
     rts_note_launch(), k_scatter<<<rts_blocks((long long)p->n_fluid + p->n_bound, kThreads), kThreads, 0, s>>>(
         *p, *b);
     RTS_LAUNCH_CHECK();
-    rts_note_launch(), k_sort_runs<<<rts_blocks(p->n_cells, kThreads), kThreads, 0, s>>>(*p, *b);
+    if (b->sort_key)
+        rts_note_launch(), k_sort_runs_keyed<<<rts_blocks(p->n_cells, kThreads), kThreads, 0, s>>>(*p, *b);
+    else
+        rts_note_launch(), k_sort_runs<<<rts_blocks(p->n_cells, kThreads), kThreads, 0, s>>>(*p, *b);
     RTS_LAUNCH_CHECK();
     return 0;
 }

@@ -35,10 +35,16 @@ k_halo(const RtsHaloSpec s, const int32_t *__restrict__ rows, long long n,
         const RtsHaloField &fd = s.f[f];
         long long row = rows[r];
         if (fd.remap) row = fd.remap[row];
-        uint32_t *p = (uint32_t *)fd.ptr + row * fd.stride + w;
         uint32_t *m = msg + r * s.msg_words + fd.msg_off + w;
-        if (kPack) *m = *p;
-        else *p = *m;
+        if (fd.esize == 1) {  // byte elements (int8 / bool fields): one per word
+            uint8_t *p = (uint8_t *)fd.ptr + row * fd.stride + w;
+            if (kPack) *m = *p;
+            else *p = (uint8_t)*m;
+        } else {
+            uint32_t *p = (uint32_t *)fd.ptr + row * fd.stride + w;
+            if (kPack) *m = *p;
+            else *p = *m;
+        }
     }
 }
 
@@ -73,6 +79,7 @@ int check_spec(const RtsHaloSpec *s) {
     for (int f = 0; f < s->n_fields; ++f) {
         const RtsHaloField &fd = s->f[f];
         if (!fd.ptr || fd.words < 1 || fd.stride < fd.words || fd.msg_off < 0 ||
+            (fd.esize != 0 && fd.esize != 1 && fd.esize != 4) ||
             fd.msg_off + fd.words > s->msg_words)
             return (int)cudaErrorInvalidValue;
         words += fd.words;

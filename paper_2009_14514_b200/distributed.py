@@ -130,7 +130,7 @@ class Exchanger:
         self.compute_device = torch.device(device)
         self.device = torch.device(comm_device) if comm_device is not None else self.compute_device
 
-    def _sendrecv(self, send: dict, width: int) -> list:
+    def _sendrecv(self, send: dict, width: int, dtype=torch.float64) -> list:
         """send: {peer: rows}; returns received row blocks from every peer
         that has a matching entry in its own ``send`` (symmetric pattern)."""
         peers = sorted(send)
@@ -144,7 +144,7 @@ class Exchanger:
         if ops:  # no peers (a single slab): nothing to exchange
             for r in dist.batch_isend_irecv(ops):
                 r.wait()
-        bufs = {q: torch.empty((int(counts_in[q].item()), width), dtype=torch.float64,
+        bufs = {q: torch.empty((int(counts_in[q].item()), width), dtype=dtype,
                                device=self.device) for q in peers}
         ops = []
         for q in peers:
@@ -181,8 +181,10 @@ class SlabDriver:
     """Owns the rank's particles and runs the ghost / migrate protocol around
     a local step function ``local_step(fluid_state, gid) -> fluid_state``.
 
-    The local step is the B200 solver in production (``DistributedWcsph``);
-    the CPU tests plug the oracle in to check the protocol bit for bit.
+    ``SlabWcsph`` runs it around the oracle in the CPU tests (protocol
+    checked bit for bit); the B200 ranks run the same ownership / band rules
+    on resident rows (``_ResidentRank``) and use this class for the
+    partition bounds and the transport.
     """
 
     def __init__(self, part: SlabPartition, rank: int, device, fields=WCSPH_FIELDS,
@@ -259,12 +261,15 @@ def initial_ownership(scene: Scene, part: SlabPartition, rank: int):
     return gid, fluid, wall, wsel
 
 
-class DistributedWcsph:
-    """RTS-WCSPH over x-slabs: ``step()`` = ghost exchange, one B200 step on
-    owned + ghosts, extraction of the owned rows, migration."""
+class SlabWcsph:
+    """The x-slab protocol of RTS-WCSPH around any local step (the CPU tests
+    plug the oracle in): ``step()`` = ghost exchange, one local step on
+    owned + ghosts merged by global id, extraction of the owned rows,
+    migration.  The B200 ranks run the same protocol on resident rows
+    (``DistributedWcsph``)."""
 
-    def __init__(self, scene: Scene, mode: str = "rts", device=None, halo: int = 2,
-                 jitter=None, local=None, comm_device=None, velocity=None, **kw):
+    def __init__(self, scene: Scene, local, mode: str = "rts", device=None, halo: int = 2,
+                 jitter=None, comm_device=None, velocity=None):
         self.rank = dist.get_rank()
         self.world = dist.get_world_size()
         self.device = torch.device(device) if device is not None else torch.device("cuda")
@@ -276,9 +281,6 @@ class DistributedWcsph:
             comm_device = "cpu"
         self.driver = SlabDriver(self.part, self.rank, self.device, comm_device=comm_device)
         self.n_global = len(fluid)
-        if local is None:  # the B200 solver (graphs off: the particle count changes)
-            from .wcsph import WcsphSolver
-            local = WcsphSolver(scene, mode=mode, device=self.device, use_graphs=False, **kw)
         self.solver = local
         self.solver._set_local_particles(None, wall[wsel], capacity=None, init=True)
         self.gid = torch.as_tensor(gid, device=self.device)
@@ -458,12 +460,233 @@ class PcisphExchange:
         self._channels(s)["integrate"].run()
 
 
-class DistributedPcisph:
-    """RTS-PCISPH over x-slabs: ``advance()`` = migration and 6-column ghost
-    exchange at the major-step start (region expansion reaches 4 blocks,
-    smoothing 1 more), then one B200 major step whose correction loops
-    exchange the 2 inner ghost columns and all-reduce the convergence
-    scalars every iteration."""
+class RankRows:
+    """Full-row moves of a rank's resident fluid rows (pos, every state
+    field of the solver, and the global id kept in ``sort_key``) through
+    ``rts_halo_pack`` / ``rts_halo_unpack``: migrants out, arrivals and
+    ghosts in, hole filling -- no per-field host indexing, no re-sort."""
+
+    def __init__(self, solver):
+        self.s = solver
+        self._key = None
+
+    @staticmethod
+    def _layout(t: torch.Tensor, width: int) -> tuple[int, int, int]:
+        """(elements per row, element stride, element bytes) of a field."""
+        if t.element_size() == 8:
+            return 2 * width, 2 * width, 4
+        if t.element_size() == 4:
+            return width, width, 4
+        if t.element_size() == 1:
+            return width, width, 1
+        raise TypeError(f"unsupported field dtype {t.dtype}")
+
+    def spec(self):
+        from . import _native as N
+        s, A = self.s, self.s.arena
+        names = [("pos", 3)] + [(arena, w) for _, arena, w, *_ in s._FIELDS] + [("sort_key", 1)]
+        key = tuple(A[n].data_ptr() for n, _ in names)
+        if key != self._key:
+            fields, off = [], 0
+            for name, w in names:
+                words, stride, esize = self._layout(A[name], w)
+                fields.append((A[name], words, stride, esize, off))
+                off += words
+            sp = N.RtsHaloSpec()
+            sp.n_fields, sp.row_words, sp.msg_words = len(fields), off, off
+            for k, (t, words, stride, esize, o) in enumerate(fields):
+                f = sp.f[k]
+                f.ptr, f.remap = t.data_ptr(), None
+                f.words, f.stride, f.msg_off, f.esize = words, stride, o, esize
+            self._spec, self._words, self._key = sp, off, key
+        return self._spec
+
+    @property
+    def words(self) -> int:
+        self.spec()
+        return self._words
+
+    def pack(self, rows: torch.Tensor) -> torch.Tensor:
+        from . import _native as N
+        sp = self.spec()
+        out = torch.empty((rows.numel(), self.words), dtype=torch.int32, device=rows.device)
+        if rows.numel():
+            r = rows.to(torch.int32).contiguous()
+            N.call("rts_halo_pack", ctypes.byref(sp), r.data_ptr(), r.numel(), out.data_ptr(),
+                   torch.cuda.current_stream(rows.device).cuda_stream)
+        return out
+
+    def unpack(self, rows: torch.Tensor, msg: torch.Tensor) -> None:
+        from . import _native as N
+        if not rows.numel():
+            return
+        sp = self.spec()
+        r = rows.to(torch.int32).contiguous()
+        m = msg.to(rows.device, torch.int32).contiguous()
+        N.call("rts_halo_unpack", ctypes.byref(sp), r.data_ptr(), r.numel(), m.data_ptr(),
+               torch.cuda.current_stream(rows.device).cuda_stream)
+
+
+class _ResidentRank:
+    """Resident rank rows: the solver's fluid rows are [owned | ghosts].
+    Migrants leave by hole filling; arrivals and the ghost band are unpacked
+    behind the owned rows -- each phase one native pack, one grouped
+    send/recv (count first) and one native unpack.  Row order is free: the
+    grid sort orders every block's fluid run by global id (``sort_key``),
+    so every neighbour row and pair sum is the single-domain one."""
+
+    def _init_rows(self, gid: np.ndarray, state: dict, halo: int) -> None:
+        s = self.solver
+        fx = state["pos"][:, 0].double().cpu().numpy()
+        bx = self.part.block_x(fx) if len(gid) else np.zeros(0, dtype=np.int64)
+        lo, hi = self.driver.lo, self.driver.hi
+        band = int(((bx < lo + halo) | (bx >= hi - halo)).sum())
+        s._set_local_particles(state, None, capacity=int(1.25 * (len(gid) + 2 * band)) + 4096)
+        self._alloc_key()
+        s.arena["sort_key"][:len(gid)] = torch.as_tensor(gid, dtype=torch.int32, device=self.device)
+        self.rows = RankRows(s)
+        self.n_own = len(gid)
+
+    def _alloc_key(self) -> None:
+        A = self.solver.arena
+        cap = self.solver._cap
+        if "sort_key" not in A.t or A["sort_key"].numel() < cap:
+            old = A.t.get("sort_key")
+            k = A.alloc("sort_key", (cap,), torch.int32, 0)
+            if old is not None:
+                k[:old.numel()] = old
+
+    @property
+    def gid(self) -> torch.Tensor:
+        return self.solver.arena["sort_key"][:self.n_own].long()
+
+    @property
+    def state(self) -> dict:
+        """Views of the owned rows (writable in place)."""
+        out = self.solver._get_local_state()
+        return {k: v[:self.n_own] for k, v in out.items()}
+
+    @property
+    def n_owned(self) -> int:
+        return self.n_own
+
+    def _resize(self, nf: int, n_ghost: int) -> None:
+        s = self.solver
+        if nf > s._cap:  # grow, keeping the current rows (rare)
+            keep = {k: v.clone() for k, v in s._get_local_state().items()}
+            key = s.arena["sort_key"][:s.n_fluid].clone()
+            s._set_local_particles(keep, None, capacity=int(1.25 * nf) + 4096)
+            self._alloc_key()
+            s.arena["sort_key"][:key.numel()] = key
+            self.rows._key = None
+        s._resize_fluid(nf, n_ghost)
+
+    def _exchange_rows(self, send: dict) -> torch.Tensor:
+        """Rows packed per peer -> the received rows, concatenated in peer order."""
+        packed = {q: self.rows.pack(idx) for q, idx in send.items()}
+        recv = self.x._sendrecv(packed, self.rows.words, torch.int32)
+        recv = [r for r in recv if r.shape[0]]
+        if not recv:
+            return torch.zeros((0, self.rows.words), dtype=torch.int32, device=self.device)
+        return torch.cat(recv) if len(recv) > 1 else recv[0]
+
+    def _migrate(self) -> None:
+        """Owned rows whose block column left the slab go to the neighbour."""
+        s, n = self.solver, self.n_own
+        own = self.part.owner(self.part.block_x(s.arena["pos"][:n, 0]))
+        leave = own != self.rank
+        far = (own - self.rank).abs() > 1
+        n_far, n_leave = torch.stack([far.sum(), leave.sum()]).tolist()  # one host sync
+        if n_far:
+            raise RuntimeError("a particle crossed more than one slab in one step")
+        arr = self._exchange_rows({q: torch.nonzero(own == q).reshape(-1)
+                                   for q in self.x.neighbours()})
+        n_keep = n - n_leave
+        if n_leave:  # fill the holes below n_keep with the kept rows above it
+            holes = torch.nonzero(leave[:n_keep]).reshape(-1)
+            fill = torch.nonzero(~leave[n_keep:]).reshape(-1) + n_keep
+            if holes.numel():
+                self.rows.unpack(holes, self.rows.pack(fill))
+        self._resize(n_keep + arr.shape[0], 0)
+        self.rows.unpack(torch.arange(n_keep, n_keep + arr.shape[0], device=self.device), arr)
+        self.n_own = n_keep + arr.shape[0]
+
+    def _ghosts(self) -> None:
+        """Owned rows in the ``halo`` block columns next to each neighbour are
+        copied to it; the received ones become this rank's ghost rows."""
+        s, n = self.solver, self.n_own
+        bx = self.part.block_x(s.arena["pos"][:n, 0])
+        lo, hi, h = self.driver.lo, self.driver.hi, self.part.halo
+        send = {}
+        for q in self.x.neighbours():
+            m = bx < lo + h if q < self.rank else bx >= hi - h
+            send[q] = torch.nonzero(m).reshape(-1)
+        g = self._exchange_rows(send)
+        self._resize(n + g.shape[0], g.shape[0])
+        self.rows.unpack(torch.arange(n, n + g.shape[0], device=self.device), g)
+
+
+class DistributedWcsph(_ResidentRank):
+    """RTS-WCSPH over x-slabs on the B200: ``step()`` = migration and a fresh
+    2-column ghost band on resident rows (the first band's densities need
+    the second band's positions, its smoothed levels the second band's raw
+    levels), then one B200 step on owned + ghosts; the ghosts are recomputed
+    redundantly and dropped, so there is no exchange inside the step.  Owned
+    results are bit-identical to the single-domain run.  The baseline's CFL
+    bound is an all-reduce MAX of |F|."""
+
+    def __init__(self, scene: Scene, mode: str = "rts", device=None, halo: int = 2,
+                 jitter=None, comm_device=None, velocity=None, **kw):
+        from .wcsph import WcsphSolver
+        self.rank = dist.get_rank()
+        self.world = dist.get_world_size()
+        self.device = torch.device(device) if device is not None else torch.device("cuda")
+        self.part = SlabPartition.for_scene(scene, "wcsph", self.world, halo)
+        gid, fluid, wall, wsel = initial_ownership(scene, self.part, self.rank)
+        if jitter is not None:
+            fluid = (fluid + jitter).astype(np.float32).astype(np.float64)
+        if comm_device is None and dist.get_backend() == "gloo":
+            comm_device = "cpu"
+        self.driver = SlabDriver(self.part, self.rank, self.device, comm_device=comm_device)
+        self.x = self.driver.x
+        self.n_global = len(fluid)
+        # graphs off: the particle count changes every step
+        s = self.solver = WcsphSolver(scene, mode=mode, device=self.device, use_graphs=False, **kw)
+        s._set_local_particles(None, wall[wsel], capacity=None, init=True)
+        s._reduce_max = self._all_max
+        fl = torch.as_tensor(fluid[gid].astype(np.float32), device=self.device)
+        st = s._fresh_state(fl)
+        if velocity is not None:  # (n_global, 3) initial velocities by global id
+            st["vel"] = torch.as_tensor(np.asarray(velocity)[gid], device=self.device,
+                                        dtype=st["vel"].dtype)
+        self._init_rows(gid, st, halo)
+        self.sim_time = 0.0
+        self.step_index = 0
+
+    def _all_max(self, v: float) -> float:
+        t = torch.tensor([v], dtype=torch.float64, device=self.x.device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def step(self):
+        s = self.solver
+        self._ghosts()
+        st = s.step()
+        n_own = self.n_own
+        st.n_compute = int(s.compute[:n_own].sum())  # owned particles only
+        s._resize_fluid(n_own)  # drop the ghost rows
+        self._migrate()
+        self.sim_time += st.dt
+        self.step_index += 1
+        return st
+
+
+class DistributedPcisph(_ResidentRank):
+    """RTS-PCISPH over x-slabs: at every major step migration and a fresh
+    6-column ghost band (fast-region expansion reaches 4 blocks, smoothing 1
+    more) on resident rows (``_ResidentRank``); the major step's correction
+    loops then exchange the 2 inner ghost columns and fold the convergence
+    scalars every iteration (``PcisphExchange``)."""
 
     def __init__(self, scene: Scene, device=None, halo: int = 6, inner: int = 2, jitter=None,
                  comm_device=None, velocity=None, **kw):
@@ -480,61 +703,53 @@ class DistributedPcisph:
             comm_device = "cpu"
         self.driver = SlabDriver(self.part, self.rank, self.device, fields=PCISPH_FIELDS,
                                  comm_device=comm_device)
+        self.x = self.driver.x
         self.n_global = len(fluid)
-        self.solver = PcisphSolver(scene, mode="rts", device=self.device, use_graphs=False, **kw)
-        self.solver._set_local_particles(None, wall[wsel], init=True)
-        self.solver.params.n_global = self.n_global
-        self.gid = torch.as_tensor(gid, device=self.device)
+        s = self.solver = PcisphSolver(scene, mode="rts", device=self.device, use_graphs=False,
+                                       **kw)
+        s._set_local_particles(None, wall[wsel], init=True)
+        s.params.n_global = self.n_global
         fl = torch.as_tensor(fluid[gid].astype(np.float32), device=self.device)
-        st = self.solver._fresh_state(fl)
+        st = s._fresh_state(fl)
         st["xstar"] = fl.clone()
         if velocity is not None:  # (n_global, 3) initial velocities by global id
             st["vel"] = torch.as_tensor(np.asarray(velocity)[gid], device=self.device,
                                         dtype=st["vel"].dtype)
-        self.state = st
+        self._init_rows(gid, st, halo)
         self.sim_time = 0.0
         self.step_index = 0
 
-    @property
-    def n_owned(self) -> int:
-        return int(self.gid.numel())
-
-    def _lists(self, allg, merged, owned):
-        bx = self.part.block_x(merged["pos"][:, 0])
+    def _lists(self):
+        s = self.solver
+        bx = self.part.block_x(s.arena["pos"][:s.n_fluid, 0])
+        owned = torch.zeros(s.n_fluid, dtype=torch.bool, device=self.device)
+        owned[:self.n_own] = True
         lo, hi = self.driver.lo, self.driver.hi
         send, recv = {}, {}
-        for q in self.driver.x.neighbours():
+        for q in self.x.neighbours():
             if q < self.rank:
-                s = owned & (bx < lo + self.inner)
-                r = (~owned) & (bx >= lo - self.inner) & (bx < lo)
+                sm = owned & (bx < lo + self.inner)
+                rm = (~owned) & (bx >= lo - self.inner) & (bx < lo)
             else:
-                s = owned & (bx >= hi - self.inner)
-                r = (~owned) & (bx >= hi) & (bx < hi + self.inner)
-            send[q] = torch.nonzero(s).reshape(-1)
-            recv[q] = torch.nonzero(r).reshape(-1)
+                sm = owned & (bx >= hi - self.inner)
+                rm = (~owned) & (bx >= hi) & (bx < hi + self.inner)
+            send[q] = torch.nonzero(sm).reshape(-1)
+            recv[q] = torch.nonzero(rm).reshape(-1)
         return send, recv
 
     def advance(self):
         s = self.solver
-        self.gid, self.state = self.driver.migrate(self.gid, self.state)
-        self.state = s._cast_state(self.state)
-        ggid, gstate = self.driver.ghost_rows(self.gid, self.state)
-        allg, merged, owned = self.driver.merged(self.gid, self.state, ggid, gstate)
-        merged = s._cast_state(merged)
-        s._set_local_particles(merged, None, ghost=~owned)
+        self._migrate()
+        self._ghosts()
         s.params.n_global = self.n_global
-        send, recv = self._lists(allg, merged, owned)
+        send, recv = self._lists()
         s._xch = PcisphExchange(self.driver, send, recv)
         try:
             rows = s.major_step()
         finally:
             s._xch = None
-        out = s._get_local_state()
-        idx = torch.nonzero(owned).reshape(-1)
-        self.state = {k: v[idx] for k, v in out.items()}
-        self.gid = allg[idx]
         nref = torch.tensor([r.n_compute for r in rows], dtype=torch.float64,
-                            device=self.driver.x.device)
+                            device=self.x.device)
         if len(rows):
             dist.all_reduce(nref)
         for r, n in zip(rows, nref.tolist()):

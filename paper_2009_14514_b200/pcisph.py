@@ -170,6 +170,16 @@ class PcisphSolver(_DeviceSolver):
         self.params.n_fluid = nf
         N.call("rts_pci_walls", self.params, self.arena.buf, self._stream().cuda_stream)
 
+    def _resize_fluid(self, nf: int, n_ghost: int = 0) -> None:
+        super()._resize_fluid(nf)
+        self.cnt = self.arena["cnt"][:nf]
+        g = self.arena["ghost"]
+        g.zero_()
+        if n_ghost:
+            g[nf - n_ghost:nf] = 1
+        self.params.n_ghost = n_ghost
+        N.call("rts_pci_walls", self.params, self.arena.buf, self._stream().cuda_stream)
+
     def __init__(self, scene: Scene, mode: str = "rts", dt: float | None = None,
                  schedule=DEFAULT_SCHEDULE, pin_region: int | None = None,
                  audit_neighbors: bool = False, iteration_cap: int = 24,

@@ -220,6 +220,22 @@ class _DeviceSolver:
         p.n_bound = nb
         p.n_bcells = self.grid.n_bcells
 
+    def _resize_fluid(self, nf: int, n_ghost: int = 0) -> None:
+        """Resident x-slab ranks (distributed.py): n_fluid = nf with the rows
+        [0, nf) left where they are (no copy); the wall rows move behind
+        them.  The caller fills any new rows."""
+        if nf > self._cap:
+            raise ValueError(f"{nf} fluid rows exceed the capacity {self._cap}")
+        nb = self.n_bound
+        self._pos[nf:nf + nb].copy_(self._walls)
+        A = self.arena
+        self.n_fluid = nf
+        for name, arena, *_ in self._FIELDS:
+            setattr(self, name, A[arena][:nf])
+        self.grid.n_fluid = nf
+        self.grid.shift_boundary(nf)
+        self.params.n_fluid = nf
+
     def _realloc_extra(self, cap: int, nb: int) -> None:
         """Solver-specific buffers sized by the particle capacity."""
 
@@ -325,14 +341,17 @@ class WcsphSolver(_DeviceSolver):
         eq2 = sc.lambda_f * math.sqrt(r * self.mass / f_max) if f_max > 0.0 else math.inf
         return min(eq1, eq2)
 
+    _reduce_max = None  # x-slab ranks: all-reduce MAX across ranks (distributed.py)
+
     def _force_max(self) -> float:
         if not self.n_fluid:
-            return 0.0
+            return self._reduce_max(0.0) if self._reduce_max is not None else 0.0
         stream = torch.cuda.current_stream(self.device)
         self.counters.reset(stream)
         N.call("rts_force_max", self.params, self.arena.buf, stream.cuda_stream)
         c = self.counters.read(stream)
-        return float(np.array([c.fmax_bits], dtype=np.uint64).view(np.float64)[0])
+        f = float(np.array([c.fmax_bits], dtype=np.uint64).view(np.float64)[0])
+        return self._reduce_max(f) if self._reduce_max is not None else f
 
     def particle_regions(self) -> torch.Tensor:
         if self.mode == "rts":

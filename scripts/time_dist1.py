@@ -36,23 +36,13 @@ print(f"host-driven major_step only: {(time.perf_counter() - t0) / K * 1e3:.2f} 
 def timed(f, *a):
     torch.cuda.synchronize(); t = time.perf_counter(); r = f(*a); torch.cuda.synchronize()
     return r, (time.perf_counter() - t) * 1e3
-s = d.solver
+from paper_2009_14514_b200.distributed import PcisphExchange
 T = {}
 for _ in range(5):
-    (d.gid, d.state), T["migrate"] = timed(d.driver.migrate, d.gid, d.state)
-    d.state, T["cast"] = timed(s._cast_state, d.state)
-    (ggid, gstate), T["ghost_rows"] = timed(d.driver.ghost_rows, d.gid, d.state)
-    (allg, merged, owned), T["merged"] = timed(d.driver.merged, d.gid, d.state, ggid, gstate)
-    merged, T["cast2"] = timed(s._cast_state, merged)
-    _, T["set_local"] = timed(s._set_local_particles, merged, None, None, False, ~owned)
-    (send, recv), T["lists"] = timed(d._lists, allg, merged, owned)
-    from paper_2009_14514_b200.distributed import PcisphExchange
+    _, T["migrate"] = timed(d._migrate)
+    _, T["ghosts"] = timed(d._ghosts)
+    (send, recv), T["lists"] = timed(d._lists)
     s._xch = PcisphExchange(d.driver, send, recv)
     rows, T["major"] = timed(s.major_step)
     s._xch = None
-    out, T["get_local"] = timed(s._get_local_state)
-    def ext():
-        idx = torch.nonzero(owned).reshape(-1)
-        return {k: v[idx] for k, v in out.items()}, allg[idx]
-    (d.state, d.gid), T["extract"] = timed(ext)
 print({k: round(v, 2) for k, v in T.items()})

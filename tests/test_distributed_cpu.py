@@ -89,12 +89,11 @@ def _worker(rank, world, port, steps, q):
     try:
         import sys
         sys.path.insert(0, ROOT)
-        from paper_2009_14514_b200.distributed import DistributedWcsph
+        from paper_2009_14514_b200.distributed import SlabWcsph
         from paper_2009_14514_b200.scene import seed_particles
         sc = _scene()
         nf = len(seed_particles(sc)[0])
-        d = DistributedWcsph(sc, mode="rts", device="cpu", local=OracleLocal(sc),
-                             jitter=_jitter(nf))
+        d = SlabWcsph(sc, OracleLocal(sc), mode="rts", device="cpu", jitter=_jitter(nf))
         ncomp = []
         for _ in range(steps):
             st = d.step()
