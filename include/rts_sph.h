@@ -389,13 +389,36 @@ typedef struct {
     RtsHaloField f[RTS_HALO_MAX_FIELDS];
 } RtsHaloSpec;
 /* out[r * msg_words + f.msg_off + w] = word w of field f of row rows[r]
- * (r < n), bit copies (fp64 fields travel as two words). */
+ * (r < n), bit copies (fp64 fields travel as two words); rows[r] < 0 is a
+ * padding entry (skipped, here and in rts_halo_unpack). */
 int rts_halo_pack(const RtsHaloSpec *s, const int32_t *rows, int64_t n, uint32_t *out,
                   void *stream);
 /* Inverse of rts_halo_pack: word w of field f of row rows[r] =
  * in[r * msg_words + f.msg_off + w]. */
 int rts_halo_unpack(const RtsHaloSpec *s, const int32_t *rows, int64_t n, const uint32_t *in,
                     void *stream);
+/* Slab geometry of one rank (block columns along x of the padded grid). */
+typedef struct {
+    double origin_x, inv_block;   /* grid.py:225-229 */
+    int32_t nx;                   /* block columns of the whole grid */
+    int32_t lo, hi;               /* owned columns [lo, hi) */
+    int32_t halo;                 /* ghost band width in columns */
+    int32_t has_left, has_right;  /* neighbour ranks exist */
+    int32_t left_lo, right_hi;    /* owned range of the neighbours: [left_lo, lo), [hi, right_hi) */
+} RtsSlabGeom;
+/* Rows [0, n) of pos (fp32, stride 3), block column as grid.py:248-250, into
+ * six lists (row stride list_stride >= n; order free): 0/1 migrants to the
+ * left/right neighbour, 2/3 kept rows in the band next to the left/right
+ * neighbour, 4/5 migrants inside that neighbour's band next to this slab;
+ * leave[i] = 1 for migrants; counts[0..5] list lengths, counts[6] rows
+ * beyond a neighbour's slab (an error for the caller). */
+int rts_slab_classify(const RtsSlabGeom *g, const float *pos, int n, int32_t *lists,
+                      int64_t list_stride, uint8_t *leave, int32_t *counts, void *stream);
+/* Hole-filling plan after migration: holes = rows < n_keep with leave set,
+ * fill = rows >= n_keep without (equal counts), both lists -1-padded to
+ * n_pad entries (rts_halo_pack / unpack skip rows < 0). */
+int rts_slab_holes(const uint8_t *leave, int n, int n_keep, int n_pad, int32_t *holes,
+                   int32_t *fill, int32_t *counter, void *stream);
 /* out[0..3] = (max_err, any_se, sum_rho, n_pred) of ctr, as fp64. */
 int rts_ctl_publish(const RtsBuffers *b, double *out, void *stream);
 /* ctr = fold of the all-gathered (world, 4) publish rows: MAX of max_err /

@@ -95,6 +95,12 @@ class RtsHaloField(_c.Structure):
                 ("esize", _I)]
 
 
+class RtsSlabGeom(_c.Structure):
+    _fields_ = [("origin_x", _D), ("inv_block", _D), ("nx", _I), ("lo", _I), ("hi", _I),
+                ("halo", _I), ("has_left", _I), ("has_right", _I), ("left_lo", _I),
+                ("right_hi", _I)]
+
+
 class RtsHaloSpec(_c.Structure):
     _fields_ = [("n_fields", _I), ("row_words", _I), ("msg_words", _I), ("pad", _I),
                 ("f", RtsHaloField * HALO_MAX_FIELDS)]
@@ -150,6 +156,8 @@ SIGNATURES = {
     "rts_halo_pack": [_c.POINTER(RtsHaloSpec), _P, _c.c_int64, _P, _P],
     "rts_halo_unpack": [_c.POINTER(RtsHaloSpec), _P, _c.c_int64, _P, _P],
     "rts_ctl_publish": [_PB, _P, _P],
+    "rts_slab_classify": [_c.POINTER(RtsSlabGeom), _P, _c.c_int, _P, _c.c_int64, _P, _P, _P],
+    "rts_slab_holes": [_P, _c.c_int, _c.c_int, _c.c_int, _P, _P, _P, _P],
     "rts_ctl_fold": [_PB, _P, _c.c_int, _P],
 }
 

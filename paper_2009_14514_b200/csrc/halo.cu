@@ -34,6 +34,7 @@ k_halo(const RtsHaloSpec s, const int32_t *__restrict__ rows, long long n,
         while (f < s.n_fields - 1 && w >= s.f[f].words) w -= s.f[f++].words;
         const RtsHaloField &fd = s.f[f];
         long long row = rows[r];
+        if (row < 0) continue;  // padding entry (hole-filling plans)
         if (fd.remap) row = fd.remap[row];
         uint32_t *m = msg + r * s.msg_words + fd.msg_off + w;
         if (fd.esize == 1) {  // byte elements (int8 / bool fields): one per word
@@ -71,6 +72,53 @@ __global__ void k_ctl_fold(RtsCounters *__restrict__ c, const double *__restrict
     c->any_se = (int32_t)se;
     c->sum_rho = sr;
     c->n_pred = (int32_t)np_;
+}
+
+// Slab bookkeeping of a rank's owned rows [0, n) in one pass: block column
+// bx = floor((x - origin_x) * inv_block) clipped to [0, nx) (the fp64
+// expression of grid.py:248-250), then six row lists (order free: the grid
+// sort orders block runs by global id):
+//   0 / 1  migrants to the left / right neighbour (bx left the slab),
+//   2 / 3  kept rows in the band of `halo` columns next to the left / right
+//          neighbour (its ghosts),
+//   4 / 5  migrants inside the neighbour's band next to this slab (they stay
+//          here as ghosts: the neighbour would send them straight back);
+// counts[6] = rows beyond a neighbour's slab (more than one slab per step).
+__global__ void k_slab_classify(const RtsSlabGeom g, const float *__restrict__ pos, int n,
+                                int32_t *__restrict__ lists, long long ls,
+                                uint8_t *__restrict__ leave, int32_t *__restrict__ counts) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const double v = floor(__dmul_rn(__dsub_rn((double)pos[3 * i], g.origin_x), g.inv_block));
+        const int bx = !(v >= 0.0) ? 0 : (v >= (double)(g.nx - 1) ? g.nx - 1 : (int)v);
+        uint8_t lv = 0;
+        if (bx < g.lo) {
+            if (!g.has_left || bx < g.left_lo) { atomicAdd(&counts[6], 1); continue; }
+            lists[0 * ls + atomicAdd(&counts[0], 1)] = i;
+            if (bx >= g.lo - g.halo) lists[4 * ls + atomicAdd(&counts[4], 1)] = i;
+            lv = 1;
+        } else if (bx >= g.hi) {
+            if (!g.has_right || bx >= g.right_hi) { atomicAdd(&counts[6], 1); continue; }
+            lists[1 * ls + atomicAdd(&counts[1], 1)] = i;
+            if (bx < g.hi + g.halo) lists[5 * ls + atomicAdd(&counts[5], 1)] = i;
+            lv = 1;
+        } else {
+            if (g.has_left && bx < g.lo + g.halo) lists[2 * ls + atomicAdd(&counts[2], 1)] = i;
+            if (g.has_right && bx >= g.hi - g.halo) lists[3 * ls + atomicAdd(&counts[3], 1)] = i;
+        }
+        leave[i] = lv;
+    }
+}
+
+// hole-filling plan: holes = leaving rows below n_keep, fill = kept rows at
+// or above it (equal counts, paired in any order); the lists are pre-set to
+// -1 (skipped by pack / unpack) up to the caller's bound
+__global__ void k_slab_holes(const uint8_t *__restrict__ leave, int n, int n_keep,
+                             int32_t *__restrict__ holes, int32_t *__restrict__ fill,
+                             int32_t *__restrict__ counter) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        if (i < n_keep && leave[i]) holes[atomicAdd(&counter[0], 1)] = i;
+        if (i >= n_keep && !leave[i]) fill[atomicAdd(&counter[1], 1)] = i;
+    }
 }
 
 int check_spec(const RtsHaloSpec *s) {
@@ -124,6 +172,35 @@ int rts_ctl_fold(const RtsBuffers *b, const double *gathered, int world, void *s
     if (world < 1) return (int)cudaErrorInvalidValue;
     rts_note_launch();
     k_ctl_fold<<<1, 1, 0, (cudaStream_t)stream>>>(b->ctr, gathered, world);
+    RTS_LAUNCH_CHECK();
+    return 0;
+}
+
+int rts_slab_classify(const RtsSlabGeom *g, const float *pos, int n, int32_t *lists,
+                      int64_t list_stride, uint8_t *leave, int32_t *counts, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e = cudaMemsetAsync(counts, 0, 8 * sizeof(int32_t), st);
+    if (e != cudaSuccess) return (int)e;
+    if (n <= 0) return 0;
+    if (list_stride < n) return (int)cudaErrorInvalidValue;
+    rts_note_launch();
+    k_slab_classify<<<rts_blocks(n, kThreads), kThreads, 0, st>>>(*g, pos, n, lists, list_stride,
+                                                                   leave, counts);
+    RTS_LAUNCH_CHECK();
+    return 0;
+}
+
+int rts_slab_holes(const uint8_t *leave, int n, int n_keep, int n_pad, int32_t *holes,
+                   int32_t *fill, int32_t *counter, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n_pad <= 0) return 0;
+    cudaError_t e;
+    if ((e = cudaMemsetAsync(holes, 0xff, (size_t)n_pad * 4, st)) != cudaSuccess) return (int)e;
+    if ((e = cudaMemsetAsync(fill, 0xff, (size_t)n_pad * 4, st)) != cudaSuccess) return (int)e;
+    if ((e = cudaMemsetAsync(counter, 0, 2 * sizeof(int32_t), st)) != cudaSuccess) return (int)e;
+    rts_note_launch();
+    k_slab_holes<<<rts_blocks(n, kThreads), kThreads, 0, st>>>(leave, n, n_keep, holes, fill,
+                                                              counter);
     RTS_LAUNCH_CHECK();
     return 0;
 }

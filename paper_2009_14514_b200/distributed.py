@@ -506,10 +506,11 @@ class RankRows:
         self.spec()
         return self._words
 
-    def pack(self, rows: torch.Tensor) -> torch.Tensor:
+    def pack(self, rows: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         from . import _native as N
         sp = self.spec()
-        out = torch.empty((rows.numel(), self.words), dtype=torch.int32, device=rows.device)
+        if out is None:
+            out = torch.empty((rows.numel(), self.words), dtype=torch.int32, device=rows.device)
         if rows.numel():
             r = rows.to(torch.int32).contiguous()
             N.call("rts_halo_pack", ctypes.byref(sp), r.data_ptr(), r.numel(), out.data_ptr(),
@@ -589,6 +590,101 @@ class _ResidentRank:
         if not recv:
             return torch.zeros((0, self.rows.words), dtype=torch.int32, device=self.device)
         return torch.cat(recv) if len(recv) > 1 else recv[0]
+
+    def _single_round(self) -> bool:
+        """Migration and the ghost band fit one exchange round when every slab
+        is wider than halo + 1 columns: an arrival (it moved less than one
+        column) can then never land in the band next to the *other*
+        neighbour, so a rank's post-migration band = its kept band rows plus
+        the migrants it just received from that same neighbour -- which the
+        neighbour keeps as ghosts itself (lists 4 / 5 of rts_slab_classify)."""
+        if not hasattr(self, "_one_round"):
+            widths = [b - a for a, b in (self.part.bounds(r) for r in range(self.world))]
+            self._one_round = min(widths) > self.part.halo + 1
+        return self._one_round
+
+    def _exchange(self) -> None:
+        """Migration + fresh ghost band (one round when ``_single_round``)."""
+        if not self._single_round():
+            self._migrate()
+            self._ghosts()
+            return
+        from . import _native as N
+        s, n, dev = self.solver, self.n_own, self.device
+        st = torch.cuda.current_stream(dev).cuda_stream
+        part, r = self.part, self.rank
+        lo, hi = part.bounds(r)
+        g = N.RtsSlabGeom(origin_x=part.origin_x, inv_block=part.inv_block, nx=part.nx, lo=lo,
+                          hi=hi, halo=part.halo, has_left=int(r > 0),
+                          has_right=int(r < self.world - 1),
+                          left_lo=part.bounds(r - 1)[0] if r > 0 else lo,
+                          right_hi=part.bounds(r + 1)[1] if r < self.world - 1 else hi)
+        ls = max(n, 1)
+        lists = torch.empty((6, ls), dtype=torch.int32, device=dev)
+        leave = torch.empty(ls, dtype=torch.uint8, device=dev)
+        counts = torch.empty(8, dtype=torch.int32, device=dev)
+        N.call("rts_slab_classify", ctypes.byref(g), s.arena["pos"].data_ptr(), n,
+               lists.data_ptr(), ls, leave.data_ptr(), counts.data_ptr(), st)
+        c = counts.tolist()  # one host sync: the message sizes
+        if c[6]:
+            raise RuntimeError("a particle crossed more than one slab in one step")
+        W = self.rows.words
+        send, keepg = {}, []
+        for q, (mig, band, selfg) in ((r - 1, (0, 2, 4)), (r + 1, (1, 3, 5))):
+            if not 0 <= q < self.world:
+                continue
+            nm, nb = c[mig], c[band]
+            buf = torch.empty((nm + nb, W), dtype=torch.int32, device=dev)
+            self.rows.pack(lists[mig, :nm], buf[:nm])
+            self.rows.pack(lists[band, :nb], buf[nm:])
+            send[q] = (nm, buf)
+            keepg.append(lists[selfg, :c[selfg]])
+        selfg = self.rows.pack(torch.cat(keepg)) if keepg else None
+        recv = self._sendrecv_split(send)
+        n_leave = c[0] + c[1]
+        n_keep = n - n_leave
+        if n_leave:  # fill the holes below n_keep with the kept rows above it
+            plan = torch.empty((2, n_leave), dtype=torch.int32, device=dev)
+            N.call("rts_slab_holes", leave.data_ptr(), n, n_keep, n_leave, plan[0].data_ptr(),
+                   plan[1].data_ptr(), counts.data_ptr(), st)
+            self.rows.unpack(plan[0], self.rows.pack(plan[1]))
+        arr = [m[:k] for k, m in recv]
+        gh = [m[k:] for k, m in recv] + ([selfg] if selfg is not None else [])
+        arr = torch.cat(arr) if arr else torch.zeros((0, W), dtype=torch.int32, device=dev)
+        gh = torch.cat(gh) if gh else torch.zeros((0, W), dtype=torch.int32, device=dev)
+        n_own = n_keep + arr.shape[0]
+        self._resize(n_own + gh.shape[0], gh.shape[0])
+        self.rows.unpack(torch.arange(n_keep, n_own, device=dev), arr)
+        self.rows.unpack(torch.arange(n_own, n_own + gh.shape[0], device=dev), gh)
+        self.n_own = n_own
+
+    def _sendrecv_split(self, send: dict) -> list:
+        """send {peer: (n_first, rows)} -> [(n_first, rows)] per peer: the row
+        counts of both parts travel first (one int64 pair per peer)."""
+        x, dev = self.x, self.x.device
+        peers = sorted(send)
+        cout = {q: torch.tensor([send[q][0], send[q][1].shape[0]], dtype=torch.int64, device=dev)
+                for q in peers}
+        cin = {q: torch.zeros(2, dtype=torch.int64, device=dev) for q in peers}
+        ops = []
+        for q in peers:
+            ops += [dist.P2POp(dist.isend, cout[q], q), dist.P2POp(dist.irecv, cin[q], q)]
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        sizes = {q: cin[q].tolist() for q in peers}
+        bufs = {q: torch.empty((sizes[q][1], self.rows.words), dtype=torch.int32, device=dev)
+                for q in peers}
+        ops = []
+        for q in peers:
+            if send[q][1].shape[0]:
+                ops.append(dist.P2POp(dist.isend, send[q][1].to(dev).contiguous(), q))
+            if bufs[q].shape[0]:
+                ops.append(dist.P2POp(dist.irecv, bufs[q], q))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        return [(sizes[q][0], bufs[q].to(self.device)) for q in peers]
 
     def _migrate(self) -> None:
         """Owned rows whose block column left the slab go to the neighbour."""
@@ -670,12 +766,11 @@ class DistributedWcsph(_ResidentRank):
 
     def step(self):
         s = self.solver
-        self._ghosts()
+        self._exchange()  # migration of the last step's leavers + fresh ghosts
         st = s.step()
         n_own = self.n_own
         st.n_compute = int(s.compute[:n_own].sum())  # owned particles only
         s._resize_fluid(n_own)  # drop the ghost rows
-        self._migrate()
         self.sim_time += st.dt
         self.step_index += 1
         return st
@@ -733,14 +828,18 @@ class DistributedPcisph(_ResidentRank):
             else:
                 sm = owned & (bx >= hi - self.inner)
                 rm = (~owned) & (bx >= hi) & (bx < hi + self.inner)
-            send[q] = torch.nonzero(sm).reshape(-1)
-            recv[q] = torch.nonzero(rm).reshape(-1)
+            # both sides list the rows in global-id order: a rank's local row
+            # order is free (hole filling, arrivals, ghosts in message order)
+            send[q] = self._by_gid(torch.nonzero(sm).reshape(-1))
+            recv[q] = self._by_gid(torch.nonzero(rm).reshape(-1))
         return send, recv
+
+    def _by_gid(self, idx: torch.Tensor) -> torch.Tensor:
+        return idx[torch.argsort(self.solver.arena["sort_key"][idx])]
 
     def advance(self):
         s = self.solver
-        self._migrate()
-        self._ghosts()
+        self._exchange()
         s.params.n_global = self.n_global
         send, recv = self._lists()
         s._xch = PcisphExchange(self.driver, send, recv)

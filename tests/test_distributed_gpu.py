@@ -18,10 +18,10 @@ from conftest import ROOT
 pytestmark = pytest.mark.gpu
 
 
-def _scene():
+def _scene(width=0.6):
     from paper_2009_14514_b200 import Scene
-    return Scene(domain_min=(0, 0, 0), domain_max=(0.6, 0.3, 0.2),
-                 fluid_boxes=(((0.0, 0.0, 0.0), (0.5, 0.2, 0.2)),), spacing=0.02)
+    return Scene(domain_min=(0, 0, 0), domain_max=(width, 0.3, 0.2),
+                 fluid_boxes=(((0.0, 0.0, 0.0), (width - 0.1, 0.2, 0.2)),), spacing=0.02)
 
 
 def _jitter(n, s=0.02):
@@ -33,7 +33,7 @@ def _collect(q, procs, n=2):
     once (the other rank is then stuck in a collective and is terminated)."""
     res = []
     for _ in range(n):
-        r = q.get(timeout=600)
+        r = q.get(timeout=300)
         if r[0] == "error":
             for p in procs:
                 p.kill()
@@ -42,7 +42,7 @@ def _collect(q, procs, n=2):
     return res
 
 
-def _worker(rank, world, port, steps, q):
+def _worker(rank, world, port, steps, q, drift=0.0):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -53,28 +53,38 @@ def _worker(rank, world, port, steps, q):
         from paper_2009_14514_b200.scene import seed_particles
         sc = _scene()
         nf = len(seed_particles(sc)[0])
-        d = DistributedWcsph(sc, mode="rts", device="cuda:0", jitter=_jitter(nf))
+        vel = np.zeros((nf, 3))
+        vel[:, 0] = drift
+        d = DistributedWcsph(sc, mode="rts", device="cuda:0", jitter=_jitter(nf), velocity=vel)
+        g0 = set(d.gid.tolist())
         for _ in range(steps):
             d.step()
         q.put((rank, d.gid.cpu().numpy(), d.state["pos"].cpu().numpy(),
-               d.state["vel"].cpu().numpy(), d.state["rho"].cpu().numpy()))
+               d.state["vel"].cpu().numpy(), d.state["rho"].cpu().numpy(),
+               len(g0 ^ set(d.gid.tolist()))))
     except Exception:  # report instead of leaving the parent waiting
         import traceback
         q.put(("error", rank, traceback.format_exc()))
+        q.close()
+        q.join_thread()  # flush the report before the hard exit
         os._exit(1)
     finally:
         dist.destroy_process_group()
 
 
-def test_two_ranks_on_one_gpu_match_single_gpu_bitwise():
+@pytest.mark.parametrize("steps,drift", [(12, 0.0), (40, 3.0)])
+def test_two_ranks_on_one_gpu_match_single_gpu_bitwise(steps, drift):
+    """Owned rows of two WCSPH x-slab ranks equal the single-GPU run bit for
+    bit; with a uniform +x drift (3 m/s, 1.6 cm over 40 steps) particles
+    migrate across the cut, exercising hole filling and arrivals."""
     from paper_2009_14514_b200 import WcsphSolver
-    steps = 12
     sc = _scene()
     ref = WcsphSolver(sc, mode="rts")
     nf = ref.n_fluid
     from paper_2009_14514_b200.scene import seed_particles
     x = (seed_particles(sc)[0] + _jitter(nf)).astype(np.float32)
     ref.pos[:nf] = torch.as_tensor(x, device=ref.device)
+    ref.vel[:, 0] = drift
     for _ in range(steps):
         ref.step()
     s = socket.socket()
@@ -83,7 +93,7 @@ def test_two_ranks_on_one_gpu_match_single_gpu_bitwise():
     s.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, steps, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, steps, q, drift)) for r in range(2)]
     for p in procs:
         p.start()
     res = _collect(q, procs)
@@ -95,9 +105,11 @@ def test_two_ranks_on_one_gpu_match_single_gpu_bitwise():
     assert np.array_equal(np.concatenate([r[2] for r in res])[order], ref.host("pos")[:nf])
     assert np.array_equal(np.concatenate([r[3] for r in res])[order], ref.host("vel"))
     assert np.array_equal(np.concatenate([r[4] for r in res])[order], ref.host("rho"))
+    if drift:
+        assert sum(r[5] for r in res) > 0, "no particle migrated"
 
 
-def _pworker(rank, world, port, majors, q):
+def _pworker(rank, world, port, majors, q, width=0.6, drift=0.0):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -106,36 +118,46 @@ def _pworker(rank, world, port, majors, q):
         sys.path.insert(0, ROOT)
         from paper_2009_14514_b200.distributed import DistributedPcisph
         from paper_2009_14514_b200.scene import seed_particles
-        sc = _scene()
+        sc = _scene(width)
         nf = len(seed_particles(sc)[0])
-        d = DistributedPcisph(sc, device="cuda:0", jitter=_jitter(nf) * 0.2)
+        vel = np.zeros((nf, 3))
+        vel[:, 0] = drift
+        d = DistributedPcisph(sc, device="cuda:0", jitter=_jitter(nf) * 0.2, velocity=vel)
+        g0 = set(d.gid.tolist())
         stats = []
         for _ in range(majors):
             stats += [(r.n_compute, r.iterations, r.corrected, r.early_term) for r in d.advance()]
         q.put((rank, d.gid.cpu().numpy(), d.state["pos"].cpu().numpy(),
-               d.state["rho_star"].cpu().numpy(), stats))
+               d.state["rho_star"].cpu().numpy(), stats, d._single_round(),
+               len(g0 ^ set(d.gid.tolist()))))
     except Exception:  # report instead of leaving the parent waiting
         import traceback
         q.put(("error", rank, traceback.format_exc()))
+        q.close()
+        q.join_thread()  # flush the report before the hard exit
         os._exit(1)
     finally:
         dist.destroy_process_group()
 
 
-def test_pcisph_two_ranks_on_one_gpu_match_single_gpu():
+@pytest.mark.parametrize("width,one_round,drift", [(0.6, False, 0.0), (1.0, True, 2.5)])
+def test_pcisph_two_ranks_on_one_gpu_match_single_gpu(width, one_round, drift):
     """RTS-PCISPH over two x-slabs (per-iteration ghost x*/p/err exchange and
     all-reduced convergence scalars) takes the single-GPU run's decisions
     (refresh counts, iterations, corrected work per minor step) and stays
-    within fp32 rounding of its trajectory."""
+    within fp32 rounding of its trajectory -- with the two-round major-start
+    exchange (slabs of 7 columns, halo 6) and the single round (12 columns,
+    with a +x drift of 2.5 m/s over 7 majors so that particles migrate across the cut)."""
     from paper_2009_14514_b200 import PcisphSolver
     from paper_2009_14514_b200.scene import seed_particles
-    majors = 3
-    sc = _scene()
+    majors = 7 if drift else 3
+    sc = _scene(width)
     ref = PcisphSolver(sc, mode="rts")
     nf = ref.n_fluid
     x = (seed_particles(sc)[0] + _jitter(nf) * 0.2).astype(np.float32)
     ref.pos[:nf] = torch.as_tensor(x, device=ref.device)
     ref.xstar[:] = ref.pos[:nf]
+    ref.vel[:, 0] = drift
     rstats = []
     for _ in range(majors):
         rstats += [(r.n_compute, r.iterations, r.corrected, r.early_term) for r in ref.advance()]
@@ -145,12 +167,15 @@ def test_pcisph_two_ranks_on_one_gpu_match_single_gpu():
     s.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_pworker, args=(r, 2, port, majors, q)) for r in range(2)]
+    procs = [ctx.Process(target=_pworker, args=(r, 2, port, majors, q, width, drift)) for r in range(2)]
     for p in procs:
         p.start()
     res = sorted(_collect(q, procs), key=lambda r: r[0])
     for p in procs:
         p.join(timeout=60)
+    assert res[0][5] == one_round and res[1][5] == one_round
+    if drift:
+        assert res[0][6] + res[1][6] > 0, "no particle migrated"
     assert res[0][4] == rstats and res[1][4] == rstats
     gid = np.concatenate([r[1] for r in res])
     order = np.argsort(gid)
