@@ -359,7 +359,8 @@ def run_wcsph_workload(args, rank: int, world: int, device, barrier) -> None:
         lattice = seed_particles(sc)[0]
         n_total = len(lattice)
         driver = DistributedWcsph(sc, device=device, jitter=jitter_np(n_total, sc.spacing),
-                                  velocity=initial_velocity(args.workload, lattice))
+                                  velocity=initial_velocity(args.workload, lattice),
+                                  rebalance_every=args.rebalance)
         solver = driver.solver
     stream = torch.cuda.current_stream(device)
     steps = args.steps * 4  # one bench step = 4 base steps (a major's worth)
@@ -489,6 +490,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-wcsph", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--rebalance", type=int, default=0,
+                    help="x-slab ranks: re-cut by work every K majors (WCSPH: base steps)")
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS),
                     help="cfg2 (default, the headline) or the BASELINE configs[3..4] "
                          "workloads")
@@ -540,7 +543,7 @@ def main():
         n_total = len(lattice)
         driver = DistributedPcisph(sc, device=device, jitter=jitter_np(n_total, sc.spacing),
                                    velocity=initial_velocity(args.workload, lattice),
-                                   iteration_cap=50)
+                                   iteration_cap=50, rebalance_every=args.rebalance)
         solver = driver.solver
     nf = n_total
     stream = torch.cuda.current_stream(device)

@@ -77,6 +77,25 @@ class SlabPartition:
             part.cuts = tuple(cuts)
         return part
 
+    def rebalanced(self, weights) -> tuple:
+        """Cuts at equal cumulative ``weights`` (per block column, summed over
+        all ranks), each cut moved by less than the narrower slab next to it
+        so that every particle's new owner is its old owner or a neighbour
+        (rebalance at rebuilds from active-work counts)."""
+        w = np.asarray(weights, dtype=np.float64).reshape(-1)
+        cum = np.cumsum(w)
+        total = cum[-1] if len(cum) else 0.0
+        old = [self.bounds(r)[0] for r in range(self.world)] + [self.nx]
+        cuts = [0]
+        for r in range(1, self.world):
+            want = int(np.searchsorted(cum, r * total / self.world, side="left")) + 1
+            shift = min(old[r] - old[r - 1], old[r + 1] - old[r]) - 1
+            c = min(max(want, old[r] - shift), old[r] + shift)
+            c = min(max(c, cuts[-1] + 1), self.nx - (self.world - r))
+            cuts.append(c)
+        cuts.append(self.nx)
+        return tuple(cuts)
+
     def bounds(self, rank: int) -> tuple[int, int]:
         """[first, last) block columns owned by ``rank``."""
         if self.cuts:
@@ -548,6 +567,58 @@ class _ResidentRank:
         self.rows = RankRows(s)
         self.n_own = len(gid)
 
+    # -- work rebalancing ----------------------------------------
+    rebalance_every = 0   # majors (PCISPH) / steps (WCSPH) between checks; 0 = off
+    rebalance_tol = 1.10  # rebalance when the busiest rank has > tol x the mean work
+
+    def _work_weights(self, n: int) -> torch.Tensor:
+        """Relative work of the owned rows for one major step / step."""
+        return torch.ones(n, dtype=torch.float64, device=self.device)
+
+    def rebalance(self) -> bool:
+        """Move the slab cuts to equal work: per-column work of the owned rows,
+        all-reduced; new cuts where the busiest rank exceeds ``rebalance_tol``
+        times the mean.  The rows follow by the next exchange (two rounds:
+        arrivals may land deeper than one column); the wall samples of the
+        new slab + halo are re-selected.  Returns whether the cuts moved."""
+        s, n, part = self.solver, self.n_own, self.part
+        bx = part.block_x(s.arena["pos"][:n, 0])
+        hist = torch.zeros(part.nx, dtype=torch.float64, device=self.device)
+        hist.index_add_(0, bx, self._work_weights(n))
+        h = hist.to(self.x.device)
+        dist.all_reduce(h)
+        h = h.cpu().numpy()
+        per_rank = [h[a:b].sum() for a, b in (part.bounds(r) for r in range(self.world))]
+        mean = sum(per_rank) / self.world
+        if self.world < 2 or mean <= 0 or max(per_rank) <= self.rebalance_tol * mean:
+            return False
+        cuts = part.rebalanced(h)
+        if cuts == tuple(part.bounds(r)[0] for r in range(self.world)) + (part.nx,):
+            return False
+        part.cuts = cuts
+        self.driver.lo, self.driver.hi = part.bounds(self.rank)
+        self._one_round = None  # re-derived; this exchange takes two rounds
+        self._force_two_rounds = True
+        lo, hi, h2 = self.driver.lo, self.driver.hi, part.halo + 1
+        wsel = np.flatnonzero((self._wall_bx >= lo - h2) & (self._wall_bx < hi + h2))
+        keep = {k: v.clone() for k, v in s._get_local_state().items()}
+        key = s.arena["sort_key"][:s.n_fluid].clone()
+        s._set_local_particles(keep, self._wall_all[wsel], capacity=s._cap)
+        self._alloc_key()
+        s.arena["sort_key"][:key.numel()] = key
+        self.rows._key = None
+        s._resize_fluid(self.n_own, s.n_fluid - self.n_own)
+        return True
+
+    def _keep_walls(self, wall: np.ndarray) -> None:
+        self._wall_all = wall
+        self._wall_bx = (self.part.block_x(wall[:, 0]) if len(wall)
+                         else np.zeros(0, dtype=np.int64))
+
+    def _maybe_rebalance(self, count: int) -> None:
+        if self.rebalance_every and count and count % self.rebalance_every == 0:
+            self.rebalance()
+
     def _alloc_key(self) -> None:
         A = self.solver.arena
         cap = self.solver._cap
@@ -598,14 +669,15 @@ class _ResidentRank:
         neighbour, so a rank's post-migration band = its kept band rows plus
         the migrants it just received from that same neighbour -- which the
         neighbour keeps as ghosts itself (lists 4 / 5 of rts_slab_classify)."""
-        if not hasattr(self, "_one_round"):
+        if getattr(self, "_one_round", None) is None:
             widths = [b - a for a, b in (self.part.bounds(r) for r in range(self.world))]
             self._one_round = min(widths) > self.part.halo + 1
         return self._one_round
 
     def _exchange(self) -> None:
         """Migration + fresh ghost band (one round when ``_single_round``)."""
-        if not self._single_round():
+        if getattr(self, "_force_two_rounds", False) or not self._single_round():
+            self._force_two_rounds = False
             self._migrate()
             self._ghosts()
             return
@@ -732,13 +804,16 @@ class DistributedWcsph(_ResidentRank):
     bound is an all-reduce MAX of |F|."""
 
     def __init__(self, scene: Scene, mode: str = "rts", device=None, halo: int = 2,
-                 jitter=None, comm_device=None, velocity=None, **kw):
+                 jitter=None, comm_device=None, velocity=None, balance: bool = True,
+                 rebalance_every: int = 0, **kw):
         from .wcsph import WcsphSolver
         self.rank = dist.get_rank()
         self.world = dist.get_world_size()
         self.device = torch.device(device) if device is not None else torch.device("cuda")
-        self.part = SlabPartition.for_scene(scene, "wcsph", self.world, halo)
+        self.part = SlabPartition.for_scene(scene, "wcsph", self.world, halo, balance)
+        self.rebalance_every = rebalance_every
         gid, fluid, wall, wsel = initial_ownership(scene, self.part, self.rank)
+        self._keep_walls(wall)
         if jitter is not None:
             fluid = (fluid + jitter).astype(np.float32).astype(np.float64)
         if comm_device is None and dist.get_backend() == "gloo":
@@ -759,6 +834,11 @@ class DistributedWcsph(_ResidentRank):
         self.sim_time = 0.0
         self.step_index = 0
 
+    def _work_weights(self, n: int) -> torch.Tensor:
+        """Region n is active every 2^(n-1) base steps (wcsph.py:237-266)."""
+        reg = self.solver.arena["region"][:n].double().clamp(min=1)
+        return 1.0 + torch.pow(2.0, 1.0 - reg)
+
     def _all_max(self, v: float) -> float:
         t = torch.tensor([v], dtype=torch.float64, device=self.x.device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -766,6 +846,7 @@ class DistributedWcsph(_ResidentRank):
 
     def step(self):
         s = self.solver
+        self._maybe_rebalance(self.step_index)
         self._exchange()  # migration of the last step's leavers + fresh ghosts
         st = s.step()
         n_own = self.n_own
@@ -784,14 +865,17 @@ class DistributedPcisph(_ResidentRank):
     scalars every iteration (``PcisphExchange``)."""
 
     def __init__(self, scene: Scene, device=None, halo: int = 6, inner: int = 2, jitter=None,
-                 comm_device=None, velocity=None, **kw):
+                 comm_device=None, velocity=None, balance: bool = True, rebalance_every: int = 0,
+                 **kw):
         from .pcisph import PcisphSolver
         self.rank = dist.get_rank()
         self.world = dist.get_world_size()
         self.device = torch.device(device) if device is not None else torch.device("cuda")
-        self.part = SlabPartition.for_scene(scene, "pcisph", self.world, halo)
+        self.part = SlabPartition.for_scene(scene, "pcisph", self.world, halo, balance)
+        self.rebalance_every = rebalance_every
         self.inner = inner
         gid, fluid, wall, wsel = initial_ownership(scene, self.part, self.rank)
+        self._keep_walls(wall)
         if jitter is not None:
             fluid = (fluid + jitter).astype(np.float32).astype(np.float64)
         if comm_device is None and dist.get_backend() == "gloo":
@@ -813,6 +897,16 @@ class DistributedPcisph(_ResidentRank):
         self._init_rows(gid, st, halo)
         self.sim_time = 0.0
         self.step_index = 0
+        self._majors = 0
+
+    def _work_weights(self, n: int) -> torch.Tensor:
+        """Refreshes per major of each owned row: region n is refreshed every
+        VALIDITY_PERIOD[n] minor steps (pcisph.py:63-66), plus the per-row
+        passes every particle takes."""
+        from .pcisph import VALIDITY_PERIOD
+        per = torch.as_tensor(VALIDITY_PERIOD, dtype=torch.float64, device=self.device)
+        reg = self.solver.arena["region"][:n].long().clamp(1, len(VALIDITY_PERIOD) - 1)
+        return 1.0 + self.solver.scene.minor_steps / per[reg]
 
     def _lists(self):
         s = self.solver
@@ -839,6 +933,8 @@ class DistributedPcisph(_ResidentRank):
 
     def advance(self):
         s = self.solver
+        self._maybe_rebalance(self._majors)
+        self._majors += 1
         self._exchange()
         s.params.n_global = self.n_global
         send, recv = self._lists()

@@ -187,7 +187,7 @@ class _DeviceSolver:
         nb = self._walls.shape[0]
         nf = 0 if state is None else int(state["pos"].shape[0])
         cap = getattr(self, "_cap", -1)
-        if init or nf > cap or nf + nb > self._pos.shape[0]:
+        if init or nf > cap or nf + nb > self._pos.shape[0] or (capacity or 0) > cap:
             cap = max(nf, int(1.25 * nf) + 1024, capacity or 0)
             self._cap = cap
             self._pos = A.alloc("pos", (cap + nb, 3), torch.float32, 0)

@@ -145,3 +145,31 @@ def test_slab_decomposition_matches_single_domain_bitwise(world):
     assert res[0][5] == ref_nc
     # the cut actually had traffic: both ranks own particles
     assert all(len(r[1]) > 0 for r in res)
+
+
+def test_rebalanced_cuts_move_toward_equal_work_one_slab_at_most():
+    """SlabPartition.rebalanced: cuts at equal cumulative work, each moved by
+    less than the narrower neighbouring slab (migrants only go next door)."""
+    from paper_2009_14514_b200.distributed import SlabPartition
+    part = SlabPartition(origin_x=0.0, inv_block=1.0, nx=40, world=4, halo=2)  # even: 10 each
+    w = np.zeros(40)
+    w[:10] = 10.0  # all the work in the first slab
+    w[10:] = 1.0
+    cuts = part.rebalanced(w)
+    old = [0, 10, 20, 30, 40]
+    assert cuts[0] == 0 and cuts[-1] == 40
+    assert all(a < b for a, b in zip(cuts, cuts[1:]))
+    for r in range(1, 4):
+        shift = min(old[r] - old[r - 1], old[r + 1] - old[r]) - 1
+        assert abs(cuts[r] - old[r]) <= shift
+    work = [w[a:b].sum() for a, b in zip(cuts, cuts[1:])]
+    assert max(work) < w[:10].sum()  # the busiest slab shed work
+    # repeated rebalancing converges to near-equal work
+    for _ in range(6):
+        part.cuts = cuts
+        cuts = part.rebalanced(w)
+    work = [w[a:b].sum() for a, b in zip(cuts, cuts[1:])]
+    assert max(work) <= 1.25 * (w.sum() / 4)
+    # uniform work: the even cuts stay
+    part.cuts = ()
+    assert part.rebalanced(np.ones(40)) == (0, 10, 20, 30, 40)

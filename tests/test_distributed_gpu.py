@@ -42,7 +42,7 @@ def _collect(q, procs, n=2):
     return res
 
 
-def _worker(rank, world, port, steps, q, drift=0.0):
+def _worker(rank, world, port, steps, q, drift=0.0, rebalance=0):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -55,13 +55,16 @@ def _worker(rank, world, port, steps, q, drift=0.0):
         nf = len(seed_particles(sc)[0])
         vel = np.zeros((nf, 3))
         vel[:, 0] = drift
-        d = DistributedWcsph(sc, mode="rts", device="cuda:0", jitter=_jitter(nf), velocity=vel)
+        d = DistributedWcsph(sc, mode="rts", device="cuda:0", jitter=_jitter(nf), velocity=vel,
+                             balance=not rebalance, rebalance_every=rebalance)
+        cuts0 = [d.part.bounds(r) for r in range(world)]
         g0 = set(d.gid.tolist())
         for _ in range(steps):
             d.step()
         q.put((rank, d.gid.cpu().numpy(), d.state["pos"].cpu().numpy(),
                d.state["vel"].cpu().numpy(), d.state["rho"].cpu().numpy(),
-               len(g0 ^ set(d.gid.tolist()))))
+               len(g0 ^ set(d.gid.tolist())),
+               cuts0 != [d.part.bounds(r) for r in range(world)]))
     except Exception:  # report instead of leaving the parent waiting
         import traceback
         q.put(("error", rank, traceback.format_exc()))
@@ -72,11 +75,13 @@ def _worker(rank, world, port, steps, q, drift=0.0):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("steps,drift", [(12, 0.0), (40, 3.0)])
-def test_two_ranks_on_one_gpu_match_single_gpu_bitwise(steps, drift):
+@pytest.mark.parametrize("steps,drift,rebalance", [(12, 0.0, 0), (40, 3.0, 0), (24, 0.0, 4)])
+def test_two_ranks_on_one_gpu_match_single_gpu_bitwise(steps, drift, rebalance):
     """Owned rows of two WCSPH x-slab ranks equal the single-GPU run bit for
     bit; with a uniform +x drift (3 m/s, 1.6 cm over 40 steps) particles
-    migrate across the cut, exercising hole filling and arrivals."""
+    migrate across the cut, exercising hole filling and arrivals; with an
+    unbalanced initial split (even columns) and rebalancing every 4 steps
+    the cut moves and whole columns of particles change rank."""
     from paper_2009_14514_b200 import WcsphSolver
     sc = _scene()
     ref = WcsphSolver(sc, mode="rts")
@@ -93,7 +98,8 @@ def test_two_ranks_on_one_gpu_match_single_gpu_bitwise(steps, drift):
     s.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, steps, q, drift)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, steps, q, drift, rebalance))
+             for r in range(2)]
     for p in procs:
         p.start()
     res = _collect(q, procs)
@@ -105,11 +111,12 @@ def test_two_ranks_on_one_gpu_match_single_gpu_bitwise(steps, drift):
     assert np.array_equal(np.concatenate([r[2] for r in res])[order], ref.host("pos")[:nf])
     assert np.array_equal(np.concatenate([r[3] for r in res])[order], ref.host("vel"))
     assert np.array_equal(np.concatenate([r[4] for r in res])[order], ref.host("rho"))
-    if drift:
+    if drift or rebalance:
         assert sum(r[5] for r in res) > 0, "no particle migrated"
+    assert all(r[6] for r in res) == bool(rebalance)
 
 
-def _pworker(rank, world, port, majors, q, width=0.6, drift=0.0):
+def _pworker(rank, world, port, majors, q, width=0.6, drift=0.0, rebalance=0):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -122,14 +129,17 @@ def _pworker(rank, world, port, majors, q, width=0.6, drift=0.0):
         nf = len(seed_particles(sc)[0])
         vel = np.zeros((nf, 3))
         vel[:, 0] = drift
-        d = DistributedPcisph(sc, device="cuda:0", jitter=_jitter(nf) * 0.2, velocity=vel)
+        d = DistributedPcisph(sc, device="cuda:0", jitter=_jitter(nf) * 0.2, velocity=vel,
+                              balance=not rebalance, rebalance_every=rebalance)
+        cuts0 = [d.part.bounds(r) for r in range(world)]
         g0 = set(d.gid.tolist())
         stats = []
         for _ in range(majors):
             stats += [(r.n_compute, r.iterations, r.corrected, r.early_term) for r in d.advance()]
         q.put((rank, d.gid.cpu().numpy(), d.state["pos"].cpu().numpy(),
                d.state["rho_star"].cpu().numpy(), stats, d._single_round(),
-               len(g0 ^ set(d.gid.tolist()))))
+               len(g0 ^ set(d.gid.tolist())),
+               cuts0 != [d.part.bounds(r) for r in range(world)]))
     except Exception:  # report instead of leaving the parent waiting
         import traceback
         q.put(("error", rank, traceback.format_exc()))
@@ -140,17 +150,19 @@ def _pworker(rank, world, port, majors, q, width=0.6, drift=0.0):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("width,one_round,drift", [(0.6, False, 0.0), (1.0, True, 2.5)])
-def test_pcisph_two_ranks_on_one_gpu_match_single_gpu(width, one_round, drift):
+@pytest.mark.parametrize("width,one_round,drift,rebalance",
+                         [(0.6, False, 0.0, 0), (1.0, True, 2.5, 0), (1.0, True, 0.0, 2)])
+def test_pcisph_two_ranks_on_one_gpu_match_single_gpu(width, one_round, drift, rebalance):
     """RTS-PCISPH over two x-slabs (per-iteration ghost x*/p/err exchange and
     all-reduced convergence scalars) takes the single-GPU run's decisions
     (refresh counts, iterations, corrected work per minor step) and stays
     within fp32 rounding of its trajectory -- with the two-round major-start
     exchange (slabs of 7 columns, halo 6) and the single round (12 columns,
-    with a +x drift of 2.5 m/s over 7 majors so that particles migrate across the cut)."""
+    with a +x drift of 2.5 m/s over 7 majors so that particles migrate across
+    the cut; and from an even-column split rebalanced by work every 2 majors)."""
     from paper_2009_14514_b200 import PcisphSolver
     from paper_2009_14514_b200.scene import seed_particles
-    majors = 7 if drift else 3
+    majors = 7 if drift else (5 if rebalance else 3)
     sc = _scene(width)
     ref = PcisphSolver(sc, mode="rts")
     nf = ref.n_fluid
@@ -167,15 +179,17 @@ def test_pcisph_two_ranks_on_one_gpu_match_single_gpu(width, one_round, drift):
     s.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_pworker, args=(r, 2, port, majors, q, width, drift)) for r in range(2)]
+    procs = [ctx.Process(target=_pworker, args=(r, 2, port, majors, q, width, drift,
+                                                           rebalance)) for r in range(2)]
     for p in procs:
         p.start()
     res = sorted(_collect(q, procs), key=lambda r: r[0])
     for p in procs:
         p.join(timeout=60)
     assert res[0][5] == one_round and res[1][5] == one_round
-    if drift:
+    if drift or rebalance:
         assert res[0][6] + res[1][6] > 0, "no particle migrated"
+    assert res[0][7] == res[1][7] == bool(rebalance)
     assert res[0][4] == rstats and res[1][4] == rstats
     gid = np.concatenate([r[1] for r in res])
     order = np.argsort(gid)
