@@ -642,6 +642,27 @@ class _ResidentRank:
     def n_owned(self) -> int:
         return self.n_own
 
+    # reference-facing view of a rank (WcsphSolver / PcisphSolver attributes
+    # callers read, bench.py:129-166): the owned rows
+    @property
+    def n_fluid(self) -> int:
+        return self.n_own
+
+    @property
+    def pos(self) -> torch.Tensor:
+        return self.solver.arena["pos"][:self.n_own]
+
+    @property
+    def vel(self) -> torch.Tensor:
+        return self.solver.arena["vel"][:self.n_own]
+
+    @property
+    def missed_neighbors_total(self) -> int:
+        return int(getattr(self.solver, "missed_neighbors_total", 0))
+
+    def particle_regions(self) -> torch.Tensor:
+        return self.solver.particle_regions()[:self.n_own]
+
     def _resize(self, nf: int, n_ghost: int) -> None:
         s = self.solver
         if nf > s._cap:  # grow, keeping the current rows (rare)
@@ -839,6 +860,9 @@ class DistributedWcsph(_ResidentRank):
         reg = self.solver.arena["region"][:n].double().clamp(min=1)
         return 1.0 + torch.pow(2.0, 1.0 - reg)
 
+    def advance(self):
+        return [self.step()]
+
     def _all_max(self, v: float) -> float:
         t = torch.tensor([v], dtype=torch.float64, device=self.x.device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -953,3 +977,28 @@ class DistributedPcisph(_ResidentRank):
         self.sim_time = s.sim_time
         self.step_index = s.step_index
         return rows
+
+    def major_step(self):
+        return self.advance()
+
+
+def rank_solver(kind: str, scene: Scene, comm, *args, **kw):
+    """``WcsphSolver(..., comm=group)`` / ``PcisphSolver(..., comm=group)``: this
+    process is one x-slab rank (one GPU per process; ``device`` defaults to
+    the current CUDA device).  ``comm`` must be the default process group."""
+    if comm is not dist.group.WORLD and comm != dist.group.WORLD:
+        raise ValueError("comm must be torch.distributed.group.WORLD (x-slab ranks use the "
+                         "default process group)")
+    kw.pop("use_graphs", None)  # ranks launch per kernel (the row count changes)
+    names = ("mode",) + (("dt_cap", "pin_region", "apply_correction", "track_rho_variance",
+                          "audit_neighbors", "n_regions") if kind == "wcsph" else
+                         ("dt", "schedule", "pin_region", "audit_neighbors", "iteration_cap",
+                          "local_attempts", "n_regions"))
+    kw.update(zip(names, args))
+    if kw.get("device") is None:
+        kw["device"] = torch.device("cuda", torch.cuda.current_device())
+    if kind == "wcsph":
+        return DistributedWcsph(scene, **kw)
+    if kw.pop("mode", "rts") != "rts":
+        raise ValueError("x-slab ranks run RTS-PCISPH (mode='rts')")
+    return DistributedPcisph(scene, **kw)

@@ -135,6 +135,15 @@ class PcisphSolver(_DeviceSolver):
     """PCISPH with ``mode`` "const", "adaptive" or "rts" (pcisph.py:279)."""
 
     mode_names = ("const", "adaptive", "rts")
+
+    def __new__(cls, scene=None, *args, comm=None, **kw):
+        """``comm`` (the default torch.distributed group): this process is one
+        x-slab rank -- a ``DistributedPcisph`` (RTS mode) with the same solver
+        keywords (SURVEY.md 8b "extra kwargs: device, comm")."""
+        if comm is not None:
+            from .distributed import rank_solver
+            return rank_solver("pcisph", scene, comm, *args, **kw)
+        return super().__new__(cls)
     _FIELDS = (("vel", "vel", 3, torch.float32, 0.0), ("f_ext", "force", 3, torch.float32, 0.0),
                ("f_p", "f_p", 3, torch.float32, 0.0), ("p", "pres", 1, torch.float32, 0.0),
                ("rho_star", "rho", 1, torch.float32, None), ("err", "err", 1, torch.float64, 0.0),
@@ -184,7 +193,7 @@ class PcisphSolver(_DeviceSolver):
                  schedule=DEFAULT_SCHEDULE, pin_region: int | None = None,
                  audit_neighbors: bool = False, iteration_cap: int = 24,
                  local_attempts: int = 4, n_regions: int = 4, device="cuda",
-                 use_graphs: bool = True):
+                 use_graphs: bool = True, comm=None):
         if mode not in self.mode_names:
             raise ValueError(f"unknown pcisph mode {mode!r}")
         validate_schedule(schedule, n_regions)

@@ -251,6 +251,15 @@ class WcsphSolver(_DeviceSolver):
 
     mode_names = ("baseline", "rts")
 
+    def __new__(cls, scene=None, *args, comm=None, **kw):
+        """``comm`` (the default torch.distributed group): this process is one
+        x-slab rank of a multi-GPU run -- a ``DistributedWcsph`` with the same
+        solver keywords (SURVEY.md 8b "extra kwargs: device, comm")."""
+        if comm is not None:
+            from .distributed import rank_solver
+            return rank_solver("wcsph", scene, comm, *args, **kw)
+        return super().__new__(cls)
+
     def _realloc_extra(self, cap: int, nb: int) -> None:
         # the density pass's neighbour lists (slots), reused by the force pass
         stride = -(-max(cap, 1) // 32) * 32
@@ -269,7 +278,7 @@ class WcsphSolver(_DeviceSolver):
     def __init__(self, scene: Scene, mode: str = "rts", dt_cap: float | None = None,
                  pin_region: int | None = None, apply_correction: bool = True,
                  track_rho_variance: bool = False, audit_neighbors: bool = False,
-                 n_regions: int = 4, device="cuda", use_graphs: bool = True):
+                 n_regions: int = 4, device="cuda", use_graphs: bool = True, comm=None):
         if mode not in self.mode_names:
             raise ValueError(f"unknown wcsph mode {mode!r}")
         self.mode = mode

@@ -198,3 +198,64 @@ def test_pcisph_two_ranks_on_one_gpu_match_single_gpu(width, one_round, drift, r
     assert np.abs(pos - ref.host("pos")[:nf]).max() < 1e-5
     rho = np.concatenate([r[3] for r in res])[order]
     assert np.abs(rho - ref.host("rho_star")).max() / 1000.0 < 1e-5
+
+
+def _cworker(rank, world, port, steps, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import sys
+        sys.path.insert(0, ROOT)
+        from paper_2009_14514_b200 import PcisphSolver, WcsphSolver
+        from paper_2009_14514_b200.distributed import DistributedPcisph, DistributedWcsph
+        sc = _scene()
+        w = WcsphSolver(sc, "rts", comm=dist.group.WORLD, device="cuda:0")
+        p = PcisphSolver(sc, mode="rts", comm=dist.group.WORLD, device="cuda:0")
+        assert isinstance(w, DistributedWcsph) and isinstance(p, DistributedPcisph)
+        for _ in range(steps):
+            w.advance()
+        rows = p.advance()
+        q.put((rank, w.gid.cpu().numpy(), w.pos.cpu().numpy(), w.n_fluid, w.step_index,
+               [(r.n_compute, r.iterations) for r in rows]))
+    except Exception:  # report instead of leaving the parent waiting
+        import traceback
+        q.put(("error", rank, traceback.format_exc()))
+        q.close()
+        q.join_thread()
+        os._exit(1)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_comm_keyword_makes_the_solvers_x_slab_ranks():
+    """``WcsphSolver(..., comm=WORLD)`` / ``PcisphSolver(..., comm=WORLD)`` (the
+    drop-in's extra keyword) run as x-slab ranks; their owned rows
+    reproduce the single-GPU run."""
+    from paper_2009_14514_b200 import PcisphSolver, WcsphSolver
+    steps = 6
+    sc = _scene()
+    ref = WcsphSolver(sc, mode="rts")
+    for _ in range(steps):
+        ref.step()
+    pref = PcisphSolver(sc, mode="rts")
+    prows = [(r.n_compute, r.iterations) for r in pref.advance()]
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_cworker, args=(r, 2, port, steps, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = _collect(q, procs)
+    for p in procs:
+        p.join(timeout=60)
+    gid = np.concatenate([r[1] for r in res])
+    order = np.argsort(gid)
+    assert np.array_equal(gid[order], np.arange(ref.n_fluid))
+    assert sum(r[3] for r in res) == ref.n_fluid
+    assert np.array_equal(np.concatenate([r[2] for r in res])[order], ref.host("pos")[:ref.n_fluid])
+    assert all(r[4] == steps for r in res)
+    assert all(r[5] == prows for r in res)

@@ -173,3 +173,14 @@ def test_row_mask_encoding_matches_schedule_rows():
     c = N.RtsControl()
     assert ctypes.sizeof(c) == ctypes.sizeof(N.RtsControl)
     assert dataclasses.is_dataclass(StepStats)
+
+
+def test_comm_keyword_requires_the_default_group():
+    """The ``comm`` keyword accepts only the default process group."""
+    from paper_2009_14514_b200 import PcisphSolver, WcsphSolver
+    from paper_2009_14514_b200.scene import Scene
+    sc = Scene(domain_min=(0, 0, 0), domain_max=(0.2, 0.2, 0.2),
+               fluid_boxes=(((0.0, 0.0, 0.0), (0.1, 0.1, 0.1)),), spacing=0.02)
+    for cls in (WcsphSolver, PcisphSolver):
+        with pytest.raises(ValueError, match="comm must be"):
+            cls(sc, comm=object())
