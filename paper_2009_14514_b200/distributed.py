@@ -176,11 +176,14 @@ class Exchanger:
                 r.wait()
         return [bufs[q].to(self.compute_device) for q in peers]
 
-    def swap(self, send: dict, recv_rows: dict, width: int, dtype) -> dict:
+    def swap(self, send: dict, recv_rows: dict, width: int, dtype, out: dict | None = None) -> dict:
         """Exchange with known sizes (no count round): ``send`` {peer: rows},
-        ``recv_rows`` {peer: expected row count}; returns {peer: rows}."""
-        bufs = {q: torch.empty((recv_rows[q], width), dtype=dtype, device=self.device)
-                for q in recv_rows}
+        ``recv_rows`` {peer: expected row count}; returns {peer: rows}.  With
+        ``out`` ({peer: preallocated rows} on the transport device) the rows
+        are received in place."""
+        bufs = out if out is not None else {
+            q: torch.empty((recv_rows[q], width), dtype=dtype, device=self.device)
+            for q in recv_rows}
         ops = []
         for q in sorted(send):
             if send[q].shape[0]:
@@ -383,6 +386,12 @@ class HaloChannel:
         self.unpack_spec = self._spec(unpack or pack)
         self.send_buf = torch.empty((sum(self.n_send), self.msg_words), dtype=torch.int32,
                                     device=dev)
+        self.recv_buf = torch.empty((sum(self.n_recv), self.msg_words), dtype=torch.int32,
+                                    device=dev)
+        self.recv_views, b = {}, 0
+        for q, nr in zip(self.peers, self.n_recv):
+            self.recv_views[q] = self.recv_buf[b:b + nr]
+            b += nr
 
     def _spec(self, fields):
         N = self.N
@@ -409,13 +418,18 @@ class HaloChannel:
         for q, ns in zip(self.peers, self.n_send):
             send[q] = self.send_buf[a:a + ns]
             a += ns
-        got = self.x.swap(send, dict(zip(self.peers, self.n_recv)), self.msg_words, torch.int32)
-        parts = [got[q] for q in self.peers if got[q].shape[0]]
-        if not parts:
+        direct = self.x.device == self.x.compute_device  # NCCL: receive in place
+        got = self.x.swap(send, dict(zip(self.peers, self.n_recv)), self.msg_words, torch.int32,
+                          out=self.recv_views if direct else None)
+        if not self.recv_rows.numel():
             return
-        recv = torch.cat(parts) if len(parts) > 1 else parts[0].contiguous()
+        if not direct:
+            b = 0
+            for q, nr in zip(self.peers, self.n_recv):
+                self.recv_buf[b:b + nr].copy_(got[q])
+                b += nr
         N.call("rts_halo_unpack", ctypes.byref(self.unpack_spec), self.recv_rows.data_ptr(),
-               self.recv_rows.numel(), recv.data_ptr(), st)
+               self.recv_rows.numel(), self.recv_buf.data_ptr(), st)
 
 
 class PcisphExchange:
@@ -469,10 +483,13 @@ class PcisphExchange:
         self._channels(s)
         st = torch.cuda.current_stream(self.x.compute_device).cuda_stream
         N.call("rts_ctl_publish", s.arena.buf, self._pub.data_ptr(), st)
-        pub = self._pub.to(self.x.device)
-        parts = [torch.empty_like(pub) for _ in range(self.x.world)]
-        dist.all_gather(parts, pub)
-        self._gath.copy_(torch.stack(parts))
+        if self.x.device == self.x.compute_device:  # NCCL: gather in place, stream-ordered
+            dist.all_gather_into_tensor(self._gath, self._pub)
+        else:
+            pub = self._pub.to(self.x.device)
+            parts = [torch.empty_like(pub) for _ in range(self.x.world)]
+            dist.all_gather(parts, pub)
+            self._gath.copy_(torch.stack(parts))
         N.call("rts_ctl_fold", s.arena.buf, self._gath.data_ptr(), self.x.world, st)
 
     def after_integrate(self, s) -> None:
