@@ -340,6 +340,80 @@ def wcsph_algo_bytes(name: str, nf: int, active: int, launches: int) -> float:
     return 0.0
 
 
+def wcsph_comparison(world: int, device, stream, barrier) -> dict:
+    """configs[2]: RTS-WCSPH on the 1M dam break against the global adaptive
+    baseline (CFL step, dt_cap = 4 dt_base), per
+    simulated time.  N > 1: the same scene cut into N x-slab ranks (strong
+    scaling), device time max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2009_14514_b200 import WcsphSolver
+
+    def make(mode: str):
+        sc = scene_cfg3()
+        if world == 1:
+            if mode == "rts":
+                return make_device_solver("wcsph", device), None
+            s = WcsphSolver(sc, mode=mode, device=device)
+            nf = s.n_fluid
+            x = (s.host("pos")[:nf] + jitter_np(nf, sc.spacing)).astype("float32")
+            s.pos[:nf] = torch.as_tensor(x, device=s.device)
+            return s, s
+        from paper_2009_14514_b200.distributed import DistributedWcsph
+        from paper_2009_14514_b200.scene import seed_particles
+        n = len(seed_particles(sc)[0])
+        d = DistributedWcsph(sc, mode=mode, device=device, jitter=jitter_np(n, sc.spacing))
+        return d, d.solver
+
+    def timed(drv, steps: int):
+        barrier()
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fr, sim = 0.0, 0.0
+        for _ in range(steps):
+            st = drv.step()
+            fr += st.n_compute
+            sim += st.dt
+        b.record(stream)
+        b.synchronize()
+        t = a.elapsed_time(b) * 1e-3
+        if world > 1:
+            v = torch.tensor([t], dtype=torch.float64, device=device)
+            dist.all_reduce(v, op=dist.ReduceOp.MAX)
+            t = float(v.item())
+            c = torch.tensor([fr], dtype=torch.float64, device=device)
+            dist.all_reduce(c)
+            fr = float(c.item())
+        return t, fr, sim
+
+    n_w = 40
+    ws, _ = make("rts")
+    for _ in range(8):
+        ws.step()
+    tw, act, sim_rts = timed(ws, n_w)
+    n_total = ws.n_global if world > 1 else ws.n_fluid
+    wc = {"metric": "particle-updates/s (RTS-WCSPH, 1M, base steps)",
+          "value": n_total * n_w / tw, "ms_per_step": 1e3 * tw / n_w,
+          "mean_active_fraction": act / (n_total * n_w), "steps": n_w,
+          "wall_s_per_simulated_ms": tw / (1e3 * sim_rts), "n_gpus": world,
+          "scaling": "strong" if world > 1 else None}
+    del ws
+    wb, solver = make("baseline")
+    solver.dt_cap = 4 * solver.dt_base
+    for _ in range(4):
+        wb.step()
+    tb, _, sim_b = timed(wb, n_w // 2)
+    wc["baseline_adaptive"] = {
+        "ms_per_step": 1e3 * tb / (n_w // 2), "mean_dt": sim_b / (n_w // 2),
+        "wall_s_per_simulated_ms": tb / (1e3 * sim_b),
+        "rts_speedup_per_simulated_time": (tb / sim_b) / (tw / sim_rts)}
+    del wb
+    return wc
+
+
 def run_wcsph_workload(args, rank: int, world: int, device, barrier) -> None:
     """RTS-WCSPH bench line (cfg5-wcsph): K base steps, device time, max over
     ranks; roofline of the dominant kernel from an instrumented pass."""
@@ -681,52 +755,11 @@ def main():
                "steps": k_e2e, "note": "pinned host pos+vel uploaded before and downloaded "
                                        "after every advance(); wall clock"}
 
-    # ---- WCSPH extra (configs[2] geometry, 1M RTS-WCSPH) ----------------------
+    # ---- WCSPH extra (configs[2]: the 1M scene, RTS-WCSPH vs the global -------
+    # adaptive baseline; one GPU, or the same scene cut into N x-slab ranks)
     wc = None
-    if not args.no_wcsph and world == 1 and args.workload == "cfg2":
-        ws = make_device_solver("wcsph", device)
-        for _ in range(8):
-            ws.step()
-        torch.cuda.synchronize()
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        n_w = 40
-        a.record(stream)
-        fr = 0.0
-        for _ in range(n_w):
-            fr += ws.step().frac_compute
-        b.record(stream)
-        b.synchronize()
-        tw = a.elapsed_time(b) * 1e-3
-        sim_rts = n_w * ws.dt_base
-        wc = {"metric": "particle-updates/s (RTS-WCSPH, 1M, base steps)",
-              "value": ws.n_fluid * n_w / tw, "ms_per_step": 1e3 * tw / n_w,
-              "mean_active_fraction": fr / n_w, "steps": n_w,
-              "wall_s_per_simulated_ms": tw / (1e3 * sim_rts)}
-        del ws
-        # configs[2]'s comparison: the global adaptive baseline (CFL step,
-        # dt_cap = 4 dt_base) on the same scene
-        from paper_2009_14514_b200 import WcsphSolver
-        wb = WcsphSolver(scene_cfg3(), mode="baseline", device=device)
-        wb.dt_cap = 4 * wb.dt_base
-        nfb = wb.n_fluid
-        xb = (wb.host("pos")[:nfb] + jitter_np(nfb, wb.scene.spacing)).astype("float32")
-        wb.pos[:nfb] = torch.as_tensor(xb, device=wb.device)
-        for _ in range(4):
-            wb.step()
-        torch.cuda.synchronize()
-        sim_b = 0.0
-        a.record(stream)
-        for _ in range(n_w // 2):
-            sim_b += wb.step().dt
-        b.record(stream)
-        b.synchronize()
-        tb = a.elapsed_time(b) * 1e-3
-        wc["baseline_adaptive"] = {
-            "ms_per_step": 1e3 * tb / (n_w // 2), "mean_dt": sim_b / (n_w // 2),
-            "wall_s_per_simulated_ms": tb / (1e3 * sim_b),
-            "rts_speedup_per_simulated_time": (tb / sim_b) / (tw / sim_rts)}
-        del wb
+    if not args.no_wcsph and args.workload == "cfg2":
+        wc = wcsph_comparison(world, device, stream, barrier)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
