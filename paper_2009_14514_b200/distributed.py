@@ -1,27 +1,24 @@
 """Multi-GPU RTS-SPH by x-slab decomposition.
 
-One process per GPU (``torch.distributed``, NCCL over NVLink; gloo works for
-CPU tests).  The padded block grid of the whole scene (grid.py:223-244) is
-cut into x-slabs aligned to block faces; a rank owns the fluid particles
-whose block column lies in its slab.  Each step:
+One process per GPU (``torch.distributed``, NCCL over NVLink; gloo for the
+1-GPU and CPU tests).  The padded block grid of the whole scene
+(grid.py:223-244) is cut into x-slabs aligned to block faces; a rank owns
+the fluid particles whose block column lies in its slab.
 
-1. **ghost exchange** -- every rank sends the full state of its particles in
-   the ``halo`` block columns next to each neighbour (2 for WCSPH: the
-   first band's densities need the second band's positions, and the first
-   band's smoothed levels need the second band's raw levels);
-2. **local step** -- the B200 solver runs on owned + ghost particles (sorted
-   by global id, so every within-block order -- and therefore every sum --
-   is the single-domain order) and the wall samples of the slab + halo; the
-   ghosts are recomputed redundantly and discarded, so no second exchange
-   is needed inside the step;
-3. **migration** -- owned particles whose block column left the slab are
-   sent to the new owner.
-
-Owned results are therefore bit-identical to the single-domain run
-(``tests/test_distributed_cpu.py`` checks this with gloo on CPU ranks, the
-GPU test with two processes on one device).  The only global reduction of
-RTS-WCSPH is none (the base step is global by construction); the baseline's
-CFL bound is an all-reduce MAX of |F|.
+* ``DistributedWcsph`` / ``DistributedPcisph`` (the B200 ranks; also what
+  ``WcsphSolver(..., comm=...)`` / ``PcisphSolver(..., comm=...)`` return):
+  resident rank rows [owned | ghosts] in the solver arena.  At a step start
+  (WCSPH) or major-step start (PCISPH) one exchange round moves migrants
+  and a fresh ghost band (``rts_slab_classify``, ``rts_halo_pack`` /
+  ``unpack``, ``rts_slab_holes``); the grid sort orders every block's fluid
+  run by global id (``sort_key``), so each neighbour row and pair sum is the
+  single-domain one.  WCSPH ghosts are recomputed redundantly and dropped
+  (owned rows bit-identical to the single-domain run); PCISPH exchanges the
+  inner ghost columns and folds the convergence scalars every correction
+  iteration (``PcisphExchange``).  The cuts can be rebalanced by work.
+* ``SlabWcsph``: the same slab protocol around any local step with the
+  particle sets merged by global id -- the CPU tests run it with the oracle
+  as the local step to check the protocol bit for bit.
 """
 
 from __future__ import annotations
@@ -337,25 +334,6 @@ class SlabWcsph:
 # ---------------------------------------------------------------------------
 # RTS-PCISPH over x-slabs
 # ---------------------------------------------------------------------------
-
-PCISPH_FIELDS = (("pos", 3), ("vel", 3), ("f_ext", 3), ("f_p", 3), ("p", 1), ("rho_star", 1),
-                 ("err", 1), ("xstar", 3), ("region", 1), ("validity", 1), ("compute", 1),
-                 ("in_se", 1), ("in_sob", 1))
-
-# counters fields reduced across ranks before every k_control decision
-_CTR = None
-
-
-def _ctr_views(ctr: torch.Tensor) -> dict:
-    import ctypes
-
-    from ._native import RtsCounters
-    off = {f[0]: getattr(RtsCounters, f[0]).offset for f in RtsCounters._fields_}
-    return {"max_err": ctr[off["max_err"]:off["max_err"] + 8].view(torch.float64),
-            "sum_rho": ctr[off["sum_rho"]:off["sum_rho"] + 8].view(torch.float64),
-            "any_se": ctr[off["any_se"]:off["any_se"] + 4].view(torch.int32),
-            "n_pred": ctr[off["n_pred"]:off["n_pred"] + 4].view(torch.int32)}
-
 
 class HaloChannel:
     """One fixed-row exchange phase of a major step, native end to end:
@@ -921,8 +899,7 @@ class DistributedPcisph(_ResidentRank):
             fluid = (fluid + jitter).astype(np.float32).astype(np.float64)
         if comm_device is None and dist.get_backend() == "gloo":
             comm_device = "cpu"
-        self.driver = SlabDriver(self.part, self.rank, self.device, fields=PCISPH_FIELDS,
-                                 comm_device=comm_device)
+        self.driver = SlabDriver(self.part, self.rank, self.device, comm_device=comm_device)
         self.x = self.driver.x
         self.n_global = len(fluid)
         s = self.solver = PcisphSolver(scene, mode="rts", device=self.device, use_graphs=False,
