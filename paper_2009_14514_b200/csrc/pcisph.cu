@@ -21,6 +21,17 @@
 //   pforces  pressure forces over the force list (pcisph.py:238-271)
 #include "common.cuh"
 
+// density pass variants (scripts/build_variant.sh A/B)
+#ifndef RTS_DENS_PF
+#define RTS_DENS_PF 1
+#endif
+#ifndef RTS_DENS_CH
+#define RTS_DENS_CH 3
+#endif
+#ifndef RTS_DENS_MINB
+#define RTS_DENS_MINB 10
+#endif
+
 using namespace rts;
 
 namespace {
@@ -602,7 +613,34 @@ RTS_DEV void density_one(const RtsParams &p, const RtsBuffers &b, int i, int lan
     const int *row = b.nbr + i;  // entry q at row[q * S]: coalesced across lanes
     const size_t S = p.nbr_stride;
     double acc = 0.0;
-    if (LG == 1) {
+    if (LG == 1 && RTS_DENS_PF) {
+        // two-stage pipeline: table entries two chunks ahead, x* gathers one
+        // chunk ahead of the chunk being summed
+        int jn[CH];
+        float4 on[CH];
+#pragma unroll
+        for (int u = 0; u < CH; ++u) jn[u] = u < c ? __ldcs(row + u * S) : i;
+#pragma unroll
+        for (int u = 0; u < CH; ++u) on[u] = xs4[jn[u]];
+#pragma unroll
+        for (int u = 0; u < CH; ++u) jn[u] = CH + u < c ? __ldcs(row + (CH + u) * S) : i;
+        for (int q = 0; q < c; q += CH) {
+            float4 o[CH];
+#pragma unroll
+            for (int u = 0; u < CH; ++u) {
+                o[u] = on[u];
+                on[u] = xs4[jn[u]];
+                jn[u] = q + 2 * CH + u < c ? __ldcs(row + (q + 2 * CH + u) * S) : i;
+            }
+#pragma unroll
+            for (int u = 0; u < CH; ++u) {
+                if (q + u < c)
+                    acc = xadd(acc, poly6(dist2(xsub(xi, (double)o[u].x), xsub(yi, (double)o[u].y),
+                                                xsub(zi, (double)o[u].z)),
+                                          p.h2, p.c_poly6));
+            }
+        }
+    } else if (LG == 1) {
         // software-pipelined: the next chunk's table entries (mostly DRAM:
         // the tables exceed L2) are requested before this chunk's gathers
         int jn[CH];
@@ -1417,7 +1455,7 @@ int rts_pci_density(const RtsParams *p, const RtsBuffers *b, void *stream) {
     const int nb = pass_blocks(p);
     cudaStream_t s = (cudaStream_t)stream;
     // 4-deep chunks, <= 48 registers: 10 CTAs of 128 threads per SM
-    rts_note_launch(), k_density<4, 10><<<nb, kThreads, 0, s>>>(*p, *b);
+    rts_note_launch(), k_density<RTS_DENS_CH, RTS_DENS_MINB><<<nb, kThreads, 0, s>>>(*p, *b);
     RTS_LAUNCH_CHECK();
     return 0;
 }
