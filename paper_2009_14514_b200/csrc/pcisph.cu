@@ -31,6 +31,15 @@
 #ifndef RTS_DENS_MINB
 #define RTS_DENS_MINB 10
 #endif
+#ifndef RTS_PFOR_PF
+#define RTS_PFOR_PF 1
+#endif
+#ifndef RTS_PFOR_CH
+#define RTS_PFOR_CH 3
+#endif
+#ifndef RTS_PFOR_MINB
+#define RTS_PFOR_MINB 8
+#endif
 
 using namespace rts;
 
@@ -882,7 +891,38 @@ RTS_DEV void pforce_one(const RtsParams &p, const RtsBuffers &b, int i, int lane
     const int *row = b.nbr + i;  // entry q at row[q * S]: coalesced across lanes
     const size_t S = p.nbr_stride;
     double fx = 0.0, fy = 0.0, fz = 0.0;
-    if (LG == 1) {
+    if (LG == 1 && RTS_PFOR_PF) {
+        // x* / p gathers one chunk ahead, table entries two chunks ahead
+        int jn[kPF], jc[kPF];
+        float4 on[kPF];
+#pragma unroll
+        for (int u = 0; u < kPF; ++u) jc[u] = u < c ? __ldcs(row + u * S) : i;
+#pragma unroll
+        for (int u = 0; u < kPF; ++u) on[u] = ldg_keep(xs4 + jc[u], pol);
+#pragma unroll
+        for (int u = 0; u < kPF; ++u) jn[u] = kPF + u < c ? __ldcs(row + (kPF + u) * S) : i;
+        for (int q = 0; q < c; q += kPF) {
+            int j4[kPF];
+            float4 o4[kPF];
+#pragma unroll
+            for (int u = 0; u < kPF; ++u) {
+                j4[u] = jc[u];
+                o4[u] = on[u];
+                jc[u] = jn[u];
+                on[u] = ldg_keep(xs4 + jn[u], pol);
+                jn[u] = q + 2 * kPF + u < c ? __ldcs(row + (q + 2 * kPF + u) * S) : i;
+            }
+            float gx = 0.f, gy = 0.f, gz = 0.f;
+#pragma unroll
+            for (int u = 0; u < kPF; ++u)
+                if (q + u < c)
+                    pforce_pair(p, xi, yi, zi, term_i, wall, m2, inv_rho0_sq, i, j4[u], o4[u],
+                                gx, gy, gz);
+            fx += (double)gx;
+            fy += (double)gy;
+            fz += (double)gz;
+        }
+    } else if (LG == 1) {
         int jn[kPF];  // software-pipelined table reads, as in density_one
 #pragma unroll
         for (int u = 0; u < kPF; ++u) jn[u] = u < c ? __ldcs(row + u * S) : i;
@@ -1486,7 +1526,7 @@ int rts_pci_sob(const RtsParams *p, const RtsBuffers *b, void *stream) {
 int rts_pci_pforces(const RtsParams *p, const RtsBuffers *b, void *stream) {
     const int nb = pass_blocks(p);
     cudaStream_t s = (cudaStream_t)stream;
-    rts_note_launch(), k_pforces<4, 7><<<nb, kThreads, 0, s>>>(*p, *b);
+    rts_note_launch(), k_pforces<RTS_PFOR_CH, RTS_PFOR_MINB><<<nb, kThreads, 0, s>>>(*p, *b);
     RTS_LAUNCH_CHECK();
     return 0;
 }
