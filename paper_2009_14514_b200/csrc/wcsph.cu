@@ -12,6 +12,12 @@
 // reference's from a common state; only the final fp32 store rounds.
 #include "common.cuh"
 
+// WCSPH force pass: table entries per gather chunk (1 = one at a time;
+// scripts/build_variant.sh A/B)
+#ifndef RTS_WF_CH
+#define RTS_WF_CH 4
+#endif
+
 using namespace rts;
 
 namespace {
@@ -265,7 +271,27 @@ __global__ void __launch_bounds__(kThreads) k_forces(const __grid_constant__ Rts
         const int n_all = b.cnt[t];  // the density pass's neighbour list of slot k
         const int *col = b.nbr + t;
         double fx = 0.0, fy = 0.0, fz = 0.0;
-        if (n_all <= kHitCap) {
+        if (n_all <= kHitCap && RTS_WF_CH > 1) {
+            // chunks of RTS_WF_CH entries: the chunk's table entries, then its
+            // candidate gathers, are all in flight before its terms are
+            // summed (same row order, so the same fp64 sums)
+            for (int q0 = 0; q0 < n_all; q0 += RTS_WF_CH) {
+                int kq[RTS_WF_CH];
+                float4 pq[RTS_WF_CH], vq[RTS_WF_CH];
+#pragma unroll
+                for (int u = 0; u < RTS_WF_CH; ++u) kq[u] = q0 + u < n_all ? col[(q0 + u) * S] : k;
+#pragma unroll
+                for (int u = 0; u < RTS_WF_CH; ++u) {
+                    pq[u] = cpos[kq[u]];
+                    vq[u] = cvel[kq[u]];
+                }
+#pragma unroll
+                for (int u = 0; u < RTS_WF_CH; ++u)
+                    if (kq[u] != k)
+                        force_pair(p, xi, yi, zi, va, inv_rho_i, term_i, wall_term, m2, mum2, pq[u],
+                                   vq[u], fx, fy, fz);
+            }
+        } else if (n_all <= kHitCap) {
             for (int q = 0; q < n_all; ++q) {
                 const int kq = col[q * S];
                 if (kq == k) continue;
