@@ -34,6 +34,9 @@
 #ifndef RTS_PFOR_PF
 #define RTS_PFOR_PF 1
 #endif
+#ifndef RTS_LG_CH
+#define RTS_LG_CH 3
+#endif
 #ifndef RTS_PFOR_CH
 #define RTS_PFOR_CH 3
 #endif
@@ -674,11 +677,20 @@ RTS_DEV void density_one(const RtsParams &p, const RtsBuffers &b, int i, int lan
             }
         }
     } else {
-        for (int q = lane; q < c; q += LG) {
-            const float4 o = xs4[row[q * S]];
-            acc = xadd(acc, poly6(dist2(xsub(xi, (double)o.x), xsub(yi, (double)o.y),
-                                        xsub(zi, (double)o.z)),
-                                  p.h2, p.c_poly6));
+        // RTS_LG_CH entries per lane in flight (same per-lane order)
+        for (int q0 = lane; q0 < c; q0 += LG * RTS_LG_CH) {
+            float4 o[RTS_LG_CH];
+#pragma unroll
+            for (int u = 0; u < RTS_LG_CH; ++u) {
+                const int q = q0 + u * LG;
+                o[u] = xs4[q < c ? row[q * S] : i];
+            }
+#pragma unroll
+            for (int u = 0; u < RTS_LG_CH; ++u)
+                if (q0 + u * LG < c)
+                    acc = xadd(acc, poly6(dist2(xsub(xi, (double)o[u].x), xsub(yi, (double)o[u].y),
+                                                xsub(zi, (double)o[u].z)),
+                                          p.h2, p.c_poly6));
         }
 #pragma unroll
         for (int o = LG / 2; o > 0; o >>= 1) acc = xadd(acc, __shfl_xor_sync(gmask, acc, o, LG));
@@ -948,9 +960,20 @@ RTS_DEV void pforce_one(const RtsParams &p, const RtsBuffers &b, int i, int lane
             fz += (double)gz;
         }
     } else {
-        for (int q = lane; q < c; q += LG) {
-            const int j = row[q * S];
-            pforce_pair(p, xi, yi, zi, term_i, wall, m2, inv_rho0_sq, i, j, xs4[j], fx, fy, fz);
+        for (int q0 = lane; q0 < c; q0 += LG * RTS_LG_CH) {
+            int j[RTS_LG_CH];
+            float4 o[RTS_LG_CH];
+#pragma unroll
+            for (int u = 0; u < RTS_LG_CH; ++u) {
+                const int q = q0 + u * LG;
+                j[u] = q < c ? row[q * S] : i;
+                o[u] = xs4[j[u]];
+            }
+#pragma unroll
+            for (int u = 0; u < RTS_LG_CH; ++u)
+                if (q0 + u * LG < c)
+                    pforce_pair(p, xi, yi, zi, term_i, wall, m2, inv_rho0_sq, i, j[u], o[u], fx, fy,
+                                fz);
         }
 #pragma unroll
         for (int o = LG / 2; o > 0; o >>= 1) {
