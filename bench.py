@@ -147,8 +147,10 @@ def make_device_solver(kind: str, device, workload: str | None = None):
         s = PcisphSolver(sc, mode="rts", iteration_cap=50, device=device)
     else:
         s = WcsphSolver(sc, mode="rts", device=device)
+    from paper_2009_14514_b200.scene import seed_particles
     nf = s.n_fluid
-    lattice = s.host("pos")[:nf]
+    lattice = seed_particles(sc)[0]  # fp64 seeds: the oracle jitters the same values
+    assert len(lattice) == nf
     x = (lattice + jitter_np(nf, s.scene.spacing)).astype(np.float32)
     s.pos[:nf] = torch.as_tensor(x, device=s.device)
     v0 = initial_velocity(workload, lattice) if workload else None
@@ -187,12 +189,50 @@ def algo_bytes(name: str, solver, c_mean: float, rec: dict, launches: int = 1) -
 
 
 class ClockSampler:
-    def __init__(self, gpu_index: int):
+    """SM clock and throttle reasons sampled DURING the timed region: an NVML
+    thread polling every 2 ms (a 20-major timed region lasts ~50 ms, too short
+    for nvidia-smi's loop), falling back to ``nvidia-smi -lms 5``."""
+
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
+
+    def __init__(self, gpu_index: int, period_s: float = 0.002):
         self.gpu = gpu_index
+        self.period = period_s
         self.proc = None
+        self.thread = None
+        self.samples: list = []
         self.path = os.path.join("/tmp", f"rts_clocks_{os.getpid()}.csv")
 
     def start(self):
+        try:
+            import threading
+
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.gpu)
+            self._nv, self._h = nv, h
+            self._max = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            self._stop = threading.Event()
+
+            def poll():
+                get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons",
+                                getattr(nv, "nvmlDeviceGetCurrentClocksThrottleReasons", None))
+                while not self._stop.is_set():
+                    try:
+                        self.samples.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM),
+                                             get_r(h) if get_r else 0))
+                    except Exception:
+                        pass
+                    time.sleep(self.period)
+
+            self.thread = threading.Thread(target=poll, daemon=True)
+            self.thread.start()
+            return
+        except Exception:
+            self.thread = None
         q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -200,18 +240,37 @@ class ClockSampler:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={q}", "--format=csv,noheader",
-                 "-lms", "20"], stdout=self.fh, stderr=subprocess.DEVNULL)
+                 "-lms", "5"], stdout=self.fh, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
 
+    @staticmethod
+    def _summary(sm, mx, reasons, how) -> dict:
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": ["no samples"], "how": how}
+        loaded = sorted(v for v in sm if v > 0.5 * max(sm)) or sorted(sm)
+        return {"sm_mhz": loaded[len(loaded) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm), "how": how}
+
     def stop(self) -> dict:
+        if self.thread is not None:
+            self._stop.set()
+            self.thread.join()
+            nv = self._nv
+            reasons = set()
+            for _, r in self.samples:
+                for name, attr in self.REASONS:
+                    if r & getattr(nv, attr, 0):
+                        reasons.add(name)
+            return self._summary([c for c, _ in self.samples], self._max, reasons,
+                                 f"NVML poll every {self.period * 1e3:g} ms")
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
         self.proc.wait()
         self.fh.close()
         sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        names = [n for n, _ in self.REASONS]
         for line in open(self.path):
             f = [x.strip() for x in line.split(",")]
             if len(f) < 9:
@@ -224,12 +283,7 @@ class ClockSampler:
             for nm, v in zip(names, f[5:9]):
                 if v.lower() == "active":
                     reasons.add(nm)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
-        loaded = [v for v in sm if v > 0.5 * max(sm)] or sm
-        loaded.sort()
-        return {"sm_mhz": loaded[len(loaded) // 2], "sm_max_mhz": max(mx),
-                "reasons": sorted(reasons), "samples": len(sm)}
+        return self._summary(sm, max(mx) if mx else None, reasons, "nvidia-smi -lms 5")
 
 
 METRICS = {
@@ -240,14 +294,15 @@ METRICS = {
 }
 
 
-def _oracle_for(workload: str):
-    """The CPU oracle on the workload's one-GPU scene, jittered (and with the
-    workload's initial velocities) exactly as the device solver."""
+def _oracle_for(workload: str, world: int = 1):
+    """The CPU oracle on the workload's scene at ``world`` ranks (the whole
+    scene the N-GPU run simulates), jittered (and with the workload's initial
+    velocities) exactly as the device solver."""
     import numpy as np
 
     from oracle import sph as O
     kind = WORKLOADS[workload][0]
-    sc = workload_scene(workload, 1)
+    sc = workload_scene(workload, world)
     if kind == "pcisph":
         o = O.OraclePcisph(sc, mode="rts", iteration_cap=50)
     else:
@@ -297,30 +352,48 @@ def cpu_oracle_sample(majors: int = 2, warm: int = 1, workload: str = "cfg2") ->
             "seconds": round(dt, 3), "setup_s": round(t0 - t_setup, 1)}
 
 
+def bench_config(workload: str, world: int, n_fluid: int, n_boundary: int) -> dict:
+    """The ``config`` of both arms' JSON line: the workload only (scene,
+    sizes, step unit), so the two lines compare like for like."""
+    kind, wl_name, _ = WORKLOADS[workload]
+    return {"workload": wl_name, "n_fluid": n_fluid, "n_boundary": n_boundary,
+            "bench_step": ("one major step (advance(): up to 4 minor steps)" if kind == "pcisph"
+                           else "4 base steps (step())"),
+            "scene_ranks": world, "seed": SEED, "jitter": "+-1% of spacing",
+            "l2": "working set > L2 (state, tables) -- no flush needed"}
+
+
 def run_reference_arm(args, rank: int, world: int) -> None:
+    """The reference path on the host: the CPU oracle (fp64 C/OpenMP
+    restatement of the reference's numba kernels + numpy bookkeeping, all
+    host threads) on the same scene, the same --warmup and --steps."""
     if rank != 0:
         return
     kind, wl_name, scaling = WORKLOADS[args.workload]
-    o, O = _oracle_for(args.workload)
+    o, O = _oracle_for(args.workload, world)
     nf = o.n_fluid
-    warm = min(args.warmup, 1)
-    for _ in range(warm):
+    per_step = 1 if kind == "pcisph" else 4  # a WCSPH bench step = 4 base steps
+    for _ in range(args.warmup * per_step):
         o.advance()
-    # bounded sample: ~3 s CPU per 1M major here; stop after ~60 s
-    units, steps, dt = _oracle_steps(o, 60.0, max(1, min(args.steps, 6)))
+    t0 = time.perf_counter()
+    units = 0
+    for _ in range(args.steps * per_step):
+        units += len(o.advance())
+    dt = time.perf_counter() - t0
     v = nf * units / dt
     line = {
         "impl": "reference", "metric": METRICS[args.workload], "value": v, "unit": UNIT,
-        "n_gpus": world, "steps": steps, "warmup": warm, "ms_per_step": 1e3 * dt / steps,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * dt / max(1, args.steps),
         "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": wl_name, "n_fluid": nf, "updates_per_particle": units,
-                   "host_threads": O.num_threads(),
-                   "scene": "the one-GPU scene of the workload (host-sized sample)"},
+        "config": bench_config(args.workload, world, nf, len(o.pos) - nf),
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": O.num_threads(), "kind": "port",
-                         "sample": f"{steps} steps ({units} updates per particle) after "
-                                   f"{warm} untimed; CPU oracle restating the reference"},
+                         "sample": f"the full run: {args.steps} bench steps ({units} updates "
+                                   f"of each of {nf} particles) after {args.warmup} untimed; "
+                                   "CPU oracle restating the reference"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "host_threads": O.num_threads(),
     }
     print(json.dumps(line), flush=True)
 
@@ -426,12 +499,13 @@ def run_wcsph_workload(args, rank: int, world: int, device, barrier) -> None:
         solver = make_device_solver("wcsph", device, args.workload)
         driver = solver
         n_total = solver.n_fluid
+        n_bound_total = solver.n_bound
     else:
         from paper_2009_14514_b200.distributed import DistributedWcsph
         from paper_2009_14514_b200.scene import seed_particles
         sc = workload_scene(args.workload, world)
-        lattice = seed_particles(sc)[0]
-        n_total = len(lattice)
+        lattice, walls = seed_particles(sc)
+        n_total, n_bound_total = len(lattice), len(walls)
         driver = DistributedWcsph(sc, device=device, jitter=jitter_np(n_total, sc.spacing),
                                   velocity=initial_velocity(args.workload, lattice),
                                   rebalance_every=args.rebalance)
@@ -541,14 +615,13 @@ def run_wcsph_workload(args, rank: int, world: int, device, barrier) -> None:
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
             "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": wl_name, "n_fluid": n_total, "n_boundary": solver.n_bound,
-                       "base_steps": steps, "bench_step": "4 base steps",
-                       "mean_active_fraction": round(sum(r.frac_compute for r in rows) /
-                                                     max(1, len(rows)), 4),
-                       "l2": "working set > L2 (state + hit tables)",
-                       "parallelism": ("single GPU" if world == 1 else
-                                       f"x-slabs x{world} (ghost exchange + migration)"),
-                       "arithmetic": "fp32 state, fp64 density sums"},
+            "config": bench_config(args.workload, world, n_total, n_bound_total),
+            "run": {"base_steps": steps,
+                    "mean_active_fraction": round(sum(r.frac_compute for r in rows) /
+                                                  max(1, len(rows)), 4),
+                    "parallelism": ("single GPU" if world == 1 else
+                                    f"x-slabs x{world} (ghost exchange + migration)"),
+                    "arithmetic": "fp32 particle state; fp64 pair terms and sums"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk,
         }
@@ -609,12 +682,13 @@ def main():
         solver = make_device_solver("pcisph", device, args.workload)
         driver = solver
         n_total = solver.n_fluid
+        n_bound_total = solver.n_bound
     else:  # x-slab decomposition (paper_2009_14514_b200/distributed.py)
         from paper_2009_14514_b200.distributed import DistributedPcisph
         from paper_2009_14514_b200.scene import seed_particles
         sc = workload_scene(args.workload, world)
-        lattice = seed_particles(sc)[0]
-        n_total = len(lattice)
+        lattice, walls = seed_particles(sc)
+        n_total, n_bound_total = len(lattice), len(walls)
         driver = DistributedPcisph(sc, device=device, jitter=jitter_np(n_total, sc.spacing),
                                    velocity=initial_velocity(args.workload, lattice),
                                    iteration_cap=50, rebalance_every=args.rebalance)
@@ -775,16 +849,15 @@ def main():
             "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
             "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
-            "config": {"workload": wl_name, "n_fluid": nf,
-                       "n_boundary": solver.n_bound, "minor_steps": minors,
-                       "iterations_per_minor": round(sum(r.iterations for r in rows) /
-                                                     max(1, minors), 3),
-                       "corrected_per_minor_over_nf": round(sum(r.corrected for r in rows) /
-                                                           max(1, minors) / nf, 3),
-                       "l2": "working set > L2 (neighbour tables >= 512 MB + state)",
-                       "parallelism": ("single GPU" if world == 1 else
-                                       f"x-slabs x{world} (ghost exchange + allreduce)"),
-                       "arithmetic": "fp32 state, fp64 pair sums"},
+            "config": bench_config(args.workload, world, nf, n_bound_total),
+            "run": {"minor_steps": minors,
+                    "iterations_per_minor": round(sum(r.iterations for r in rows) /
+                                                  max(1, minors), 3),
+                    "corrected_per_minor_over_nf": round(sum(r.corrected for r in rows) /
+                                                        max(1, minors) / nf, 3),
+                    "parallelism": ("single GPU" if world == 1 else
+                                    f"x-slabs x{world} (ghost exchange + allreduce)"),
+                    "arithmetic": "fp32 particle state; fp64 x*, p, pair terms and sums"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk, "wcsph_rts_1m": wc,
         }

@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define RTS_ABI_VERSION 20
+#define RTS_ABI_VERSION 25
 
 /* err_flags bits */
 #define RTS_ERR_ESCAPED   0x1u  /* fluid left the padded grid or non-finite (grid.py:268-273) */
@@ -99,7 +99,12 @@ typedef struct RtsCounters {
     int32_t  pad3;
     int64_t  stamps[4];        /* RTS-WCSPH step graph: %globaltimer (ns) at the start, end of
                                 * the grid rebuild, start of the density pass, end */
-    double   reserved[2];
+    float    disp_cur;         /* PCISPH: max |dx| of one coordinate of any fluid particle in
+                                * the current minor step's integration (>= 0 float bits) */
+    float    disp_total;       /* PCISPH: sum of disp_cur over the completed minor steps of
+                                * this major: bound on any coordinate's displacement since
+                                * the rebuild (the partial refreshes cull by it) */
+    double   reserved1;
 } RtsCounters;
 
 /* Per-minor-step record written by the device loop control (StepStats,
@@ -191,6 +196,8 @@ typedef struct RtsBuffers {
     /* sorted candidate copies, slot k of the CSR */
     float   *cpos;         /* (Nf+Nb, 4)  x y z p   (p = -1 marks a boundary slot) */
     float   *cvel;         /* (Nf+Nb, 4)  vx vy vz rho */
+    double  *cterm;        /* (Nf+Nb, 4)  WCSPH: fp64 {p/rho^2, 1/rho, p, 0} of the slot's
+                            * particle from this step's density pass (force pair terms) */
     int32_t *active;       /* (Nf) compacted CSR slots of active fluid particles */
     int32_t *list2;        /* (Nf) second compacted list */
     int32_t *list3;        /* (Nf) PCISPH: force list of the previous iteration (motion
@@ -200,10 +207,11 @@ typedef struct RtsBuffers {
     int32_t *nbr;          /* (width, nbr_stride) column-major neighbour particle indices
                             * (grid.py:146-149 rows, transposed) */
     int32_t *cnt;          /* (Nf) */
-    float   *xs4;          /* (Nf+Nb, 4) fluid: x* p ; wall: pos -1 */
+    double  *xs;           /* (Nf+Nb, 4) fp64 rows {x*, p}: the pressure solve's state
+                            * (pres is p's fp32 mirror); wall rows {pos, -1} */
     uint8_t *pflag;        /* (Nf) per-iteration set bits (1 = force set) */
     double  *partial;      /* (>= 4096) deterministic reduction partials */
-    float   *snap_p;       /* (Nf)    local-phase snapshot of p */
+    double  *snap_p;       /* (Nf)    local-phase snapshot of the fp64 p (xs rows) */
     float   *snap_fp;      /* (Nf, 3) local-phase snapshot of f_p */
     int32_t *slot_of;      /* (Nf) CSR slot of each fluid particle (inverse of order) */
     RtsControl *ctl;       /* correction-loop control block */
@@ -261,7 +269,7 @@ int rts_block_levels(const RtsParams *p, const RtsBuffers *b, int expand, void *
 int rts_region_op(const RtsParams *p, const RtsBuffers *b, int op, int arg, void *stream);
 
 /* ---- RTS-PCISPH (pcisph.py) ------------------------------------------- */
-/* Wall rows of xs4 (static positions, marker -1). */
+/* Wall rows of xs (static positions as fp64, p = -1). */
 int rts_pci_walls(const RtsParams *p, const RtsBuffers *b, void *stream);
 /* Sorted candidate positions cpos[k] = pos[order[k]] and slot_of, at major
  * start; k_integrate keeps them current so the stale-grid search of later
@@ -360,6 +368,10 @@ int rts_wcsph_density(const RtsParams *p, const RtsBuffers *b, void *stream);
  * (wcsph.py:63-105) and acc = F/m (wcsph.py:296). */
 int rts_wcsph_forces(const RtsParams *p, const RtsBuffers *b, void *stream);
 /* Predictor for all, corrector for active, clamp (wcsph.py:299-319). */
+/* np.var(rho) over the fluid (wcsph.py:231-232, track_rho_variance): two
+ * fixed-order fp64 passes over b->rho using b->partial (>= 513 doubles);
+ * *out (device) = the population variance.  Deterministic. */
+int rts_rho_variance(const RtsParams *p, const RtsBuffers *b, double *out, void *stream);
 int rts_wcsph_integrate(const RtsParams *p, const RtsBuffers *b, void *stream);
 /* One whole RTS-WCSPH step as a CUDA graph (launch with rts_graph_launch,
  * destroy with rts_graph_destroy); NULL + *err on failure. */
@@ -419,10 +431,13 @@ int rts_slab_classify(const RtsSlabGeom *g, const float *pos, int n, int32_t *li
  * n_pad entries (rts_halo_pack / unpack skip rows < 0). */
 int rts_slab_holes(const uint8_t *leave, int n, int n_keep, int n_pad, int32_t *holes,
                    int32_t *fill, int32_t *counter, void *stream);
-/* out[0..3] = (max_err, any_se, sum_rho, n_pred) of ctr, as fp64. */
+#define RTS_CTL_WORDS 5
+/* out[0..4] = (max_err, any_se, sum_rho, n_pred, err_flags) of ctr, as fp64. */
 int rts_ctl_publish(const RtsBuffers *b, double *out, void *stream);
-/* ctr = fold of the all-gathered (world, 4) publish rows: MAX of max_err /
- * any_se, rank-order SUM of sum_rho / n_pred (before rts_pci_control). */
+/* ctr = fold of the all-gathered (world, RTS_CTL_WORDS) publish rows: MAX of
+ * max_err (NaN propagates) / any_se, rank-order SUM of sum_rho / n_pred, OR
+ * of err_flags into ctr->err_flags (before rts_pci_control), so every rank
+ * takes the same done / failed decision. */
 int rts_ctl_fold(const RtsBuffers *b, const double *gathered, int world, void *stream);
 
 #ifdef __cplusplus

@@ -548,10 +548,16 @@ class OraclePcisph:
 
     def __init__(self, scene: Scene, mode="rts", dt=None, schedule=DEFAULT_SCHEDULE,
                  pin_region=None, audit_neighbors=False, iteration_cap=24, local_attempts=4,
-                 n_regions=4):
+                 n_regions=4, state_f32=False):
+        """``state_f32``: not the reference -- the reference algorithm with its
+        particle state (pos, vel, f_ext, f_p, rho*) rounded to fp32 wherever
+        the B200 solver stores it as fp32 (BASELINE.json's fp32 state).  The
+        parity tests use it as the noise floor of fp32 state: how far the
+        reference itself moves when its state is stored at that precision."""
         if mode not in self.mode_names:
             raise ValueError(f"unknown pcisph mode {mode!r}")
         validate_schedule(schedule, n_regions)
+        self.state_f32 = state_f32
         self.scene, self.mode, self.schedule = scene, mode, schedule
         self.pin_region = pin_region
         self.audit_neighbors = audit_neighbors
@@ -603,6 +609,11 @@ class OraclePcisph:
         self._timers = {"neighbor": 0.0, "physics": 0.0, "rts": 0.0}
 
     # -- kernels ---------------------------------------------------------
+    def _f32(self, *arrays):
+        if self.state_f32:
+            for a in arrays:
+                a[...] = a.astype(np.float32)
+
     def delta(self, dt):
         rho0 = self.scene.rest_density
         return rho0 * rho0 / (2.0 * dt * dt * self.mass * self.mass * self._delta_factor)
@@ -782,6 +793,7 @@ class OraclePcisph:
         t0 = time.perf_counter()
         if refresh.size:
             self._ext(refresh)
+            self._f32(self.f_ext)
         self.p[:] = 0.0
         self.f_p[:] = 0.0
         self._timers["physics"] += time.perf_counter() - t0
@@ -835,9 +847,11 @@ class OraclePcisph:
             self._motion(dt)
             self._density(pred)
             self._accumulate_pressure(force, delta)
+            self._f32(self.rho_star)
             self.in_se = self.err > 0.5 * sc.eta_max
             self._refresh_observed()
             self._pforces(force)
+            self._f32(self.f_p)
             it += 1
             corrected += int(pred.size)
             if local_active:
@@ -898,6 +912,7 @@ class OraclePcisph:
         fl = self.pos[:self.n_fluid]
         fl += self.vel * dt
         _clamp(fl, self.vel, self._lo, self._hi)
+        self._f32(fl, self.vel)
 
 
 def make_oracle(scene: Scene, name: str, **kw):

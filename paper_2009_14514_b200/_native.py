@@ -12,7 +12,7 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "librtssph.so")
-ABI_VERSION = 20
+ABI_VERSION = 25
 
 _c = ctypes
 _D = _c.c_double
@@ -41,7 +41,7 @@ class RtsCounters(_c.Structure):
         ("n_list", _I), ("fmax_bits", _c.c_uint64), ("sum_rho", _D), ("max_err", _D),
         ("any_se", _I), ("lists_all", _I), ("missing", _c.c_int64),
         ("blocks_done", _c.c_uint32), ("pad3", _I), ("stamps", _c.c_int64 * 4),
-        ("reserved", _D * 2),
+        ("disp_cur", _c.c_float), ("disp_total", _c.c_float), ("reserved1", _D),
     ]
 
 
@@ -78,7 +78,7 @@ BUFFER_FIELDS = (
     "dt_corr", "validity", "region", "compute", "in_se", "in_sob", "fluid_cells", "cell_count",
     "cell_bcount", "starts", "order", "fill", "scan_tmp", "bcell_ids", "bcell_start", "bidx",
     "bcell_of", "bcell_active", "vmax", "fmax", "block_raw", "block_field", "block_tmp",
-    "block_flag", "cpos", "cvel", "active", "list2", "list3", "nbr", "cnt", "xs4", "pflag", "partial",
+    "block_flag", "cpos", "cvel", "cterm", "active", "list2", "list3", "nbr", "cnt", "xs", "pflag", "partial",
     "snap_p", "snap_fp", "slot_of", "ctl", "se_stamp", "near_stamp", "ghost", "sort_key", "ctr",
 )
 
@@ -88,6 +88,7 @@ class RtsBuffers(_c.Structure):
 
 
 HALO_MAX_FIELDS = 16
+CTL_WORDS = 5  # RTS_CTL_WORDS: rts_ctl_publish row (fp64 words)
 
 
 class RtsHaloField(_c.Structure):
@@ -156,6 +157,7 @@ SIGNATURES = {
     "rts_halo_pack": [_c.POINTER(RtsHaloSpec), _P, _c.c_int64, _P, _P],
     "rts_halo_unpack": [_c.POINTER(RtsHaloSpec), _P, _c.c_int64, _P, _P],
     "rts_ctl_publish": [_PB, _P, _P],
+    "rts_rho_variance": [_PP, _PB, _P, _P],
     "rts_slab_classify": [_c.POINTER(RtsSlabGeom), _P, _c.c_int, _P, _c.c_int64, _P, _P, _P],
     "rts_slab_holes": [_P, _c.c_int, _c.c_int, _c.c_int, _P, _P, _P, _P],
     "rts_ctl_fold": [_PB, _P, _c.c_int, _P],

@@ -70,6 +70,74 @@ RTS_DEV float4 ldg_keep(const float4 *ptr, unsigned long long pol) {
     return v;
 }
 
+// ---- predicted-position rows of the PCISPH pair passes -------------------
+// One 32-byte, 32-byte-aligned record per particle: fp64 x* (wall rows: the
+// static position) and fp64 p -- the pressure solve's internal state, kept
+// at the reference's precision (pcisph.py:202-271, 432-437): rho*, err and
+// the pressure update from a common state then equal the reference's fp64
+// results, instead of inheriting a 1e-7 rounding of x* or p that
+// p = delta (rho* - rho0) and the pressure-force sums amplify where
+// rho* ~ rho0 or the pair terms cancel.  The public p (RtsBuffers.pres) is
+// its fp32 mirror.  A neighbour gather is a single 256-bit load (one L2
+// sector) with no fp32 -> fp64 conversions.
+struct __align__(32) XsRow {
+    double x, y, z, p;
+};
+
+RTS_DEV XsRow xs_unpack(unsigned long long r0, unsigned long long r1, unsigned long long r2,
+                        unsigned long long r3) {
+    XsRow r;
+    r.x = __longlong_as_double((long long)r0);
+    r.y = __longlong_as_double((long long)r1);
+    r.z = __longlong_as_double((long long)r2);
+    r.p = __longlong_as_double((long long)r3);
+    return r;
+}
+RTS_DEV XsRow ld_xs(const XsRow *ptr) {
+    unsigned long long r0, r1, r2, r3;
+    asm volatile("ld.global.v4.b64 {%0, %1, %2, %3}, [%4];"
+                 : "=l"(r0), "=l"(r1), "=l"(r2), "=l"(r3) : "l"(ptr));
+    return xs_unpack(r0, r1, r2, r3);
+}
+RTS_DEV XsRow ld_xs_keep(const XsRow *ptr, unsigned long long pol) {
+    unsigned long long r0, r1, r2, r3;
+    asm volatile("ld.global.L2::cache_hint.v4.b64 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=l"(r0), "=l"(r1), "=l"(r2), "=l"(r3) : "l"(ptr), "l"(pol));
+    return xs_unpack(r0, r1, r2, r3);
+}
+// x* only (the density pass): the p word is not brought into registers
+RTS_DEV XsRow ld_xs3(const XsRow *ptr) {
+    XsRow r;
+    asm volatile("ld.global.v4.f64 {%0, %1, %2, _}, [%3];"
+                 : "=d"(r.x), "=d"(r.y), "=d"(r.z) : "l"(ptr));
+    r.p = 0.0;
+    return r;
+}
+RTS_DEV void st_xs(XsRow *ptr, double x, double y, double z, double p) {
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(ptr), "d"(x), "d"(y), "d"(z),
+                 "d"(p)
+                 : "memory");
+}
+// x* only (the prediction leaves p alone)
+RTS_DEV void st_xs3(XsRow *ptr, double x, double y, double z) {
+    asm volatile("st.global.v2.f64 [%0], {%1, %2};\n\tst.global.f64 [%0+16], %3;" ::"l"(ptr),
+                 "d"(x), "d"(y), "d"(z)
+                 : "memory");
+}
+
+// 32-byte fp64 records (one 256-bit access)
+RTS_DEV void st_f64x4(double *ptr, double a, double b, double c, double d) {
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(ptr), "d"(a), "d"(b), "d"(c),
+                 "d"(d)
+                 : "memory");
+}
+RTS_DEV double4 ld_f64x4(const double *ptr) {
+    double4 r;
+    asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];"
+                 : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(ptr));
+    return r;
+}
+
 // ---- exact neighbour membership ------------------------------------------
 // The reference keeps j iff fp64 ((dx^2 + dy^2) + dz^2) < h^2 (grid.py:140-144).
 // Candidates are first classified in fp32 with a +-1e-5 relative band around

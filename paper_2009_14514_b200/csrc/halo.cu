@@ -49,29 +49,38 @@ k_halo(const RtsHaloSpec s, const int32_t *__restrict__ rows, long long n,
     }
 }
 
-// ctr scalars of this rank -> out[4] (fp64): max_err, any_se, sum_rho, n_pred
+// ctr scalars of this rank -> out[5] (fp64): max_err, any_se, sum_rho,
+// n_pred, err_flags (a uint32, exact in fp64)
 __global__ void k_ctl_publish(const RtsCounters *__restrict__ c, double *__restrict__ out) {
     out[0] = c->max_err;
     out[1] = (double)c->any_se;
     out[2] = c->sum_rho;
     out[3] = (double)c->n_pred;
+    out[4] = (double)c->err_flags;
 }
 
-// all-gathered (world, 4) -> ctr: MAX of max_err / any_se, SUM (rank order)
-// of sum_rho / n_pred
+// NaN-propagating max: a rank whose err went non-finite must stop every rank
+RTS_DEV double nan_max(double a, double b) { return (a != a || b != b) ? a + b : fmax(a, b); }
+
+// all-gathered (world, 5) -> ctr: MAX of max_err / any_se (NaN wins), SUM
+// (rank order) of sum_rho / n_pred, OR of err_flags -- every rank then takes
+// the same done / failed decision in k_control
 __global__ void k_ctl_fold(RtsCounters *__restrict__ c, const double *__restrict__ g, int world) {
     double mx = g[0], se = g[1], sr = g[2], np_ = g[3];
+    uint32_t fl = (uint32_t)g[4];
     for (int r = 1; r < world; ++r) {
-        const double *q = g + 4 * r;
-        mx = fmax(mx, q[0]);
+        const double *q = g + RTS_CTL_WORDS * r;
+        mx = nan_max(mx, q[0]);
         se = fmax(se, q[1]);
         sr = __dadd_rn(sr, q[2]);
         np_ = __dadd_rn(np_, q[3]);
+        fl |= (uint32_t)q[4];
     }
     c->max_err = mx;
     c->any_se = (int32_t)se;
     c->sum_rho = sr;
     c->n_pred = (int32_t)np_;
+    c->err_flags |= fl;
 }
 
 // Slab bookkeeping of a rank's owned rows [0, n) in one pass: block column

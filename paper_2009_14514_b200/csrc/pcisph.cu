@@ -3,9 +3,9 @@
 // Neighbour tables are materialised (the minor steps deliberately reuse
 // stale tables, pcisph.py:7-10, 553-557): `nbr` row i holds reference
 // particle indices in the reference's fill order, `cnt[i]` its length.
-// Predicted positions live in `xs4` (fluid rows: x* and p; wall rows: the
-// static position and -1), so every pair kernel reads one float4 per
-// neighbour regardless of its kind.
+// Predicted positions live in `xs` (32-byte rows, common.cuh XsRow: fluid
+// rows fp64 x* and fp32 p; wall rows the static position and -1), so every
+// pair kernel reads one 256-bit record per neighbour regardless of its kind.
 //
 // Per correction iteration the host enqueues
 //   motion   x* for all fluid (first iteration / after a revert) or only for
@@ -29,7 +29,7 @@
 #define RTS_DENS_CH 3
 #endif
 #ifndef RTS_DENS_MINB
-#define RTS_DENS_MINB 10
+#define RTS_DENS_MINB 8
 #endif
 #ifndef RTS_PFOR_PF
 #define RTS_PFOR_PF 1
@@ -41,7 +41,7 @@
 #define RTS_PFOR_CH 3
 #endif
 #ifndef RTS_PFOR_MINB
-#define RTS_PFOR_MINB 8
+#define RTS_PFOR_MINB 5
 #endif
 
 using namespace rts;
@@ -78,13 +78,14 @@ RTS_DEV int trunc_axis(double x, double o, double inv, int n) {
     return (int)v;
 }
 
-// wall rows of xs4 (static positions, marker -1)
-__global__ void k_xs4_walls(const __grid_constant__ RtsParams p, RtsBuffers b) {
+RTS_DEV XsRow *xs_rows(const RtsBuffers &b) { return reinterpret_cast<XsRow *>(b.xs); }
+
+// wall rows of xs (static positions, marker -1)
+__global__ void k_xs_walls(const __grid_constant__ RtsParams p, RtsBuffers b) {
     const int nb = p.n_bound;
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nb; t += gridDim.x * blockDim.x) {
         const int j = p.n_fluid + t;
-        reinterpret_cast<float4 *>(b.xs4)[j] =
-            make_float4(b.pos[3 * j], b.pos[3 * j + 1], b.pos[3 * j + 2], -1.0f);
+        st_xs(xs_rows(b) + j, b.pos[3 * j], b.pos[3 * j + 1], b.pos[3 * j + 2], -1.0);
     }
 }
 
@@ -217,9 +218,20 @@ RTS_DEV void finish_refresh(const RtsParams &p, const RtsBuffers &b, int i, int 
 // (region-1 particles scan 125 blocks, ~1300 candidates).
 // EXT = false: the bare search (BlockGrid.search_into, grid.py:297-331) --
 // rows and counts only, `lay_in` block layers for this particle.
+//
+// Culling (D >= 0): a block of the stale window is scanned only if one of
+// its candidates can lie within h of the particle -- candidates sit in the
+// block of their position at the rebuild and have moved by at most D per
+// coordinate since (the integrator's bound, RtsCounters.disp_*).  Whole
+// block columns farther than h in x-y are skipped and each column's span is
+// clipped to the z blocks within +-sqrt(h^2 - d_xy^2) (+ D).  Rows are
+// unchanged: skipped blocks hold no member, and the kept blocks stay
+// contiguous slot ranges in the reference's order.  The region-1 two-layer
+// windows of the later minor steps (125 blocks) shrink ~5x.
 template <int G, bool EXT = true>
 RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshConsts &k, int i,
-                         int two_layer_r1, int lane, unsigned gmask, int gshift, int lay_in = 0) {
+                         int two_layer_r1, int lane, unsigned gmask, int gshift, int lay_in = 0,
+                         double D = -1.0) {
     const float4 *cpos = reinterpret_cast<const float4 *>(b.cpos);
     const int nx = p.dims[0], ny = p.dims[1], nz = p.dims[2];
     const float fxi = b.pos[3 * i], fyi = b.pos[3 * i + 1], fzi = b.pos[3 * i + 2];
@@ -237,10 +249,33 @@ RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshC
     double vfx = 0.0, vfy = 0.0, vfz = 0.0;
     int *row = b.nbr + i;  // entry q at row[q * S]
     const size_t S = p.nbr_stride;
-    for (int ax = max(0, cx - lay); ax <= min(nx - 1, cx + lay); ++ax)
+    const bool cull = D >= 0.0;
+    const double B = p.block_size, eps = 1e-9 * B;
+    const double hw2 = p.h2 * (1.0 + 2e-6);
+    for (int ax = max(0, cx - lay); ax <= min(nx - 1, cx + lay); ++ax) {
+        double ddx = 0.0;
+        if (cull) {  // x distance from the column's candidates (stale extent +- D)
+            const double xl = ax == 0 ? -1e300 : p.origin[0] + ax * B - D - eps;
+            const double xh = ax == nx - 1 ? 1e300 : p.origin[0] + (ax + 1) * B + D + eps;
+            ddx = xi < xl ? xl - xi : (xi > xh ? xi - xh : 0.0);
+        }
         for (int ay = max(0, cy - lay); ay <= min(ny - 1, cy + lay); ++ay) {
             const int base = (ax * ny + ay) * nz;
-            const int k0 = b.starts[base + z0], k1 = b.starts[base + z1 + 1];
+            int za = z0, zb = z1;
+            if (cull) {
+                const double yl = ay == 0 ? -1e300 : p.origin[1] + ay * B - D - eps;
+                const double yh = ay == ny - 1 ? 1e300 : p.origin[1] + (ay + 1) * B + D + eps;
+                const double ddy = yi < yl ? yl - yi : (yi > yh ? yi - yh : 0.0);
+                const double dxy2 = ddx * ddx + ddy * ddy;
+                if (dxy2 >= hw2) continue;  // no candidate of the column within h
+                const double w = sqrt(hw2 - dxy2) + D + eps;
+                const double fa = floor((zi - w - p.origin[2]) * p.inv_block);
+                const double fb = floor((zi + w - p.origin[2]) * p.inv_block);
+                za = fa > (double)z0 ? (int)fa : z0;
+                zb = fb < (double)z1 ? (int)fb : z1;
+                if (za > zb) continue;
+            }
+            const int k0 = b.starts[base + za], k1 = b.starts[base + zb + 1];
             if (G == 1) {
                 // Branch-free classification of 32 candidates at a time: two
                 // 32-bit masks (r2 < h2_lo: member; r2 > h2_hi: not) built
@@ -348,6 +383,7 @@ RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshC
                 }
             }
         }
+    }
     if (G > 1) __syncwarp(gmask);
     if (!EXT) {
         if (lane == 0) finish_search(p, b, i, cntn);
@@ -373,7 +409,14 @@ RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshC
     if (lane == 0) finish_refresh(p, b, i, cntn, fx, fy, fz);
 }
 
-__global__ void __launch_bounds__(kThreads, 8) k_refresh(const __grid_constant__ RtsParams p,
+#ifndef RTS_CULL_G1
+#define RTS_CULL_G1 0  // culling in the one-thread-per-particle path (lanes diverge)
+#endif
+#ifndef RTS_REF_MINB
+#define RTS_REF_MINB 8
+#endif
+
+__global__ void __launch_bounds__(kThreads, RTS_REF_MINB) k_refresh(const __grid_constant__ RtsParams p,
                                                       RtsBuffers b, int two_layer_r1) {
     RTS_MINOR_GUARD();
     const int n = b.ctr->n_compute;
@@ -381,17 +424,21 @@ __global__ void __launch_bounds__(kThreads, 8) k_refresh(const __grid_constant__
     const int nthreads = gridDim.x * blockDim.x;
     const int tid = blockIdx.x * blockDim.x + threadIdx.x;
     const int wl = threadIdx.x & 31;
+    // displacement bound of the candidates since the rebuild (+1e-5 relative:
+    // measured in fp32); x-slab ranks: ghosts move on other ranks -> no culling
+    const double D = b.ghost ? -1.0
+                             : 1.00001 * ((double)b.ctr->disp_total + (double)b.ctr->disp_cur);
     if ((long long)n * 32 <= nthreads) {
         for (int t = tid / 32; t < n; t += nthreads / 32)
-            refresh_one<32>(p, b, k, b.active[t], two_layer_r1, wl, 0xffffffffu, 0);
+            refresh_one<32>(p, b, k, b.active[t], two_layer_r1, wl, 0xffffffffu, 0, 0, D);
     } else if ((long long)n * 8 <= nthreads) {
         const int lane = wl & 7, gshift = wl & ~7;
         const unsigned gmask = 0xffu << gshift;
         for (int t = tid / 8; t < n; t += nthreads / 8)
-            refresh_one<8>(p, b, k, b.active[t], two_layer_r1, lane, gmask, gshift);
+            refresh_one<8>(p, b, k, b.active[t], two_layer_r1, lane, gmask, gshift, 0, D);
     } else {
         for (int t = tid; t < n; t += nthreads)
-            refresh_one<1>(p, b, k, b.active[t], two_layer_r1, 0, 0u, 0);
+            refresh_one<1>(p, b, k, b.active[t], two_layer_r1, 0, 0u, 0, 0, RTS_CULL_G1 ? D : -1.0);
     }
 }
 
@@ -404,22 +451,28 @@ __global__ void __launch_bounds__(kThreads) k_search(const __grid_constant__ Rts
         refresh_one<1, false>(p, b, k, b.active[t], 0, 0, 0u, 0, layers[t]);
 }
 
-// x* = pos + dt * (vel + dt/m (f_ext + f_p)) (pcisph.py:202-213); xs4.w = p
+// x* = pos + dt * (vel + dt/m (f_ext + f_p)) (pcisph.py:202-213), kept in
+// fp64 in the xs row (the row's p is the density pass's)
 RTS_DEV void motion_one(const RtsParams &p, const RtsBuffers &b, int i, double dt_inv_m) {
-    float xs[3];
+    double xs[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
         const double f = xadd((double)b.force[3 * i + a], (double)b.f_p[3 * i + a]);
         const double v = xadd((double)b.vel[3 * i + a], xmul(dt_inv_m, f));
-        xs[a] = (float)xadd((double)b.pos[3 * i + a], xmul(p.dt, v));
+        xs[a] = xadd((double)b.pos[3 * i + a], xmul(p.dt, v));
     }
-    reinterpret_cast<float4 *>(b.xs4)[i] = make_float4(xs[0], xs[1], xs[2], b.pres[i]);
+    st_xs3(xs_rows(b) + i, xs[0], xs[1], xs[2]);
 }
 
+// the fp64 p of row i (and its fp32 public mirror)
+RTS_DEV void set_p(const RtsBuffers &b, int i, double pr) {
+    b.pres[i] = (float)pr;
+    b.xs[4 * i + 3] = pr;
+}
 
 // restore p, f_p of particle i from the local-phase entry snapshot
 RTS_DEV void restore_one(const RtsBuffers &b, int i) {
-    b.pres[i] = b.snap_p[i];
+    set_p(b, i, b.snap_p[i]);
     b.f_p[3 * i] = b.snap_fp[3 * i];
     b.f_p[3 * i + 1] = b.snap_fp[3 * i + 1];
     b.f_p[3 * i + 2] = b.snap_fp[3 * i + 2];
@@ -450,42 +503,47 @@ __global__ void k_motion(const __grid_constant__ RtsParams p, RtsBuffers b, int 
         return;
     }
     const int nf = p.n_fluid, ng = nf / 4;
-    float4 *xs4 = reinterpret_cast<float4 *>(b.xs4);
+    XsRow *xsr = xs_rows(b);
     for (int g = tid; g < ng; g += nt) {
         float fe[12], fp[12], v[12], x[12];
         load12(b.force, g, fe);
         load12(b.vel, g, v);
         load12(b.pos, g, x);
-        float4 pr;
+        double pr[4] = {0.0, 0.0, 0.0, 0.0};
         if (zero) {
 #pragma unroll
             for (int c = 0; c < 12; ++c) fp[c] = 0.f;
-            pr = make_float4(0.f, 0.f, 0.f, 0.f);
         } else {
             load12(restore ? b.snap_fp : b.f_p, g, fp);
-            pr = reinterpret_cast<const float4 *>(restore ? b.snap_p : b.pres)[g];
+            if (restore) {
+                const double2 s01 = reinterpret_cast<const double2 *>(b.snap_p)[2 * g];
+                const double2 s23 = reinterpret_cast<const double2 *>(b.snap_p)[2 * g + 1];
+                pr[0] = s01.x, pr[1] = s01.y, pr[2] = s23.x, pr[3] = s23.y;
+            }
         }
         if (restore || zero) {
             store12(b.f_p, g, fp);
-            reinterpret_cast<float4 *>(b.pres)[g] = pr;
+            reinterpret_cast<float4 *>(b.pres)[g] =
+                make_float4((float)pr[0], (float)pr[1], (float)pr[2], (float)pr[3]);
         }
-        const float prs[4] = {pr.x, pr.y, pr.z, pr.w};
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            float xs[3];
+            double xs[3];
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
                 const int c = 3 * q + a;
                 const double vv = xadd((double)v[c], xmul(dim, xadd((double)fe[c], (double)fp[c])));
-                xs[a] = (float)xadd((double)x[c], xmul(p.dt, vv));
+                xs[a] = xadd((double)x[c], xmul(p.dt, vv));
             }
-            if (!is_ghost(b, 4 * g + q)) xs4[4 * g + q] = make_float4(xs[0], xs[1], xs[2], prs[q]);
+            if (is_ghost(b, 4 * g + q)) continue;
+            if (restore || zero) st_xs(xsr + 4 * g + q, xs[0], xs[1], xs[2], pr[q]);
+            else st_xs3(xsr + 4 * g + q, xs[0], xs[1], xs[2]);
         }
     }
     for (int i = 4 * ng + tid; i < nf; i += nt) {
         if (restore) restore_one(b, i);
         if (zero) {
-            b.pres[i] = 0.f;
+            set_p(b, i, 0.0);
             b.f_p[3 * i] = b.f_p[3 * i + 1] = b.f_p[3 * i + 2] = 0.f;
         }
         if (!is_ghost(b, i)) motion_one(p, b, i, dim);
@@ -506,7 +564,7 @@ __global__ void __launch_bounds__(256) k_sets(const __grid_constant__ RtsParams 
     // snapshots p, f_p of every fluid particle here (motion leaves them alone)
     if (b.ctl && b.ctl->snap_op == 1) {
         for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nf; i += gridDim.x * blockDim.x) {
-            b.snap_p[i] = b.pres[i];
+            b.snap_p[i] = b.xs[4 * i + 3];
             b.snap_fp[3 * i] = b.f_p[3 * i];
             b.snap_fp[3 * i + 1] = b.f_p[3 * i + 1];
             b.snap_fp[3 * i + 2] = b.f_p[3 * i + 2];
@@ -618,8 +676,8 @@ template <int LG, int CH = 8>
 RTS_DEV void density_one(const RtsParams &p, const RtsBuffers &b, int i, int lane,
                          unsigned gmask) {
     if (is_ghost(b, i)) return;
-    const float4 *xs4 = reinterpret_cast<const float4 *>(b.xs4);
-    const float4 a = xs4[i];
+    const XsRow *xsr = xs_rows(b);
+    const XsRow a = ld_xs(xsr + i);  // own row: x* and the fp64 p of the last update
     const double xi = a.x, yi = a.y, zi = a.z;
     const int c = b.cnt[i];
     const int *row = b.nbr + i;  // entry q at row[q * S]: coalesced across lanes
@@ -629,26 +687,26 @@ RTS_DEV void density_one(const RtsParams &p, const RtsBuffers &b, int i, int lan
         // two-stage pipeline: table entries two chunks ahead, x* gathers one
         // chunk ahead of the chunk being summed
         int jn[CH];
-        float4 on[CH];
+        XsRow on[CH];
 #pragma unroll
         for (int u = 0; u < CH; ++u) jn[u] = u < c ? __ldcs(row + u * S) : i;
 #pragma unroll
-        for (int u = 0; u < CH; ++u) on[u] = xs4[jn[u]];
+        for (int u = 0; u < CH; ++u) on[u] = ld_xs3(xsr + jn[u]);
 #pragma unroll
         for (int u = 0; u < CH; ++u) jn[u] = CH + u < c ? __ldcs(row + (CH + u) * S) : i;
         for (int q = 0; q < c; q += CH) {
-            float4 o[CH];
+            XsRow o[CH];
 #pragma unroll
             for (int u = 0; u < CH; ++u) {
                 o[u] = on[u];
-                on[u] = xs4[jn[u]];
+                on[u] = ld_xs3(xsr + jn[u]);
                 jn[u] = q + 2 * CH + u < c ? __ldcs(row + (q + 2 * CH + u) * S) : i;
             }
 #pragma unroll
             for (int u = 0; u < CH; ++u) {
                 if (q + u < c)
-                    acc = xadd(acc, poly6(dist2(xsub(xi, (double)o[u].x), xsub(yi, (double)o[u].y),
-                                                xsub(zi, (double)o[u].z)),
+                    acc = xadd(acc, poly6(dist2(xsub(xi, o[u].x), xsub(yi, o[u].y),
+                                                xsub(zi, o[u].z)),
                                           p.h2, p.c_poly6));
             }
         }
@@ -665,31 +723,31 @@ RTS_DEV void density_one(const RtsParams &p, const RtsBuffers &b, int i, int lan
                 j8[u] = jn[u];
                 jn[u] = q + CH + u < c ? __ldcs(row + (q + CH + u) * S) : i;
             }
-            float4 o[CH];
+            XsRow o[CH];
 #pragma unroll
-            for (int u = 0; u < CH; ++u) o[u] = xs4[j8[u]];
+            for (int u = 0; u < CH; ++u) o[u] = ld_xs3(xsr + j8[u]);
 #pragma unroll
             for (int u = 0; u < CH; ++u) {
                 if (q + u < c)
-                    acc = xadd(acc, poly6(dist2(xsub(xi, (double)o[u].x), xsub(yi, (double)o[u].y),
-                                                xsub(zi, (double)o[u].z)),
+                    acc = xadd(acc, poly6(dist2(xsub(xi, o[u].x), xsub(yi, o[u].y),
+                                                xsub(zi, o[u].z)),
                                           p.h2, p.c_poly6));
             }
         }
     } else {
         // RTS_LG_CH entries per lane in flight (same per-lane order)
         for (int q0 = lane; q0 < c; q0 += LG * RTS_LG_CH) {
-            float4 o[RTS_LG_CH];
+            XsRow o[RTS_LG_CH];
 #pragma unroll
             for (int u = 0; u < RTS_LG_CH; ++u) {
                 const int q = q0 + u * LG;
-                o[u] = xs4[q < c ? row[q * S] : i];
+                o[u] = ld_xs3(xsr + (q < c ? row[q * S] : i));
             }
 #pragma unroll
             for (int u = 0; u < RTS_LG_CH; ++u)
                 if (q0 + u * LG < c)
-                    acc = xadd(acc, poly6(dist2(xsub(xi, (double)o[u].x), xsub(yi, (double)o[u].y),
-                                                xsub(zi, (double)o[u].z)),
+                    acc = xadd(acc, poly6(dist2(xsub(xi, o[u].x), xsub(yi, o[u].y),
+                                                xsub(zi, o[u].z)),
                                           p.h2, p.c_poly6));
         }
 #pragma unroll
@@ -702,10 +760,9 @@ RTS_DEV void density_one(const RtsParams &p, const RtsBuffers &b, int i, int lan
         b.err[i] = diff > 0.0 ? xdiv(diff, p.rho0) : 0.0;
         if (!isfinite(rho)) atomicOr(&b.ctr->err_flags, RTS_ERR_NONFINITE);
         if (b.ctr->lists_all || b.pflag[i]) {
-            double pr = xadd((double)b.pres[i], xmul(p.delta, diff));
+            double pr = xadd(a.p, xmul(p.delta, diff));
             pr = pr > 0.0 ? pr : 0.0;
-            b.pres[i] = (float)pr;
-            reinterpret_cast<float *>(b.xs4)[4 * i + 3] = (float)pr;  // .w only
+            set_p(b, i, pr);
         }
     }
 }
@@ -741,8 +798,11 @@ RTS_DEV void se_one(const RtsParams &p, const RtsBuffers &b, int i, double e, fl
                     uint8_t &flag) {
     const bool se = with_se && e > thr;
     flag = se;
+    const bool ghost = is_ghost(b, i);
     if (se) {
-        any = 1;
+        // ghost rows keep their S_e flag and block stamps, but any(S_e) is
+        // the owners' to report (a ghost's err may be stale here)
+        if (!ghost) any = 1;
         const int c = b.fluid_cells[i];
         if (atomicExch(&b.se_stamp[c], gen) != gen) {  // first S_e particle of block c
             const int nx = p.dims[0], ny = p.dims[1], nz = p.dims[2];
@@ -755,7 +815,7 @@ RTS_DEV void se_one(const RtsParams &p, const RtsBuffers &b, int i, double e, fl
                 }
         }
     }
-    if (is_ghost(b, i)) return;  // reductions over owned particles (all-reduced)
+    if (ghost) return;  // reductions over owned particles (all-reduced)
     if (e > m) m = e;
     s = xadd(s, (double)rho);
 }
@@ -869,35 +929,36 @@ __global__ void k_observed(const __grid_constant__ RtsParams p, RtsBuffers b, in
 // adaptive granularity as k_density.
 template <class T>
 RTS_DEV void pforce_pair(const RtsParams &p, double xi, double yi, double zi, double term_i,
-                         double wall, double m2c, double inv_rho0_sq, int i, int j, float4 o,
+                         double wall, double m2c, double inv_rho0_sq, int i, int j, XsRow o,
                          T &fx, T &fy, T &fz) {
-    // f_p is a 1e-4-parity quantity: each pair term in fp32 (differences of
-    // the fp32 positions, rsqrt for 1/r; ~1e-7 relative per term, below the
-    // fp32 state's own rounding of x* and p), summed in fp64 in row order
+    // One pair term of _pressure_forces (pcisph.py:255-268) in fp64, in the
+    // reference's operand order except 1/r (fp64 rsqrt, ~1 ulp, instead of
+    // a division): ~1e-16 relative per term, so f_p keeps 1e-4 parity even
+    // where the pair terms cancel (|f_p| << sum |terms|)
     if (j == i) return;
-    const float dx = (float)xi - o.x, dy = (float)yi - o.y, dz = (float)zi - o.z;
-    const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-    if (!(r2 > 0.f) || !(r2 < (float)p.h2)) return;  // r <= 0 or r >= h
-    const float term = j < p.n_fluid ? fmaf(o.w, (float)inv_rho0_sq, (float)term_i) : (float)wall;
-    const float rinv = rsqrtf(r2);
-    const float d = fmaf(-r2, rinv, (float)p.h);  // h - r
-    const float s = (float)m2c * term * d * d * rinv;
-    fx -= (T)(s * dx);
-    fy -= (T)(s * dy);
-    fz -= (T)(s * dz);
+    const double dx = xsub(xi, o.x), dy = xsub(yi, o.y), dz = xsub(zi, o.z);
+    const double r2 = dist2(dx, dy, dz);
+    if (!(r2 > 0.0) || !(r2 < p.h2)) return;  // r <= 0 or r >= h
+    const double term = j < p.n_fluid ? xadd(term_i, xmul(o.p, inv_rho0_sq)) : wall;
+    const double rinv = rsqrt(r2);
+    const double d = xsub(p.h, xmul(r2, rinv));  // h - r
+    const double s = xmul(xmul(m2c, term), xmul(xmul(xmul(p.c_spiky, d), d), rinv));
+    fx = xsub(fx, xmul(s, dx));
+    fy = xsub(fy, xmul(s, dy));
+    fz = xsub(fz, xmul(s, dz));
 }
 
 template <int LG, int kPF = 4>
 RTS_DEV void pforce_one(const RtsParams &p, const RtsBuffers &b, int i, int lane,
                         unsigned gmask) {
     if (is_ghost(b, i)) return;
-    const float4 *xs4 = reinterpret_cast<const float4 *>(b.xs4);
-    const double m2 = xmul(xmul(p.mass, p.mass), p.c_spiky);  // m^2 c_spiky
+    const XsRow *xsr = xs_rows(b);
+    const double m2 = xmul(p.mass, p.mass);  // m^2 (c_spiky applied per pair)
     const double inv_rho0_sq = xdiv(1.0, xmul(p.rho0, p.rho0));
-    const float4 a = xs4[i];
+    const XsRow a = ld_xs(xsr + i);
     const unsigned long long pol = l2_keep_policy();
     const double xi = a.x, yi = a.y, zi = a.z;
-    const double term_i = xmul((double)a.w, inv_rho0_sq);
+    const double term_i = xmul(a.p, inv_rho0_sq);
     const double wall = xadd(term_i, term_i);
     const int c = b.cnt[i];
     const int *row = b.nbr + i;  // entry q at row[q * S]: coalesced across lanes
@@ -906,33 +967,29 @@ RTS_DEV void pforce_one(const RtsParams &p, const RtsBuffers &b, int i, int lane
     if (LG == 1 && RTS_PFOR_PF) {
         // x* / p gathers one chunk ahead, table entries two chunks ahead
         int jn[kPF], jc[kPF];
-        float4 on[kPF];
+        XsRow on[kPF];
 #pragma unroll
         for (int u = 0; u < kPF; ++u) jc[u] = u < c ? __ldcs(row + u * S) : i;
 #pragma unroll
-        for (int u = 0; u < kPF; ++u) on[u] = ldg_keep(xs4 + jc[u], pol);
+        for (int u = 0; u < kPF; ++u) on[u] = ld_xs_keep(xsr + jc[u], pol);
 #pragma unroll
         for (int u = 0; u < kPF; ++u) jn[u] = kPF + u < c ? __ldcs(row + (kPF + u) * S) : i;
         for (int q = 0; q < c; q += kPF) {
             int j4[kPF];
-            float4 o4[kPF];
+            XsRow o4[kPF];
 #pragma unroll
             for (int u = 0; u < kPF; ++u) {
                 j4[u] = jc[u];
                 o4[u] = on[u];
                 jc[u] = jn[u];
-                on[u] = ldg_keep(xs4 + jn[u], pol);
+                on[u] = ld_xs_keep(xsr + jn[u], pol);
                 jn[u] = q + 2 * kPF + u < c ? __ldcs(row + (q + 2 * kPF + u) * S) : i;
             }
-            float gx = 0.f, gy = 0.f, gz = 0.f;
 #pragma unroll
             for (int u = 0; u < kPF; ++u)
                 if (q + u < c)
                     pforce_pair(p, xi, yi, zi, term_i, wall, m2, inv_rho0_sq, i, j4[u], o4[u],
-                                gx, gy, gz);
-            fx += (double)gx;
-            fy += (double)gy;
-            fz += (double)gz;
+                                fx, fy, fz);
         }
     } else if (LG == 1) {
         int jn[kPF];  // software-pipelined table reads, as in density_one
@@ -945,29 +1002,24 @@ RTS_DEV void pforce_one(const RtsParams &p, const RtsBuffers &b, int i, int lane
                 j4[u] = jn[u];
                 jn[u] = q + kPF + u < c ? __ldcs(row + (q + kPF + u) * S) : i;
             }
-            float4 o4[kPF];
+            XsRow o4[kPF];
 #pragma unroll
-            for (int u = 0; u < kPF; ++u) o4[u] = ldg_keep(xs4 + j4[u], pol);
-            // the chunk's terms summed in fp32, the chunk sums in fp64
-            float gx = 0.f, gy = 0.f, gz = 0.f;
+            for (int u = 0; u < kPF; ++u) o4[u] = ld_xs_keep(xsr + j4[u], pol);
 #pragma unroll
             for (int u = 0; u < kPF; ++u)
                 if (q + u < c)
                     pforce_pair(p, xi, yi, zi, term_i, wall, m2, inv_rho0_sq, i, j4[u], o4[u],
-                                gx, gy, gz);
-            fx += (double)gx;
-            fy += (double)gy;
-            fz += (double)gz;
+                                fx, fy, fz);
         }
     } else {
         for (int q0 = lane; q0 < c; q0 += LG * RTS_LG_CH) {
             int j[RTS_LG_CH];
-            float4 o[RTS_LG_CH];
+            XsRow o[RTS_LG_CH];
 #pragma unroll
             for (int u = 0; u < RTS_LG_CH; ++u) {
                 const int q = q0 + u * LG;
                 j[u] = q < c ? row[q * S] : i;
-                o[u] = xs4[j[u]];
+                o[u] = ld_xs(xsr + j[u]);
             }
 #pragma unroll
             for (int u = 0; u < RTS_LG_CH; ++u)
@@ -1025,20 +1077,30 @@ RTS_DEV void block_maxima_one(const RtsBuffers &b, int c, const float *v, const 
     atomic_max_pos(&b.fmax[c], xsqrt(dist2(fx, fy, fz)));
 }
 
+// the refresh culling bound: max coordinate displacement of this minor step
+// (one atomic per warp; non-negative floats order as their bit patterns)
+RTS_DEV void note_displacement(const RtsBuffers &b, int countdown, float dmax) {
+    if (!countdown) return;
+    for (int o = 16; o > 0; o >>= 1) dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+    if ((threadIdx.x & 31) == 0 && dmax > 0.f)
+        atomicMax(reinterpret_cast<unsigned *>(&b.ctr->disp_cur), __float_as_uint(dmax));
+}
+
 RTS_DEV void integrate_one(const RtsParams &p, const RtsBuffers &b, int i, int countdown,
-                           int gen, double dim) {
+                           int gen, double dim, float &dmax) {
     // public x* = the last prediction; S_ob from the final S_e generation
-    const float4 xs = reinterpret_cast<const float4 *>(b.xs4)[i];
-    b.xstar[3 * i] = xs.x;
-    b.xstar[3 * i + 1] = xs.y;
-    b.xstar[3 * i + 2] = xs.z;
+    const XsRow xs = ld_xs(xs_rows(b) + i);
+    b.xstar[3 * i] = (float)xs.x;
+    b.xstar[3 * i + 1] = (float)xs.y;
+    b.xstar[3 * i + 2] = (float)xs.z;
     if (countdown) b.in_sob[i] = observed_block(b, b.fluid_cells[i], gen);
     float nx[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
         const double f = xadd((double)b.force[3 * i + a], (double)b.f_p[3 * i + a]);
         double v = xadd((double)b.vel[3 * i + a], xmul(f, dim));
-        double x = xadd((double)b.pos[3 * i + a], xmul(v, p.dt));
+        const float x0 = b.pos[3 * i + a];
+        double x = xadd((double)x0, xmul(v, p.dt));
         if (x < p.clamp_lo[a]) {
             x = p.clamp_lo[a];
             v = 0.0;
@@ -1049,6 +1111,7 @@ RTS_DEV void integrate_one(const RtsParams &p, const RtsBuffers &b, int i, int c
         b.pos[3 * i + a] = (float)x;
         b.vel[3 * i + a] = (float)v;
         nx[a] = (float)x;
+        dmax = fmaxf(dmax, fabsf(nx[a] - x0));
     }
     if (countdown & 2) block_maxima_one(b, b.fluid_cells[i], &b.vel[3 * i], &b.force[3 * i],
                                         &b.f_p[3 * i]);
@@ -1080,9 +1143,11 @@ __global__ void k_integrate(const __grid_constant__ RtsParams p, RtsBuffers b, i
         b.ctl->stats[b.ctl->minor].t_looped = gtimer();
     const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
     const int nf = p.n_fluid;
+    float dmax = 0.f;  // max |dx| of one coordinate (refresh culling bound)
     if (b.ghost) {
         for (int i = tid; i < nf; i += nt)
-            if (!is_ghost(b, i)) integrate_one(p, b, i, countdown, gen, dim);
+            if (!is_ghost(b, i)) integrate_one(p, b, i, countdown, gen, dim, dmax);
+        note_displacement(b, countdown, dmax);
         return;
     }
     const int ng = nf / 4;
@@ -1094,10 +1159,10 @@ __global__ void k_integrate(const __grid_constant__ RtsParams p, RtsBuffers b, i
         load12(b.pos, g, x);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            const float4 xs = reinterpret_cast<const float4 *>(b.xs4)[4 * g + q];
-            xsv[3 * q] = xs.x;
-            xsv[3 * q + 1] = xs.y;
-            xsv[3 * q + 2] = xs.z;
+            const XsRow xs = ld_xs(xs_rows(b) + 4 * g + q);
+            xsv[3 * q] = (float)xs.x;
+            xsv[3 * q + 1] = (float)xs.y;
+            xsv[3 * q + 2] = (float)xs.z;
         }
         store12(b.xstar, g, xsv);
 #pragma unroll
@@ -1113,8 +1178,10 @@ __global__ void k_integrate(const __grid_constant__ RtsParams p, RtsBuffers b, i
                 xx = p.clamp_hi[a];
                 vv = 0.0;
             }
+            const float x0 = x[c];
             x[c] = (float)xx;
             v[c] = (float)vv;
+            dmax = fmaxf(dmax, fabsf(x[c] - x0));
         }
         store12(b.pos, g, x);
         store12(b.vel, g, v);
@@ -1145,7 +1212,8 @@ __global__ void k_integrate(const __grid_constant__ RtsParams p, RtsBuffers b, i
             reinterpret_cast<uchar4 *>(b.in_sob)[g] = make_uchar4(sob[0], sob[1], sob[2], sob[3]);
         }
     }
-    for (int i = 4 * ng + tid; i < nf; i += nt) integrate_one(p, b, i, countdown, gen, dim);
+    for (int i = 4 * ng + tid; i < nf; i += nt) integrate_one(p, b, i, countdown, gen, dim, dmax);
+    note_displacement(b, countdown, dmax);
 }
 
 // _mark_timestep_updates (pcisph.py:718-755), block part: block_raw holds the
@@ -1225,12 +1293,12 @@ __global__ void k_snapshot(const __grid_constant__ RtsParams p, RtsBuffers b, in
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.n_fluid;
          i += gridDim.x * blockDim.x) {
         if (!restore) {
-            b.snap_p[i] = b.pres[i];
+            b.snap_p[i] = b.xs[4 * i + 3];
             b.snap_fp[3 * i] = b.f_p[3 * i];
             b.snap_fp[3 * i + 1] = b.f_p[3 * i + 1];
             b.snap_fp[3 * i + 2] = b.f_p[3 * i + 2];
         } else {
-            b.pres[i] = b.snap_p[i];
+            set_p(b, i, b.snap_p[i]);
             b.f_p[3 * i] = b.snap_fp[3 * i];
             b.f_p[3 * i + 1] = b.snap_fp[3 * i + 1];
             b.f_p[3 * i + 2] = b.snap_fp[3 * i + 2];
@@ -1246,7 +1314,7 @@ __global__ void k_zero_pressure(const __grid_constant__ RtsParams p, RtsBuffers 
         b.ctl->stats[b.ctl->minor].t_refreshed = gtimer();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.n_fluid;
          i += gridDim.x * blockDim.x) {
-        b.pres[i] = 0.0f;
+        set_p(b, i, 0.0);
         b.f_p[3 * i] = 0.0f;
         b.f_p[3 * i + 1] = 0.0f;
         b.f_p[3 * i + 2] = 0.0f;
@@ -1277,6 +1345,9 @@ __global__ void k_minor_begin(RtsBuffers b, int minor, int sync_mode) {
     }
     c->minor = minor;
     c->stats[minor].t_begin = gtimer();
+    // refresh culling: the last minor step's displacement joins the bound
+    b.ctr->disp_total = __fadd_ru(b.ctr->disp_total, b.ctr->disp_cur);
+    b.ctr->disp_cur = 0.f;
     c->it = c->g_count = c->local_active = c->local_banned = c->local_run = 0;
     c->early = 0;
     c->done = 0;
@@ -1462,7 +1533,7 @@ int rts_pci_audit(const RtsParams *pa, const RtsBuffers *a, const RtsBuffers *b,
 
 int rts_pci_walls(const RtsParams *p, const RtsBuffers *b, void *stream) {
     if (p->n_bound <= 0) return 0;
-    rts_note_launch(), k_xs4_walls<<<rts_blocks(p->n_bound, 256), 256, 0, (cudaStream_t)stream>>>(*p, *b);
+    rts_note_launch(), k_xs_walls<<<rts_blocks(p->n_bound, 256), 256, 0, (cudaStream_t)stream>>>(*p, *b);
     RTS_LAUNCH_CHECK();
     return 0;
 }

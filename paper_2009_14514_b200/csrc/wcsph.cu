@@ -39,10 +39,13 @@ __global__ void __launch_bounds__(256) k_propagate(const __grid_constant__ RtsPa
             const float x = b.pos[3 * j], y = b.pos[3 * j + 1], z = b.pos[3 * j + 2];
             if (j < p.n_fluid) {
                 const double rho = b.rho[j], pr = b.pres[j];
-                reinterpret_cast<float4 *>(b.cpos)[k] =
-                    make_float4(x, y, z, (float)xdiv(pr, xmul(rho, rho)));
+                const double term = xdiv(pr, xmul(rho, rho)), inv_rho = xdiv(1.0, rho);
+                reinterpret_cast<float4 *>(b.cpos)[k] = make_float4(x, y, z, (float)term);
                 reinterpret_cast<float4 *>(b.cvel)[k] = make_float4(
-                    b.vel[3 * j], b.vel[3 * j + 1], b.vel[3 * j + 2], (float)xdiv(1.0, rho));
+                    b.vel[3 * j], b.vel[3 * j + 1], b.vel[3 * j + 2], (float)inv_rho);
+                // the stored density / pressure of the slot's particle, fp64
+                // (active particles overwrite it in the density pass)
+                st_f64x4(b.cterm + 4 * (size_t)k, term, inv_rho, pr, rho);
                 if (p.rts) {
                     const int8_t blk = b.block_field[b.fluid_cells[j]];
                     int v = b.validity[j] - 1;
@@ -206,43 +209,44 @@ __global__ void __launch_bounds__(kThreads) k_density(const __grid_constant__ Rt
         if (!isfinite(rho)) atomicOr(&b.ctr->err_flags, RTS_ERR_NONFINITE);
         b.rho[j] = (float)rho;
         b.pres[j] = (float)pr;
-        // publish p/rho^2 and 1/rho for the force pass (only .w of slot k
-        // changes; the concurrent readers of cpos in this kernel use .xyz)
-        const double rho_s = (float)rho, pr_s = (float)pr;  // the stored fp32 state
-        reinterpret_cast<float *>(b.cpos)[4 * k + 3] = (float)xdiv(pr_s, xmul(rho_s, rho_s));
-        reinterpret_cast<float *>(b.cvel)[4 * k + 3] = (float)xdiv(1.0, rho_s);
+        // publish p/rho^2 (wcsph.py:78, the reference's expression), 1/rho and
+        // p in fp64 for the force pass: the pair terms then use this step's
+        // fp64 density and pressure, as the reference does, not their fp32
+        // stores (whose 6e-8 rounding the cancelling pair sums amplify)
+        st_f64x4(b.cterm + 4 * (size_t)k, xdiv(pr, xmul(rho, rho)), xdiv(1.0, rho), pr, rho);
     }
 }
 
-// One pair term of _forces (wcsph.py:75-101), accumulated in fp64 in the
-// reference's neighbour order.  The per-particle factors p_j/rho_j^2 and
-// 1/rho_j are published once per particle (fp32) and r, 1/r come from one
-// fp64 rsqrt, so a pair costs no fp64 division or sqrt; the deviation from
-// the reference's per-pair divisions is ~1e-7 relative (bar: 1e-4).
+// One pair term of _forces (wcsph.py:75-101) in fp64, accumulated in the
+// reference's neighbour order, in its operand order except that 1/r comes
+// from an fp64 rsqrt (~1 ulp) instead of a sqrt and a division, and the
+// viscosity's 1/(rho_i rho_j) from the published fp64 reciprocals: ~1e-16
+// relative per term, so the force keeps 1e-4 parity even where the pair
+// terms cancel (hydrostatic rest: |F| << sum |terms|).
 RTS_DEV void force_pair(const RtsParams &p, double xi, double yi, double zi, float4 va,
                         double inv_rho_i, double term_i, double wall_term, double m2, double mum2,
-                        float4 o, float4 vo, double &fx, double &fy, double &fz) {
-    // one pair term in fp32 (force / acc are 1e-4-parity quantities: ~1e-7
-    // relative per term), accumulated in fp64 in the reference's order
-    const float dx = (float)xi - o.x, dy = (float)yi - o.y, dz = (float)zi - o.z;
-    const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-    const float rinv = r2 > 0.f ? rsqrtf(r2) : 0.f;  // r = 0: spiky 0, viscosity kept
-    const float r = r2 * rinv;
-    const float hf = (float)p.h;
-    if (r >= hf) return;
-    const float d = hf - r;
-    const float spk = (float)p.c_spiky * d * d * rinv;
-    if (o.w >= 0.0f) {  // fluid neighbour: o.w = p_j / rho_j^2, vo.w = 1 / rho_j
-        const float sc = (float)m2 * ((float)term_i + o.w) * spk;
-        const float lap = (float)xmul(mum2, p.c_visc) * d * (float)inv_rho_i * vo.w;
-        fx += (double)(lap * (vo.x - va.x) - sc * dx);
-        fy += (double)(lap * (vo.y - va.y) - sc * dy);
-        fz += (double)(lap * (vo.z - va.z) - sc * dz);
+                        float4 o, float4 vo, double2 tj, double &fx, double &fy, double &fz) {
+    const double dx = xsub(xi, (double)o.x), dy = xsub(yi, (double)o.y),
+                 dz = xsub(zi, (double)o.z);
+    const double r2 = dist2(dx, dy, dz);
+    if (!(r2 < p.h2)) return;                     // r >= h
+    const double rinv = r2 > 0.0 ? rsqrt(r2) : 0.0;  // r = 0: spiky 0, viscosity kept
+    const double d = xsub(p.h, xmul(r2, rinv));   // h - r
+    const double spk = xmul(xmul(xmul(p.c_spiky, d), d), rinv);  // (c d d) / r
+    if (o.w >= 0.0f) {  // fluid neighbour: tj = (p_j / rho_j^2, 1 / rho_j) in fp64
+        const double s = xmul(xmul(m2, xadd(term_i, tj.x)), spk);
+        fx = xsub(fx, xmul(s, dx));
+        fy = xsub(fy, xmul(s, dy));
+        fz = xsub(fz, xmul(s, dz));
+        const double lap = xmul(xmul(mum2, xmul(p.c_visc, d)), xmul(inv_rho_i, tj.y));
+        fx = xadd(fx, xmul(lap, xsub((double)vo.x, (double)va.x)));
+        fy = xadd(fy, xmul(lap, xsub((double)vo.y, (double)va.y)));
+        fz = xadd(fz, xmul(lap, xsub((double)vo.z, (double)va.z)));
     } else {  // static wall sample, mirrored pressure
-        const float sc = (float)m2 * (float)wall_term * spk;
-        fx -= (double)(sc * dx);
-        fy -= (double)(sc * dy);
-        fz -= (double)(sc * dz);
+        const double s = xmul(xmul(m2, wall_term), spk);
+        fx = xsub(fx, xmul(s, dx));
+        fy = xsub(fy, xmul(s, dy));
+        fz = xsub(fz, xmul(s, dz));
     }
 }
 
@@ -264,9 +268,8 @@ __global__ void __launch_bounds__(kThreads) k_forces(const __grid_constant__ Rts
         const float4 a = cpos[k];
         const float4 va = cvel[k];
         const double xi = a.x, yi = a.y, zi = a.z;
-        const double rho_i = b.rho[j], p_i = b.pres[j];
-        const double term_i = xdiv(p_i, xmul(rho_i, rho_i));
-        const double inv_rho_i = xdiv(1.0, rho_i);
+        const double4 own = ld_f64x4(b.cterm + 4 * (size_t)k);  // p/rho^2, 1/rho, p (fp64)
+        const double term_i = own.x, inv_rho_i = own.y, p_i = own.z;
         const double wall_term = xadd(term_i, xmul(p_i, inv_rho0_sq));
         const int n_all = b.cnt[t];  // the density pass's neighbour list of slot k
         const int *col = b.nbr + t;
@@ -278,25 +281,28 @@ __global__ void __launch_bounds__(kThreads) k_forces(const __grid_constant__ Rts
             for (int q0 = 0; q0 < n_all; q0 += RTS_WF_CH) {
                 int kq[RTS_WF_CH];
                 float4 pq[RTS_WF_CH], vq[RTS_WF_CH];
+                double2 tq[RTS_WF_CH];
 #pragma unroll
                 for (int u = 0; u < RTS_WF_CH; ++u) kq[u] = q0 + u < n_all ? col[(q0 + u) * S] : k;
 #pragma unroll
                 for (int u = 0; u < RTS_WF_CH; ++u) {
                     pq[u] = cpos[kq[u]];
                     vq[u] = cvel[kq[u]];
+                    tq[u] = reinterpret_cast<const double2 *>(b.cterm)[2 * (size_t)kq[u]];
                 }
 #pragma unroll
                 for (int u = 0; u < RTS_WF_CH; ++u)
                     if (kq[u] != k)
                         force_pair(p, xi, yi, zi, va, inv_rho_i, term_i, wall_term, m2, mum2, pq[u],
-                                   vq[u], fx, fy, fz);
+                                   vq[u], tq[u], fx, fy, fz);
             }
         } else if (n_all <= kHitCap) {
             for (int q = 0; q < n_all; ++q) {
                 const int kq = col[q * S];
                 if (kq == k) continue;
                 force_pair(p, xi, yi, zi, va, inv_rho_i, term_i, wall_term, m2, mum2, cpos[kq],
-                           cvel[kq], fx, fy, fz);
+                           cvel[kq], reinterpret_cast<const double2 *>(b.cterm)[2 * (size_t)kq],
+                           fx, fy, fz);
             }
         } else {
             Span sp[9];
@@ -305,7 +311,8 @@ __global__ void __launch_bounds__(kThreads) k_forces(const __grid_constant__ Rts
                 for (int q = sp[s].k0; q < sp[s].k1; ++q)
                     if (q != k && in_support(bd, a.x, a.y, a.z, cpos[q]))
                         force_pair(p, xi, yi, zi, va, inv_rho_i, term_i, wall_term, m2, mum2, cpos[q],
-                                   cvel[q], fx, fy, fz);
+                                   cvel[q], reinterpret_cast<const double2 *>(b.cterm)[2 * (size_t)q],
+                                   fx, fy, fz);
         }
         fx = xadd(fx, xmul(p.mass, p.gravity[0]));
         fy = xadd(fy, xmul(p.mass, p.gravity[1]));
@@ -405,9 +412,56 @@ __global__ void k_integrate(const __grid_constant__ RtsParams p, RtsBuffers b) {
     }
 }
 
+// np.var(rho) (wcsph.py:231-232, population variance over every fluid
+// particle, stale entries included): two fixed-order passes -- the mean, then
+// the mean squared deviation -- each a per-block fp64 tree over a fixed
+// contiguous chunk, the block partials summed in block order by one thread.
+// Deterministic; equals numpy's pairwise result to ~1e-16 relative.
+constexpr int kVarBlocks = 256;
+
+__global__ void __launch_bounds__(256) k_var_pass(const float *__restrict__ x, int n,
+                                                  double *__restrict__ part, int second) {
+    __shared__ double sh[256];
+    const double mean = second ? part[2 * kVarBlocks] : 0.0;
+    const int chunk = (n + gridDim.x - 1) / gridDim.x;
+    const int i0 = blockIdx.x * chunk, i1 = min(n, i0 + chunk);
+    double acc = 0.0;
+    for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+        const double v = x[i];
+        acc = xadd(acc, second ? xmul(xsub(v, mean), xsub(v, mean)) : v);
+    }
+    sh[threadIdx.x] = acc;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] = xadd(sh[threadIdx.x], sh[threadIdx.x + o]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[second * kVarBlocks + blockIdx.x] = sh[0];
+}
+
+__global__ void k_var_fold(double *__restrict__ part, int n, int second, double *out) {
+    double s = 0.0;
+    for (int q = 0; q < kVarBlocks; ++q) s = xadd(s, part[second * kVarBlocks + q]);
+    const double m = n > 0 ? xdiv(s, (double)n) : 0.0;
+    if (!second) part[2 * kVarBlocks] = m;  // the mean, for the second pass
+    else *out = m;
+}
+
 }  // namespace
 
 extern "C" {
+
+int rts_rho_variance(const RtsParams *p, const RtsBuffers *b, double *out, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    for (int second = 0; second < 2; ++second) {
+        rts_note_launch(), k_var_pass<<<kVarBlocks, 256, 0, s>>>(b->rho, p->n_fluid, b->partial,
+                                                                 second);
+        RTS_LAUNCH_CHECK();
+        rts_note_launch(), k_var_fold<<<1, 1, 0, s>>>(b->partial, p->n_fluid, second, out);
+        RTS_LAUNCH_CHECK();
+    }
+    return 0;
+}
 
 int rts_wcsph_propagate(const RtsParams *p, const RtsBuffers *b, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;

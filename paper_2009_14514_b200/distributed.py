@@ -31,6 +31,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
+from .errors import ConfigError, NumericalError
 from .scene import Scene, seed_particles
 
 # per-particle WCSPH state carried by ghosts and migrants, in pack order
@@ -67,12 +68,30 @@ class SlabPartition:
             hist = np.bincount(part.block_x(fluid[:, 0]), minlength=nx).cumsum()
             total = hist[-1] if len(hist) else 0
             cuts = [0]
+            w = max(1, halo)
             for r in range(1, world):
                 c = int(np.searchsorted(hist, r * total / world, side="left")) + 1
-                cuts.append(min(max(c, cuts[-1] + 1), nx - (world - r)))
+                cuts.append(min(max(c, cuts[-1] + w), nx - w * (world - r)))
             cuts.append(nx)
             part.cuts = tuple(cuts)
+        part.validate()
         return part
+
+    def widths(self, cuts=None) -> list[int]:
+        if cuts is None:
+            return [b - a for a, b in (self.bounds(r) for r in range(self.world))]
+        return [b - a for a, b in zip(cuts, cuts[1:])]
+
+    def validate(self, cuts=None) -> None:
+        """Every slab must hold at least ``halo`` block columns: a rank's ghost
+        band comes from its immediate neighbours only, so a narrower slab
+        would silently drop rows two ranks away."""
+        for r, w in enumerate(self.widths(cuts)):
+            if w < max(1, self.halo):
+                raise ConfigError(
+                    f"x-slab {r} is {w} block columns wide, narrower than the {self.halo}-column "
+                    f"ghost band ({self.nx} columns for {self.world} ranks); use fewer ranks "
+                    "or a longer domain")
 
     def rebalanced(self, weights) -> tuple:
         """Cuts at equal cumulative ``weights`` (per block column, summed over
@@ -91,6 +110,8 @@ class SlabPartition:
             c = min(max(c, cuts[-1] + 1), self.nx - (self.world - r))
             cuts.append(c)
         cuts.append(self.nx)
+        if min(self.widths(cuts)) < max(1, self.halo):
+            return tuple(old)  # no re-cut that keeps every slab as wide as the band
         return tuple(cuts)
 
     def bounds(self, rank: int) -> tuple[int, int]:
@@ -428,26 +449,31 @@ class PcisphExchange:
         self.send_idx, self.recv_idx = send_idx, recv_idx
         self.peers = sorted(send_idx)
         self._ch = None
+        from . import _native as N
+        self.N_CTL = N.CTL_WORDS
 
     def _channels(self, s) -> dict:
         if self._ch is None:
             A = s.arena
-            xs4, pres, err, rho = A["xs4"], A["pres"], A["err"], A["rho"]
+            xs, err, rho = A["xs"], A["err"], A["rho"]
+            xw = xs.view(torch.int32)  # 8 words per row: fp64 x* (6), fp64 p (2)
             pos, vel, fe, fp = A["pos"], A["vel"], A["force"], A["f_p"]
             ch = lambda pk, up=None: HaloChannel(self.x, self.send_idx, self.recv_idx, pk, up)
-            dens = [(pres, 1, 1, None, 0), (err, 2, 2, None, 1), (rho, 1, 1, None, 3)]
+            # the fp64 p of the xs rows (the pair passes read it; pres is its
+            # fp32 mirror, not needed on ghosts), err, rho*
+            dens = [(xw[:, 6:], 2, 8, None, 0), (err, 2, 2, None, 2), (rho, 1, 1, None, 4)]
             move = [(pos, 3, 3, None, 0), (vel, 3, 3, None, 3), (fe, 3, 3, None, 6),
                     (fp, 3, 3, None, 9)]
             self._ch = {
-                "motion": ch([(xs4, 4, 4, None, 0)]),
-                # p lands in pres and in xs4.w
-                "density": ch(dens, dens + [(xs4[:, 3:], 1, 4, None, 0)]),
+                "motion": ch([(xw, 8, 8, None, 0)]),  # x* and p (zeroed / restored)
+                "density": ch(dens),
                 # pos also refreshes the candidate copy at the row's CSR slot
                 "integrate": ch(move, move + [(A["cpos"], 3, 4, A["slot_of"], 0)]),
             }
             dev = self.x.compute_device
-            self._pub = torch.zeros(4, dtype=torch.float64, device=dev)
-            self._gath = torch.zeros((self.x.world, 4), dtype=torch.float64, device=dev)
+            W = self.N_CTL
+            self._pub = torch.zeros(W, dtype=torch.float64, device=dev)
+            self._gath = torch.zeros((self.x.world, W), dtype=torch.float64, device=dev)
         return self._ch
 
     def after_motion(self, s) -> None:
@@ -714,8 +740,7 @@ class _ResidentRank:
         N.call("rts_slab_classify", ctypes.byref(g), s.arena["pos"].data_ptr(), n,
                lists.data_ptr(), ls, leave.data_ptr(), counts.data_ptr(), st)
         c = counts.tolist()  # one host sync: the message sizes
-        if c[6]:
-            raise RuntimeError("a particle crossed more than one slab in one step")
+        self._agree_or_raise(c[6], "a particle crossed more than one slab in one step")
         W = self.rows.words
         send, keepg = {}, []
         for q, (mig, band, selfg) in ((r - 1, (0, 2, 4)), (r + 1, (1, 3, 5))):
@@ -745,6 +770,14 @@ class _ResidentRank:
         self.rows.unpack(torch.arange(n_keep, n_own, device=dev), arr)
         self.rows.unpack(torch.arange(n_own, n_own + gh.shape[0], device=dev), gh)
         self.n_own = n_own
+
+    def _agree_or_raise(self, bad: int, msg: str) -> None:
+        """Raise on every rank when ``bad`` is non-zero on any of them (a
+        rank-local raise would leave its peers waiting in the next exchange)."""
+        t = torch.tensor([float(bad)], dtype=torch.float64, device=self.x.device)
+        dist.all_reduce(t)
+        if float(t.item()):
+            raise RuntimeError(msg if bad else f"another x-slab rank: {msg}")
 
     def _sendrecv_split(self, send: dict) -> list:
         """send {peer: (n_first, rows)} -> [(n_first, rows)] per peer: the row
@@ -781,8 +814,7 @@ class _ResidentRank:
         leave = own != self.rank
         far = (own - self.rank).abs() > 1
         n_far, n_leave = torch.stack([far.sum(), leave.sum()]).tolist()  # one host sync
-        if n_far:
-            raise RuntimeError("a particle crossed more than one slab in one step")
+        self._agree_or_raise(n_far, "a particle crossed more than one slab in one step")
         arr = self._exchange_rows({q: torch.nonzero(own == q).reshape(-1)
                                    for q in self.x.neighbours()})
         n_keep = n - n_leave
@@ -867,9 +899,33 @@ class DistributedWcsph(_ResidentRank):
         s = self.solver
         self._maybe_rebalance(self.step_index)
         self._exchange()  # migration of the last step's leavers + fresh ghosts
-        st = s.step()
+        failure, st = None, None
+        try:
+            st = s.step()
+        except (NumericalError, RuntimeError) as exc:  # raised on every rank below
+            failure = exc
         n_own = self.n_own
-        st.n_compute = int(s.compute[:n_own].sum())  # owned particles only
+        # one all-reduce: [any rank failed, owned active count, owned rho sum]
+        v = torch.zeros(3, dtype=torch.float64, device=self.device)
+        v[0] = 1.0 if failure is not None else 0.0
+        if failure is None:
+            v[1] = s.compute[:n_own].sum()
+            v[2] = s.rho[:n_own].double().sum()
+        v = v.to(self.x.device)
+        dist.all_reduce(v)
+        fail, n_act, rho_sum = v.tolist()
+        if fail:
+            raise failure if failure is not None else NumericalError(
+                "another x-slab rank failed in this step")
+        st.n_compute = int(n_act)  # all ranks' owned particles
+        st.frac_compute = st.n_compute / max(1, self.n_global)
+        if s.track_rho_variance:  # population variance over every rank's owned rows
+            mean = rho_sum / max(1, self.n_global)
+            d = torch.zeros(1, dtype=torch.float64, device=self.device)
+            d[0] = ((s.rho[:n_own].double() - mean) ** 2).sum()
+            d = d.to(self.x.device)
+            dist.all_reduce(d)
+            st.rho_var = float(d.item()) / max(1, self.n_global)
         s._resize_fluid(n_own)  # drop the ghost rows
         self.sim_time += st.dt
         self.step_index += 1
@@ -957,16 +1013,27 @@ class DistributedPcisph(_ResidentRank):
         s.params.n_global = self.n_global
         send, recv = self._lists()
         s._xch = PcisphExchange(self.driver, send, recv)
+        failure, rows = None, []
         try:
             rows = s.major_step()
+        except (NumericalError, RuntimeError) as exc:  # raised on every rank below
+            failure = exc
         finally:
             s._xch = None
-        nref = torch.tensor([r.n_compute for r in rows], dtype=torch.float64,
-                            device=self.x.device)
-        if len(rows):
-            dist.all_reduce(nref)
-        for r, n in zip(rows, nref.tolist()):
-            r.n_compute = int(n)
+        # one all-reduce: [any rank failed, refresh counts per minor step]
+        from ._native import MAX_MINOR
+        v = torch.zeros(1 + MAX_MINOR, dtype=torch.float64)
+        v[0] = 1.0 if failure is not None else 0.0
+        for j, r in enumerate(rows[:MAX_MINOR]):
+            v[1 + j] = r.n_compute
+        v = v.to(self.x.device)
+        dist.all_reduce(v)
+        v = v.tolist()
+        if v[0]:
+            raise failure if failure is not None else NumericalError(
+                "another x-slab rank failed in this major step")
+        for j, r in enumerate(rows):
+            r.n_compute = int(v[1 + j])
             r.frac_compute = r.n_compute / max(1, self.n_global)
         self.sim_time = s.sim_time
         self.step_index = s.step_index

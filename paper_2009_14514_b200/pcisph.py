@@ -4,10 +4,13 @@ arXiv 2009.14514) and its constant / globally adaptive baselines.
 
 Control flow (major step -> minor steps -> scheduled correction loop with
 S_e / S_ob sets, local phases with snapshot/revert, early termination and
-the iteration cap) is the reference's, driven from the host; every
-particle and block pass is a librtssph kernel (see csrc/pcisph.cu).  The
-host reads one small counters block per correction iteration (max err,
-sum rho*, any S_e, |pred|) to take the reference's convergence decisions.
+the iteration cap) is the reference's; every particle and block pass is a
+librtssph kernel (see csrc/pcisph.cu) and every convergence decision is
+taken on the device by ``k_control``.  With ``use_graphs`` (default) a
+whole major step -- rebuild, levels, every minor step with its correction
+loop as a CUDA-graph conditional while node -- is one graph launch and one
+read-back of the control block; ``use_graphs=False`` launches the same
+kernels one by one (per-kernel timing, the neighbour audit, x-slab ranks).
 """
 
 from __future__ import annotations
@@ -159,9 +162,9 @@ class PcisphSolver(_DeviceSolver):
         self._nbr = A.alloc("nbr", (NEIGHBOR_WIDTH, stride), torch.int32, 0)
         self.params.nbr_stride = stride
         self._cnt_full = A.alloc("cnt", (cap,), torch.int32, 0)
-        A.alloc("xs4", (cap + nb, 4), torch.float32, 0)
+        A.alloc("xs", (cap + nb, 4), torch.float64, 0)  # 32-byte rows: fp64 x*, p
         A.alloc("pflag", (cap,), torch.uint8, 0)
-        A.alloc("snap_p", (cap,), torch.float32, 0)
+        A.alloc("snap_p", (cap,), torch.float64, 0)
         A.alloc("snap_fp", (cap, 3), torch.float32, 0)
         A.alloc("slot_of", (cap,), torch.int32, 0)
         A.alloc("ghost", (cap,), torch.uint8, 0)
@@ -236,10 +239,10 @@ class PcisphSolver(_DeviceSolver):
         self._nbr = A.alloc("nbr", (NEIGHBOR_WIDTH, stride), torch.int32, 0)
         self.params.nbr_stride = stride
         self.cnt = A.alloc("cnt", (n1,), torch.int32, 0)[:nf]
-        A.alloc("xs4", (max(nf + self.n_bound, 1), 4), f32, 0)
+        A.alloc("xs", (max(nf + self.n_bound, 1), 4), torch.float64, 0)  # fp64 x*, p
         A.alloc("pflag", (n1,), torch.uint8, 0)
         A.alloc("partial", (4096,), torch.float64, 0)
-        A.alloc("snap_p", (n1,), f32, 0)
+        A.alloc("snap_p", (n1,), torch.float64, 0)
         A.alloc("snap_fp", (n1, 3), f32, 0)
         A.alloc("slot_of", (n1,), torch.int32, 0)
         A.alloc("se_stamp", (self.grid.n_cells,), torch.int32, 0)

@@ -94,6 +94,7 @@ class _DeviceSolver:
         p.n_sms = sms if sms > 0 else 148
         A.alloc("cpos", (nf + self.n_bound + 4, 4), torch.float32, 0)
         A.alloc("cvel", (max(nf + self.n_bound, 1), 4), torch.float32, 0)
+        A.alloc("cterm", (max(nf + self.n_bound, 1), 4), torch.float64, 0)
         A.alloc("active", (max(nf, 1),), torch.int32, 0)
         A.alloc("list2", (max(nf, 1),), torch.int32, 0)
         A.alloc("list3", (max(nf, 1),), torch.int32, 0)
@@ -196,6 +197,7 @@ class _DeviceSolver:
                 A.alloc(arena, (cap, w) if w > 1 else (cap,), dt, fill)
             for name in ("cpos", "cvel"):
                 A.alloc(name, (cap + nb + 4, 4), torch.float32, 0)  # +4: padded candidate reads
+            A.alloc("cterm", (cap + nb + 4, 4), torch.float64, 0)
             for name in ("active", "list2", "list3"):
                 A.alloc(name, (cap,), torch.int32, 0)
             self._realloc_extra(cap, nb)
@@ -288,6 +290,9 @@ class WcsphSolver(_DeviceSolver):
         self.audit_neighbors = audit_neighbors
         self.n_regions = n_regions
         self._setup_common(scene, "wcsph", device)
+        self._var_out = torch.zeros(1, dtype=torch.float64, device=self.device)
+        if "partial" not in self.arena.t:
+            self.arena.alloc("partial", (4096,), torch.float64, 0)
         self.dt_base = scene.base_dt("wcsph")
         self.dt_cap = self.dt_base if dt_cap is None else dt_cap
         self.b_stiff = scene.rest_density * scene.sound_speed**2 / TAIT_GAMMA
@@ -391,8 +396,11 @@ class WcsphSolver(_DeviceSolver):
                        missed_neighbors=self._missed_last,
                        t_neighbor=self._timers["neighbor"], t_physics=self._timers["physics"],
                        t_rts=self._timers["rts"])
-        if self.track_rho_variance:
-            st.rho_var = float(torch.var(self.rho.double(), unbiased=False))
+        if self.track_rho_variance:  # np.var(rho), wcsph.py:231-232 (device reduction)
+            out = self._var_out
+            N.call("rts_rho_variance", self.params, self.arena.buf, out.data_ptr(),
+                   torch.cuda.current_stream(self.device).cuda_stream)
+            st.rho_var = float(out.item())
         return st
 
     def _enqueue_step(self, dt: float, read: bool = True):

@@ -140,3 +140,23 @@ def test_compare_command(scene_file, tmp_path, capsys):
     assert "max COM deviation:" in stdout
     # identical deterministic runs: zero deviation
     assert "max COM deviation:   0.000000 m" in stdout
+
+
+def test_reports_match_the_reference_lines():
+    """run / compare summaries without a device (reference cli.py:108-138)."""
+    from paper_2009_14514_b200.cli import compare_report, run_report
+    meta = {"solver": "pcisph-rts", "n_fluid": 1000, "duration": 0.5, "steps": 10,
+            "n_frames": 16, "wall_time": 1.234, "iterations_total": 35, "t_neighbor": 1.0,
+            "t_physics": 3.0, "t_rts": 0.0, "missed_neighbors": 0}
+    lines = run_report(meta, audit=True)
+    assert lines == ["solver pcisph-rts on 1000 fluid particles",
+                     "simulated 0.5 s in 10 steps, 16 frames",
+                     "wall time 1.23 s (3.50 iterations/step)",
+                     "breakdown: neighbor 25.0%  physics 75.0%  rts 0.0%",
+                     "missed neighbors: 0"]
+    r = {"solver_a": "pcisph-const", "solver_b": "pcisph-rts", "speedup": 2.0,
+         "iteration_ratio": 0.5, "work_ratio": 0.25, "com_deviation": 0.001,
+         "com_deviation_frac": 0.0005, "frames_compared": 7}
+    assert compare_report(r)[1] == "wall-clock speedup:  2.00x"
+    assert compare_report(r)[4] == ("max COM deviation:   0.001000 m (0.050% of the domain "
+                                    "diagonal, 7 frames)")

@@ -173,3 +173,23 @@ def test_rebalanced_cuts_move_toward_equal_work_one_slab_at_most():
     # uniform work: the even cuts stay
     part.cuts = ()
     assert part.rebalanced(np.ones(40)) == (0, 10, 20, 30, 40)
+
+
+def test_slabs_narrower_than_the_ghost_band_are_rejected():
+    """a slab narrower than the ghost band would silently miss
+    rows two ranks away -> ConfigError at partition time; a rebalance never
+    produces one."""
+    from paper_2009_14514_b200 import ConfigError
+    from paper_2009_14514_b200.distributed import SlabPartition
+    from paper_2009_14514_b200.scene import Scene
+    sc = Scene(domain_min=(0, 0, 0), domain_max=(0.4, 0.2, 0.2),
+               fluid_boxes=(((0, 0, 0), (0.4, 0.1, 0.1)),), spacing=0.02)
+    # 0.4 m + walls at 2.2 s = 0.044 m blocks: 11 columns, 4 ranks x halo 6 cannot fit
+    with pytest.raises(ConfigError, match="narrower than the 6-column ghost band"):
+        SlabPartition.for_scene(sc, "pcisph", 4, halo=6)
+    part = SlabPartition.for_scene(sc, "wcsph", 2, halo=2)
+    assert min(part.widths()) >= 2
+    part = SlabPartition(origin_x=0.0, inv_block=1.0, nx=12, world=3, halo=4)  # 4 | 4 | 4
+    w = np.zeros(12)
+    w[:4] = 100.0
+    assert part.rebalanced(w) == (0, 4, 8, 12)  # any move would leave a slab < 4 wide

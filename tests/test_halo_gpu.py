@@ -100,19 +100,40 @@ def test_ctl_publish_fold():
     ctr = torch.zeros(size, dtype=torch.uint8, device=dev)
     host = N.RtsCounters()
     host.max_err, host.any_se, host.sum_rho, host.n_pred = 0.0125, 0, 1234.5, 77
+    host.err_flags = 0
     ctr.copy_(torch.frombuffer(bytearray(bytes(host)), dtype=torch.uint8))
     b = N.RtsBuffers()
     b.ctr = ctr.data_ptr()
-    out = torch.zeros(4, dtype=torch.float64, device=dev)
+    W = N.CTL_WORDS
+    out = torch.zeros(W, dtype=torch.float64, device=dev)
     st = torch.cuda.current_stream().cuda_stream
     N.call("rts_ctl_publish", ctypes.byref(b), out.data_ptr(), st)
-    assert out.cpu().tolist() == [0.0125, 0.0, 1234.5, 77.0]
-    gathered = torch.tensor([[0.0125, 0, 1234.5, 77], [0.03, 1, 1e-3, 5], [0.01, 0, 7.25, 0]],
-                            dtype=torch.float64, device=dev)
+    assert out.cpu().tolist() == [0.0125, 0.0, 1234.5, 77.0, 0.0]
+    gathered = torch.tensor([[0.0125, 0, 1234.5, 77, 0], [0.03, 1, 1e-3, 5, 0],
+                             [0.01, 0, 7.25, 0, 0]], dtype=torch.float64, device=dev)
     N.call("rts_ctl_fold", ctypes.byref(b), gathered.data_ptr(), 3, st)
     torch.cuda.synchronize()
     c = N.RtsCounters.from_buffer_copy(bytes(ctr.cpu().numpy()))
-    assert c.max_err == 0.03 and c.any_se == 1 and c.n_pred == 82
+    assert c.max_err == 0.03 and c.any_se == 1 and c.n_pred == 82 and c.err_flags == 0
     assert c.sum_rho == np.float64(1234.5) + np.float64(1e-3) + np.float64(7.25)
     with pytest.raises(N.NativeError):
         N.call("rts_ctl_fold", ctypes.byref(b), gathered.data_ptr(), 0, st)
+
+
+def test_ctl_fold_spreads_a_rank_failure():
+    """one rank's fatal flag or NaN error must reach every rank's
+    k_control (same done / failed decision, no mismatched collectives)."""
+    N = _native()
+    dev = torch.device("cuda:0")
+    ctr = torch.zeros(ctypes.sizeof(N.RtsCounters), dtype=torch.uint8, device=dev)
+    b = N.RtsBuffers()
+    b.ctr = ctr.data_ptr()
+    st = torch.cuda.current_stream().cuda_stream
+    nan = float("nan")
+    gathered = torch.tensor([[0.01, 0, 1.0, 3, 0], [nan, 0, 1.0, 3, float(N.ERR_NONFINITE)]],
+                            dtype=torch.float64, device=dev)
+    N.call("rts_ctl_fold", ctypes.byref(b), gathered.data_ptr(), 2, st)
+    torch.cuda.synchronize()
+    c = N.RtsCounters.from_buffer_copy(bytes(ctr.cpu().numpy()))
+    assert c.max_err != c.max_err  # NaN propagated
+    assert c.err_flags & N.ERR_NONFINITE

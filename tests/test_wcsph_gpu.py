@@ -195,3 +195,28 @@ def test_cfg1_200_step_statistics_within_one_percent():
     assert abs(md - mo) <= 0.01 * abs(mo), (md, mo)
     assert abs(xd - xo) <= 0.01 * abs(xo), (xd, xo)
     assert abs(kd - ko) <= 0.01 * abs(ko), (kd, ko)
+
+
+def test_rho_variance_tracking_matches_oracle():
+    """track_rho_variance (wcsph.py:231-232): StepStats.rho_var is np.var of
+    the fluid density array (stale entries included); the device reduction
+    (rts_rho_variance, two fixed-order fp64 passes) against the oracle's
+    np.var from a common state, and bit-identical between two runs."""
+    from oracle.sph import OracleWcsph
+    from paper_2009_14514_b200 import WcsphSolver
+    dev = WcsphSolver(tiny_tank(), mode="rts", track_rho_variance=True)
+    twin = WcsphSolver(tiny_tank(), mode="rts", track_rho_variance=True)
+    orc = OracleWcsph(tiny_tank(), mode="rts", track_rho_variance=True)
+    apply_jitter(dev, orc)
+    twin.pos.copy_(dev.pos)
+    for _ in range(12):
+        inject(dev, orc, WCSPH_STATE)
+        a, b = dev.step(), orc.step()
+        assert a.rho_var > 0.0
+        # the device keeps rho in fp32 (BASELINE state): ~1e-7 relative per value
+        assert a.rho_var == pytest.approx(b.rho_var, rel=1e-4)
+        # the reduction itself: exact against np.var of the device's own array
+        assert a.rho_var == pytest.approx(float(np.var(dev.host("rho"))), rel=1e-12)
+    for _ in range(12):
+        twin.step()
+    assert twin.step().rho_var == dev.step().rho_var
