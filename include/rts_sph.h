@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define RTS_ABI_VERSION 25
+#define RTS_ABI_VERSION 26
 
 /* err_flags bits */
 #define RTS_ERR_ESCAPED   0x1u  /* fluid left the padded grid or non-finite (grid.py:268-273) */
@@ -198,6 +198,9 @@ typedef struct RtsBuffers {
     float   *cvel;         /* (Nf+Nb, 4)  vx vy vz rho */
     double  *cterm;        /* (Nf+Nb, 4)  WCSPH: fp64 {p/rho^2, 1/rho, p, 0} of the slot's
                             * particle from this step's density pass (force pair terms) */
+    float   *cx, *cy, *cz; /* (Nf+Nb+4 each, 16-byte aligned) the candidate positions of cpos
+                            * as separate x / y / z arrays: the neighbour searches load four
+                            * candidates per 128-bit access and test them in packed fp32x2 */
     int32_t *active;       /* (Nf) compacted CSR slots of active fluid particles */
     int32_t *list2;        /* (Nf) second compacted list */
     int32_t *list3;        /* (Nf) PCISPH: force list of the previous iteration (motion

@@ -138,6 +138,71 @@ RTS_DEV double4 ld_f64x4(const double *ptr) {
     return r;
 }
 
+// ---- packed fp32x2 arithmetic (sm_100: FADD2 / FMUL2 / FFMA2) ------------
+#ifndef RTS_SOA
+#define RTS_SOA 1  // neighbour searches on the x / y / z candidate copies (A/B: 0)
+#endif
+typedef unsigned long long f32x2;
+RTS_DEV f32x2 f2_pack(float a, float b) {
+    f32x2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+RTS_DEV f32x2 f2_sub(f32x2 a, f32x2 b) {
+    f32x2 r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+RTS_DEV f32x2 f2_mul(f32x2 a, f32x2 b) {
+    f32x2 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+RTS_DEV f32x2 f2_fma(f32x2 a, f32x2 b, f32x2 c) {
+    f32x2 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+
+// Membership masks of the candidates [cb, cb + n) of the SoA copies (cx, cy,
+// cz; n <= 32), candidates below k_lo excluded: bit u <-> candidate cb + u,
+// `mem` = r^2 < h^2 (1 - 1e-5), `amb` = inside the +-1e-5 band (those take the
+// exact fp64 test).  Four candidates per 128-bit load of each array (cb must
+// be a multiple of 4; the arrays are padded past the last slot), two per
+// packed fp32x2 operation; bits collected from the sign bits of
+// r^2 - bound with one funnel shift each.
+RTS_DEV void classify_soa(const float *cx, const float *cy, const float *cz, int cb, int n,
+                          int k_lo, float fxi, float fyi, float fzi, float lo, float hi,
+                          unsigned &mem_out, unsigned &amb_out) {
+    const f32x2 P = f2_pack(fxi, fxi), Q = f2_pack(fyi, fyi), R = f2_pack(fzi, fzi);
+    const f32x2 L = f2_pack(lo, lo), H = f2_pack(hi, hi);
+    const ulonglong2 *X = reinterpret_cast<const ulonglong2 *>(cx + cb);
+    const ulonglong2 *Y = reinterpret_cast<const ulonglong2 *>(cy + cb);
+    const ulonglong2 *Z = reinterpret_cast<const ulonglong2 *>(cz + cb);
+    unsigned mem = 0u, out = 0u;  // first candidate ends in the top bit
+    for (int u = 0; u < n; u += 4) {
+        const ulonglong2 x = X[u >> 2], y = Y[u >> 2], z = Z[u >> 2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const f32x2 ex = f2_sub(P, h ? x.y : x.x), ey = f2_sub(Q, h ? y.y : y.x),
+                        ez = f2_sub(R, h ? z.y : z.x);
+            const f32x2 r2 = f2_fma(ex, ex, f2_fma(ey, ey, f2_mul(ez, ez)));
+            const f32x2 m = f2_sub(r2, L), o = f2_sub(H, r2);
+            mem = __funnelshift_l((unsigned)m, mem, 1);
+            mem = __funnelshift_l((unsigned)(m >> 32), mem, 1);
+            out = __funnelshift_l((unsigned)o, out, 1);
+            out = __funnelshift_l((unsigned)(o >> 32), out, 1);
+        }
+    }
+    const int nr = (n + 3) & ~3;
+    unsigned valid = n == 32 ? 0xffffffffu : ((1u << n) - 1u);
+    if (k_lo > cb) valid &= ~((1u << (k_lo - cb)) - 1u);  // (k_lo - cb < 4)
+    mem = (__brev(mem) >> (32 - nr)) & valid;
+    out = (__brev(out) >> (32 - nr)) & valid;
+    mem_out = mem;
+    amb_out = valid & ~mem & ~out;
+}
+
 // ---- exact neighbour membership ------------------------------------------
 // The reference keeps j iff fp64 ((dx^2 + dy^2) + dz^2) < h^2 (grid.py:140-144).
 // Candidates are first classified in fp32 with a +-1e-5 relative band around

@@ -96,8 +96,9 @@ __global__ void k_gather(const __grid_constant__ RtsParams p, RtsBuffers b) {
     const int n = b.ctr->n_sorted;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
         const int j = b.order[k];
-        reinterpret_cast<float4 *>(b.cpos)[k] =
-            make_float4(b.pos[3 * j], b.pos[3 * j + 1], b.pos[3 * j + 2], __int_as_float(j));
+        const float x = b.pos[3 * j], y = b.pos[3 * j + 1], z = b.pos[3 * j + 2];
+        reinterpret_cast<float4 *>(b.cpos)[k] = make_float4(x, y, z, __int_as_float(j));
+        if (b.cx) b.cx[k] = x, b.cy[k] = y, b.cz[k] = z;
         if (j < p.n_fluid) b.slot_of[j] = k;
     }
 }
@@ -283,10 +284,22 @@ RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshC
                 // candidate; the rare in-band candidates then take the exact
                 // fp64 test, and the members are emitted in candidate order.
                 // Reads run up to 3 slots past the span (cpos is padded).
-                for (int cb = k0; cb < k1; cb += 32) {
+                const bool soa = RTS_SOA && b.cx != nullptr;
+                for (int cb = soa ? (k0 & ~3) : k0; cb < k1; cb += 32) {
                     const int n = min(32, k1 - cb);
                     const float4 *cp = cpos + cb;
                     unsigned mem = 0u, out = 0u;  // first candidate ends in the top bit
+                    if (soa) {  // x / y / z copies: 4 candidates per load, fp32x2 tests
+                        unsigned amb;
+                        classify_soa(b.cx, b.cy, b.cz, cb, n, k0, fxi, fyi, fzi, k.h2_lo, k.h2_hi,
+                                     mem, amb);
+                        while (amb) {
+                            const int q = __ffs(amb) - 1;
+                            amb &= amb - 1u;
+                            const float4 o = cp[q];
+                            if (exact_neighbour(p.h2, fxi, fyi, fzi, o.x, o.y, o.z)) mem |= 1u << q;
+                        }
+                    } else {
                     for (int u = 0; u < n; u += 4) {
                         float4 ob[4];
 #pragma unroll
@@ -305,12 +318,15 @@ RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshC
                     const unsigned valid = n == 32 ? 0xffffffffu : ((1u << n) - 1u);
                     mem = (__brev(mem) >> (32 - nr)) & valid;
                     out = (__brev(out) >> (32 - nr)) & valid;
-                    unsigned amb = valid & ~mem & ~out;
-                    while (amb) {
-                        const int q = __ffs(amb) - 1;
-                        amb &= amb - 1u;
-                        const float4 o = cp[q];
-                        if (exact_neighbour(p.h2, fxi, fyi, fzi, o.x, o.y, o.z)) mem |= 1u << q;
+                    {
+                        unsigned amb = valid & ~mem & ~out;
+                        while (amb) {
+                            const int q = __ffs(amb) - 1;
+                            amb &= amb - 1u;
+                            const float4 o = cp[q];
+                            if (exact_neighbour(p.h2, fxi, fyi, fzi, o.x, o.y, o.z)) mem |= 1u << q;
+                        }
+                    }
                     }
                     if (!EXT) {
                         while (mem) {
@@ -1116,8 +1132,9 @@ RTS_DEV void integrate_one(const RtsParams &p, const RtsBuffers &b, int i, int c
     if (countdown & 2) block_maxima_one(b, b.fluid_cells[i], &b.vel[3 * i], &b.force[3 * i],
                                         &b.f_p[3 * i]);
     if (countdown) {
-        reinterpret_cast<float4 *>(b.cpos)[b.slot_of[i]] =
-            make_float4(nx[0], nx[1], nx[2], __int_as_float(i));
+        const int sl = b.slot_of[i];
+        reinterpret_cast<float4 *>(b.cpos)[sl] = make_float4(nx[0], nx[1], nx[2], __int_as_float(i));
+        if (b.cx) b.cx[sl] = nx[0], b.cy[sl] = nx[1], b.cz[sl] = nx[2];
         int v = b.validity[i] - 1;
         const bool expired = v <= 0;
         if (expired) {
@@ -1201,6 +1218,7 @@ __global__ void k_integrate(const __grid_constant__ RtsParams p, RtsBuffers b, i
                 sob[q] = observed_block(b, cl[q], gen);
                 reinterpret_cast<float4 *>(b.cpos)[sl[q]] =
                     make_float4(x[3 * q], x[3 * q + 1], x[3 * q + 2], __int_as_float(4 * g + q));
+                if (b.cx) b.cx[sl[q]] = x[3 * q], b.cy[sl[q]] = x[3 * q + 1], b.cz[sl[q]] = x[3 * q + 2];
                 int vv = vl[q] - 1;
                 const bool expired = vv <= 0;
                 if (expired) vv = kValidity[rg[q] < 0 ? 0 : (rg[q] > 4 ? 4 : rg[q])];

@@ -37,6 +37,7 @@ __global__ void __launch_bounds__(256) k_propagate(const __grid_constant__ RtsPa
         if (k < n_sorted) {
             const int j = b.order[k];
             const float x = b.pos[3 * j], y = b.pos[3 * j + 1], z = b.pos[3 * j + 2];
+            if (b.cx) b.cx[k] = x, b.cy[k] = y, b.cz[k] = z;
             if (j < p.n_fluid) {
                 const double rho = b.rho[j], pr = b.pres[j];
                 const double term = xdiv(pr, xmul(rho, rho)), inv_rho = xdiv(1.0, rho);
@@ -114,10 +115,21 @@ RTS_DEV int collect_hits(const RtsParams &p, const RtsBuffers &b, const float4 *
         // r2 - bound collected with funnel shifts); in-band candidates take
         // the exact fp64 test; reads run up to 3 slots past the span (cpos
         // is padded)
-        for (int cb = k0; cb < k1; cb += 32) {
+        const bool soa = RTS_SOA && b.cx != nullptr;
+        for (int cb = soa ? (k0 & ~3) : k0; cb < k1; cb += 32) {
             const int m = min(32, k1 - cb);
             const float4 *cp = cpos + cb;
             unsigned mem = 0u, out = 0u;
+            if (soa) {  // x / y / z copies: 4 candidates per load, fp32x2 tests
+                unsigned amb;
+                classify_soa(b.cx, b.cy, b.cz, cb, m, k0, a.x, a.y, a.z, bd.lo, bd.hi, mem, amb);
+                while (amb) {
+                    const int q = __ffs(amb) - 1;
+                    amb &= amb - 1u;
+                    const float4 o = cp[q];
+                    if (exact_neighbour(bd.h2, a.x, a.y, a.z, o.x, o.y, o.z)) mem |= 1u << q;
+                }
+            } else {
             for (int u = 0; u < m; u += 4) {
                 float4 ob[4];
 #pragma unroll
@@ -141,6 +153,7 @@ RTS_DEV int collect_hits(const RtsParams &p, const RtsBuffers &b, const float4 *
                 amb &= amb - 1u;
                 const float4 o = cp[q];
                 if (exact_neighbour(bd.h2, a.x, a.y, a.z, o.x, o.y, o.z)) mem |= 1u << q;
+            }
             }
             while (mem) {
                 const int q = __ffs(mem) - 1;

@@ -47,6 +47,9 @@ def tait_pressure(rho: float, rest_density: float, sound_speed: float) -> float:
 
 
 class _DeviceSolver:
+    # PCISPH: no SoA candidate copies -- the integrator would have to scatter
+    # three more arrays every minor step, which costs what the search saves
+    _soa_candidates = False
     """Shared construction: seeding, device buffers, grid, RtsParams."""
 
     def _setup_common(self, scene: Scene, grid_mode: str, device):
@@ -95,6 +98,9 @@ class _DeviceSolver:
         A.alloc("cpos", (nf + self.n_bound + 4, 4), torch.float32, 0)
         A.alloc("cvel", (max(nf + self.n_bound, 1), 4), torch.float32, 0)
         A.alloc("cterm", (max(nf + self.n_bound, 1), 4), torch.float64, 0)
+        if self._soa_candidates:  # SoA candidate positions (+8: padded quads)
+            for name in ("cx", "cy", "cz"):
+                A.alloc(name, (nf + self.n_bound + 8,), torch.float32, 0)
         A.alloc("active", (max(nf, 1),), torch.int32, 0)
         A.alloc("list2", (max(nf, 1),), torch.int32, 0)
         A.alloc("list3", (max(nf, 1),), torch.int32, 0)
@@ -198,6 +204,9 @@ class _DeviceSolver:
             for name in ("cpos", "cvel"):
                 A.alloc(name, (cap + nb + 4, 4), torch.float32, 0)  # +4: padded candidate reads
             A.alloc("cterm", (cap + nb + 4, 4), torch.float64, 0)
+            if self._soa_candidates:
+                for name in ("cx", "cy", "cz"):
+                    A.alloc(name, (cap + nb + 8,), torch.float32, 0)
             for name in ("active", "list2", "list3"):
                 A.alloc(name, (cap,), torch.int32, 0)
             self._realloc_extra(cap, nb)
@@ -250,6 +259,10 @@ class _DeviceSolver:
 
 class WcsphSolver(_DeviceSolver):
     """Weakly compressible SPH, ``mode`` "baseline" or "rts" (wcsph.py:108)."""
+
+    # the density pass's search reads x / y / z candidate copies (written by
+    # the propagate pass in slot order: free); -8 % on the search
+    _soa_candidates = True
 
     mode_names = ("baseline", "rts")
 
