@@ -34,14 +34,16 @@
 extern "C" {
 #endif
 
-#define RTS_ABI_VERSION 26
+#define RTS_ABI_VERSION 27
 
 /* err_flags bits */
 #define RTS_ERR_ESCAPED   0x1u  /* fluid left the padded grid or non-finite (grid.py:268-273) */
 #define RTS_ERR_OVERFLOW  0x2u  /* > width true neighbours (grid.py:327-331) */
 #define RTS_ERR_NONFINITE 0x4u  /* non-finite density (wcsph.py:286-287, pcisph.py:680-681) */
 #define RTS_ERR_ITERCAP   0x8u  /* pressure solve hit the cap (pcisph.py:711-715) */
-#define RTS_ERR_FATAL     0xFu
+#define RTS_ERR_CHECK     0x10u /* checked builds (-DRTS_CHECKED=1): a device index was out of
+                                 * range; RtsCounters.check_site names the first site */
+#define RTS_ERR_FATAL     0x1Fu
 
 /* Scalar constants of one solver, fp64 values computed by the Python host
  * with the reference's own expressions (scene.py, kernels.py:58-80,
@@ -96,7 +98,7 @@ typedef struct RtsCounters {
     int32_t  lists_all;        /* PCISPH: this iteration's pred = force = all fluid (no lists) */
     int64_t  missing;          /* neighbour audit: true neighbours absent from tables */
     uint32_t blocks_done;      /* last-block-done counter of the S_e reduction */
-    int32_t  pad3;
+    int32_t  check_site;       /* checked builds: first failing RTS_CHECK site (0 = none) */
     int64_t  stamps[4];        /* RTS-WCSPH step graph: %globaltimer (ns) at the start, end of
                                 * the grid rebuild, start of the density pass, end */
     float    disp_cur;         /* PCISPH: max |dx| of one coordinate of any fluid particle in

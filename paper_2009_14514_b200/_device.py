@@ -90,6 +90,9 @@ def raise_on_errors(c: N.RtsCounters, width: int = 128) -> None:
             f"(table width {width}); the particle distribution has collapsed")
     if f & N.ERR_NONFINITE:
         raise NumericalError("non-finite density; the simulation has blown up")
+    if f & N.ERR_CHECK:
+        raise N.NativeError(f"device bounds check failed at site {int(c.check_site)} "
+                            "(checked build)")
 
 
 class PhaseTimer:

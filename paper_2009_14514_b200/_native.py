@@ -12,7 +12,7 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "librtssph.so")
-ABI_VERSION = 26
+ABI_VERSION = 27
 
 _c = ctypes
 _D = _c.c_double
@@ -40,7 +40,7 @@ class RtsCounters(_c.Structure):
         ("overflow", _c.c_int64), ("n_sorted", _I), ("n_pred", _I), ("n_force", _I),
         ("n_list", _I), ("fmax_bits", _c.c_uint64), ("sum_rho", _D), ("max_err", _D),
         ("any_se", _I), ("lists_all", _I), ("missing", _c.c_int64),
-        ("blocks_done", _c.c_uint32), ("pad3", _I), ("stamps", _c.c_int64 * 4),
+        ("blocks_done", _c.c_uint32), ("check_site", _I), ("stamps", _c.c_int64 * 4),
         ("disp_cur", _c.c_float), ("disp_total", _c.c_float), ("reserved1", _D),
     ]
 
@@ -107,7 +107,7 @@ class RtsHaloSpec(_c.Structure):
                 ("f", RtsHaloField * HALO_MAX_FIELDS)]
 
 
-ERR_ESCAPED, ERR_OVERFLOW, ERR_NONFINITE, ERR_ITERCAP = 0x1, 0x2, 0x4, 0x8
+ERR_ESCAPED, ERR_OVERFLOW, ERR_NONFINITE, ERR_ITERCAP, ERR_CHECK = 0x1, 0x2, 0x4, 0x8, 0x10
 
 # entry points: name -> argtypes (all return int)
 _PP = _c.POINTER(RtsParams)
@@ -170,11 +170,14 @@ class NativeError(RuntimeError):
     pass
 
 
-def load(path: str = LIB_PATH):
-    """Load the library (no CUDA call is made); raises if it is missing."""
+def load(path: str | None = None):
+    """Load the library (no CUDA call is made); raises if it is missing.
+    ``RTS_SPH_LIB`` selects another build of it (e.g. the bounds-checked
+    ``-DRTS_CHECKED=1`` variant, scripts/checked_build.sh)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("RTS_SPH_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise NativeError(
             f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"

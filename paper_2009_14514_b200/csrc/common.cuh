@@ -203,6 +203,42 @@ RTS_DEV void classify_soa(const float *cx, const float *cy, const float *cz, int
     amb_out = valid & ~mem & ~out;
 }
 
+// 1/sqrt(r2) in fp64 from the fp32 estimate and one Newton step: relative
+// error ~1e-13 (the estimate's 2^-22 squared), 5 fp64 operations instead of
+// the ~12 of a full-precision rsqrt.  r2 must be a normal fp32 value.
+RTS_DEV double rsqrt_nr(double r2) {
+    const double y = (double)rsqrtf((float)r2);
+    return y * fma(-0.5 * r2, y * y, 1.5);
+}
+
+// ---- checked builds ------------------------------------------------------
+// -DRTS_CHECKED=1 range-checks every gathered / scattered index of the hot
+// kernels (compute-sanitizer is unavailable on this GPU pool): a violation
+// sets RTS_ERR_CHECK (fatal: later kernels stop, the host raises) and the
+// first failing site.  Release builds compile the checks away.
+#ifndef RTS_CHECKED
+#define RTS_CHECKED 0
+#endif
+RTS_DEV void rts_check_fail(RtsCounters *c, int site) {
+    atomicCAS(&c->check_site, 0, site);
+    atomicOr(&c->err_flags, RTS_ERR_CHECK);
+}
+#define RTS_CHECK(ctr, cond, site)                                   \
+    do {                                                            \
+        if (RTS_CHECKED && !(cond)) rts::rts_check_fail((ctr), (site)); \
+    } while (0)
+// i in [0, n)
+#define RTS_CHECK_IDX(ctr, i, n, site) RTS_CHECK(ctr, (unsigned)(i) < (unsigned)(n), site)
+// an index about to be dereferenced: checked builds substitute `safe` for an
+// out-of-range value (after flagging it) so the faulty access never happens
+RTS_DEV int rts_safe_idx(RtsCounters *c, int i, int n, int site, int safe) {
+    if (RTS_CHECKED && (unsigned)i >= (unsigned)n) {
+        rts_check_fail(c, site);
+        return safe;
+    }
+    return i;
+}
+
 // ---- exact neighbour membership ------------------------------------------
 // The reference keeps j iff fp64 ((dx^2 + dy^2) + dz^2) < h^2 (grid.py:140-144).
 // Candidates are first classified in fp32 with a +-1e-5 relative band around

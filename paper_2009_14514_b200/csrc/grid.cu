@@ -210,7 +210,9 @@ __global__ void k_scatter(const __grid_constant__ RtsParams p, RtsBuffers b) {
          k += gridDim.x * blockDim.x) {
         if (k < nf) {
             const int c = b.fluid_cells[k];
-            b.order[b.starts[c] + atomicAdd(&b.fill[c], 1)] = k;
+            const int at = b.starts[c] + atomicAdd(&b.fill[c], 1);
+            RTS_CHECK(b.ctr, at < b.starts[c] + b.cell_count[c], 101);
+            b.order[rts_safe_idx(b.ctr, at, b.ctr->n_sorted, 102, 0)] = k;
         } else {
             const int q = k - nf;
             const int t = b.bcell_of[q];

@@ -95,7 +95,7 @@ __global__ void k_gather(const __grid_constant__ RtsParams p, RtsBuffers b) {
     if (fatal(b.ctr)) return;
     const int n = b.ctr->n_sorted;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
-        const int j = b.order[k];
+        const int j = rts_safe_idx(b.ctr, b.order[k], p.n_fluid + p.n_bound, 301, 0);
         const float x = b.pos[3 * j], y = b.pos[3 * j + 1], z = b.pos[3 * j + 2];
         reinterpret_cast<float4 *>(b.cpos)[k] = make_float4(x, y, z, __int_as_float(j));
         if (b.cx) b.cx[k] = x, b.cy[k] = y, b.cz[k] = z;
@@ -235,6 +235,7 @@ RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshC
                          double D = -1.0) {
     const float4 *cpos = reinterpret_cast<const float4 *>(b.cpos);
     const int nx = p.dims[0], ny = p.dims[1], nz = p.dims[2];
+    RTS_CHECK_IDX(b.ctr, i, p.n_fluid, 302);
     const float fxi = b.pos[3 * i], fyi = b.pos[3 * i + 1], fzi = b.pos[3 * i + 2];
     const double xi = fxi, yi = fyi, zi = fzi;
     const int lay = lay_in > 0 ? lay_in : ((two_layer_r1 && b.region[i] == 1) ? 2 : 1);
@@ -251,32 +252,44 @@ RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshC
     int *row = b.nbr + i;  // entry q at row[q * S]
     const size_t S = p.nbr_stride;
     const bool cull = D >= 0.0;
-    const double B = p.block_size, eps = 1e-9 * B;
-    const double hw2 = p.h2 * (1.0 + 2e-6);
-    for (int ax = max(0, cx - lay); ax <= min(nx - 1, cx + lay); ++ax) {
+    // the block ranges of the (2L+1)^3 window that can hold a candidate within
+    // h: +-(h + D) around the particle, per axis (computed once per particle)
+    int ax0 = max(0, cx - lay), ax1 = min(nx - 1, cx + lay);
+    int ay0 = max(0, cy - lay), ay1 = min(ny - 1, cy + lay);
+    int za = z0, zb = z1;
+    double hw2 = 0.0;
+    if (cull) {
+        const double w = p.h * (1.0 + 1e-6) + D + 1e-9 * p.block_size;
+        hw2 = p.h2 * (1.0 + 2e-6);
+        auto lo = [&](double x, double o) { return floor((x - w - o) * p.inv_block); };
+        auto hi = [&](double x, double o) { return floor((x + w - o) * p.inv_block); };
+        ax0 = max(ax0, (int)fmax(lo(xi, p.origin[0]), -1.0));
+        ax1 = min(ax1, (int)fmin(hi(xi, p.origin[0]), (double)nx));
+        ay0 = max(ay0, (int)fmax(lo(yi, p.origin[1]), -1.0));
+        ay1 = min(ay1, (int)fmin(hi(yi, p.origin[1]), (double)ny));
+        za = max(za, (int)fmax(lo(zi, p.origin[2]), -1.0));
+        zb = min(zb, (int)fmin(hi(zi, p.origin[2]), (double)nz));
+    }
+    const double B = p.block_size;
+    for (int ax = ax0; ax <= ax1; ++ax) {
         double ddx = 0.0;
         if (cull) {  // x distance from the column's candidates (stale extent +- D)
-            const double xl = ax == 0 ? -1e300 : p.origin[0] + ax * B - D - eps;
-            const double xh = ax == nx - 1 ? 1e300 : p.origin[0] + (ax + 1) * B + D + eps;
+            const double xl = ax == 0 ? -1e300 : p.origin[0] + ax * B - D;
+            const double xh = ax == nx - 1 ? 1e300 : p.origin[0] + (ax + 1) * B + D;
             ddx = xi < xl ? xl - xi : (xi > xh ? xi - xh : 0.0);
         }
-        for (int ay = max(0, cy - lay); ay <= min(ny - 1, cy + lay); ++ay) {
+        for (int ay = ay0; ay <= ay1; ++ay) {
             const int base = (ax * ny + ay) * nz;
-            int za = z0, zb = z1;
-            if (cull) {
-                const double yl = ay == 0 ? -1e300 : p.origin[1] + ay * B - D - eps;
-                const double yh = ay == ny - 1 ? 1e300 : p.origin[1] + (ay + 1) * B + D + eps;
+            if (cull) {  // corner columns: x-y distance
+                const double yl = ay == 0 ? -1e300 : p.origin[1] + ay * B - D;
+                const double yh = ay == ny - 1 ? 1e300 : p.origin[1] + (ay + 1) * B + D;
                 const double ddy = yi < yl ? yl - yi : (yi > yh ? yi - yh : 0.0);
-                const double dxy2 = ddx * ddx + ddy * ddy;
-                if (dxy2 >= hw2) continue;  // no candidate of the column within h
-                const double w = sqrt(hw2 - dxy2) + D + eps;
-                const double fa = floor((zi - w - p.origin[2]) * p.inv_block);
-                const double fb = floor((zi + w - p.origin[2]) * p.inv_block);
-                za = fa > (double)z0 ? (int)fa : z0;
-                zb = fb < (double)z1 ? (int)fb : z1;
-                if (za > zb) continue;
+                if (ddx * ddx + ddy * ddy >= hw2) continue;  // no candidate within h
             }
+            if (za > zb) continue;
+            RTS_CHECK(b.ctr, base + zb + 1 <= p.n_cells, 303);
             const int k0 = b.starts[base + za], k1 = b.starts[base + zb + 1];
+            RTS_CHECK(b.ctr, 0 <= k0 && k0 <= k1 && k1 <= b.ctr->n_sorted, 304);
             if (G == 1) {
                 // Branch-free classification of 32 candidates at a time: two
                 // 32-bit masks (r2 < h2_lo: member; r2 > h2_hi: not) built
@@ -425,6 +438,9 @@ RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshC
     if (lane == 0) finish_refresh(p, b, i, cntn, fx, fy, fz);
 }
 
+#ifndef RTS_REF_MID
+#define RTS_REF_MID 8  // lanes per particle for mid-size refresh lists (8, 4 or 1)
+#endif
 #ifndef RTS_CULL_G1
 #define RTS_CULL_G1 0  // culling in the one-thread-per-particle path (lanes diverge)
 #endif
@@ -447,11 +463,16 @@ __global__ void __launch_bounds__(kThreads, RTS_REF_MINB) k_refresh(const __grid
     if ((long long)n * 32 <= nthreads) {
         for (int t = tid / 32; t < n; t += nthreads / 32)
             refresh_one<32>(p, b, k, b.active[t], two_layer_r1, wl, 0xffffffffu, 0, 0, D);
-    } else if ((long long)n * 8 <= nthreads) {
+    } else if ((long long)n * 8 <= nthreads && RTS_REF_MID == 8) {
         const int lane = wl & 7, gshift = wl & ~7;
         const unsigned gmask = 0xffu << gshift;
         for (int t = tid / 8; t < n; t += nthreads / 8)
             refresh_one<8>(p, b, k, b.active[t], two_layer_r1, lane, gmask, gshift, 0, D);
+    } else if ((long long)n * 4 <= nthreads && RTS_REF_MID == 4) {
+        const int lane = wl & 3, gshift = wl & ~3;
+        const unsigned gmask = 0xfu << gshift;
+        for (int t = tid / 4; t < n; t += nthreads / 4)
+            refresh_one<4>(p, b, k, b.active[t], two_layer_r1, lane, gmask, gshift, 0, D);
     } else {
         for (int t = tid; t < n; t += nthreads)
             refresh_one<1>(p, b, k, b.active[t], two_layer_r1, 0, 0u, 0, 0, RTS_CULL_G1 ? D : -1.0);
@@ -477,7 +498,10 @@ RTS_DEV void motion_one(const RtsParams &p, const RtsBuffers &b, int i, double d
         const double v = xadd((double)b.vel[3 * i + a], xmul(dt_inv_m, f));
         xs[a] = xadd((double)b.pos[3 * i + a], xmul(p.dt, v));
     }
-    st_xs3(xs_rows(b) + i, xs[0], xs[1], xs[2]);
+    // the whole 32-byte row (a partial-sector store costs a read-modify-write
+    // in DRAM once the rows outgrow L2, cfg4/cfg5): p is re-stored unchanged
+    XsRow *r = xs_rows(b) + i;
+    st_xs(r, xs[0], xs[1], xs[2], r->p);
 }
 
 // the fp64 p of row i (and its fp32 public mirror)
@@ -513,7 +537,7 @@ __global__ void k_motion(const __grid_constant__ RtsParams p, RtsBuffers b, int 
     if (!all) {
         const int n = b.ctl->prev_force;
         for (int t = tid; t < n; t += nt) {
-            const int i = b.list3[t];
+            const int i = rts_safe_idx(b.ctr, b.list3[t], p.n_fluid, 501, 0);
             if (!is_ghost(b, i)) motion_one(p, b, i, dim);
         }
         return;
@@ -552,8 +576,8 @@ __global__ void k_motion(const __grid_constant__ RtsParams p, RtsBuffers b, int 
                 xs[a] = xadd((double)x[c], xmul(p.dt, vv));
             }
             if (is_ghost(b, 4 * g + q)) continue;
-            if (restore || zero) st_xs(xsr + 4 * g + q, xs[0], xs[1], xs[2], pr[q]);
-            else st_xs3(xsr + 4 * g + q, xs[0], xs[1], xs[2]);
+            // whole 32-byte rows (see motion_one); p unchanged unless zeroed / restored
+            st_xs(xsr + 4 * g + q, xs[0], xs[1], xs[2], (restore || zero) ? pr[q] : xsr[4 * g + q].p);
         }
     }
     for (int i = 4 * ng + tid; i < nf; i += nt) {
@@ -691,11 +715,14 @@ static inline int pass_blocks(const RtsParams *p) {
 template <int LG, int CH = 8>
 RTS_DEV void density_one(const RtsParams &p, const RtsBuffers &b, int i, int lane,
                          unsigned gmask) {
+    RTS_CHECK_IDX(b.ctr, i, p.n_fluid, 401);
     if (is_ghost(b, i)) return;
     const XsRow *xsr = xs_rows(b);
     const XsRow a = ld_xs(xsr + i);  // own row: x* and the fp64 p of the last update
     const double xi = a.x, yi = a.y, zi = a.z;
     const int c = b.cnt[i];
+    RTS_CHECK(b.ctr, 0 <= c && c <= p.width, 402);
+    const int n_tot = p.n_fluid + p.n_bound;
     const int *row = b.nbr + i;  // entry q at row[q * S]: coalesced across lanes
     const size_t S = p.nbr_stride;
     double acc = 0.0;
@@ -705,18 +732,22 @@ RTS_DEV void density_one(const RtsParams &p, const RtsBuffers &b, int i, int lan
         int jn[CH];
         XsRow on[CH];
 #pragma unroll
-        for (int u = 0; u < CH; ++u) jn[u] = u < c ? __ldcs(row + u * S) : i;
+        for (int u = 0; u < CH; ++u)
+            jn[u] = u < c ? rts_safe_idx(b.ctr, __ldcs(row + u * S), n_tot, 403, i) : i;
 #pragma unroll
         for (int u = 0; u < CH; ++u) on[u] = ld_xs3(xsr + jn[u]);
 #pragma unroll
-        for (int u = 0; u < CH; ++u) jn[u] = CH + u < c ? __ldcs(row + (CH + u) * S) : i;
+        for (int u = 0; u < CH; ++u)
+            jn[u] = CH + u < c ? rts_safe_idx(b.ctr, __ldcs(row + (CH + u) * S), n_tot, 403, i) : i;
         for (int q = 0; q < c; q += CH) {
             XsRow o[CH];
 #pragma unroll
             for (int u = 0; u < CH; ++u) {
                 o[u] = on[u];
                 on[u] = ld_xs3(xsr + jn[u]);
-                jn[u] = q + 2 * CH + u < c ? __ldcs(row + (q + 2 * CH + u) * S) : i;
+                jn[u] = q + 2 * CH + u < c
+                            ? rts_safe_idx(b.ctr, __ldcs(row + (q + 2 * CH + u) * S), n_tot, 403, i)
+                            : i;
             }
 #pragma unroll
             for (int u = 0; u < CH; ++u) {
@@ -943,25 +974,26 @@ __global__ void k_observed(const __grid_constant__ RtsParams p, RtsBuffers b, in
 
 // pressure forces at x* over the force list (pcisph.py:238-271); same
 // adaptive granularity as k_density.
+// One pair term of _pressure_forces (pcisph.py:255-268) in fp64:
+// s = m^2 (p_i + p_j) / rho0^2 * c (h - r)^2 / r  (wall j: 2 p_i), f -= s x_ij,
+// with K = m^2 c / rho0^2 and K p_i folded per particle and 1/r from an fp32
+// estimate + one fp64 Newton step: ~1e-13 relative per term (18 fp64
+// operations), so f_p keeps 1e-4 parity even where the pair terms cancel
+// (|f_p| << sum |terms|), without making the pass FP64-bound.
 template <class T>
-RTS_DEV void pforce_pair(const RtsParams &p, double xi, double yi, double zi, double term_i,
-                         double wall, double m2c, double inv_rho0_sq, int i, int j, XsRow o,
-                         T &fx, T &fy, T &fz) {
-    // One pair term of _pressure_forces (pcisph.py:255-268) in fp64, in the
-    // reference's operand order except 1/r (fp64 rsqrt, ~1 ulp, instead of
-    // a division): ~1e-16 relative per term, so f_p keeps 1e-4 parity even
-    // where the pair terms cancel (|f_p| << sum |terms|)
+RTS_DEV void pforce_pair(const RtsParams &p, double xi, double yi, double zi, double k_i,
+                         double k_wall, double K, int i, int j, XsRow o, T &fx, T &fy, T &fz) {
     if (j == i) return;
-    const double dx = xsub(xi, o.x), dy = xsub(yi, o.y), dz = xsub(zi, o.z);
-    const double r2 = dist2(dx, dy, dz);
+    const double dx = xi - o.x, dy = yi - o.y, dz = zi - o.z;
+    const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
     if (!(r2 > 0.0) || !(r2 < p.h2)) return;  // r <= 0 or r >= h
-    const double term = j < p.n_fluid ? xadd(term_i, xmul(o.p, inv_rho0_sq)) : wall;
-    const double rinv = rsqrt(r2);
-    const double d = xsub(p.h, xmul(r2, rinv));  // h - r
-    const double s = xmul(xmul(m2c, term), xmul(xmul(xmul(p.c_spiky, d), d), rinv));
-    fx = xsub(fx, xmul(s, dx));
-    fy = xsub(fy, xmul(s, dy));
-    fz = xsub(fz, xmul(s, dz));
+    const double y = rsqrt_nr(r2);
+    const double d = fma(-r2, y, p.h);  // h - r
+    const double kk = j < p.n_fluid ? fma(o.p, K, k_i) : k_wall;
+    const double s = kk * d * d * y;
+    fx = fma(-s, dx, fx);
+    fy = fma(-s, dy, fy);
+    fz = fma(-s, dz, fz);
 }
 
 template <int LG, int kPF = 4>
@@ -969,14 +1001,15 @@ RTS_DEV void pforce_one(const RtsParams &p, const RtsBuffers &b, int i, int lane
                         unsigned gmask) {
     if (is_ghost(b, i)) return;
     const XsRow *xsr = xs_rows(b);
-    const double m2 = xmul(p.mass, p.mass);  // m^2 (c_spiky applied per pair)
-    const double inv_rho0_sq = xdiv(1.0, xmul(p.rho0, p.rho0));
+    // K = m^2 c_spiky / rho0^2; K p_i, and 2 K p_i for wall neighbours
+    const double K = xmul(xmul(xmul(p.mass, p.mass), p.c_spiky), xdiv(1.0, xmul(p.rho0, p.rho0)));
     const XsRow a = ld_xs(xsr + i);
     const unsigned long long pol = l2_keep_policy();
     const double xi = a.x, yi = a.y, zi = a.z;
-    const double term_i = xmul(a.p, inv_rho0_sq);
-    const double wall = xadd(term_i, term_i);
+    const double k_i = K * a.p, k_wall = 2.0 * k_i;
     const int c = b.cnt[i];
+    RTS_CHECK(b.ctr, 0 <= c && c <= p.width, 404);
+    const int n_tot = p.n_fluid + p.n_bound;
     const int *row = b.nbr + i;  // entry q at row[q * S]: coalesced across lanes
     const size_t S = p.nbr_stride;
     double fx = 0.0, fy = 0.0, fz = 0.0;
@@ -985,11 +1018,13 @@ RTS_DEV void pforce_one(const RtsParams &p, const RtsBuffers &b, int i, int lane
         int jn[kPF], jc[kPF];
         XsRow on[kPF];
 #pragma unroll
-        for (int u = 0; u < kPF; ++u) jc[u] = u < c ? __ldcs(row + u * S) : i;
+        for (int u = 0; u < kPF; ++u)
+            jc[u] = u < c ? rts_safe_idx(b.ctr, __ldcs(row + u * S), n_tot, 405, i) : i;
 #pragma unroll
         for (int u = 0; u < kPF; ++u) on[u] = ld_xs_keep(xsr + jc[u], pol);
 #pragma unroll
-        for (int u = 0; u < kPF; ++u) jn[u] = kPF + u < c ? __ldcs(row + (kPF + u) * S) : i;
+        for (int u = 0; u < kPF; ++u)
+            jn[u] = kPF + u < c ? rts_safe_idx(b.ctr, __ldcs(row + (kPF + u) * S), n_tot, 405, i) : i;
         for (int q = 0; q < c; q += kPF) {
             int j4[kPF];
             XsRow o4[kPF];
@@ -999,12 +1034,14 @@ RTS_DEV void pforce_one(const RtsParams &p, const RtsBuffers &b, int i, int lane
                 o4[u] = on[u];
                 jc[u] = jn[u];
                 on[u] = ld_xs_keep(xsr + jn[u], pol);
-                jn[u] = q + 2 * kPF + u < c ? __ldcs(row + (q + 2 * kPF + u) * S) : i;
+                jn[u] = q + 2 * kPF + u < c
+                            ? rts_safe_idx(b.ctr, __ldcs(row + (q + 2 * kPF + u) * S), n_tot, 405, i)
+                            : i;
             }
 #pragma unroll
             for (int u = 0; u < kPF; ++u)
                 if (q + u < c)
-                    pforce_pair(p, xi, yi, zi, term_i, wall, m2, inv_rho0_sq, i, j4[u], o4[u],
+                    pforce_pair(p, xi, yi, zi, k_i, k_wall, K, i, j4[u], o4[u],
                                 fx, fy, fz);
         }
     } else if (LG == 1) {
@@ -1024,7 +1061,7 @@ RTS_DEV void pforce_one(const RtsParams &p, const RtsBuffers &b, int i, int lane
 #pragma unroll
             for (int u = 0; u < kPF; ++u)
                 if (q + u < c)
-                    pforce_pair(p, xi, yi, zi, term_i, wall, m2, inv_rho0_sq, i, j4[u], o4[u],
+                    pforce_pair(p, xi, yi, zi, k_i, k_wall, K, i, j4[u], o4[u],
                                 fx, fy, fz);
         }
     } else {
@@ -1040,7 +1077,7 @@ RTS_DEV void pforce_one(const RtsParams &p, const RtsBuffers &b, int i, int lane
 #pragma unroll
             for (int u = 0; u < RTS_LG_CH; ++u)
                 if (q0 + u * LG < c)
-                    pforce_pair(p, xi, yi, zi, term_i, wall, m2, inv_rho0_sq, i, j[u], o[u], fx, fy,
+                    pforce_pair(p, xi, yi, zi, k_i, k_wall, K, i, j[u], o[u], fx, fy,
                                 fz);
         }
 #pragma unroll
@@ -1132,7 +1169,7 @@ RTS_DEV void integrate_one(const RtsParams &p, const RtsBuffers &b, int i, int c
     if (countdown & 2) block_maxima_one(b, b.fluid_cells[i], &b.vel[3 * i], &b.force[3 * i],
                                         &b.f_p[3 * i]);
     if (countdown) {
-        const int sl = b.slot_of[i];
+        const int sl = rts_safe_idx(b.ctr, b.slot_of[i], b.ctr->n_sorted, 502, 0);
         reinterpret_cast<float4 *>(b.cpos)[sl] = make_float4(nx[0], nx[1], nx[2], __int_as_float(i));
         if (b.cx) b.cx[sl] = nx[0], b.cy[sl] = nx[1], b.cz[sl] = nx[2];
         int v = b.validity[i] - 1;
@@ -1208,7 +1245,11 @@ __global__ void k_integrate(const __grid_constant__ RtsParams p, RtsBuffers b, i
             int4 val = reinterpret_cast<const int4 *>(b.validity)[g];
             const char4 reg = reinterpret_cast<const char4 *>(b.region)[g];
             const int cl[4] = {cells.x, cells.y, cells.z, cells.w};
-            const int sl[4] = {slots.x, slots.y, slots.z, slots.w};
+            const int nso = b.ctr->n_sorted;
+            const int sl[4] = {rts_safe_idx(b.ctr, slots.x, nso, 503, 0),
+                               rts_safe_idx(b.ctr, slots.y, nso, 503, 0),
+                               rts_safe_idx(b.ctr, slots.z, nso, 503, 0),
+                               rts_safe_idx(b.ctr, slots.w, nso, 503, 0)};
             int vl[4] = {val.x, val.y, val.z, val.w};
             const int rg[4] = {reg.x, reg.y, reg.z, reg.w};
             uint8_t sob[4], cmp[4];

@@ -35,7 +35,7 @@ __global__ void __launch_bounds__(256) k_propagate(const __grid_constant__ RtsPa
         const int k = base + threadIdx.x;
         bool act = false;
         if (k < n_sorted) {
-            const int j = b.order[k];
+            const int j = rts_safe_idx(b.ctr, b.order[k], p.n_fluid + p.n_bound, 201, 0);
             const float x = b.pos[3 * j], y = b.pos[3 * j + 1], z = b.pos[3 * j + 2];
             if (b.cx) b.cx[k] = x, b.cy[k] = y, b.cz[k] = z;
             if (j < p.n_fluid) {
@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(kThreads) k_density(const __grid_constant__ Rt
     const Band bd = make_band(p.h2);
     const size_t S = p.nbr_stride;
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n_act; t += gridDim.x * blockDim.x) {
-        const int k = b.active[t];
+        const int k = rts_safe_idx(b.ctr, b.active[t], b.ctr->n_sorted, 202, 0);
         const int j = b.order[k];
         const float4 a = cpos[k];
         const double xi = a.x, yi = a.y, zi = a.z;
@@ -231,35 +231,34 @@ __global__ void __launch_bounds__(kThreads) k_density(const __grid_constant__ Rt
 }
 
 // One pair term of _forces (wcsph.py:75-101) in fp64, accumulated in the
-// reference's neighbour order, in its operand order except that 1/r comes
-// from an fp64 rsqrt (~1 ulp) instead of a sqrt and a division, and the
-// viscosity's 1/(rho_i rho_j) from the published fp64 reciprocals: ~1e-16
-// relative per term, so the force keeps 1e-4 parity even where the pair
-// terms cancel (hydrostatic rest: |F| << sum |terms|).
-RTS_DEV void force_pair(const RtsParams &p, double xi, double yi, double zi, float4 va,
-                        double inv_rho_i, double term_i, double wall_term, double m2, double mum2,
-                        float4 o, float4 vo, double2 tj, double &fx, double &fy, double &fz) {
-    const double dx = xsub(xi, (double)o.x), dy = xsub(yi, (double)o.y),
-                 dz = xsub(zi, (double)o.z);
-    const double r2 = dist2(dx, dy, dz);
-    if (!(r2 < p.h2)) return;                     // r >= h
-    const double rinv = r2 > 0.0 ? rsqrt(r2) : 0.0;  // r = 0: spiky 0, viscosity kept
-    const double d = xsub(p.h, xmul(r2, rinv));   // h - r
-    const double spk = xmul(xmul(xmul(p.c_spiky, d), d), rinv);  // (c d d) / r
+// reference's neighbour order: with M = m^2 c_spiky and
+// L_i = mu m^2 c_visc / rho_i folded per particle,
+//   fluid j: F += L_i (h - r) / rho_j (v_j - v_i) - M (p_i/rho_i^2 + p_j/rho_j^2) (h - r)^2 / r x_ij
+//   wall j:  F -= M (p_i/rho_i^2 + p_i/rho0^2) (h - r)^2 / r x_ij
+// 1/r from an fp32 estimate + one fp64 Newton step: ~1e-13 relative per
+// term, so the force keeps 1e-4 parity even where the pair terms cancel
+// (hydrostatic rest: |F| << sum |terms|).
+RTS_DEV void force_pair(const RtsParams &p, double xi, double yi, double zi, double vxi,
+                        double vyi, double vzi, double L_i, double term_i, double wall_term,
+                        double M, float4 o, float4 vo, double2 tj, double &fx, double &fy,
+                        double &fz) {
+    const double dx = xi - (double)o.x, dy = yi - (double)o.y, dz = zi - (double)o.z;
+    const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
+    if (!(r2 < p.h2)) return;                       // r >= h
+    const double y = r2 > 0.0 ? rsqrt_nr(r2) : 0.0;  // r = 0: spiky 0, viscosity kept
+    const double d = fma(-r2, y, p.h);              // h - r
+    const double spk = M * d * d * y;               // m^2 c (h - r)^2 / r
     if (o.w >= 0.0f) {  // fluid neighbour: tj = (p_j / rho_j^2, 1 / rho_j) in fp64
-        const double s = xmul(xmul(m2, xadd(term_i, tj.x)), spk);
-        fx = xsub(fx, xmul(s, dx));
-        fy = xsub(fy, xmul(s, dy));
-        fz = xsub(fz, xmul(s, dz));
-        const double lap = xmul(xmul(mum2, xmul(p.c_visc, d)), xmul(inv_rho_i, tj.y));
-        fx = xadd(fx, xmul(lap, xsub((double)vo.x, (double)va.x)));
-        fy = xadd(fy, xmul(lap, xsub((double)vo.y, (double)va.y)));
-        fz = xadd(fz, xmul(lap, xsub((double)vo.z, (double)va.z)));
+        const double s = (term_i + tj.x) * spk;
+        const double lap = L_i * d * tj.y;
+        fx = fma(lap, (double)vo.x - vxi, fma(-s, dx, fx));
+        fy = fma(lap, (double)vo.y - vyi, fma(-s, dy, fy));
+        fz = fma(lap, (double)vo.z - vzi, fma(-s, dz, fz));
     } else {  // static wall sample, mirrored pressure
-        const double s = xmul(xmul(m2, wall_term), spk);
-        fx = xsub(fx, xmul(s, dx));
-        fy = xsub(fy, xmul(s, dy));
-        fz = xsub(fz, xmul(s, dz));
+        const double s = wall_term * spk;
+        fx = fma(-s, dx, fx);
+        fy = fma(-s, dy, fy);
+        fz = fma(-s, dz, fz);
     }
 }
 
@@ -274,7 +273,7 @@ __global__ void __launch_bounds__(kThreads) k_forces(const __grid_constant__ Rts
     const Band bd = make_band(p.h2);
     const double m2 = xmul(p.mass, p.mass);
     const double inv_rho0_sq = xdiv(1.0, xmul(p.rho0, p.rho0));
-    const double mum2 = xmul(p.mu, m2);
+    const double M = xmul(m2, p.c_spiky), mum2c = xmul(xmul(p.mu, m2), p.c_visc);
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n_act; t += gridDim.x * blockDim.x) {
         const int k = b.active[t];
         const int j = b.order[k];
@@ -282,8 +281,10 @@ __global__ void __launch_bounds__(kThreads) k_forces(const __grid_constant__ Rts
         const float4 va = cvel[k];
         const double xi = a.x, yi = a.y, zi = a.z;
         const double4 own = ld_f64x4(b.cterm + 4 * (size_t)k);  // p/rho^2, 1/rho, p (fp64)
-        const double term_i = own.x, inv_rho_i = own.y, p_i = own.z;
+        const double term_i = own.x, p_i = own.z;
+        const double L_i = mum2c * own.y;
         const double wall_term = xadd(term_i, xmul(p_i, inv_rho0_sq));
+        const double vxi = va.x, vyi = va.y, vzi = va.z;
         const int n_all = b.cnt[t];  // the density pass's neighbour list of slot k
         const int *col = b.nbr + t;
         double fx = 0.0, fy = 0.0, fz = 0.0;
@@ -296,7 +297,10 @@ __global__ void __launch_bounds__(kThreads) k_forces(const __grid_constant__ Rts
                 float4 pq[RTS_WF_CH], vq[RTS_WF_CH];
                 double2 tq[RTS_WF_CH];
 #pragma unroll
-                for (int u = 0; u < RTS_WF_CH; ++u) kq[u] = q0 + u < n_all ? col[(q0 + u) * S] : k;
+                for (int u = 0; u < RTS_WF_CH; ++u)
+                    kq[u] = q0 + u < n_all
+                                ? rts_safe_idx(b.ctr, col[(q0 + u) * S], b.ctr->n_sorted, 203, k)
+                                : k;
 #pragma unroll
                 for (int u = 0; u < RTS_WF_CH; ++u) {
                     pq[u] = cpos[kq[u]];
@@ -306,14 +310,14 @@ __global__ void __launch_bounds__(kThreads) k_forces(const __grid_constant__ Rts
 #pragma unroll
                 for (int u = 0; u < RTS_WF_CH; ++u)
                     if (kq[u] != k)
-                        force_pair(p, xi, yi, zi, va, inv_rho_i, term_i, wall_term, m2, mum2, pq[u],
+                        force_pair(p, xi, yi, zi, vxi, vyi, vzi, L_i, term_i, wall_term, M, pq[u],
                                    vq[u], tq[u], fx, fy, fz);
             }
         } else if (n_all <= kHitCap) {
             for (int q = 0; q < n_all; ++q) {
                 const int kq = col[q * S];
                 if (kq == k) continue;
-                force_pair(p, xi, yi, zi, va, inv_rho_i, term_i, wall_term, m2, mum2, cpos[kq],
+                force_pair(p, xi, yi, zi, vxi, vyi, vzi, L_i, term_i, wall_term, M, cpos[kq],
                            cvel[kq], reinterpret_cast<const double2 *>(b.cterm)[2 * (size_t)kq],
                            fx, fy, fz);
             }
@@ -323,7 +327,7 @@ __global__ void __launch_bounds__(kThreads) k_forces(const __grid_constant__ Rts
             for (int s = 0; s < ns; ++s)
                 for (int q = sp[s].k0; q < sp[s].k1; ++q)
                     if (q != k && in_support(bd, a.x, a.y, a.z, cpos[q]))
-                        force_pair(p, xi, yi, zi, va, inv_rho_i, term_i, wall_term, m2, mum2, cpos[q],
+                        force_pair(p, xi, yi, zi, vxi, vyi, vzi, L_i, term_i, wall_term, M, cpos[q],
                                    cvel[q], reinterpret_cast<const double2 *>(b.cterm)[2 * (size_t)q],
                                    fx, fy, fz);
         }

@@ -7,6 +7,7 @@ common state <= 1e-4 relative (BASELINE.json north_star).
 """
 
 import dataclasses
+import os
 
 import numpy as np
 import pytest
@@ -309,3 +310,22 @@ def test_audit_counts_missing_entries():
     s._audit_refresh()
     c = s.counters.read(s._stream())
     assert c.missing == s.n_fluid
+
+
+@pytest.mark.skipif(not os.environ.get("RTS_SPH_LIB", "").endswith("checked.so"),
+                    reason="needs the bounds-checked build (scripts/checked_build.sh)")
+def test_checked_build_flags_a_corrupt_neighbour_entry():
+    """The checked build's range checks fire instead of a wild access: a
+    neighbour-table entry past the last particle stops the pass with
+    RTS_ERR_CHECK at the density gather (site 403)."""
+    from paper_2009_14514_b200 import PcisphSolver
+    from paper_2009_14514_b200 import _native as N
+    dev = PcisphSolver(tiny_tank(), mode="rts", use_graphs=False)
+    dev.advance()
+    dev._nbr[1, 5] = dev.n_fluid + dev.n_bound + 1000  # row 5, entry 1
+    dev._call("rts_pci_minor_begin", 0, 0)
+    dev._call("rts_pci_motion", 1)
+    dev._call("rts_pci_sets", 0b11110, 0)
+    dev._call("rts_pci_density")
+    c = dev.counters.read(dev._stream())
+    assert c.err_flags & N.ERR_CHECK and c.check_site == 403
