@@ -474,16 +474,22 @@ def wcsph_comparison(world: int, device, stream, barrier) -> dict:
           "wall_s_per_simulated_ms": tw / (1e3 * sim_rts), "n_gpus": world,
           "scaling": "strong" if world > 1 else None}
     del ws
-    wb, solver = make("baseline")
-    solver.dt_cap = 4 * solver.dt_base
-    for _ in range(4):
-        wb.step()
-    tb, _, sim_b = timed(wb, n_w // 2)
-    wc["baseline_adaptive"] = {
-        "ms_per_step": 1e3 * tb / (n_w // 2), "mean_dt": sim_b / (n_w // 2),
-        "wall_s_per_simulated_ms": tb / (1e3 * sim_b),
-        "rts_speedup_per_simulated_time": (tb / sim_b) / (tw / sim_rts)}
-    del wb
+    # the global baseline (wcsph.py:199-233, every particle every step) at both
+    # caps BASELINE.md section 2 reports: dt_cap = 4 dt_base (CFL-adaptive,
+    # mean dt ~4 dt_base on this calm start) and the reference's default
+    # dt_cap = dt_base (wcsph.py:143-144: a constant dt_base step)
+    for key, cap in (("baseline_adaptive", 4.0), ("baseline_default_cap", 1.0)):
+        wb, solver = make("baseline")
+        solver.dt_cap = cap * solver.dt_base
+        for _ in range(4):
+            wb.step()
+        tb, _, sim_b = timed(wb, n_w // 2)
+        wc[key] = {
+            "dt_cap_over_dt_base": cap,
+            "ms_per_step": 1e3 * tb / (n_w // 2), "mean_dt": sim_b / (n_w // 2),
+            "wall_s_per_simulated_ms": tb / (1e3 * sim_b),
+            "rts_speedup_per_simulated_time": (tb / sim_b) / (tw / sim_rts)}
+        del wb, solver
     return wc
 
 

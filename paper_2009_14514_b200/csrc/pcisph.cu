@@ -762,7 +762,8 @@ RTS_DEV void density_one(const RtsParams &p, const RtsBuffers &b, int i, int lan
         // the tables exceed L2) are requested before this chunk's gathers
         int jn[CH];
 #pragma unroll
-        for (int u = 0; u < CH; ++u) jn[u] = u < c ? __ldcs(row + u * S) : i;
+        for (int u = 0; u < CH; ++u)
+            jn[u] = u < c ? rts_safe_idx(b.ctr, __ldcs(row + u * S), n_tot, 403, i) : i;
         for (int q = 0; q < c; q += CH) {
             int j8[CH];
 #pragma unroll
@@ -788,7 +789,7 @@ RTS_DEV void density_one(const RtsParams &p, const RtsBuffers &b, int i, int lan
 #pragma unroll
             for (int u = 0; u < RTS_LG_CH; ++u) {
                 const int q = q0 + u * LG;
-                o[u] = ld_xs3(xsr + (q < c ? row[q * S] : i));
+                o[u] = ld_xs3(xsr + (q < c ? rts_safe_idx(b.ctr, row[q * S], n_tot, 403, i) : i));
             }
 #pragma unroll
             for (int u = 0; u < RTS_LG_CH; ++u)
@@ -1071,7 +1072,7 @@ RTS_DEV void pforce_one(const RtsParams &p, const RtsBuffers &b, int i, int lane
 #pragma unroll
             for (int u = 0; u < RTS_LG_CH; ++u) {
                 const int q = q0 + u * LG;
-                j[u] = q < c ? row[q * S] : i;
+                j[u] = q < c ? rts_safe_idx(b.ctr, row[q * S], n_tot, 405, i) : i;
                 o[u] = ld_xs(xsr + j[u]);
             }
 #pragma unroll

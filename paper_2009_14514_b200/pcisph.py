@@ -15,8 +15,10 @@ kernels one by one (per-kernel timing, the neighbour audit, x-slab ranks).
 
 from __future__ import annotations
 
+import collections
 import ctypes
 import dataclasses
+import itertools
 import math
 
 import numpy as np
@@ -46,34 +48,39 @@ DEFAULT_SCHEDULE = (
 )
 
 
-def validate_schedule(schedule, n_regions: int = 4) -> None:
-    """The five legality rules of pcisph.py:80-117; ConfigError on failure."""
-    n_minor = len(schedule)
-    tally = np.zeros((n_minor, n_regions + 1), dtype=int)
-    for j, rows in enumerate(schedule):
-        for row in rows:
-            for n in row:
-                if not 1 <= n <= n_regions:
-                    raise ConfigError(f"schedule names region {n} outside 1..{n_regions}")
-                tally[j, n] += 1
-    for j in range(n_minor):
-        for n in range(1, n_regions + 1):
-            if tally[j, n] < 1:
-                raise ConfigError(f"region {n} receives no iteration on minor step {j + 1}")
-    for n in range(1, n_regions + 1):
-        if tally[0, n] < 2:
-            raise ConfigError(
-                f"region {n} receives fewer than 2 iterations on the first minor step")
-    for j in range(n_minor):
-        if tally[j, 1] < 3:
-            raise ConfigError(f"region 1 receives fewer than 3 iterations on minor step {j + 1}")
-    for n in range(1, n_regions + 1):
-        window = 2 if n == 2 else min(n, n_minor)
+def _violations(tally, n_regions: int):
+    """The schedule rules of pcisph.py:80-117, as messages, in the order the
+    reference checks them: every region on every minor step; every region
+    twice on the first; region 1 three times on each; region n (window 2 for
+    region 2) at least 3 times in every cyclic window of its own step."""
+    n_minor = len(tally)
+    regions = range(1, n_regions + 1)
+    yield from (f"region {n} receives no iteration on minor step {j + 1}"
+                for j in range(n_minor) for n in regions if tally[j][n] < 1)
+    yield from (f"region {n} receives fewer than 2 iterations on the first minor step"
+                for n in regions if tally[0][n] < 2)
+    yield from (f"region 1 receives fewer than 3 iterations on minor step {j + 1}"
+                for j in range(n_minor) if tally[j][1] < 3)
+    for n in regions:
+        w = 2 if n == 2 else min(n, n_minor)
         for j in range(n_minor):
-            total = sum(tally[(j + q) % n_minor, n] for q in range(window))
-            if total < 3:
-                raise ConfigError(f"region {n} receives {total} < 3 iterations in the "
-                                  f"{window}-minor window starting at minor step {j + 1}")
+            got = sum(tally[(j + q) % n_minor][n] for q in range(w))
+            if got < 3:
+                yield (f"region {n} receives {got} < 3 iterations in the {w}-minor window "
+                       f"starting at minor step {j + 1}")
+
+
+def validate_schedule(schedule, n_regions: int = 4) -> None:
+    """ConfigError unless ``schedule`` meets the reference's legality rules."""
+    tally = [collections.Counter() for _ in schedule]
+    for j, rows in enumerate(schedule):
+        for n in itertools.chain.from_iterable(rows):
+            if not 1 <= n <= n_regions:
+                raise ConfigError(f"schedule names region {n} outside 1..{n_regions}")
+            tally[j][n] += 1
+    first = next(_violations(tally, n_regions), None)
+    if first is not None:
+        raise ConfigError(first)
 
 
 def _template_factor(h: float, spacing: float) -> float:
@@ -117,12 +124,12 @@ class MajorStepController:
     recovery_left: int = 0
 
     def note_major(self, early_terminated: bool) -> None:
-        if early_terminated:
-            self.n_current = 2
-            self.recovery_left = 10
-        elif self.recovery_left > 0:
+        if early_terminated:  # N = 2 for the next ten majors
+            self.n_current, self.recovery_left = 2, 10
+            return
+        if self.recovery_left:
             self.recovery_left -= 1
-            if self.recovery_left == 0:
+            if not self.recovery_left:
                 self.n_current = self.n_nominal
 
 

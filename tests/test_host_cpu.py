@@ -184,3 +184,31 @@ def test_comm_keyword_requires_the_default_group():
     for cls in (WcsphSolver, PcisphSolver):
         with pytest.raises(ValueError, match="comm must be"):
             cls(sc, comm=object())
+
+
+def test_schedule_validation_matches_the_reference_rules_on_random_schedules():
+    """validate_schedule (table-driven rewrite) against the oracle's
+    statement of pcisph.py:80-117: same verdict, same first message."""
+    import random
+
+    from oracle.sph import validate_schedule as reference_rules
+    from paper_2009_14514_b200.pcisph import validate_schedule
+    rng = random.Random(1)
+
+    def verdict(f, sch):
+        try:
+            f(sch)
+            return None
+        except ConfigError as exc:
+            return str(exc)
+
+    legal = 0
+    for _ in range(2000):
+        sch = tuple(tuple(tuple(rng.sample(range(1, 6 if rng.random() < 0.05 else 5),
+                                           rng.randint(1, 4)))
+                          for _ in range(rng.randint(1, 4)))
+                    for _ in range(rng.choice([2, 4])))
+        a, b = verdict(validate_schedule, sch), verdict(reference_rules, sch)
+        assert a == b, (sch, a, b)
+        legal += a is None
+    assert legal > 0
