@@ -763,9 +763,9 @@ def main():
     peak = float(peaks.get("hbm_gbs", 6650.0))
     alg = algo_bytes(dom, solver, c_mean, rec, counts[dom])
     achieved = alg / totals[dom] / 1e9 if totals[dom] > 0 else 0.0
-    traffic = None
+    traffic = None  # ncu DRAM bytes per launch: captured for the default workload only
     tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tf):
+    if os.path.exists(tf) and args.workload == "cfg2" and world == 1:
         traffic = json.load(open(tf)).get(dom)
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": dom,
