@@ -106,10 +106,20 @@ RTS_DEV XsRow ld_xs_keep(const XsRow *ptr, unsigned long long pol) {
     return xs_unpack(r0, r1, r2, r3);
 }
 // x* only (the density pass): the p word is not brought into registers
+#ifndef RTS_XS_KEEP
+#define RTS_XS_KEEP 0  // density gathers tagged L2 evict-last (A/B)
+#endif
 RTS_DEV XsRow ld_xs3(const XsRow *ptr) {
     XsRow r;
+#if RTS_XS_KEEP
+    unsigned long long pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("ld.global.L2::cache_hint.v4.f64 {%0, %1, %2, _}, [%3], %4;"
+                 : "=d"(r.x), "=d"(r.y), "=d"(r.z) : "l"(ptr), "l"(pol));
+#else
     asm volatile("ld.global.v4.f64 {%0, %1, %2, _}, [%3];"
                  : "=d"(r.x), "=d"(r.y), "=d"(r.z) : "l"(ptr));
+#endif
     r.p = 0.0;
     return r;
 }

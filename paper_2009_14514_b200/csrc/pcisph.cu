@@ -40,6 +40,9 @@
 #ifndef RTS_PFOR_CH
 #define RTS_PFOR_CH 3
 #endif
+#ifndef RTS_CVEL
+#define RTS_CVEL 1  // slot-ordered velocity copy for the refresh's viscosity sums (A/B: 0)
+#endif
 #ifndef RTS_PFOR_MINB
 #define RTS_PFOR_MINB 5
 #endif
@@ -99,6 +102,10 @@ __global__ void k_gather(const __grid_constant__ RtsParams p, RtsBuffers b) {
         const float x = b.pos[3 * j], y = b.pos[3 * j + 1], z = b.pos[3 * j + 2];
         reinterpret_cast<float4 *>(b.cpos)[k] = make_float4(x, y, z, __int_as_float(j));
         if (b.cx) b.cx[k] = x, b.cy[k] = y, b.cz[k] = z;
+        if (RTS_CVEL && b.cvel)  // slot-ordered velocities for the refresh's viscosity
+            reinterpret_cast<float4 *>(b.cvel)[k] =
+                j < p.n_fluid ? make_float4(b.vel[3 * j], b.vel[3 * j + 1], b.vel[3 * j + 2], 0.f)
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
         if (j < p.n_fluid) b.slot_of[j] = k;
     }
 }
@@ -358,6 +365,26 @@ RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshC
                         float4 o[4];
                         float vj[4][3];
                         int nq = 0;
+                        if (RTS_CVEL && b.cvel) {
+                            // velocities from the slot-ordered copy: loaded with
+                            // the candidate, not after its id (no dependent chain)
+                            const float4 *cv = reinterpret_cast<const float4 *>(b.cvel) + cb;
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                o[u] = make_float4(fxi, fyi, fzi, __int_as_float(i));
+                                float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
+                                if (mem) {
+                                    const int q = __ffs(mem) - 1;
+                                    o[u] = cp[q];
+                                    w = cv[q];
+                                    mem &= mem - 1u;
+                                    nq = u + 1;
+                                }
+                                vj[u][0] = w.x;
+                                vj[u][1] = w.y;
+                                vj[u][2] = w.z;
+                            }
+                        } else {
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
                             o[u] = make_float4(fxi, fyi, fzi, __int_as_float(i));
@@ -374,6 +401,7 @@ RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshC
                             vj[u][0] = b.vel[3 * jc];
                             vj[u][1] = b.vel[3 * jc + 1];
                             vj[u][2] = b.vel[3 * jc + 2];
+                        }
                         }
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
@@ -1142,11 +1170,8 @@ RTS_DEV void note_displacement(const RtsBuffers &b, int countdown, float dmax) {
 
 RTS_DEV void integrate_one(const RtsParams &p, const RtsBuffers &b, int i, int countdown,
                            int gen, double dim, float &dmax) {
-    // public x* = the last prediction; S_ob from the final S_e generation
-    const XsRow xs = ld_xs(xs_rows(b) + i);
-    b.xstar[3 * i] = (float)xs.x;
-    b.xstar[3 * i + 1] = (float)xs.y;
-    b.xstar[3 * i + 2] = (float)xs.z;
+    // S_ob from the final S_e generation (the public x* is the host's fp32
+    // view of the xs rows, PcisphSolver.xstar)
     if (countdown) b.in_sob[i] = observed_block(b, b.fluid_cells[i], gen);
     float nx[3];
 #pragma unroll
@@ -1173,6 +1198,9 @@ RTS_DEV void integrate_one(const RtsParams &p, const RtsBuffers &b, int i, int c
         const int sl = rts_safe_idx(b.ctr, b.slot_of[i], b.ctr->n_sorted, 502, 0);
         reinterpret_cast<float4 *>(b.cpos)[sl] = make_float4(nx[0], nx[1], nx[2], __int_as_float(i));
         if (b.cx) b.cx[sl] = nx[0], b.cy[sl] = nx[1], b.cz[sl] = nx[2];
+        if (RTS_CVEL && b.cvel)
+            reinterpret_cast<float4 *>(b.cvel)[sl] =
+                make_float4(b.vel[3 * i], b.vel[3 * i + 1], b.vel[3 * i + 2], 0.f);
         int v = b.validity[i] - 1;
         const bool expired = v <= 0;
         if (expired) {
@@ -1207,19 +1235,11 @@ __global__ void k_integrate(const __grid_constant__ RtsParams p, RtsBuffers b, i
     }
     const int ng = nf / 4;
     for (int g = tid; g < ng; g += nt) {
-        float fe[12], fp[12], v[12], x[12], xsv[12];
+        float fe[12], fp[12], v[12], x[12];
         load12(b.force, g, fe);
         load12(b.f_p, g, fp);
         load12(b.vel, g, v);
         load12(b.pos, g, x);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const XsRow xs = ld_xs(xs_rows(b) + 4 * g + q);
-            xsv[3 * q] = (float)xs.x;
-            xsv[3 * q + 1] = (float)xs.y;
-            xsv[3 * q + 2] = (float)xs.z;
-        }
-        store12(b.xstar, g, xsv);
 #pragma unroll
         for (int c = 0; c < 12; ++c) {
             const int a = c % 3;
@@ -1261,6 +1281,9 @@ __global__ void k_integrate(const __grid_constant__ RtsParams p, RtsBuffers b, i
                 reinterpret_cast<float4 *>(b.cpos)[sl[q]] =
                     make_float4(x[3 * q], x[3 * q + 1], x[3 * q + 2], __int_as_float(4 * g + q));
                 if (b.cx) b.cx[sl[q]] = x[3 * q], b.cy[sl[q]] = x[3 * q + 1], b.cz[sl[q]] = x[3 * q + 2];
+                if (RTS_CVEL && b.cvel)
+                    reinterpret_cast<float4 *>(b.cvel)[sl[q]] =
+                        make_float4(v[3 * q], v[3 * q + 1], v[3 * q + 2], 0.f);
                 int vv = vl[q] - 1;
                 const bool expired = vv <= 0;
                 if (expired) vv = kValidity[rg[q] < 0 ? 0 : (rg[q] > 4 ? 4 : rg[q])];

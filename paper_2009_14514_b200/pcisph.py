@@ -391,6 +391,22 @@ class PcisphSolver(_DeviceSolver):
         return self.arena["block_field"]
 
     @property
+    def xstar(self) -> torch.Tensor:
+        """Predicted positions of the last prediction (pcisph.py:202-213): the
+        fp32 view of the fp64 x* the kernels keep in the xs rows, refreshed
+        on access after a step (the integrator no longer copies it out)."""
+        t = self._xstar_t
+        if getattr(self, "_xstar_dirty", False) and self.n_fluid:
+            t.copy_(self.arena["xs"][: self.n_fluid, :3])
+        self._xstar_dirty = False
+        return t
+
+    @xstar.setter
+    def xstar(self, t: torch.Tensor) -> None:
+        self._xstar_t = t
+        self._xstar_dirty = False
+
+    @property
     def vstar(self) -> torch.Tensor:
         """Predicted velocities of the last prediction (pcisph.py:202-213),
         recovered as (x* - pos) / dt from the stored fp32 x* (the kernels keep
@@ -424,6 +440,7 @@ class PcisphSolver(_DeviceSolver):
 
     def _call(self, name, *args):
         self._launch(name, *args)
+        self._xstar_dirty = True  # any pass may have rewritten the xs rows
 
     def _prepare(self, dt: float) -> None:
         self._sync_params()
@@ -489,6 +506,7 @@ class PcisphSolver(_DeviceSolver):
             self._call("rts_pci_integrate", 0)
             self._call("rts_pci_minor_end", 0)
         ctl, c = self._read_control()
+        self._xstar_dirty = True
         if graph is not None:
             n_static, n_body = N.graph_kernel_counts(graph)
             N.note_graph_kernels(n_static + n_body * max(0, ctl.stats[0].iterations))
@@ -575,6 +593,7 @@ class PcisphSolver(_DeviceSolver):
                         self._call("rts_pci_mark_updates")
                     self._call("rts_pci_minor_end", j)
         ctl, c = self._read_control()
+        self._xstar_dirty = True
         if graph is not None:  # launch accounting of the graph's kernel nodes
             n_static, n_body = N.graph_kernel_counts(graph)
             its = sum(max(0, ctl.stats[j].iterations) for j in range(n_minor))
