@@ -40,9 +40,6 @@
 #ifndef RTS_PFOR_CH
 #define RTS_PFOR_CH 3
 #endif
-#ifndef RTS_CVEL
-#define RTS_CVEL 1  // slot-ordered velocity copy for the refresh's viscosity sums (A/B: 0)
-#endif
 #ifndef RTS_PFOR_MINB
 #define RTS_PFOR_MINB 5
 #endif
@@ -102,10 +99,6 @@ __global__ void k_gather(const __grid_constant__ RtsParams p, RtsBuffers b) {
         const float x = b.pos[3 * j], y = b.pos[3 * j + 1], z = b.pos[3 * j + 2];
         reinterpret_cast<float4 *>(b.cpos)[k] = make_float4(x, y, z, __int_as_float(j));
         if (b.cx) b.cx[k] = x, b.cy[k] = y, b.cz[k] = z;
-        if (RTS_CVEL && b.cvel)  // slot-ordered velocities for the refresh's viscosity
-            reinterpret_cast<float4 *>(b.cvel)[k] =
-                j < p.n_fluid ? make_float4(b.vel[3 * j], b.vel[3 * j + 1], b.vel[3 * j + 2], 0.f)
-                              : make_float4(0.f, 0.f, 0.f, 0.f);
         if (j < p.n_fluid) b.slot_of[j] = k;
     }
 }
@@ -365,26 +358,6 @@ RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshC
                         float4 o[4];
                         float vj[4][3];
                         int nq = 0;
-                        if (RTS_CVEL && b.cvel) {
-                            // velocities from the slot-ordered copy: loaded with
-                            // the candidate, not after its id (no dependent chain)
-                            const float4 *cv = reinterpret_cast<const float4 *>(b.cvel) + cb;
-#pragma unroll
-                            for (int u = 0; u < 4; ++u) {
-                                o[u] = make_float4(fxi, fyi, fzi, __int_as_float(i));
-                                float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
-                                if (mem) {
-                                    const int q = __ffs(mem) - 1;
-                                    o[u] = cp[q];
-                                    w = cv[q];
-                                    mem &= mem - 1u;
-                                    nq = u + 1;
-                                }
-                                vj[u][0] = w.x;
-                                vj[u][1] = w.y;
-                                vj[u][2] = w.z;
-                            }
-                        } else {
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
                             o[u] = make_float4(fxi, fyi, fzi, __int_as_float(i));
@@ -401,7 +374,6 @@ RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshC
                             vj[u][0] = b.vel[3 * jc];
                             vj[u][1] = b.vel[3 * jc + 1];
                             vj[u][2] = b.vel[3 * jc + 2];
-                        }
                         }
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
@@ -1198,9 +1170,6 @@ RTS_DEV void integrate_one(const RtsParams &p, const RtsBuffers &b, int i, int c
         const int sl = rts_safe_idx(b.ctr, b.slot_of[i], b.ctr->n_sorted, 502, 0);
         reinterpret_cast<float4 *>(b.cpos)[sl] = make_float4(nx[0], nx[1], nx[2], __int_as_float(i));
         if (b.cx) b.cx[sl] = nx[0], b.cy[sl] = nx[1], b.cz[sl] = nx[2];
-        if (RTS_CVEL && b.cvel)
-            reinterpret_cast<float4 *>(b.cvel)[sl] =
-                make_float4(b.vel[3 * i], b.vel[3 * i + 1], b.vel[3 * i + 2], 0.f);
         int v = b.validity[i] - 1;
         const bool expired = v <= 0;
         if (expired) {
@@ -1281,9 +1250,6 @@ __global__ void k_integrate(const __grid_constant__ RtsParams p, RtsBuffers b, i
                 reinterpret_cast<float4 *>(b.cpos)[sl[q]] =
                     make_float4(x[3 * q], x[3 * q + 1], x[3 * q + 2], __int_as_float(4 * g + q));
                 if (b.cx) b.cx[sl[q]] = x[3 * q], b.cy[sl[q]] = x[3 * q + 1], b.cz[sl[q]] = x[3 * q + 2];
-                if (RTS_CVEL && b.cvel)
-                    reinterpret_cast<float4 *>(b.cvel)[sl[q]] =
-                        make_float4(v[3 * q], v[3 * q + 1], v[3 * q + 2], 0.f);
                 int vv = vl[q] - 1;
                 const bool expired = vv <= 0;
                 if (expired) vv = kValidity[rg[q] < 0 ? 0 : (rg[q] > 4 ? 4 : rg[q])];

@@ -468,8 +468,7 @@ class PcisphExchange:
                 "motion": ch([(xw, 8, 8, None, 0)]),  # x* and p (zeroed / restored)
                 "density": ch(dens),
                 # pos also refreshes the candidate copy at the row's CSR slot
-                "integrate": ch(move, move + [(A["cpos"], 3, 4, A["slot_of"], 0),
-                                              (A["cvel"], 3, 4, A["slot_of"], 3)]),
+                "integrate": ch(move, move + [(A["cpos"], 3, 4, A["slot_of"], 0)]),
             }
             dev = self.x.compute_device
             W = self.N_CTL
