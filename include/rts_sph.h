@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define RTS_ABI_VERSION 27
+#define RTS_ABI_VERSION 28
 
 /* err_flags bits */
 #define RTS_ERR_ESCAPED   0x1u  /* fluid left the padded grid or non-finite (grid.py:268-273) */
@@ -198,8 +198,10 @@ typedef struct RtsBuffers {
     /* sorted candidate copies, slot k of the CSR */
     float   *cpos;         /* (Nf+Nb, 4)  x y z p   (p = -1 marks a boundary slot) */
     float   *cvel;         /* (Nf+Nb, 4)  vx vy vz rho */
-    double  *cterm;        /* (Nf+Nb, 4)  WCSPH: fp64 {p/rho^2, 1/rho, p, 0} of the slot's
-                            * particle from this step's density pass (force pair terms) */
+    double  *cterm;        /* (Nf+Nb, 4)  WCSPH: 32-byte rows {fp64 p/rho^2, fp64 1/rho, fp32 v}
+                            * of the slot's particle (this step's density pass for active
+                            * slots): one 256-bit gather per force pair */
+    double  *cwall;        /* (Nf+Nb)     WCSPH: fp64 p/rho^2 + p/rho0^2 (wall pair term) */
     float   *cx, *cy, *cz; /* (Nf+Nb+4 each, 16-byte aligned) the candidate positions of cpos
                             * as separate x / y / z arrays: the neighbour searches load four
                             * candidates per 128-bit access and test them in packed fp32x2 */

@@ -12,7 +12,7 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "librtssph.so")
-ABI_VERSION = 27
+ABI_VERSION = 28
 
 _c = ctypes
 _D = _c.c_double
@@ -78,7 +78,7 @@ BUFFER_FIELDS = (
     "dt_corr", "validity", "region", "compute", "in_se", "in_sob", "fluid_cells", "cell_count",
     "cell_bcount", "starts", "order", "fill", "scan_tmp", "bcell_ids", "bcell_start", "bidx",
     "bcell_of", "bcell_active", "vmax", "fmax", "block_raw", "block_field", "block_tmp",
-    "block_flag", "cpos", "cvel", "cterm", "cx", "cy", "cz", "active", "list2", "list3", "nbr", "cnt", "xs", "pflag", "partial",
+    "block_flag", "cpos", "cvel", "cterm", "cwall", "cx", "cy", "cz", "active", "list2", "list3", "nbr", "cnt", "xs", "pflag", "partial",
     "snap_p", "snap_fp", "slot_of", "ctl", "se_stamp", "near_stamp", "ghost", "sort_key", "ctr",
 )
 

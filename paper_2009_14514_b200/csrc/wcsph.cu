@@ -4,7 +4,8 @@
 // the 3x3x3 block neighbourhood of each active particle directly in the CSR
 // (the three z-adjacent blocks of each (x, y) column are one contiguous
 // span, so nine spans), reading the sorted candidate copies `cpos`
-// (x y z p) / `cvel` (v rho) written by the propagate pass.  The set of j
+// (x y z, p/rho^2 marker) and `cterm` (fp64 p/rho^2, 1/rho; v) written by the
+// propagate pass.  The set of j
 // with r^2 < h^2 (fp64, un-fused) and the visiting order (blocks in
 // (ax, ay, az) order, CSR order inside a block) are exactly those of the
 // reference's table fill (grid.py:133-149) followed by its table walk
@@ -24,6 +25,37 @@ namespace {
 
 constexpr int kThreads = 128;
 
+// 32-byte per-slot force-pass row: fp64 p/rho^2 and 1/rho of the slot's
+// particle (this step's density for active slots, the stored state
+// otherwise) and its fp32 velocity -- a neighbour is one 256-bit gather
+// here plus its cpos row
+struct TermRow {
+    double term, inv_rho;
+    float vx, vy, vz;
+};
+RTS_DEV void st_term(double *rows, int k, double term, double inv_rho, float vx, float vy,
+                     float vz) {
+    const unsigned long long v01 =
+        (unsigned long long)__float_as_uint(vx) | ((unsigned long long)__float_as_uint(vy) << 32);
+    const unsigned long long v2 = (unsigned long long)__float_as_uint(vz);
+    asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(rows + 4 * (size_t)k),
+                 "l"((unsigned long long)__double_as_longlong(term)),
+                 "l"((unsigned long long)__double_as_longlong(inv_rho)), "l"(v01), "l"(v2)
+                 : "memory");
+}
+RTS_DEV TermRow ld_term(const double *rows, int k) {
+    unsigned long long r0, r1, r2, r3;
+    asm volatile("ld.global.v4.b64 {%0, %1, %2, %3}, [%4];"
+                 : "=l"(r0), "=l"(r1), "=l"(r2), "=l"(r3) : "l"(rows + 4 * (size_t)k));
+    TermRow t;
+    t.term = __longlong_as_double((long long)r0);
+    t.inv_rho = __longlong_as_double((long long)r1);
+    t.vx = __uint_as_float((unsigned)(r2 & 0xffffffffull));
+    t.vy = __uint_as_float((unsigned)(r2 >> 32));
+    t.vz = __uint_as_float((unsigned)(r3 & 0xffffffffull));
+    return t;
+}
+
 // wcsph.py:262-266 (validity / pre-emption) + sorted-copy gather + active list
 __global__ void __launch_bounds__(256) k_propagate(const __grid_constant__ RtsParams p,
                                                    RtsBuffers b) {
@@ -42,11 +74,9 @@ __global__ void __launch_bounds__(256) k_propagate(const __grid_constant__ RtsPa
                 const double rho = b.rho[j], pr = b.pres[j];
                 const double term = xdiv(pr, xmul(rho, rho)), inv_rho = xdiv(1.0, rho);
                 reinterpret_cast<float4 *>(b.cpos)[k] = make_float4(x, y, z, (float)term);
-                reinterpret_cast<float4 *>(b.cvel)[k] = make_float4(
-                    b.vel[3 * j], b.vel[3 * j + 1], b.vel[3 * j + 2], (float)inv_rho);
                 // the stored density / pressure of the slot's particle, fp64
-                // (active particles overwrite it in the density pass)
-                st_f64x4(b.cterm + 4 * (size_t)k, term, inv_rho, pr, rho);
+                // (active particles overwrite them in the density pass)
+                st_term(b.cterm, k, term, inv_rho, b.vel[3 * j], b.vel[3 * j + 1], b.vel[3 * j + 2]);
                 if (p.rts) {
                     const int8_t blk = b.block_field[b.fluid_cells[j]];
                     int v = b.validity[j] - 1;
@@ -63,7 +93,7 @@ __global__ void __launch_bounds__(256) k_propagate(const __grid_constant__ RtsPa
                 }
             } else {
                 reinterpret_cast<float4 *>(b.cpos)[k] = make_float4(x, y, z, -1.0f);
-                reinterpret_cast<float4 *>(b.cvel)[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+                st_term(b.cterm, k, 0.0, 0.0, 0.f, 0.f, 0.f);
             }
         }
         block_append2<256>(act, k, b.active, &b.ctr->n_compute, false, 0, nullptr, nullptr);
@@ -226,7 +256,13 @@ __global__ void __launch_bounds__(kThreads) k_density(const __grid_constant__ Rt
         // p in fp64 for the force pass: the pair terms then use this step's
         // fp64 density and pressure, as the reference does, not their fp32
         // stores (whose 6e-8 rounding the cancelling pair sums amplify)
-        st_f64x4(b.cterm + 4 * (size_t)k, xdiv(pr, xmul(rho, rho)), xdiv(1.0, rho), pr, rho);
+        {
+            const double term = xdiv(pr, xmul(rho, rho));
+            st_term(b.cterm, k, term, xdiv(1.0, rho), b.vel[3 * j], b.vel[3 * j + 1],
+                    b.vel[3 * j + 2]);
+            // the wall pair term of this particle (wcsph.py:97): p/rho^2 + p/rho0^2
+            b.cwall[k] = xadd(term, xmul(pr, xdiv(1.0, xmul(p.rho0, p.rho0))));
+        }
     }
 }
 
@@ -240,20 +276,19 @@ __global__ void __launch_bounds__(kThreads) k_density(const __grid_constant__ Rt
 // (hydrostatic rest: |F| << sum |terms|).
 RTS_DEV void force_pair(const RtsParams &p, double xi, double yi, double zi, double vxi,
                         double vyi, double vzi, double L_i, double term_i, double wall_term,
-                        double M, float4 o, float4 vo, double2 tj, double &fx, double &fy,
-                        double &fz) {
+                        double M, float4 o, TermRow tj, double &fx, double &fy, double &fz) {
     const double dx = xi - (double)o.x, dy = yi - (double)o.y, dz = zi - (double)o.z;
     const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
     if (!(r2 < p.h2)) return;                       // r >= h
     const double y = r2 > 0.0 ? rsqrt_nr(r2) : 0.0;  // r = 0: spiky 0, viscosity kept
     const double d = fma(-r2, y, p.h);              // h - r
     const double spk = M * d * d * y;               // m^2 c (h - r)^2 / r
-    if (o.w >= 0.0f) {  // fluid neighbour: tj = (p_j / rho_j^2, 1 / rho_j) in fp64
-        const double s = (term_i + tj.x) * spk;
-        const double lap = L_i * d * tj.y;
-        fx = fma(lap, (double)vo.x - vxi, fma(-s, dx, fx));
-        fy = fma(lap, (double)vo.y - vyi, fma(-s, dy, fy));
-        fz = fma(lap, (double)vo.z - vzi, fma(-s, dz, fz));
+    if (o.w >= 0.0f) {  // fluid neighbour: tj = (p_j / rho_j^2, 1 / rho_j in fp64; v_j)
+        const double s = (term_i + tj.term) * spk;
+        const double lap = L_i * d * tj.inv_rho;
+        fx = fma(lap, (double)tj.vx - vxi, fma(-s, dx, fx));
+        fy = fma(lap, (double)tj.vy - vyi, fma(-s, dy, fy));
+        fz = fma(lap, (double)tj.vz - vzi, fma(-s, dz, fz));
     } else {  // static wall sample, mirrored pressure
         const double s = wall_term * spk;
         fx = fma(-s, dx, fx);
@@ -269,7 +304,6 @@ __global__ void __launch_bounds__(kThreads) k_forces(const __grid_constant__ Rts
     const size_t S = p.nbr_stride;
     const int n_act = b.ctr->n_compute;
     const float4 *cpos = reinterpret_cast<const float4 *>(b.cpos);
-    const float4 *cvel = reinterpret_cast<const float4 *>(b.cvel);
     const Band bd = make_band(p.h2);
     const double m2 = xmul(p.mass, p.mass);
     const double inv_rho0_sq = xdiv(1.0, xmul(p.rho0, p.rho0));
@@ -278,13 +312,12 @@ __global__ void __launch_bounds__(kThreads) k_forces(const __grid_constant__ Rts
         const int k = b.active[t];
         const int j = b.order[k];
         const float4 a = cpos[k];
-        const float4 va = cvel[k];
         const double xi = a.x, yi = a.y, zi = a.z;
-        const double4 own = ld_f64x4(b.cterm + 4 * (size_t)k);  // p/rho^2, 1/rho, p (fp64)
-        const double term_i = own.x, p_i = own.z;
-        const double L_i = mum2c * own.y;
-        const double wall_term = xadd(term_i, xmul(p_i, inv_rho0_sq));
-        const double vxi = va.x, vyi = va.y, vzi = va.z;
+        const TermRow own = ld_term(b.cterm, k);  // this step's fp64 p/rho^2, 1/rho; v
+        const double term_i = own.term;
+        const double L_i = mum2c * own.inv_rho;
+        const double wall_term = b.cwall[k];
+        const double vxi = own.vx, vyi = own.vy, vzi = own.vz;
         const int n_all = b.cnt[t];  // the density pass's neighbour list of slot k
         const int *col = b.nbr + t;
         double fx = 0.0, fy = 0.0, fz = 0.0;
@@ -294,8 +327,8 @@ __global__ void __launch_bounds__(kThreads) k_forces(const __grid_constant__ Rts
             // summed (same row order, so the same fp64 sums)
             for (int q0 = 0; q0 < n_all; q0 += RTS_WF_CH) {
                 int kq[RTS_WF_CH];
-                float4 pq[RTS_WF_CH], vq[RTS_WF_CH];
-                double2 tq[RTS_WF_CH];
+                float4 pq[RTS_WF_CH];
+                TermRow tq[RTS_WF_CH];
 #pragma unroll
                 for (int u = 0; u < RTS_WF_CH; ++u)
                     kq[u] = q0 + u < n_all
@@ -304,22 +337,20 @@ __global__ void __launch_bounds__(kThreads) k_forces(const __grid_constant__ Rts
 #pragma unroll
                 for (int u = 0; u < RTS_WF_CH; ++u) {
                     pq[u] = cpos[kq[u]];
-                    vq[u] = cvel[kq[u]];
-                    tq[u] = reinterpret_cast<const double2 *>(b.cterm)[2 * (size_t)kq[u]];
+                    tq[u] = ld_term(b.cterm, kq[u]);
                 }
 #pragma unroll
                 for (int u = 0; u < RTS_WF_CH; ++u)
                     if (kq[u] != k)
                         force_pair(p, xi, yi, zi, vxi, vyi, vzi, L_i, term_i, wall_term, M, pq[u],
-                                   vq[u], tq[u], fx, fy, fz);
+                                   tq[u], fx, fy, fz);
             }
         } else if (n_all <= kHitCap) {
             for (int q = 0; q < n_all; ++q) {
                 const int kq = col[q * S];
                 if (kq == k) continue;
                 force_pair(p, xi, yi, zi, vxi, vyi, vzi, L_i, term_i, wall_term, M, cpos[kq],
-                           cvel[kq], reinterpret_cast<const double2 *>(b.cterm)[2 * (size_t)kq],
-                           fx, fy, fz);
+                           ld_term(b.cterm, kq), fx, fy, fz);
             }
         } else {
             Span sp[9];
@@ -328,8 +359,7 @@ __global__ void __launch_bounds__(kThreads) k_forces(const __grid_constant__ Rts
                 for (int q = sp[s].k0; q < sp[s].k1; ++q)
                     if (q != k && in_support(bd, a.x, a.y, a.z, cpos[q]))
                         force_pair(p, xi, yi, zi, vxi, vyi, vzi, L_i, term_i, wall_term, M, cpos[q],
-                                   cvel[q], reinterpret_cast<const double2 *>(b.cterm)[2 * (size_t)q],
-                                   fx, fy, fz);
+                                   ld_term(b.cterm, q), fx, fy, fz);
         }
         fx = xadd(fx, xmul(p.mass, p.gravity[0]));
         fy = xadd(fy, xmul(p.mass, p.gravity[1]));

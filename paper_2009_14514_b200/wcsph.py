@@ -98,6 +98,7 @@ class _DeviceSolver:
         A.alloc("cpos", (nf + self.n_bound + 4, 4), torch.float32, 0)
         A.alloc("cvel", (max(nf + self.n_bound, 1), 4), torch.float32, 0)
         A.alloc("cterm", (max(nf + self.n_bound, 1), 4), torch.float64, 0)
+        A.alloc("cwall", (max(nf + self.n_bound, 1),), torch.float64, 0)
         if self._soa_candidates:  # SoA candidate positions (+8: padded quads)
             for name in ("cx", "cy", "cz"):
                 A.alloc(name, (nf + self.n_bound + 8,), torch.float32, 0)
@@ -204,6 +205,7 @@ class _DeviceSolver:
             for name in ("cpos", "cvel"):
                 A.alloc(name, (cap + nb + 4, 4), torch.float32, 0)  # +4: padded candidate reads
             A.alloc("cterm", (cap + nb + 4, 4), torch.float64, 0)
+            A.alloc("cwall", (cap + nb + 4,), torch.float64, 0)
             if self._soa_candidates:
                 for name in ("cx", "cy", "cz"):
                     A.alloc(name, (cap + nb + 8,), torch.float32, 0)
