@@ -813,24 +813,16 @@ def main():
         t0 = time.perf_counter()
         e_minors = 0
         nbytes = 0
-        # vel travels on a second copy stream, so the download of one array
-        # overlaps the upload of the other (PCIe is full duplex); the step still
-        # waits for both inputs and every result is back before the clock stops
-        cs = torch.cuda.Stream(device) if world == 1 else stream
         for _ in range(k_e2e):
             dp, dv = dev_state()
             n = dp.shape[0]
             dp.copy_(hp_all[:n], non_blocking=True)  # step inputs: host -> device
-            with torch.cuda.stream(cs):
-                dv.copy_(hv_all[:n], non_blocking=True)
-            stream.wait_stream(cs)
+            dv.copy_(hv_all[:n], non_blocking=True)
             e_minors += len(driver.advance())
             dp, dv = dev_state()  # results (ownership may have changed)
             n2 = dp.shape[0]
-            cs.wait_stream(stream)
             hp_all[:n2].copy_(dp, non_blocking=True)
-            with torch.cuda.stream(cs):
-                hv_all[:n2].copy_(dv, non_blocking=True)
+            hv_all[:n2].copy_(dv, non_blocking=True)
             nbytes = (n + n2) * 24
         torch.cuda.synchronize()
         te = time.perf_counter() - t0
@@ -841,8 +833,7 @@ def main():
         e2e = {"value": n_total * e_minors / te, "unit": UNIT,
                "h2d_bytes_per_step": nbytes // 2, "d2h_bytes_per_step": nbytes // 2,
                "steps": k_e2e, "note": "pinned host pos+vel uploaded before and downloaded "
-                                       "after every advance() (pos and vel on two copy "
-                                       "streams); wall clock"}
+                                       "after every advance(); wall clock"}
 
     # ---- WCSPH extra (configs[2]: the 1M scene, RTS-WCSPH vs the global -------
     # adaptive baseline; one GPU, or the same scene cut into N x-slab ranks)

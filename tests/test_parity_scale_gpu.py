@@ -251,3 +251,55 @@ def test_cfg3_wcsph_1m_parity():
     so = density_stats(orc.rho, orc.vel, orc.mass, rho0)
     for k in ("mean_err", "max_err", "ke"):
         assert abs(sd[k] - so[k]) <= STAT_TOL * abs(so[k]), (k, sd, so)
+
+
+# -- cfg4 (8 M mixed tank) and cfg5 (4 M per GPU) at one GPU ------------------------
+
+def _workload_pair(workload):
+    import bench
+    kind = bench.WORKLOADS[workload][0]
+    dev = bench.make_device_solver(kind, torch.device("cuda", 0), workload)
+    orc, _ = bench._oracle_for(workload)
+    nf = dev.n_fluid
+    assert orc.n_fluid == nf
+    assert np.array_equal(dev.host("pos")[:nf], orc.pos[:nf])  # the same jittered start
+    orc.pos[:] = dev.host("pos")
+    if kind == "pcisph":
+        orc.xstar[:] = orc.pos[:nf]
+    orc.vel[:] = dev.host("vel")
+    return dev, orc
+
+
+@pytest.mark.parametrize("workload", ["cfg4", "cfg5-pcisph"])
+def test_large_workloads_first_iteration_parity(workload):
+    """BASELINE configs[3] (8 M, z-up, a falling block at -2 m/s over a resting
+    pool: mixed levels) and configs[4] at one GPU (4 M, N(0, 0.1) velocities):
+    one major on the device, then a major start from the common state --
+    rows exact, rho*, err, p, f_p <= 1e-4, S_e / S_ob exact."""
+    dev, orc = _workload_pair(workload)
+    dev.advance()
+    r = first_iteration(dev, orc)
+    _check_first_iteration(r)
+    del dev, orc
+    torch.cuda.empty_cache()
+
+
+def test_cfg5_wcsph_4m_common_state_steps():
+    """configs[4] RTS-WCSPH at one GPU (4 M, N(0, 0.1) velocities): three steps
+    from a common state each -- active counts and sort exact, rho and
+    accelerations <= 1e-4."""
+    dev, orc = _workload_pair("cfg5-wcsph")
+    compared = 0
+    for _ in range(3):
+        inject(dev, orc, WCSPH_STATE)
+        a, b = dev.step(), orc.step()
+        assert a.n_compute == b.n_compute
+        assert np.array_equal(dev.grid.order.cpu().numpy(), orc.grid.order)
+        act = orc.compute
+        if act.any():
+            assert rel_err(dev.host("rho")[act], orc.rho[act]) <= TOL
+            assert vec_rel_err(dev.host("acc")[act], orc.acc[act]) <= TOL
+            compared += int(act.sum())
+    assert compared > 0
+    del dev, orc
+    torch.cuda.empty_cache()
