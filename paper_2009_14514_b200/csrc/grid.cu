@@ -79,13 +79,19 @@ __global__ void k_boundary_active(const __grid_constant__ RtsParams p, RtsBuffer
          t += gridDim.x * blockDim.x) {
         const int c = b.bcell_ids[t];
         const int cz = c % nz, cy = (c / nz) % ny, cx = c / (ny * nz);
-        bool allowed = false;
-        for (int ax = max(0, cx - 1); ax <= min(nx - 1, cx + 1) && !allowed; ++ax)
-            for (int ay = max(0, cy - 1); ay <= min(ny - 1, cy + 1) && !allowed; ++ay) {
-                const int base = (ax * ny + ay) * nz;
-                for (int az = max(0, cz - 1); az <= min(nz - 1, cz + 1); ++az)
-                    if (b.cell_count[base + az] > 0) { allowed = true; break; }
-            }
+        // the 27 counts requested together (no early exit: one round trip)
+        int any = 0;
+#pragma unroll
+        for (int dx = -1; dx <= 1; ++dx)
+#pragma unroll
+            for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+                for (int dz = -1; dz <= 1; ++dz) {
+                    const int ax = cx + dx, ay = cy + dy, az = cz + dz;
+                    const bool in = ax >= 0 && ax < nx && ay >= 0 && ay < ny && az >= 0 && az < nz;
+                    any |= in ? b.cell_count[(ax * ny + ay) * nz + az] : 0;
+                }
+        const bool allowed = any > 0;
         b.bcell_active[t] = allowed;
         b.cell_bcount[c] = allowed ? (b.bcell_start[t + 1] - b.bcell_start[t]) : 0;
     }
@@ -126,7 +132,10 @@ __device__ __forceinline__ int block_incl_scan(int v, int *warp_sums) {
 // until it meets an inclusive prefix.  One launch instead of tile scan +
 // recursive tile-sum scan + add + finish.
 constexpr int kLbThreads = 256;
-constexpr int kLbItems = 4;
+#ifndef RTS_SCAN_ITEMS
+#define RTS_SCAN_ITEMS 16  // cells per thread (multiple of 4: int4 accesses)
+#endif
+constexpr int kLbItems = RTS_SCAN_ITEMS;
 constexpr int kLbTile = kLbThreads * kLbItems;
 constexpr unsigned long long kFlagAgg = 1ull << 32, kFlagPre = 2ull << 32;
 
@@ -143,13 +152,25 @@ __global__ void __launch_bounds__(kLbThreads) k_scan_lookback(const __grid_const
     const int i0 = tile * kLbTile + threadIdx.x * kLbItems;
     int v[kLbItems];
     int local = 0;
+    const bool whole = i0 + kLbItems <= n;  // int4 accesses (i0 is a multiple of 4)
+    if (whole) {
 #pragma unroll
-    for (int q = 0; q < kLbItems; ++q) {
-        const int idx = i0 + q;
-        v[q] = idx < n ? b.cell_count[idx] + b.cell_bcount[idx] : 0;
-        if (idx < n) b.fill[idx] = 0;  // the scatter's cursors
-        local += v[q];
+        for (int q = 0; q < kLbItems; q += 4) {
+            const int4 a = *reinterpret_cast<const int4 *>(b.cell_count + i0 + q);
+            const int4 w = *reinterpret_cast<const int4 *>(b.cell_bcount + i0 + q);
+            v[q] = a.x + w.x, v[q + 1] = a.y + w.y, v[q + 2] = a.z + w.z, v[q + 3] = a.w + w.w;
+            *reinterpret_cast<int4 *>(b.fill + i0 + q) = make_int4(0, 0, 0, 0);  // scatter cursors
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < kLbItems; ++q) {
+            const int idx = i0 + q;
+            v[q] = idx < n ? b.cell_count[idx] + b.cell_bcount[idx] : 0;
+            if (idx < n) b.fill[idx] = 0;
+        }
     }
+#pragma unroll
+    for (int q = 0; q < kLbItems; ++q) local += v[q];
     const int incl = block_incl_scan(local, warp_sums);
     const int lane = threadIdx.x & 31;
     if (threadIdx.x == kLbThreads - 1) {  // the tile's aggregate
@@ -188,11 +209,23 @@ __global__ void __launch_bounds__(kLbThreads) k_scan_lookback(const __grid_const
         atomicExch(status + tile, kFlagPre | (unsigned)(excl + incl));
     }
     int run = excl + incl - local;
+    if (whole) {
 #pragma unroll
-    for (int q = 0; q < kLbItems; ++q) {
-        const int idx = i0 + q;
-        if (idx < n) b.starts[idx] = run;
-        run += v[q];
+        for (int q = 0; q < kLbItems; q += 4) {
+            int4 o;
+            o.x = run, run += v[q];
+            o.y = run, run += v[q + 1];
+            o.z = run, run += v[q + 2];
+            o.w = run, run += v[q + 3];
+            *reinterpret_cast<int4 *>(b.starts + i0 + q) = o;
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < kLbItems; ++q) {
+            const int idx = i0 + q;
+            if (idx < n) b.starts[idx] = run;
+            run += v[q];
+        }
     }
     if (i0 < n && i0 + kLbItems >= n) {  // owner of the last cell: total members
         b.starts[n] = run;

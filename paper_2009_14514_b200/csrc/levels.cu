@@ -14,12 +14,10 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int8_t kEmpty = 127;  // regions.py:35
 
-// region id of block c from its maxima (regions.py:38-75)
-RTS_DEV int8_t assign_cell(const RtsParams &p, const RtsBuffers &b, int c, double sound_bound,
+// region id of an occupied block from its maxima (regions.py:38-75)
+RTS_DEV int8_t assign_from(const RtsParams &p, double vmax, double fmax, double sound_bound,
                            double rm) {
-    if (b.cell_count[c] <= 0) return 0;
     const double r = p.block_size;
-    const double vmax = b.vmax[c], fmax = b.fmax[c];
     // lambda_f * sqrt(r*m / f_max); f_max == 0 -> inf (numpy divide)
     const double fb = xmul(p.lambda_f, xsqrt(xdiv(rm, fmax)));
     int8_t region = 1;
@@ -33,6 +31,12 @@ RTS_DEV int8_t assign_cell(const RtsParams &p, const RtsBuffers &b, int c, doubl
         if (ok) region = (int8_t)n;
     }
     return region;
+}
+
+RTS_DEV int8_t assign_cell(const RtsParams &p, const RtsBuffers &b, int c, double sound_bound,
+                           double rm) {
+    if (b.cell_count[c] <= 0) return 0;
+    return assign_from(p, b.vmax[c], b.fmax[c], sound_bound, rm);
 }
 
 __global__ void k_assign(const __grid_constant__ RtsParams p, RtsBuffers b) {
@@ -50,6 +54,8 @@ __global__ void k_assign(const __grid_constant__ RtsParams p, RtsBuffers b) {
 // (WCSPH's level field, rts_block_levels expand = 0)
 constexpr int kTX = 4, kTY = 8, kTZ = 32;
 constexpr int kHX = kTX + 2, kHY = kTY + 2, kHZ = kTZ + 2;
+constexpr int kHalo = kHX * kHY * kHZ;
+constexpr int kHaloPer = (kHalo + 255) / 256;  // halo cells per thread (256 threads)
 
 __global__ void __launch_bounds__(256) k_assign_smooth(const __grid_constant__ RtsParams p,
                                                        RtsBuffers b, int8_t *out) {
@@ -62,17 +68,35 @@ __global__ void __launch_bounds__(256) k_assign_smooth(const __grid_constant__ R
     const double rm = xmul(p.block_size, p.mass);
     for (int t = blockIdx.x; t < tx * ty * tz; t += gridDim.x) {
         const int bz = (t % tz) * kTZ, by = ((t / tz) % ty) * kTY, bx = (t / (tz * ty)) * kTX;
-        for (int h = threadIdx.x; h < kHX * kHY * kHZ; h += blockDim.x) {
+        // the halo's counts, then the occupied cells' maxima, all requested
+        // before any is used (one dependent round trip each, not kHaloPer)
+        int cell[kHaloPer], cnt[kHaloPer];
+        double vm[kHaloPer], fm[kHaloPer];
+#pragma unroll
+        for (int u = 0; u < kHaloPer; ++u) {
+            const int h = threadIdx.x + u * 256;
             const int hz = h % kHZ, hy = (h / kHZ) % kHY, hx = h / (kHZ * kHY);
             const int cx = bx + hx - 1, cy = by + hy - 1, cz = bz + hz - 1;
-            int8_t r = 0;  // outside the grid: empty
-            if (cx >= 0 && cx < nx && cy >= 0 && cy < ny && cz >= 0 && cz < nz) {
-                const int c = (cx * ny + cy) * nz + cz;
-                r = assign_cell(p, b, c, sound_bound, rm);
-                const bool interior = hx >= 1 && hx <= kTX && hy >= 1 && hy <= kTY && hz >= 1 &&
-                                      hz <= kTZ;
-                if (interior) b.block_raw[c] = r;
-            }
+            const bool in = h < kHalo && cx >= 0 && cx < nx && cy >= 0 && cy < ny && cz >= 0 &&
+                            cz < nz;
+            cell[u] = in ? (cx * ny + cy) * nz + cz : -1;
+            cnt[u] = in ? __ldg(b.cell_count + cell[u]) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < kHaloPer; ++u) {
+            vm[u] = cnt[u] > 0 ? __ldg(b.vmax + cell[u]) : 0.0;
+            fm[u] = cnt[u] > 0 ? __ldg(b.fmax + cell[u]) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kHaloPer; ++u) {
+            const int h = threadIdx.x + u * 256;
+            if (h >= kHalo) break;
+            // outside the grid or empty: 0
+            const int8_t r = cnt[u] > 0 ? assign_from(p, vm[u], fm[u], sound_bound, rm) : 0;
+            const int hz = h % kHZ, hy = (h / kHZ) % kHY, hx = h / (kHZ * kHY);
+            const bool interior = hx >= 1 && hx <= kTX && hy >= 1 && hy <= kTY && hz >= 1 &&
+                                  hz <= kTZ;
+            if (interior && cell[u] >= 0) b.block_raw[cell[u]] = r;
             s_reg[h] = r;
         }
         __syncthreads();

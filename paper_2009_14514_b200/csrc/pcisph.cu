@@ -208,6 +208,123 @@ RTS_DEV void finish_refresh(const RtsParams &p, const RtsBuffers &b, int i, int 
     b.force[3 * i + 2] = (float)xadd(fz, xmul(p.mass, p.gravity[2]));
 }
 
+// One CSR span [k0, k1) of the one-thread-per-particle refresh (G = 1):
+// candidates classified 32 at a time, members emitted in candidate order
+// (with EXT, their viscosity terms summed as they are emitted).
+template <bool EXT>
+RTS_DEV void refresh_span(const RtsParams &p, const RtsBuffers &b, const RefreshConsts &k, int i,
+                          int k0, int k1, float fxi, float fyi, float fzi, double vxi, double vyi,
+                          double vzi, int *row, size_t S, int &cntn, double &vfx, double &vfy,
+                          double &vfz) {
+    const float4 *cpos = reinterpret_cast<const float4 *>(b.cpos);
+    // Branch-free classification of 32 candidates at a time: two
+    // 32-bit masks (r2 < h2_lo: member; r2 > h2_hi: not) built
+    // from the sign bits of r2 - bound with one funnel shift per
+    // candidate; the rare in-band candidates then take the exact
+    // fp64 test, and the members are emitted in candidate order.
+    // Reads run up to 3 slots past the span (cpos is padded).
+    const bool soa = RTS_SOA && b.cx != nullptr;
+    for (int cb = soa ? (k0 & ~3) : k0; cb < k1; cb += 32) {
+        const int n = min(32, k1 - cb);
+        const float4 *cp = cpos + cb;
+        unsigned mem = 0u, out = 0u;  // first candidate ends in the top bit
+        if (soa) {  // x / y / z copies: 4 candidates per load, fp32x2 tests
+            unsigned amb;
+            classify_soa(b.cx, b.cy, b.cz, cb, n, k0, fxi, fyi, fzi, k.h2_lo, k.h2_hi,
+                         mem, amb);
+            while (amb) {
+                const int q = __ffs(amb) - 1;
+                amb &= amb - 1u;
+                const float4 o = cp[q];
+                if (exact_neighbour(p.h2, fxi, fyi, fzi, o.x, o.y, o.z)) mem |= 1u << q;
+            }
+        } else {
+            for (int u = 0; u < n; u += 4) {
+                float4 ob[4];
+#pragma unroll
+                for (int v = 0; v < 4; ++v) ob[v] = cp[u + v];
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    const float ex = __fsub_rn(fxi, ob[v].x), ey = __fsub_rn(fyi, ob[v].y),
+                                ez = __fsub_rn(fzi, ob[v].z);
+                    const float r2f = __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, __fmul_rn(ez, ez)));
+                    mem = __funnelshift_l(__float_as_uint(__fsub_rn(r2f, k.h2_lo)), mem, 1);
+                    out = __funnelshift_l(__float_as_uint(__fsub_rn(k.h2_hi, r2f)), out, 1);
+                }
+            }
+            const int nr = (n + 3) & ~3;  // candidates classified
+            // bit (nr-1-u) <-> candidate u; reverse so bit u <-> candidate u
+            const unsigned valid = n == 32 ? 0xffffffffu : ((1u << n) - 1u);
+            mem = (__brev(mem) >> (32 - nr)) & valid;
+            out = (__brev(out) >> (32 - nr)) & valid;
+            {
+                unsigned amb = valid & ~mem & ~out;
+                while (amb) {
+                    const int q = __ffs(amb) - 1;
+                    amb &= amb - 1u;
+                    const float4 o = cp[q];
+                    if (exact_neighbour(p.h2, fxi, fyi, fzi, o.x, o.y, o.z)) mem |= 1u << q;
+                }
+            }
+        }
+        if (!EXT) {
+            while (mem) {
+                const int q = __ffs(mem) - 1;
+                mem &= mem - 1u;
+                if (cntn < p.width) __stcs(row + cntn * S, __float_as_int(cp[q].w));
+                ++cntn;
+            }
+            continue;
+        }
+        // members in candidate (= row) order, four at a time: the
+        // candidate copy (L1-hot) gives j and pos_j, so the row is
+        // written and its viscosity term (fp32, fp64 row-order sum;
+        // pcisph.py:183-196) taken without re-reading the row
+        while (mem) {
+            float4 o[4];
+            float vj[4][3];
+            int nq = 0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                o[u] = make_float4(fxi, fyi, fzi, __int_as_float(i));
+                if (mem) {
+                    o[u] = cp[__ffs(mem) - 1];
+                    mem &= mem - 1u;
+                    nq = u + 1;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int j = __float_as_int(o[u].w);
+                const int jc = j < p.n_fluid ? j : i;
+                vj[u][0] = b.vel[3 * jc];
+                vj[u][1] = b.vel[3 * jc + 1];
+                vj[u][2] = b.vel[3 * jc + 2];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (u >= nq) break;
+                const int j = __float_as_int(o[u].w);
+                if (cntn < p.width) {
+                    __stcs(row + cntn * S, j);
+                    if (j < p.n_fluid && j != i) {
+                        const float dx = fxi - o[u].x, dy = fyi - o[u].y,
+                                    dz = fzi - o[u].z;
+                        const float r = sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
+                        if (r < k.hf) {
+                            const float lap = k.visc_f * (k.hf - r);
+                            vfx += (double)(lap * (vj[u][0] - (float)vxi));
+                            vfy += (double)(lap * (vj[u][1] - (float)vyi));
+                            vfz += (double)(lap * (vj[u][2] - (float)vzi));
+                        }
+                    }
+                }
+                ++cntn;
+            }
+        }
+    }
+}
+
 // One thread (G = 1) or one G-lane group per refreshed particle, chosen from
 // the list length against the grid (pass_blocks): on large scenes the full
 // refresh at a major-step start keeps one thread per particle (adjacent lanes
@@ -291,112 +408,8 @@ RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshC
             const int k0 = b.starts[base + za], k1 = b.starts[base + zb + 1];
             RTS_CHECK(b.ctr, 0 <= k0 && k0 <= k1 && k1 <= b.ctr->n_sorted, 304);
             if (G == 1) {
-                // Branch-free classification of 32 candidates at a time: two
-                // 32-bit masks (r2 < h2_lo: member; r2 > h2_hi: not) built
-                // from the sign bits of r2 - bound with one funnel shift per
-                // candidate; the rare in-band candidates then take the exact
-                // fp64 test, and the members are emitted in candidate order.
-                // Reads run up to 3 slots past the span (cpos is padded).
-                const bool soa = RTS_SOA && b.cx != nullptr;
-                for (int cb = soa ? (k0 & ~3) : k0; cb < k1; cb += 32) {
-                    const int n = min(32, k1 - cb);
-                    const float4 *cp = cpos + cb;
-                    unsigned mem = 0u, out = 0u;  // first candidate ends in the top bit
-                    if (soa) {  // x / y / z copies: 4 candidates per load, fp32x2 tests
-                        unsigned amb;
-                        classify_soa(b.cx, b.cy, b.cz, cb, n, k0, fxi, fyi, fzi, k.h2_lo, k.h2_hi,
-                                     mem, amb);
-                        while (amb) {
-                            const int q = __ffs(amb) - 1;
-                            amb &= amb - 1u;
-                            const float4 o = cp[q];
-                            if (exact_neighbour(p.h2, fxi, fyi, fzi, o.x, o.y, o.z)) mem |= 1u << q;
-                        }
-                    } else {
-                    for (int u = 0; u < n; u += 4) {
-                        float4 ob[4];
-#pragma unroll
-                        for (int v = 0; v < 4; ++v) ob[v] = cp[u + v];
-#pragma unroll
-                        for (int v = 0; v < 4; ++v) {
-                            const float ex = __fsub_rn(fxi, ob[v].x), ey = __fsub_rn(fyi, ob[v].y),
-                                        ez = __fsub_rn(fzi, ob[v].z);
-                            const float r2f = __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, __fmul_rn(ez, ez)));
-                            mem = __funnelshift_l(__float_as_uint(__fsub_rn(r2f, k.h2_lo)), mem, 1);
-                            out = __funnelshift_l(__float_as_uint(__fsub_rn(k.h2_hi, r2f)), out, 1);
-                        }
-                    }
-                    const int nr = (n + 3) & ~3;  // candidates classified
-                    // bit (nr-1-u) <-> candidate u; reverse so bit u <-> candidate u
-                    const unsigned valid = n == 32 ? 0xffffffffu : ((1u << n) - 1u);
-                    mem = (__brev(mem) >> (32 - nr)) & valid;
-                    out = (__brev(out) >> (32 - nr)) & valid;
-                    {
-                        unsigned amb = valid & ~mem & ~out;
-                        while (amb) {
-                            const int q = __ffs(amb) - 1;
-                            amb &= amb - 1u;
-                            const float4 o = cp[q];
-                            if (exact_neighbour(p.h2, fxi, fyi, fzi, o.x, o.y, o.z)) mem |= 1u << q;
-                        }
-                    }
-                    }
-                    if (!EXT) {
-                        while (mem) {
-                            const int q = __ffs(mem) - 1;
-                            mem &= mem - 1u;
-                            if (cntn < p.width) __stcs(row + cntn * S, __float_as_int(cp[q].w));
-                            ++cntn;
-                        }
-                        continue;
-                    }
-                    // members in candidate (= row) order, four at a time: the
-                    // candidate copy (L1-hot) gives j and pos_j, so the row is
-                    // written and its viscosity term (fp32, fp64 row-order sum;
-                    // pcisph.py:183-196) taken without re-reading the row
-                    while (mem) {
-                        float4 o[4];
-                        float vj[4][3];
-                        int nq = 0;
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            o[u] = make_float4(fxi, fyi, fzi, __int_as_float(i));
-                            if (mem) {
-                                o[u] = cp[__ffs(mem) - 1];
-                                mem &= mem - 1u;
-                                nq = u + 1;
-                            }
-                        }
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const int j = __float_as_int(o[u].w);
-                            const int jc = j < p.n_fluid ? j : i;
-                            vj[u][0] = b.vel[3 * jc];
-                            vj[u][1] = b.vel[3 * jc + 1];
-                            vj[u][2] = b.vel[3 * jc + 2];
-                        }
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            if (u >= nq) break;
-                            const int j = __float_as_int(o[u].w);
-                            if (cntn < p.width) {
-                                __stcs(row + cntn * S, j);
-                                if (j < p.n_fluid && j != i) {
-                                    const float dx = fxi - o[u].x, dy = fyi - o[u].y,
-                                                dz = fzi - o[u].z;
-                                    const float r = sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
-                                    if (r < k.hf) {
-                                        const float lap = k.visc_f * (k.hf - r);
-                                        vfx += (double)(lap * (vj[u][0] - (float)vxi));
-                                        vfy += (double)(lap * (vj[u][1] - (float)vyi));
-                                        vfz += (double)(lap * (vj[u][2] - (float)vzi));
-                                    }
-                                }
-                            }
-                            ++cntn;
-                        }
-                    }
-                }
+                refresh_span<EXT>(p, b, k, i, k0, k1, fxi, fyi, fzi, vxi, vyi, vzi, row, S, cntn,
+                                  vfx, vfy, vfz);
             } else {
                 for (int kb = k0; kb < k1; kb += G) {
                     const int kk = kb + lane;

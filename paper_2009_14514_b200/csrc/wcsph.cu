@@ -25,6 +25,10 @@ namespace {
 
 constexpr int kThreads = 128;
 
+#ifndef RTS_PROP_CTAS
+#define RTS_PROP_CTAS 8  // propagate CTAs of 256 threads per SM (grid cap)
+#endif
+
 // 32-byte per-slot force-pass row: fp64 p/rho^2 and 1/rho of the slot's
 // particle (this step's density for active slots, the stored state
 // otherwise) and its fp32 velocity -- a neighbour is one 256-bit gather
@@ -136,11 +140,28 @@ constexpr int kHitCap = 64;  // list entries per thread (overflow -> direct path
 
 RTS_DEV int collect_hits(const RtsParams &p, const RtsBuffers &b, const float4 *cpos, int cell,
                          float4 a, const Band &bd, int *hits, int *n_all) {
-    Span sp[9];
-    const int ns = block_spans(p, b.starts, cell, sp);
+    // the nine column spans in (ax, ay) order, each one's starts requested
+    // while the previous column is scanned (registers, not a local array);
+    // columns outside the grid are empty spans
+    const int nx = p.dims[0], ny = p.dims[1], nz = p.dims[2];
+    const int cz = cell % nz, cy = (cell / nz) % ny, cx = cell / (ny * nz);
+    const int z0 = max(0, cz - 1), z1 = min(nz - 1, cz + 1);
+    auto span = [&](int s, int &k0, int &k1) {
+        const int ax = cx + s / 3 - 1, ay = cy + s % 3 - 1;
+        if (ax < 0 || ax >= nx || ay < 0 || ay >= ny) {
+            k0 = k1 = 0;
+            return;
+        }
+        const int base = (ax * ny + ay) * nz;
+        k0 = b.starts[base + z0];
+        k1 = b.starts[base + z1 + 1];
+    };
+    int nk0, nk1;
+    span(0, nk0, nk1);
     int n = 0;
-    for (int s = 0; s < ns; ++s) {
-        const int k0 = sp[s].k0, k1 = sp[s].k1;
+    for (int s = 0; s < 9; ++s) {
+        const int k0 = nk0, k1 = nk1;
+        if (s < 8) span(s + 1, nk0, nk1);
         // branch-free classification of 32 candidates at a time (sign bits of
         // r2 - bound collected with funnel shifts); in-band candidates take
         // the exact fp64 test; reads run up to 3 slots past the span (cpos
@@ -429,8 +450,8 @@ __global__ void k_integrate(const __grid_constant__ RtsParams p, RtsBuffers b) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const bool correct = p.apply_correction && (p.rts ? act[q] : true);
-            const double corr_x = xdiv(xmul(dtc[q], dtc[q]), 6.0);
-            const double corr_v = xdiv(dtc[q], 2.0);
+            const double corr_x = correct ? xdiv(xmul(dtc[q], dtc[q]), 6.0) : 0.0;
+            const double corr_v = correct ? xdiv(dtc[q], 2.0) : 0.0;
 #pragma unroll
             for (int a = 0; a < 3; ++a)
                 integrate_axis(p, dt, half_dt2, correct, corr_x, corr_v, a, x[3 * q + a],
@@ -513,7 +534,7 @@ int rts_rho_variance(const RtsParams *p, const RtsBuffers *b, double *out, void 
 int rts_wcsph_propagate(const RtsParams *p, const RtsBuffers *b, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
     cudaMemsetAsync(&b->ctr->n_compute, 0, sizeof(int), s);
-    rts_note_launch(), k_propagate<<<rts_blocks(p->n_fluid + p->n_bound, 256, 148 * 4), 256, 0, s>>>(*p, *b);
+    rts_note_launch(), k_propagate<<<rts_blocks(p->n_fluid + p->n_bound, 256, 148 * RTS_PROP_CTAS), 256, 0, s>>>(*p, *b);
     RTS_LAUNCH_CHECK();
     return 0;
 }
