@@ -764,9 +764,12 @@ def main():
     alg = algo_bytes(dom, solver, c_mean, rec, counts[dom])
     achieved = alg / totals[dom] / 1e9 if totals[dom] > 0 else 0.0
     traffic = None  # ncu DRAM bytes per launch: captured for the default workload only
+    l1 = {}  # ncu L1 LSU data-pipe utilisation (% of peak) per kernel, same capture
     tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tf) and args.workload == "cfg2" and world == 1:
-        traffic = json.load(open(tf)).get(dom)
+        tj = json.load(open(tf))
+        traffic = tj.get(dom)
+        l1 = {k: tj[k + "_l1_wavefront_pct"] for k in kernels if k + "_l1_wavefront_pct" in tj}
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": dom,
                 "launches": counts[dom], "kernel_s": round(totals[dom], 6),
@@ -779,6 +782,13 @@ def main():
                                                       max(totals[k], 1e-12) / 1e9, 1)}
                             for k in kernels if counts[k]},
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s"}
+    if l1:  # the gather kernels' own bound: wavefronts of the L1 LSU data pipe
+        roofline["l1_wavefront_pct"] = l1.get(dom)
+        roofline["l1_wavefront_pct_by_kernel"] = l1
+        roofline["l1_note"] = ("ncu l1tex__data_pipe_lsu_wavefronts % of peak (profiles/"
+                               "ncu_traffic.json): the neighbour gathers touch ~10 128-byte "
+                               "lines per warp request, so these kernels are bound by L1 "
+                               "wavefronts, not HBM bytes (DESIGN.md section 4)")
     # live cross-check inside the timed region: the device's %globaltimer
     # stamps around each minor step's refresh (StepStats.t_neighbor: refresh
     # list + search + f_ext on the launching stream) over the K timed majors

@@ -320,7 +320,10 @@ int rts_pci_pforces(const RtsParams *p, const RtsBuffers *b, void *stream);
  * also the per-block maxima of rts_block_maxima(add_fp = 1) into vmax / fmax,
  * which the caller zeroes first (no ghost rows). */
 int rts_pci_integrate(const RtsParams *p, const RtsBuffers *b, int countdown, void *stream);
-/* _mark_timestep_updates (pcisph.py:718-755); block_raw = required levels. */
+/* _mark_timestep_updates (pcisph.py:718-755) from the per-block maxima in
+ * vmax / fmax: computes the required levels itself (-> block_raw, as
+ * rts_block_levels expand = 2 would), then the new field and the particles'
+ * regions / validity / compute. */
 int rts_pci_mark_updates(const RtsParams *p, const RtsBuffers *b, void *stream);
 /* local-phase snapshot (restore=0) / revert (restore=1) of p, f_p (pcisph.py:694-707). */
 int rts_pci_snapshot(const RtsParams *p, const RtsBuffers *b, int restore, void *stream);

@@ -14,25 +14,6 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int8_t kEmpty = 127;  // regions.py:35
 
-// region id of an occupied block from its maxima (regions.py:38-75)
-RTS_DEV int8_t assign_from(const RtsParams &p, double vmax, double fmax, double sound_bound,
-                           double rm) {
-    const double r = p.block_size;
-    // lambda_f * sqrt(r*m / f_max); f_max == 0 -> inf (numpy divide)
-    const double fb = xmul(p.lambda_f, xsqrt(xdiv(rm, fmax)));
-    int8_t region = 1;
-    for (int n = 2; n <= p.n_max; ++n) {
-        const double dt_n = xmul((double)n, p.dt_base);
-        if (p.use_sound && !(dt_n <= sound_bound)) break;
-        bool ok = (region == n - 1);
-        ok = ok && ((fmax == 0.0) || (dt_n <= fb));
-        const double beta = p.betas[n];
-        if (isfinite(beta)) ok = ok && (xdiv(xmul(dt_n, vmax), r) <= xmul(p.alpha, beta));
-        if (ok) region = (int8_t)n;
-    }
-    return region;
-}
-
 RTS_DEV int8_t assign_cell(const RtsParams &p, const RtsBuffers &b, int c, double sound_bound,
                            double rm) {
     if (b.cell_count[c] <= 0) return 0;

@@ -1278,58 +1278,108 @@ __global__ void k_integrate(const __grid_constant__ RtsParams p, RtsBuffers b, i
     note_displacement(b, countdown, dmax);
 }
 
-// _mark_timestep_updates (pcisph.py:718-755), block part: block_raw holds the
-// required levels; new field -> block_tmp, changed mask -> block_flag
-__global__ void k_mark_blocks(const __grid_constant__ RtsParams p, RtsBuffers b) {
+// _mark_timestep_updates (pcisph.py:718-755) in two passes.  Block part, per
+// tile of blocks plus a one-block halo in shared memory: the required level
+// of every halo block (assign_regions, regions.py:38-75, from the per-block
+// maxima the integrator just formed) -> block_raw, and "violating" where it
+// is below the current level; each occupied block of the tile then drops to
+// min(own, lowest violating level over its 27-block neighbourhood) -> new
+// field in block_tmp, changed mask in block_flag.
+constexpr int kMX = 4, kMY = 8, kMZ = 32;
+constexpr int kMHX = kMX + 2, kMHY = kMY + 2, kMHZ = kMZ + 2;
+constexpr int kMHalo = kMHX * kMHY * kMHZ;
+constexpr int kMPer = (kMHalo + 255) / 256;
+
+__global__ void __launch_bounds__(256) k_mark_blocks(const __grid_constant__ RtsParams p,
+                                                     RtsBuffers b) {
     RTS_MINOR_GUARD();
+    __shared__ int8_t s_viol[kMHalo];  // required level where violating, else 127
+    __shared__ int8_t s_cur[kMHalo];
+    __shared__ uint8_t s_occ[kMHalo];
     const int nx = p.dims[0], ny = p.dims[1], nz = p.dims[2];
-    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < p.n_cells;
-         c += gridDim.x * blockDim.x) {
-        const bool occ = b.cell_count[c] > 0;
-        const int8_t cur = b.block_field[c];
-        int8_t nw = 0;
-        if (occ) {
-            // spread = min(vfield, min over 26 neighbours of vfield), vfield =
-            // required where violating else 127
-            const int cz = c % nz, cy = (c / nz) % ny, cx = c / (ny * nz);
-            int8_t spread = 127;
-            for (int ax = max(0, cx - 1); ax <= min(nx - 1, cx + 1); ++ax)
-                for (int ay = max(0, cy - 1); ay <= min(ny - 1, cy + 1); ++ay) {
-                    const int base = (ax * ny + ay) * nz;
-                    for (int az = max(0, cz - 1); az <= min(nz - 1, cz + 1); ++az) {
-                        const int q = base + az;
-                        const int8_t cq = b.block_field[q];
-                        const int8_t rq = b.block_raw[q];
-                        const bool viol = (b.cell_count[q] > 0) && (rq < cq) && (cq > 0);
-                        if (viol && rq < spread) spread = rq;
-                    }
-                }
-            nw = cur < spread ? cur : spread;
+    const int tx = (nx + kMX - 1) / kMX, ty = (ny + kMY - 1) / kMY, tz = (nz + kMZ - 1) / kMZ;
+    const double sound_bound = xdiv(xmul(p.lambda_v, p.block_size), p.sound_speed);
+    const double rm = xmul(p.block_size, p.mass);
+    for (int t = blockIdx.x; t < tx * ty * tz; t += gridDim.x) {
+        const int bz = (t % tz) * kMZ, by = ((t / tz) % ty) * kMY, bx = (t / (tz * ty)) * kMX;
+        int cell[kMPer], cnt[kMPer];
+        int8_t cur[kMPer];
+        double vm[kMPer], fm[kMPer];
+#pragma unroll
+        for (int u = 0; u < kMPer; ++u) {
+            const int h = threadIdx.x + u * 256;
+            const int hz = h % kMHZ, hy = (h / kMHZ) % kMHY, hx = h / (kMHZ * kMHY);
+            const int cx = bx + hx - 1, cy = by + hy - 1, cz = bz + hz - 1;
+            const bool in = h < kMHalo && cx >= 0 && cx < nx && cy >= 0 && cy < ny && cz >= 0 &&
+                            cz < nz;
+            cell[u] = in ? (cx * ny + cy) * nz + cz : -1;
+            cnt[u] = in ? __ldg(b.cell_count + cell[u]) : 0;
+            cur[u] = in ? b.block_field[cell[u]] : 0;
         }
-        b.block_tmp[c] = nw;
-        b.block_flag[c] = nw < cur;
+#pragma unroll
+        for (int u = 0; u < kMPer; ++u) {
+            vm[u] = cnt[u] > 0 ? __ldg(b.vmax + cell[u]) : 0.0;
+            fm[u] = cnt[u] > 0 ? __ldg(b.fmax + cell[u]) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kMPer; ++u) {
+            const int h = threadIdx.x + u * 256;
+            if (h >= kMHalo) break;
+            const bool occ = cnt[u] > 0;
+            const int8_t raw = occ ? assign_from(p, vm[u], fm[u], sound_bound, rm) : 0;
+            const int hz = h % kMHZ, hy = (h / kMHZ) % kMHY, hx = h / (kMHZ * kMHY);
+            const bool interior = hx >= 1 && hx <= kMX && hy >= 1 && hy <= kMY && hz >= 1 &&
+                                  hz <= kMZ;
+            if (interior && cell[u] >= 0) b.block_raw[cell[u]] = raw;
+            s_viol[h] = (occ && raw < cur[u] && cur[u] > 0) ? raw : (int8_t)127;
+            s_cur[h] = cur[u];
+            s_occ[h] = occ;
+        }
+        __syncthreads();
+        for (int q = threadIdx.x; q < kMX * kMY * kMZ; q += blockDim.x) {
+            const int iz = q % kMZ, iy = (q / kMZ) % kMY, ix = q / (kMZ * kMY);
+            const int cx = bx + ix, cy = by + iy, cz = bz + iz;
+            if (cx >= nx || cy >= ny || cz >= nz) continue;
+            const int hc = ((ix + 1) * kMHY + iy + 1) * kMHZ + iz + 1;
+            const int8_t c0 = s_cur[hc];
+            int8_t nw = 0;
+            if (s_occ[hc]) {
+                int8_t spread = 127;  // out-of-grid halo blocks hold 127
+#pragma unroll
+                for (int dx = 0; dx < 3; ++dx)
+#pragma unroll
+                    for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+                        for (int dz = 0; dz < 3; ++dz) {
+                            const int8_t v = s_viol[((ix + dx) * kMHY + iy + dy) * kMHZ + iz + dz];
+                            spread = v < spread ? v : spread;
+                        }
+                nw = c0 < spread ? c0 : spread;
+            }
+            const int c = (cx * ny + cy) * nz + cz;
+            b.block_tmp[c] = nw;
+            b.block_flag[c] = nw < c0;
+        }
+        __syncthreads();
     }
 }
 
-__global__ void k_mark_apply(const __grid_constant__ RtsParams p, RtsBuffers b) {
-    RTS_MINOR_GUARD();
-    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < p.n_cells;
-         c += gridDim.x * blockDim.x)
-        b.block_field[c] = b.block_tmp[c];
-}
-
+// particle part + apply: particles of changed blocks take the new level, a
+// fresh validity and compute = 1; the new field replaces the old one (the
+// particle loop reads block_tmp, so the two loops need no ordering)
 __global__ void k_mark_particles(const __grid_constant__ RtsParams p, RtsBuffers b) {
     RTS_MINOR_GUARD();
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.n_fluid;
-         i += gridDim.x * blockDim.x) {
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+    for (int i = tid; i < p.n_fluid; i += nt) {
         const int c = b.fluid_cells[i];
         if (b.block_flag[c]) {
-            const int8_t r = b.block_field[c];
+            const int8_t r = b.block_tmp[c];
             b.region[i] = r;
             b.compute[i] = 1;
             b.validity[i] = kValidity[r < 0 ? 0 : (r > 4 ? 4 : r)];
         }
     }
+    for (int c = tid; c < p.n_cells; c += nt) b.block_field[c] = b.block_tmp[c];
 }
 
 __global__ void k_vel_max(const __grid_constant__ RtsParams p, RtsBuffers b) {
@@ -1699,11 +1749,15 @@ int rts_pci_integrate(const RtsParams *p, const RtsBuffers *b, int countdown, vo
 }
 
 int rts_pci_mark_updates(const RtsParams *p, const RtsBuffers *b, void *stream) {
+    // required levels (block_raw) included: rts_block_levels(expand = 2)
+    // before this call is not needed
     cudaStream_t s = (cudaStream_t)stream;
-    const int cb = rts_blocks(p->n_cells, 256);
-    rts_note_launch(), k_mark_blocks<<<cb, 256, 0, s>>>(*p, *b);
-    rts_note_launch(), k_mark_apply<<<cb, 256, 0, s>>>(*p, *b);
-    rts_note_launch(), k_mark_particles<<<rts_blocks(p->n_fluid, 256), 256, 0, s>>>(*p, *b);
+    const long long tiles = (long long)((p->dims[0] + kMX - 1) / kMX) *
+                            ((p->dims[1] + kMY - 1) / kMY) * ((p->dims[2] + kMZ - 1) / kMZ);
+    const int tb = (int)(tiles < 148 * 8 ? tiles : 148 * 8);
+    rts_note_launch(), k_mark_blocks<<<tb, 256, 0, s>>>(*p, *b);
+    rts_note_launch(), k_mark_particles<<<rts_blocks(p->n_fluid > p->n_cells ? p->n_fluid : p->n_cells,
+                                                     256), 256, 0, s>>>(*p, *b);
     RTS_LAUNCH_CHECK();
     return 0;
 }
@@ -1842,8 +1896,7 @@ int rts_pci_minor_tail(const RtsParams *p, const RtsBuffers *b, int minor, int l
         cudaMemsetAsync(b->vmax, 0, sizeof(double) * (size_t)p->n_cells, s);
         cudaMemsetAsync(b->fmax, 0, sizeof(double) * (size_t)p->n_cells, s);
         if ((rc = rts_pci_integrate(p, b, 3, stream))) return rc;  // includes S_ob / x* refresh
-        if ((rc = rts_block_levels(p, b, 2, stream))) return rc;
-        if ((rc = rts_pci_mark_updates(p, b, stream))) return rc;
+        if ((rc = rts_pci_mark_updates(p, b, stream))) return rc;  // required levels included
     } else if ((rc = rts_pci_integrate(p, b, 1, stream))) {
         return rc;
     }

@@ -589,8 +589,7 @@ class PcisphSolver(_DeviceSolver):
                         x.after_integrate(self)
                     if j != n_minor - 1:
                         self._call("rts_block_maxima", 1)
-                        self._call("rts_block_levels", 2)
-                        self._call("rts_pci_mark_updates")
+                        self._call("rts_pci_mark_updates")  # required levels included
                     self._call("rts_pci_minor_end", j)
         ctl, c = self._read_control()
         self._xstar_dirty = True
@@ -650,8 +649,7 @@ class PcisphSolver(_DeviceSolver):
         p = self.params
         p.n_max = min(self.n_regions, self.controller.n_current)
         self._call("rts_block_maxima", 1)
-        self._call("rts_block_levels", 2)
-        self._call("rts_pci_mark_updates")
+        self._call("rts_pci_mark_updates")  # required levels (block_raw) included
         if not launch_only:
             self._raise(self.counters.read(self._stream()))
 

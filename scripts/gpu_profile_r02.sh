@@ -13,7 +13,7 @@ done
 B="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-wcsph --no-e2e"
 $B > gpurun_out/${T}_plain.log 2>&1 || exit 1
 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/${T}_launches.csv $B > /dev/null 2>&1
-ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum,gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/${T}_traffic.csv $B > /dev/null 2>&1
+ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum,gpu__time_duration.sum,l1tex__data_pipe_lsu_wavefronts.sum.pct_of_peak_sustained_elapsed --clock-control none -c 2000 --csv --log-file gpurun_out/${T}_traffic.csv $B > /dev/null 2>&1
 ncu --set full --import-source on --clock-control none -k regex:"k_density|k_pforces" -c 2 -o gpurun_out/${T}_full_pair $B > /dev/null 2>&1
 ncu --set full --import-source on --clock-control none -k k_refresh -c 1 -o gpurun_out/${T}_full_refresh $B > /dev/null 2>&1
 W="python bench.py --workload cfg5-wcsph --steps 1 --warmup 1 --no-cpu-baseline --no-e2e"

@@ -1,6 +1,8 @@
 """profiles/ncu_traffic.json from an ncu --csv capture of
-dram__bytes_read.sum, dram__bytes_write.sum, lts__t_bytes.sum, gpu__time_duration.sum:
-mean DRAM (and L2) bytes per launch of each PCISPH entry point's main kernel.
+dram__bytes_read.sum, dram__bytes_write.sum, lts__t_bytes.sum, gpu__time_duration.sum and
+l1tex__data_pipe_lsu_wavefronts.sum.pct_of_peak_sustained_elapsed: mean DRAM (and L2)
+bytes per launch of each PCISPH entry point's main kernel, and the launch-time-weighted
+utilisation of the L1 LSU data pipe (the bound of the gather kernels).
 usage: python scripts/make_traffic.py gpurun_out/traffic_TAG.csv > profiles/ncu_traffic.json"""
 import collections
 import csv
@@ -20,7 +22,8 @@ for d in data:
         continue
     per[(name, d["ID"])][d["Metric Name"]] += float(d["Metric Value"].replace(",", ""))
 out = {"_how": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum,"
-               "gpu__time_duration.sum --clock-control none on bench.py --steps 2 --warmup 1 "
+               "gpu__time_duration.sum,l1tex__data_pipe_lsu_wavefronts.sum.pct_of_peak_sustained_"
+               "elapsed --clock-control none on bench.py --steps 2 --warmup 1 "
                "(cfg2 1M); mean bytes per launch over all launches of the kernel (cold-cache, "
                "serialised)"}
 agg = collections.defaultdict(list)
@@ -31,4 +34,9 @@ for name, ms in agg.items():
     out[e] = round(sum(m["dram__bytes_read.sum"] + m["dram__bytes_write.sum"] for m in ms) / len(ms))
     out[e + "_l2_bytes"] = round(sum(m["lts__t_bytes.sum"] for m in ms) / len(ms))
     out[e + "_launches"] = len(ms)
+    w = [(m.get("gpu__time_duration.sum", 0.0),
+          m.get("l1tex__data_pipe_lsu_wavefronts.sum.pct_of_peak_sustained_elapsed")) for m in ms]
+    w = [(t, x) for t, x in w if x is not None]
+    if w and sum(t for t, _ in w) > 0:
+        out[e + "_l1_wavefront_pct"] = round(sum(t * x for t, x in w) / sum(t for t, _ in w), 1)
 print(json.dumps(out, indent=1))
