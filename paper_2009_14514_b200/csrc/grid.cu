@@ -98,9 +98,6 @@ __global__ void k_boundary_active(const __grid_constant__ RtsParams p, RtsBuffer
 }
 
 // ---- exclusive scan of (cell_count + cell_bcount) into starts ----------
-constexpr int kScanThreads = 1024;
-constexpr int kScanItems = 4;
-constexpr int kScanTile = kScanThreads * kScanItems;
 
 __device__ __forceinline__ int block_incl_scan(int v, int *warp_sums) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
