@@ -366,7 +366,8 @@ def bench_config(workload: str, world: int, n_fluid: int, n_boundary: int) -> di
 def run_reference_arm(args, rank: int, world: int) -> None:
     """The reference path on the host: the CPU oracle (fp64 C/OpenMP
     restatement of the reference's numba kernels + numpy bookkeeping, all
-    host threads) on the same scene, the same --warmup and --steps."""
+    host threads) on the same scene, the same --warmup and --steps (the
+    N-rank scenes: as many steps as fit RTS_REF_BUDGET_S seconds)."""
     if rank != 0:
         return
     kind, wl_name, scaling = WORKLOADS[args.workload]
@@ -375,23 +376,30 @@ def run_reference_arm(args, rank: int, world: int) -> None:
     per_step = 1 if kind == "pcisph" else 4  # a WCSPH bench step = 4 base steps
     for _ in range(args.warmup * per_step):
         o.advance()
+    # the full --steps when they fit the wall budget (N = 1: ~2 min); the
+    # N-rank scenes (N M particles) stop at the budget, a bounded sample
+    budget = float(os.environ.get("RTS_REF_BUDGET_S", "240"))
     t0 = time.perf_counter()
-    units = 0
-    for _ in range(args.steps * per_step):
-        units += len(o.advance())
+    units, steps = 0, 0
+    while steps < args.steps and (steps == 0 or time.perf_counter() - t0 < budget):
+        for _ in range(per_step):
+            units += len(o.advance())
+        steps += 1
     dt = time.perf_counter() - t0
     v = nf * units / dt
+    what = (f"the full run: {steps} bench steps" if steps == args.steps else
+            f"a bounded sample: {steps} of the {args.steps} requested bench steps "
+            f"(wall budget {budget:g} s)")
     line = {
         "impl": "reference", "metric": METRICS[args.workload], "value": v, "unit": UNIT,
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * dt / max(1, args.steps),
+        "n_gpus": world, "steps": steps, "steps_requested": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * dt / max(1, steps),
         "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": bench_config(args.workload, world, nf, len(o.pos) - nf),
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": O.num_threads(), "kind": "port",
-                         "sample": f"the full run: {args.steps} bench steps ({units} updates "
-                                   f"of each of {nf} particles) after {args.warmup} untimed; "
-                                   "CPU oracle restating the reference"},
+                         "sample": f"{what} ({units} updates of each of {nf} particles) after "
+                                   f"{args.warmup} untimed; CPU oracle restating the reference"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "host_threads": O.num_threads(),
     }

@@ -61,3 +61,20 @@ def test_workload_table_is_complete():
         assert kind in ("pcisph", "wcsph") and scaling in ("weak", "strong")
         assert name in bench.METRICS and desc.startswith(name.split("-")[0])
     json.dumps(bench.WORKLOADS)
+
+
+def test_reference_arm_bounded_sample():
+    """--impl reference: one JSON line on the same config; past the wall
+    budget it reports the steps it actually timed (a bounded sample)."""
+    import os
+    env = dict(os.environ, RTS_REF_BUDGET_S="0.001")
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference",
+                          "--steps", "3", "--warmup", "0"],
+                         capture_output=True, text=True, env=env, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = json.loads(out.stdout.strip().splitlines()[-1])
+    assert d["impl"] == "reference" and d["steps"] == 1 and d["steps_requested"] == 3
+    assert "bounded sample" in d["cpu_baseline"]["sample"] and d["value"] > 0
+    assert d["config"] == bench.bench_config("cfg2", 1, d["config"]["n_fluid"],
+                                             d["config"]["n_boundary"])
+    assert d["e2e"]["value"] == d["value"]
