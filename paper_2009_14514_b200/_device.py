@@ -17,6 +17,21 @@ from .errors import NumericalError
 
 INT32_MAX = 2**31 - 1
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
+def raw_stream(index: int) -> int:
+    """cudaStream_t of the current stream of device ``index``: the cheap
+    query (torch.cuda.current_stream builds a Stream object per call, ~7 us,
+    which the host-driven paths pay on every launch)."""
+    if _raw_stream is not None:
+        return _raw_stream(index)
+    return torch.cuda.current_stream(index).cuda_stream
+
+
+def device_index(device: torch.device) -> int:
+    return device.index if device.index is not None else torch.cuda.current_device()
+
 
 def require_cuda(device) -> torch.device:
     dev = torch.device(device)

@@ -223,7 +223,13 @@ def note_graph_kernels(n: int) -> None:
     _graph_launched += int(n)
 
 
+_fns: dict = {}
+
+
 def call(name: str, *args) -> None:
-    rc = getattr(load(), name)(*args)
+    f = _fns.get(name)
+    if f is None:
+        f = _fns[name] = getattr(load(), name)
+    rc = f(*args)
     if rc != 0:
         raise NativeError(f"{name} failed with cudaError {rc}")

@@ -31,6 +31,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
+from ._device import device_index, raw_stream
 from .errors import ConfigError, NumericalError
 from .scene import Scene, seed_particles
 
@@ -410,7 +411,7 @@ class HaloChannel:
         if not self.peers:
             return
         N = self.N
-        st = torch.cuda.current_stream(self.x.compute_device).cuda_stream
+        st = raw_stream(device_index(self.x.compute_device))
         N.call("rts_halo_pack", ctypes.byref(self.pack_spec), self.send_rows.data_ptr(),
                self.send_rows.numel(), self.send_buf.data_ptr(), st)
         send, a = {}, 0
@@ -485,7 +486,7 @@ class PcisphExchange:
     def reduce(self, s) -> None:
         from . import _native as N
         self._channels(s)
-        st = torch.cuda.current_stream(self.x.compute_device).cuda_stream
+        st = raw_stream(device_index(self.x.compute_device))
         N.call("rts_ctl_publish", s.arena.buf, self._pub.data_ptr(), st)
         if self.x.device == self.x.compute_device:  # NCCL: gather in place, stream-ordered
             dist.all_gather_into_tensor(self._gath, self._pub)
@@ -554,7 +555,7 @@ class RankRows:
         if rows.numel():
             r = rows.to(torch.int32).contiguous()
             N.call("rts_halo_pack", ctypes.byref(sp), r.data_ptr(), r.numel(), out.data_ptr(),
-                   torch.cuda.current_stream(rows.device).cuda_stream)
+                   raw_stream(device_index(rows.device)))
         return out
 
     def unpack(self, rows: torch.Tensor, msg: torch.Tensor) -> None:
@@ -565,7 +566,7 @@ class RankRows:
         r = rows.to(torch.int32).contiguous()
         m = msg.to(rows.device, torch.int32).contiguous()
         N.call("rts_halo_unpack", ctypes.byref(sp), r.data_ptr(), r.numel(), m.data_ptr(),
-               torch.cuda.current_stream(rows.device).cuda_stream)
+               raw_stream(device_index(rows.device)))
 
 
 class _ResidentRank:

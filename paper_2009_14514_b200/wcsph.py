@@ -27,7 +27,8 @@ import numpy as np
 import torch
 
 from . import _native as N
-from ._device import Arena, Counters, PhaseTimer, raise_on_errors, require_cuda
+from ._device import (Arena, Counters, PhaseTimer, device_index, raise_on_errors, raw_stream,
+                      require_cuda)
 from .grid import BlockGrid
 from .kernels import KernelSet
 from .scene import TAIT_GAMMA, Scene, seed_particles
@@ -55,6 +56,7 @@ class _DeviceSolver:
     def _setup_common(self, scene: Scene, grid_mode: str, device):
         self.scene = scene
         self.device = require_cuda(device)
+        self._dev_idx = device_index(self.device)
         self.kernel = KernelSet(scene.support_radius)
         self.mass = scene.particle_mass
         self.mu = scene.viscosity * scene.rest_density
@@ -139,9 +141,9 @@ class _DeviceSolver:
         return [a.elapsed_time(b) * 1e-3 for a, b in (self._ktimes or {}).get(name, [])]
 
     def _launch(self, name: str, *args) -> None:
-        stream = torch.cuda.current_stream(self.device)
         kt = self._ktimes
         if kt is not None and name in kt:
+            stream = torch.cuda.current_stream(self.device)
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
             a.record(stream)
@@ -149,7 +151,7 @@ class _DeviceSolver:
             b.record(stream)
             kt[name].append((a, b))
         else:
-            N.call(name, self.params, self.arena.buf, *args, stream.cuda_stream)
+            N.call(name, self.params, self.arena.buf, *args, raw_stream(self._dev_idx))
 
     @property
     def pos(self) -> torch.Tensor:
