@@ -106,7 +106,10 @@ typedef struct RtsCounters {
     float    disp_total;       /* PCISPH: sum of disp_cur over the completed minor steps of
                                 * this major: bound on any coordinate's displacement since
                                 * the rebuild (the partial refreshes cull by it) */
-    double   reserved1;
+    int32_t  soa_fresh;        /* PCISPH: the x / y / z candidate copies match cpos (set by
+                                * the gather at a major start, cleared by the integrator,
+                                * which keeps only cpos current) */
+    int32_t  reserved1;
 } RtsCounters;
 
 /* Per-minor-step record written by the device loop control (StepStats,

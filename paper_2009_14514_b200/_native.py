@@ -41,7 +41,7 @@ class RtsCounters(_c.Structure):
         ("n_list", _I), ("fmax_bits", _c.c_uint64), ("sum_rho", _D), ("max_err", _D),
         ("any_se", _I), ("lists_all", _I), ("missing", _c.c_int64),
         ("blocks_done", _c.c_uint32), ("check_site", _I), ("stamps", _c.c_int64 * 4),
-        ("disp_cur", _c.c_float), ("disp_total", _c.c_float), ("reserved1", _D),
+        ("disp_cur", _c.c_float), ("disp_total", _c.c_float), ("soa_fresh", _c.c_int32), ("reserved1", _c.c_int32),
     ]
 
 

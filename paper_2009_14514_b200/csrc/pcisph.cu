@@ -40,6 +40,9 @@
 #ifndef RTS_PFOR_CH
 #define RTS_PFOR_CH 3
 #endif
+#ifndef RTS_RF_TWO_PHASE
+#define RTS_RF_TWO_PHASE 1  // one-thread refresh: slots in the scan, ids + f_ext in a second loop
+#endif
 #ifndef RTS_PFOR_MINB
 #define RTS_PFOR_MINB 5
 #endif
@@ -101,6 +104,7 @@ __global__ void k_gather(const __grid_constant__ RtsParams p, RtsBuffers b) {
         if (b.cx) b.cx[k] = x, b.cy[k] = y, b.cz[k] = z;
         if (j < p.n_fluid) b.slot_of[j] = k;
     }
+    if (b.cx && blockIdx.x == 0 && threadIdx.x == 0) b.ctr->soa_fresh = 1;
 }
 
 // _assign_major_regions per-particle tail (pcisph.py:531-534)
@@ -223,7 +227,7 @@ RTS_DEV void refresh_span(const RtsParams &p, const RtsBuffers &b, const Refresh
     // candidate; the rare in-band candidates then take the exact
     // fp64 test, and the members are emitted in candidate order.
     // Reads run up to 3 slots past the span (cpos is padded).
-    const bool soa = RTS_SOA && b.cx != nullptr;
+    const bool soa = RTS_SOA && b.cx != nullptr && b.ctr->soa_fresh;
     for (int cb = soa ? (k0 & ~3) : k0; cb < k1; cb += 32) {
         const int n = min(32, k1 - cb);
         const float4 *cp = cpos + cb;
@@ -272,6 +276,17 @@ RTS_DEV void refresh_span(const RtsParams &p, const RtsBuffers &b, const Refresh
                 const int q = __ffs(mem) - 1;
                 mem &= mem - 1u;
                 if (cntn < p.width) __stcs(row + cntn * S, __float_as_int(cp[q].w));
+                ++cntn;
+            }
+            continue;
+        }
+        if (RTS_RF_TWO_PHASE) {
+            // phase 1: the members' CSR slots, in candidate (= row) order;
+            // refresh_one's phase 2 turns them into ids and sums f_ext
+            while (mem) {
+                const int q = __ffs(mem) - 1;
+                mem &= mem - 1u;
+                if (cntn < p.width) row[cntn * S] = cb + q;
                 ++cntn;
             }
             continue;
@@ -432,6 +447,49 @@ RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshC
         return;
     }
     const int nrow = min(cntn, p.width);
+    if (G == 1 && RTS_RF_TWO_PHASE) {
+        // phase 2, uniform across the warp (every lane walks its own row,
+        // ~30 entries): slot -> candidate copy (id, current position) ->
+        // velocity; the row entry becomes the id and the viscosity term is
+        // summed in row order (fp32 terms, fp64 sum; pcisph.py:183-196).
+        // The per-chunk emission this replaces ran at ~13 of 32 lanes.
+        const int nsorted = b.ctr->n_sorted;
+        for (int q0 = 0; q0 < nrow; q0 += 4) {
+            int sl[4];
+            float4 o[4];
+            float vj[4][3];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                sl[u] = q0 + u < nrow ? rts_safe_idx(b.ctr, row[(q0 + u) * S], nsorted, 305, 0) : -1;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                o[u] = sl[u] >= 0 ? cpos[sl[u]] : make_float4(fxi, fyi, fzi, __int_as_float(i));
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int j = __float_as_int(o[u].w);
+                const int jc = j < p.n_fluid ? j : i;
+                vj[u][0] = b.vel[3 * jc];
+                vj[u][1] = b.vel[3 * jc + 1];
+                vj[u][2] = b.vel[3 * jc + 2];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (q0 + u >= nrow) break;
+                const int j = __float_as_int(o[u].w);
+                __stcs(row + (q0 + u) * S, j);
+                if (j < p.n_fluid && j != i) {
+                    const float dx = fxi - o[u].x, dy = fyi - o[u].y, dz = fzi - o[u].z;
+                    const float r = sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
+                    if (r < k.hf) {
+                        const float lap = k.visc_f * (k.hf - r);
+                        vfx += (double)(lap * (vj[u][0] - (float)vxi));
+                        vfy += (double)(lap * (vj[u][1] - (float)vyi));
+                        vfz += (double)(lap * (vj[u][2] - (float)vzi));
+                    }
+                }
+            }
+        }
+    }
     double fx = vfx, fy = vfy, fz = vfz;
     if (G > 1) {  // (G == 1: summed above, while the row was emitted)
         for (int q = lane; q < nrow; q += G) {
@@ -1182,7 +1240,6 @@ RTS_DEV void integrate_one(const RtsParams &p, const RtsBuffers &b, int i, int c
     if (countdown) {
         const int sl = rts_safe_idx(b.ctr, b.slot_of[i], b.ctr->n_sorted, 502, 0);
         reinterpret_cast<float4 *>(b.cpos)[sl] = make_float4(nx[0], nx[1], nx[2], __int_as_float(i));
-        if (b.cx) b.cx[sl] = nx[0], b.cy[sl] = nx[1], b.cz[sl] = nx[2];
         int v = b.validity[i] - 1;
         const bool expired = v <= 0;
         if (expired) {
@@ -1206,6 +1263,8 @@ __global__ void k_integrate(const __grid_constant__ RtsParams p, RtsBuffers b, i
     const int gen = b.ctl ? b.ctl->stamp : 0;
     if (b.ctl && countdown && blockIdx.x == 0 && threadIdx.x == 0)
         b.ctl->stats[b.ctl->minor].t_looped = gtimer();
+    // positions move: only cpos is kept current, the x / y / z copies go stale
+    if (blockIdx.x == 0 && threadIdx.x == 0) b.ctr->soa_fresh = 0;
     const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
     const int nf = p.n_fluid;
     float dmax = 0.f;  // max |dx| of one coordinate (refresh culling bound)
@@ -1262,7 +1321,6 @@ __global__ void k_integrate(const __grid_constant__ RtsParams p, RtsBuffers b, i
                 sob[q] = observed_block(b, cl[q], gen);
                 reinterpret_cast<float4 *>(b.cpos)[sl[q]] =
                     make_float4(x[3 * q], x[3 * q + 1], x[3 * q + 2], __int_as_float(4 * g + q));
-                if (b.cx) b.cx[sl[q]] = x[3 * q], b.cy[sl[q]] = x[3 * q + 1], b.cz[sl[q]] = x[3 * q + 2];
                 int vv = vl[q] - 1;
                 const bool expired = vv <= 0;
                 if (expired) vv = kValidity[rg[q] < 0 ? 0 : (rg[q] > 4 ? 4 : rg[q])];

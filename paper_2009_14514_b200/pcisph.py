@@ -20,6 +20,7 @@ import ctypes
 import dataclasses
 import itertools
 import math
+import os
 
 import numpy as np
 import torch
@@ -145,6 +146,11 @@ class PcisphSolver(_DeviceSolver):
     """PCISPH with ``mode`` "const", "adaptive" or "rts" (pcisph.py:279)."""
 
     mode_names = ("const", "adaptive", "rts")
+    # x / y / z candidate copies written by the major-start gather only: the
+    # full refresh of the first minor step searches them (packed fp32x2);
+    # the integrator keeps only cpos current and the later partial refreshes
+    # read that (RtsCounters.soa_fresh)
+    _soa_candidates = os.environ.get("RTS_PCI_SOA", "1") != "0"
 
     def __new__(cls, scene=None, *args, comm=None, **kw):
         """``comm`` (the default torch.distributed group): this process is one
