@@ -43,6 +43,9 @@
 #ifndef RTS_RF_TWO_PHASE
 #define RTS_RF_TWO_PHASE 1  // one-thread refresh: slots in the scan, ids + f_ext in a second loop
 #endif
+#ifndef RTS_RF_SBUF
+#define RTS_RF_SBUF 32  // row entries per thread kept in shared memory by the two-phase refresh
+#endif
 #ifndef RTS_PFOR_MINB
 #define RTS_PFOR_MINB 5
 #endif
@@ -219,7 +222,7 @@ template <bool EXT>
 RTS_DEV void refresh_span(const RtsParams &p, const RtsBuffers &b, const RefreshConsts &k, int i,
                           int k0, int k1, float fxi, float fyi, float fzi, double vxi, double vyi,
                           double vzi, int *row, size_t S, int &cntn, double &vfx, double &vfy,
-                          double &vfz) {
+                          double &vfz, int *sbuf) {
     const float4 *cpos = reinterpret_cast<const float4 *>(b.cpos);
     // Branch-free classification of 32 candidates at a time: two
     // 32-bit masks (r2 < h2_lo: member; r2 > h2_hi: not) built
@@ -286,7 +289,8 @@ RTS_DEV void refresh_span(const RtsParams &p, const RtsBuffers &b, const Refresh
             while (mem) {
                 const int q = __ffs(mem) - 1;
                 mem &= mem - 1u;
-                if (cntn < p.width) row[cntn * S] = cb + q;
+                if (cntn < RTS_RF_SBUF) sbuf[cntn * kThreads] = cb + q;
+                else if (cntn < p.width) row[cntn * S] = cb + q;
                 ++cntn;
             }
             continue;
@@ -364,7 +368,7 @@ RTS_DEV void refresh_span(const RtsParams &p, const RtsBuffers &b, const Refresh
 template <int G, bool EXT = true>
 RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshConsts &k, int i,
                          int two_layer_r1, int lane, unsigned gmask, int gshift, int lay_in = 0,
-                         double D = -1.0) {
+                         double D = -1.0, int *sbuf = nullptr) {
     const float4 *cpos = reinterpret_cast<const float4 *>(b.cpos);
     const int nx = p.dims[0], ny = p.dims[1], nz = p.dims[2];
     RTS_CHECK_IDX(b.ctr, i, p.n_fluid, 302);
@@ -424,7 +428,7 @@ RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshC
             RTS_CHECK(b.ctr, 0 <= k0 && k0 <= k1 && k1 <= b.ctr->n_sorted, 304);
             if (G == 1) {
                 refresh_span<EXT>(p, b, k, i, k0, k1, fxi, fyi, fzi, vxi, vyi, vzi, row, S, cntn,
-                                  vfx, vfy, vfz);
+                                  vfx, vfy, vfz, sbuf);
             } else {
                 for (int kb = k0; kb < k1; kb += G) {
                     const int kk = kb + lane;
@@ -460,7 +464,12 @@ RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshC
             float vj[4][3];
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-                sl[u] = q0 + u < nrow ? rts_safe_idx(b.ctr, row[(q0 + u) * S], nsorted, 305, 0) : -1;
+                sl[u] = q0 + u < nrow
+                            ? rts_safe_idx(b.ctr,
+                                           q0 + u < RTS_RF_SBUF ? sbuf[(q0 + u) * kThreads]
+                                                                : row[(q0 + u) * S],
+                                           nsorted, 305, 0)
+                            : -1;
 #pragma unroll
             for (int u = 0; u < 4; ++u)
                 o[u] = sl[u] >= 0 ? cpos[sl[u]] : make_float4(fxi, fyi, fzi, __int_as_float(i));
@@ -521,6 +530,10 @@ RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshC
 
 __global__ void __launch_bounds__(kThreads, RTS_REF_MINB) k_refresh(const __grid_constant__ RtsParams p,
                                                       RtsBuffers b, int two_layer_r1) {
+    // phase-1 member slots of the one-thread path: the first RTS_RF_SBUF
+    // entries of each row stay on chip (entry q of thread t at [q][t]:
+    // conflict-free), the rest go through the row itself
+    __shared__ int s_slots[(RTS_RF_SBUF > 0 ? RTS_RF_SBUF : 1) * kThreads];
     RTS_MINOR_GUARD();
     const int n = b.ctr->n_compute;
     const RefreshConsts k = refresh_consts(p);
@@ -546,7 +559,8 @@ __global__ void __launch_bounds__(kThreads, RTS_REF_MINB) k_refresh(const __grid
             refresh_one<4>(p, b, k, b.active[t], two_layer_r1, lane, gmask, gshift, 0, D);
     } else {
         for (int t = tid; t < n; t += nthreads)
-            refresh_one<1>(p, b, k, b.active[t], two_layer_r1, 0, 0u, 0, 0, RTS_CULL_G1 ? D : -1.0);
+            refresh_one<1>(p, b, k, b.active[t], two_layer_r1, 0, 0u, 0, 0, RTS_CULL_G1 ? D : -1.0,
+                           s_slots + threadIdx.x);
     }
 }
 
