@@ -46,6 +46,12 @@
 #ifndef RTS_RF_SBUF
 #define RTS_RF_SBUF 32  // row entries per thread kept in shared memory by the two-phase refresh
 #endif
+#ifndef RTS_RF_SOA_PF
+#define RTS_RF_SOA_PF 1  // refresh scan: next quad's loads in flight
+#endif
+#ifndef RTS_RF_P2
+#define RTS_RF_P2 4  // phase-2 entries in flight per thread
+#endif
 #ifndef RTS_PFOR_MINB
 #define RTS_PFOR_MINB 5
 #endif
@@ -237,8 +243,12 @@ RTS_DEV void refresh_span(const RtsParams &p, const RtsBuffers &b, const Refresh
         unsigned mem = 0u, out = 0u;  // first candidate ends in the top bit
         if (soa) {  // x / y / z copies: 4 candidates per load, fp32x2 tests
             unsigned amb;
-            classify_soa(b.cx, b.cy, b.cz, cb, n, k0, fxi, fyi, fzi, k.h2_lo, k.h2_hi,
-                         mem, amb);
+            if (RTS_RF_SOA_PF)
+                classify_soa_pf(b.cx, b.cy, b.cz, cb, n, k0, fxi, fyi, fzi, k.h2_lo, k.h2_hi,
+                                mem, amb);
+            else
+                classify_soa(b.cx, b.cy, b.cz, cb, n, k0, fxi, fyi, fzi, k.h2_lo, k.h2_hi,
+                             mem, amb);
             while (amb) {
                 const int q = __ffs(amb) - 1;
                 amb &= amb - 1u;
@@ -458,12 +468,12 @@ RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshC
         // summed in row order (fp32 terms, fp64 sum; pcisph.py:183-196).
         // The per-chunk emission this replaces ran at ~13 of 32 lanes.
         const int nsorted = b.ctr->n_sorted;
-        for (int q0 = 0; q0 < nrow; q0 += 4) {
-            int sl[4];
-            float4 o[4];
-            float vj[4][3];
+        for (int q0 = 0; q0 < nrow; q0 += RTS_RF_P2) {
+            int sl[RTS_RF_P2];
+            float4 o[RTS_RF_P2];
+            float vj[RTS_RF_P2][3];
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
+            for (int u = 0; u < RTS_RF_P2; ++u)
                 sl[u] = q0 + u < nrow
                             ? rts_safe_idx(b.ctr,
                                            q0 + u < RTS_RF_SBUF ? sbuf[(q0 + u) * kThreads]
@@ -471,10 +481,10 @@ RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshC
                                            nsorted, 305, 0)
                             : -1;
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
+            for (int u = 0; u < RTS_RF_P2; ++u)
                 o[u] = sl[u] >= 0 ? cpos[sl[u]] : make_float4(fxi, fyi, fzi, __int_as_float(i));
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < RTS_RF_P2; ++u) {
                 const int j = __float_as_int(o[u].w);
                 const int jc = j < p.n_fluid ? j : i;
                 vj[u][0] = b.vel[3 * jc];
@@ -482,7 +492,7 @@ RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshC
                 vj[u][2] = b.vel[3 * jc + 2];
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < RTS_RF_P2; ++u) {
                 if (q0 + u >= nrow) break;
                 const int j = __float_as_int(o[u].w);
                 __stcs(row + (q0 + u) * S, j);
@@ -525,7 +535,7 @@ RTS_DEV void refresh_one(const RtsParams &p, const RtsBuffers &b, const RefreshC
 #define RTS_CULL_G1 0  // culling in the one-thread-per-particle path (lanes diverge)
 #endif
 #ifndef RTS_REF_MINB
-#define RTS_REF_MINB 8
+#define RTS_REF_MINB 6  // 70 registers: 331 us full refresh vs 342 at 8 CTAs/SM (64 regs), 355 at 5
 #endif
 
 __global__ void __launch_bounds__(kThreads, RTS_REF_MINB) k_refresh(const __grid_constant__ RtsParams p,
