@@ -213,42 +213,6 @@ RTS_DEV void classify_soa(const float *cx, const float *cy, const float *cz, int
     amb_out = valid & ~mem & ~out;
 }
 
-// classify_soa with the next quad's three loads in flight while the current
-// quad is tested (the refresh's scan waits on these loads: long scoreboard)
-RTS_DEV void classify_soa_pf(const float *cx, const float *cy, const float *cz, int cb, int n,
-                             int k_lo, float fxi, float fyi, float fzi, float lo, float hi,
-                             unsigned &mem_out, unsigned &amb_out) {
-    const f32x2 P = f2_pack(fxi, fxi), Q = f2_pack(fyi, fyi), R = f2_pack(fzi, fzi);
-    const f32x2 L = f2_pack(lo, lo), H = f2_pack(hi, hi);
-    const ulonglong2 *X = reinterpret_cast<const ulonglong2 *>(cx + cb);
-    const ulonglong2 *Y = reinterpret_cast<const ulonglong2 *>(cy + cb);
-    const ulonglong2 *Z = reinterpret_cast<const ulonglong2 *>(cz + cb);
-    unsigned mem = 0u, out = 0u;
-    ulonglong2 x = X[0], y = Y[0], z = Z[0];
-    for (int u = 0; u < n; u += 4) {
-        // the arrays are padded past the last slot: one quad of read-ahead is safe
-        const ulonglong2 xn = X[(u >> 2) + 1], yn = Y[(u >> 2) + 1], zn = Z[(u >> 2) + 1];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const f32x2 ex = f2_sub(P, h ? x.y : x.x), ey = f2_sub(Q, h ? y.y : y.x),
-                        ez = f2_sub(R, h ? z.y : z.x);
-            const f32x2 r2 = f2_fma(ex, ex, f2_fma(ey, ey, f2_mul(ez, ez)));
-            const f32x2 m = f2_sub(r2, L), o = f2_sub(H, r2);
-            mem = __funnelshift_l((unsigned)m, mem, 1);
-            mem = __funnelshift_l((unsigned)(m >> 32), mem, 1);
-            out = __funnelshift_l((unsigned)o, out, 1);
-            out = __funnelshift_l((unsigned)(o >> 32), out, 1);
-        }
-        x = xn, y = yn, z = zn;
-    }
-    const int nr = (n + 3) & ~3;
-    unsigned valid = n == 32 ? 0xffffffffu : ((1u << n) - 1u);
-    if (k_lo > cb) valid &= ~((1u << (k_lo - cb)) - 1u);  // (k_lo - cb < 4)
-    mem = (__brev(mem) >> (32 - nr)) & valid;
-    out = (__brev(out) >> (32 - nr)) & valid;
-    mem_out = mem;
-    amb_out = valid & ~mem & ~out;
-}
 
 // 1/sqrt(r2) in fp64 from the fp32 estimate and one Newton step: relative
 // error ~1e-13 (the estimate's 2^-22 squared), 5 fp64 operations instead of

@@ -46,9 +46,6 @@
 #ifndef RTS_RF_SBUF
 #define RTS_RF_SBUF 32  // row entries per thread kept in shared memory by the two-phase refresh
 #endif
-#ifndef RTS_RF_SOA_PF
-#define RTS_RF_SOA_PF 1  // refresh scan: next quad's loads in flight
-#endif
 #ifndef RTS_RF_P2
 #define RTS_RF_P2 4  // phase-2 entries in flight per thread
 #endif
@@ -243,12 +240,8 @@ RTS_DEV void refresh_span(const RtsParams &p, const RtsBuffers &b, const Refresh
         unsigned mem = 0u, out = 0u;  // first candidate ends in the top bit
         if (soa) {  // x / y / z copies: 4 candidates per load, fp32x2 tests
             unsigned amb;
-            if (RTS_RF_SOA_PF)
-                classify_soa_pf(b.cx, b.cy, b.cz, cb, n, k0, fxi, fyi, fzi, k.h2_lo, k.h2_hi,
-                                mem, amb);
-            else
-                classify_soa(b.cx, b.cy, b.cz, cb, n, k0, fxi, fyi, fzi, k.h2_lo, k.h2_hi,
-                             mem, amb);
+            classify_soa(b.cx, b.cy, b.cz, cb, n, k0, fxi, fyi, fzi, k.h2_lo, k.h2_hi, mem,
+                         amb);
             while (amb) {
                 const int q = __ffs(amb) - 1;
                 amb &= amb - 1u;
