@@ -62,3 +62,39 @@ timed("upload pos+vel", up)
 timed("download pos+vel", down)
 timed("up + advance + down", both)
 timed("advance", lambda: s.advance())
+
+
+# chunked round trip: D2H of chunk c on the compute stream, H2D of chunk c on
+# a side stream as soon as its D2H landed (full-duplex PCIe); the next
+# advance() waits for the last H2D chunk
+side = torch.cuda.Stream(device=dev)
+NCH = int(os.environ.get("E2E_CHUNKS", "8"))
+evs = [torch.cuda.Event() for _ in range(2 * NCH)]
+
+
+def roundtrip():
+    main = torch.cuda.current_stream()
+    k = 0
+    for dsrc, hbuf in ((s.pos[:nf], hp), (s.vel, hv)):
+        n = dsrc.shape[0]
+        for c in range(NCH):
+            a, b = n * c // NCH, n * (c + 1) // NCH
+            hbuf[a:b].copy_(dsrc[a:b], non_blocking=True)
+            evs[k].record(main)
+            side.wait_event(evs[k])
+            with torch.cuda.stream(side):
+                dsrc[a:b].copy_(hbuf[a:b], non_blocking=True)
+            k += 1
+    done = torch.cuda.Event()
+    done.record(side)
+    main.wait_event(done)
+
+
+def both_chunked():
+    s.advance()
+    roundtrip()
+
+
+timed("roundtrip chunked alone", roundtrip)
+timed("advance + chunked roundtrip", both_chunked)
+timed("up + advance + down", both)
