@@ -646,11 +646,14 @@ def run_wcsph_workload(args, rank: int, world: int, device, barrier) -> None:
         dp, dv = dev_state()
         hp[:dp.shape[0]].copy_(dp)
         hv[:dv.shape[0]].copy_(dv)
+        nbytes = 0
+        rt = HostRoundTrip(device)
+        rt.upload(dev_state(), (hp, hv))  # one untimed e2e step first
+        driver.step()
+        rt.download(dev_state(), (hp, hv))
         torch.cuda.synchronize()
         barrier()
         t0 = time.perf_counter()
-        nbytes = 0
-        rt = HostRoundTrip(device)
         rt.upload(dev_state(), (hp, hv))  # the first step's inputs
         for k in range(k_e2e):
             n = dev_state()[0].shape[0]
@@ -882,12 +885,17 @@ def main():
         dp, dv = dev_state()
         hp_all[:dp.shape[0]].copy_(dp)
         hv_all[:dv.shape[0]].copy_(dv)
-        torch.cuda.synchronize()
-        barrier()
-        t0 = time.perf_counter()
         e_minors = 0
         nbytes = 0
         rt = HostRoundTrip(device)
+        # one untimed e2e step first (the graphs were last launched before the
+        # host-driven instrumented pass above)
+        rt.upload(dev_state(), (hp_all, hv_all))
+        driver.advance()
+        rt.download(dev_state(), (hp_all, hv_all))
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
         rt.upload(dev_state(), (hp_all, hv_all))  # the first step's inputs: host -> device
         for k in range(k_e2e):
             n = dev_state()[0].shape[0]

@@ -49,6 +49,12 @@
 #ifndef RTS_RF_P2
 #define RTS_RF_P2 4  // phase-2 entries in flight per thread
 #endif
+#ifndef RTS_MOTION_1PT
+#define RTS_MOTION_1PT 1  // all-particle motion: one particle per thread
+#endif
+#ifndef RTS_INTEG_1PT
+#define RTS_INTEG_1PT 0  // integrator: one particle per thread (measured +25 us per launch: not kept)
+#endif
 #ifndef RTS_PFOR_MINB
 #define RTS_PFOR_MINB 5
 #endif
@@ -632,6 +638,47 @@ __global__ void k_motion(const __grid_constant__ RtsParams p, RtsBuffers b, int 
     }
     const int nf = p.n_fluid, ng = nf / 4;
     XsRow *xsr = xs_rows(b);
+    if (RTS_MOTION_1PT) {
+        // one particle per thread: every thread of the grid streams (the
+        // four-per-thread path below left 3/4 of them idle), a warp's loads
+        // and its 32-byte row stores each cover one contiguous range
+        for (int i = tid; i < nf; i += nt) {
+            float fe[3], fp[3], v[3], x[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                fe[a] = b.force[3 * i + a];
+                v[a] = b.vel[3 * i + a];
+                x[a] = b.pos[3 * i + a];
+            }
+            double pr;
+            if (restore) {
+                pr = b.snap_p[i];
+#pragma unroll
+                for (int a = 0; a < 3; ++a) fp[a] = b.snap_fp[3 * i + a];
+            } else if (zero) {
+                pr = 0.0;
+                fp[0] = fp[1] = fp[2] = 0.f;
+            } else {
+                pr = xsr[i].p;
+#pragma unroll
+                for (int a = 0; a < 3; ++a) fp[a] = b.f_p[3 * i + a];
+            }
+            if (restore || zero) {
+#pragma unroll
+                for (int a = 0; a < 3; ++a) b.f_p[3 * i + a] = fp[a];
+                b.pres[i] = (float)pr;
+            }
+            if (is_ghost(b, i)) continue;  // x* / p of ghost rows: the owner's (halo)
+            double xs[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const double vv = xadd((double)v[a], xmul(dim, xadd((double)fe[a], (double)fp[a])));
+                xs[a] = xadd((double)x[a], xmul(p.dt, vv));
+            }
+            st_xs(xsr + i, xs[0], xs[1], xs[2], pr);
+        }
+        return;
+    }
     for (int g = tid; g < ng; g += nt) {
         float fe[12], fp[12], v[12], x[12];
         load12(b.force, g, fe);
@@ -1285,7 +1332,7 @@ __global__ void k_integrate(const __grid_constant__ RtsParams p, RtsBuffers b, i
     const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
     const int nf = p.n_fluid;
     float dmax = 0.f;  // max |dx| of one coordinate (refresh culling bound)
-    if (b.ghost) {
+    if (b.ghost || RTS_INTEG_1PT) {  // one particle per thread (the whole grid streams)
         for (int i = tid; i < nf; i += nt)
             if (!is_ghost(b, i)) integrate_one(p, b, i, countdown, gen, dim, dmax);
         note_displacement(b, countdown, dmax);
