@@ -26,9 +26,23 @@ b = torch.cuda.Event(enable_timing=True)
 tn = tp = tr = 0.0
 its = minors = 0
 corr = 0
+per = [[0.0, 0.0, 0.0, 0, 0] for _ in range(8)]  # by minor index: refresh, loop, tail, its, n
+between = []  # last minor's end of major k -> first minor's begin of major k+1 (ns)
+prev_end = None
 a.record(st)
 for _ in range(majors):
-    for r in s.advance():
+    rows_k = s.advance()
+    ctl = s._ctl_cache
+    if prev_end is not None:
+        between.append(ctl.stats[0].t_begin - prev_end)
+    prev_end = ctl.stats[len(rows_k) - 1].t_end
+    for m, r in enumerate(rows_k):
+        q = per[m]
+        q[0] += r.t_neighbor
+        q[1] += r.t_physics
+        q[2] += r.t_rts
+        q[3] += r.iterations
+        q[4] += 1
         tn += r.t_neighbor
         tp += r.t_physics
         tr += r.t_rts
@@ -43,3 +57,11 @@ print(f"major {tot * us:8.1f} us  (minors {minors / majors:.2f}, iterations/mino
       f"corrected/minor/nf {corr / max(minors, 1) / s.n_fluid:.3f})")
 print(f"  refresh phase {tn * us:8.1f} us   loop {tp * us:8.1f} us ({tp * 1e6 / max(its, 1):.1f} us/iteration)"
       f"   integrate+marking {tr * us:8.1f} us   rest (rebuild, levels, host) {(tot - tn - tp - tr) * us:8.1f} us")
+for m, q in enumerate(per):
+    if q[4]:
+        n = q[4]
+        print(f"  minor {m}: refresh {q[0] / n * 1e6:7.1f} us  loop {q[1] / n * 1e6:7.1f} us "
+              f"({q[3] / n:.2f} it)  tail {q[2] / n * 1e6:6.1f} us")
+if between:
+    print(f"  between majors (end of the last minor -> begin of the next major's first minor: "
+          f"host gap + rebuild + levels): {sum(between) / len(between) / 1e3:7.1f} us")
