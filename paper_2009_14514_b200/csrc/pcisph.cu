@@ -55,6 +55,9 @@
 #ifndef RTS_INTEG_1PT
 #define RTS_INTEG_1PT 0  // integrator: one particle per thread (measured +25 us per launch: not kept)
 #endif
+#ifndef RTS_MAJOR_FORK
+#define RTS_MAJOR_FORK 1  // major-step graph: gather || levels
+#endif
 #ifndef RTS_PFOR_MINB
 #define RTS_PFOR_MINB 5
 #endif
@@ -2088,16 +2091,30 @@ void *rts_pci_graph_create(const RtsParams *p, const RtsBuffers *b, int mode, in
         if ((rc = rts_pci_major_begin(p, b, cs))) break;
         if ((rc = rts_grid_keys(p, b, mode == 0, 1, cs))) break;
         if ((rc = rts_grid_sort(p, b, cs))) break;
-        if ((rc = rts_pci_gather(p, b, cs))) break;
         if (mode == 0) {
+            // {candidate gather} || {levels, major particles}: independent after
+            // the sort (gather: cpos / slot_of; levels: block fields, regions)
+            cudaStream_t side = cs;
+            cudaEvent_t *ev;
+            if (RTS_MAJOR_FORK) side_stream(1, &side, &ev);
+            if (RTS_MAJOR_FORK) {
+                cudaEventRecord(ev[0], cs);
+                cudaStreamWaitEvent(side, ev[0], 0);
+            }
+            if ((rc = rts_pci_gather(p, b, side))) break;
             if ((rc = rts_block_levels(p, b, 1, cs))) break;
             if ((rc = rts_pci_major_particles(p, b, cs))) break;
+            if (RTS_MAJOR_FORK) {
+                cudaEventRecord(ev[1], side);
+                cudaStreamWaitEvent(cs, ev[1], 0);
+            }
             for (int j = 0; j < n_minor && !rc; ++j) {
                 if ((rc = rts_pci_minor_head(p, b, j, cs))) break;
                 if ((rc = add_while_loop(cs, p, b, 0, local_attempts, iteration_cap))) break;
                 rc = rts_pci_minor_tail(p, b, j, j == n_minor - 1, cs);
             }
         } else {
+            if ((rc = rts_pci_gather(p, b, cs))) break;
             if ((rc = rts_pci_minor_begin(p, b, 0, 1, cs))) break;
             if ((rc = rts_pci_refresh(p, b, 1, 0, cs))) break;  // p, f_p = 0: first motion
             if ((rc = add_while_loop(cs, p, b, 1, local_attempts, iteration_cap))) break;
