@@ -257,6 +257,9 @@ __global__ void k_scatter(const __grid_constant__ RtsParams p, RtsBuffers b) {
 // Runs of up to 16 (most WCSPH blocks, many PCISPH ones) are sorted in
 // registers by a fully unrolled bitonic network (static indices, no local
 // memory); runs up to 32 by insertion in a local array, longer ones in place.
+#ifndef RTS_SORT_NET32
+#define RTS_SORT_NET32 1  // runs of 17-32: bitonic network instead of insertion sort
+#endif
 RTS_DEV void cswap(int &a, int &b) {
     const int lo = min(a, b), hi = max(a, b);
     a = lo;
@@ -291,14 +294,32 @@ __global__ void k_sort_runs(const __grid_constant__ RtsParams p, RtsBuffers b) {
                 if (q < n) run[q] = v[q];
         } else if (n <= 32) {  // 2.2-spacing blocks hold up to 27 lattice points
             int v[32];
-            for (int q = 0; q < n; ++q) v[q] = run[q];
-            for (int q = 1; q < n; ++q) {
-                const int key = v[q];
-                int r = q - 1;
-                while (r >= 0 && v[r] > key) { v[r + 1] = v[r]; --r; }
-                v[r + 1] = key;
+#pragma unroll
+            for (int q = 0; q < 32; ++q) v[q] = q < n ? run[q] : 0x7fffffff;
+            if (RTS_SORT_NET32) {  // bitonic network: no data-dependent branches
+#pragma unroll
+                for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+                    for (int j = k >> 1; j > 0; j >>= 1)
+#pragma unroll
+                        for (int q = 0; q < 32; ++q) {
+                            const int r = q ^ j;
+                            if (r > q) {
+                                if ((q & k) == 0) cswap(v[q], v[r]);
+                                else cswap(v[r], v[q]);
+                            }
+                        }
+            } else {
+                for (int q = 1; q < n; ++q) {
+                    const int key = v[q];
+                    int r = q - 1;
+                    while (r >= 0 && v[r] > key) { v[r + 1] = v[r]; --r; }
+                    v[r + 1] = key;
+                }
             }
-            for (int q = 0; q < n; ++q) run[q] = v[q];
+#pragma unroll
+            for (int q = 0; q < 32; ++q)
+                if (q < n) run[q] = v[q];
         } else {
             for (int q = 1; q < n; ++q) {
                 const int key = run[q];
