@@ -1624,84 +1624,116 @@ __global__ void k_minor_begin(RtsBuffers b, int minor, int sync_mode) {
 __global__ void k_control(const __grid_constant__ RtsParams p, RtsBuffers b, int sync_mode,
                           unsigned long long cond_handle, int local_attempts, int iteration_cap,
                           int n_part) {
-    RtsControl *c = b.ctl;
-    RtsCounters *ctr = b.ctr;
-    int done = c->done;
     (void)n_part;  // sum_rho: completed by k_se_reduce's last block (and all-reduced on ranks)
     if (threadIdx.x != 0) return;
+    RtsControl *c = b.ctl;
+    RtsCounters *ctr = b.ctr;
+    // One thread on the critical path of every iteration.  Every read comes
+    // first (they issue back to back: one memory round trip), then the
+    // decisions on registers, then every write -- with read-modify-writes in
+    // program order, in-order issue waited a full round trip per field.
+    int done = c->done;
+    int it = c->it, g_count = c->g_count, local_active = c->local_active;
+    int local_banned = c->local_banned, local_run = c->local_run, early = c->early;
+    int failed = c->failed, minor = c->minor, stamp = c->stamp;
+    int local_entered = c->local_entered, local_reverted = c->local_reverted;
+    long long corrected = c->corrected, forced = c->forced;
+    const int n_rows_m = c->n_rows[minor < 0 ? 0 : minor];
+    const int n_pred = ctr->n_pred, n_force = ctr->n_force, any_se = ctr->any_se;
+    const int lists_all = ctr->lists_all;
+    const unsigned err_flags = ctr->err_flags;
+    const double max_err = ctr->max_err, sum_rho = ctr->sum_rho;
     const int n_all = p.n_global > 0 ? p.n_global : p.n_fluid;
     if (!done) {
-        c->snap_op = 0;
-        c->it += 1;
-        c->corrected += sync_mode ? n_all : ctr->n_pred;
-        c->forced += sync_mode ? n_all : ctr->n_force;
-        if (c->local_active) c->local_run += 1; else c->g_count += 1;
-        const double max_err = ctr->max_err;
-        const double mean = n_all ? ctr->sum_rho / (double)n_all : 0.0;
+        int snap_op = 0, motion_all = 0, fail_kind = 0, fail_g = 0, row_mask = 0;
+        double fail_err = 0.0;
+        it += 1;
+        corrected += sync_mode ? n_all : n_pred;
+        forced += sync_mode ? n_all : n_force;
+        if (local_active) local_run += 1; else g_count += 1;
+        const double mean = n_all ? sum_rho / (double)n_all : 0.0;
         double avg = n_all ? xsub(xdiv(mean, p.rho0), 1.0) : 0.0;
         avg = avg > 0.0 ? avg : 0.0;
-        c->last_max_err = max_err;
-        c->last_avg_err = avg;
-        c->motion_all = 0;
         const bool converged = max_err < p.eta_max && avg < p.eta_avg;
-        if (ctr->err_flags & RTS_ERR_FATAL) {
+        const bool was_failed = failed;
+        if (err_flags & RTS_ERR_FATAL) {
             done = 1;
-            c->failed = 1;
-            c->fail_kind = (ctr->err_flags & RTS_ERR_NONFINITE) ? 1 : 4;
+            failed = 1;
+            fail_kind = (err_flags & RTS_ERR_NONFINITE) ? 1 : 4;
         } else if (sync_mode) {
-            c->motion_all = 1;
-            if (c->it >= 3 && converged) {
+            motion_all = 1;
+            if (it >= 3 && converged) {
                 done = 1;
-            } else if (c->it > iteration_cap + 3) {
+            } else if (it > iteration_cap + 3) {
                 done = 1;
-                c->failed = 1;
-                c->fail_kind = 3;
-                c->fail_g = c->it;
-                c->fail_err = max_err;
+                failed = 1;
+                fail_kind = 3;
+                fail_g = it;
+                fail_err = max_err;
             }
-        } else if (converged && c->it >= 3) {
+        } else if (converged && it >= 3) {
             done = 1;
-        } else if (!converged && c->it >= 3) {
-            if (c->local_active) {
-                if (c->local_run >= local_attempts) {
-                    c->snap_op = 2;  // revert p, f_p to the entry snapshot
-                    c->motion_all = 1;
-                    c->local_active = 0;
-                    c->local_banned = 1;
-                    c->local_reverted += 1;
+        } else if (!converged && it >= 3) {
+            if (local_active) {
+                if (local_run >= local_attempts) {
+                    snap_op = 2;  // revert p, f_p to the entry snapshot
+                    motion_all = 1;
+                    local_active = 0;
+                    local_banned = 1;
+                    local_reverted += 1;
                 }
-            } else if (xmul(avg, 100.0) < p.rho_T && !c->local_banned && ctr->any_se) {
-                c->local_active = 1;
-                c->local_run = 0;
-                c->snap_op = 1;
-                c->local_entered += 1;
+            } else if (xmul(avg, 100.0) < p.rho_T && !local_banned && any_se) {
+                local_active = 1;
+                local_run = 0;
+                snap_op = 1;
+                local_entered += 1;
             }
-            if (c->g_count > 6) c->early = 1;
-            if (c->g_count > iteration_cap) {
+            if (g_count > 6) early = 1;
+            if (g_count > iteration_cap) {
                 done = 1;
-                c->failed = 1;
-                c->fail_kind = 2;
-                c->fail_g = c->g_count;
-                c->fail_err = max_err;
+                failed = 1;
+                fail_kind = 2;
+                fail_g = g_count;
+                fail_err = max_err;
             }
         }
         if (!done && !sync_mode) {
-            if (c->local_active) {
-                c->row_mask = 0;
-            } else {
-                const int m = c->minor;
-                const int r = c->g_count % c->n_rows[m];
-                c->row_mask = c->row_masks[m][r];
-                add_row_iters(c, m, r);
+            if (!local_active) {
+                const int r = g_count % n_rows_m;
+                row_mask = c->row_masks[minor][r];
+                const int packed = c->row_counts[minor][r];  // add_row_iters
+                for (int n = 1; n <= 4; ++n) c->riters[n] += (packed >> (4 * n)) & 0xF;
             }
+            c->row_mask = row_mask;  // 0 = local pass
         }
-        if (c->failed) c->stop_major = 1;
+        if (lists_all) motion_all = 1;  // the force set was every particle
+        // writes
+        c->snap_op = snap_op;
+        c->it = it;
+        c->corrected = corrected;
+        c->forced = forced;
+        c->local_run = local_run;
+        c->g_count = g_count;
+        c->local_active = local_active;
+        c->local_banned = local_banned;
+        c->local_entered = local_entered;
+        c->local_reverted = local_reverted;
+        c->early = early;
+        c->last_max_err = max_err;
+        c->last_avg_err = avg;
+        c->motion_all = motion_all;
+        if (failed && !was_failed) {
+            c->failed = 1;
+            c->fail_kind = fail_kind;
+            c->fail_g = fail_g;
+            c->fail_err = fail_err;
+        }
+        if (failed) c->stop_major = 1;
         c->done = done;
         // hand-over to the next iteration: motion list length, fresh counts,
         // the S_e generation just written by k_se_reduce becomes current
-        c->prev_force = ctr->n_force;
-        if (ctr->lists_all) c->motion_all = 1;  // the force set was every particle
-        c->stamp += 1;
+        c->prev_force = n_force;
+        c->stamp = stamp + 1;
         if (!done) {
             ctr->lists_all = 0;
             ctr->n_pred = 0;
