@@ -1584,15 +1584,21 @@ RTS_DEV void add_row_iters(RtsControl *c, int minor, int row) {
 // state reset of _correct_scheduled (pcisph.py:618-631) + first row; S_e = {}
 __global__ void k_minor_begin(RtsBuffers b, int minor, int sync_mode) {
     RtsControl *c = b.ctl;
-    c->skipped = c->stop_major;
-    if (c->stop_major) {
+    // reads first, then writes (one round trip, see k_control)
+    const int stop = c->stop_major;
+    const float disp_total = b.ctr->disp_total, disp_cur = b.ctr->disp_cur;
+    const int row_mask0 = sync_mode ? 0 : c->row_masks[minor][0];
+    const int packed0 = sync_mode ? 0 : c->row_counts[minor][0];
+    const int stamp = c->stamp;
+    c->skipped = stop;
+    if (stop) {
         c->done = 1;
         return;
     }
     c->minor = minor;
     c->stats[minor].t_begin = gtimer();
     // refresh culling: the last minor step's displacement joins the bound
-    b.ctr->disp_total = __fadd_ru(b.ctr->disp_total, b.ctr->disp_cur);
+    b.ctr->disp_total = __fadd_ru(disp_total, disp_cur);
     b.ctr->disp_cur = 0.f;
     c->it = c->g_count = c->local_active = c->local_banned = c->local_run = 0;
     c->early = 0;
@@ -1602,7 +1608,7 @@ __global__ void k_minor_begin(RtsBuffers b, int minor, int sync_mode) {
     for (int n = 0; n < 5; ++n) c->riters[n] = 0;
     c->motion_all = 1;
     c->snap_op = 0;
-    c->stamp += 1;  // fresh S_e generation: S_e = {} (pcisph.py:618)
+    c->stamp = stamp + 1;  // fresh S_e generation: S_e = {} (pcisph.py:618)
     c->prev_force = 0;
     b.ctr->n_pred = 0;
     b.ctr->n_force = 0;
@@ -1610,8 +1616,9 @@ __global__ void k_minor_begin(RtsBuffers b, int minor, int sync_mode) {
     b.ctr->max_err = 0.0;
     b.ctr->any_se = 0;
     if (!sync_mode) {
-        c->row_mask = c->row_masks[minor][0];
-        add_row_iters(c, minor, 0);
+        c->row_mask = row_mask0;
+        // add_row_iters on the riters just zeroed above
+        for (int n = 1; n <= 4; ++n) c->riters[n] = (packed0 >> (4 * n)) & 0xF;
     } else {
         c->row_mask = 0x1E;
     }
@@ -1748,17 +1755,23 @@ __global__ void k_control(const __grid_constant__ RtsParams p, RtsBuffers b, int
 __global__ void k_minor_end(RtsBuffers b, int minor) {
     RtsControl *c = b.ctl;
     if (c->skipped) return;
+    // reads first, then writes (one round trip, see k_control)
+    const int it = c->it, n_refresh = b.ctr->n_compute, early = c->early, failed = c->failed;
+    int riters[5];
+    for (int n = 0; n < 5; ++n) riters[n] = c->riters[n];
+    const long long corrected = c->corrected, forced = c->forced;
+    const double max_err = c->last_max_err, avg_err = c->last_avg_err;
     RtsMinorStats &s = c->stats[minor];
-    s.iterations = c->it;
-    s.n_refresh = b.ctr->n_compute;
-    s.early = c->early;
-    for (int n = 0; n < 5; ++n) s.riters[n] = c->riters[n];
-    s.corrected = c->corrected;
-    s.forced = c->forced;
-    s.max_err = c->last_max_err;
-    s.avg_err = c->last_avg_err;
+    s.iterations = it;
+    s.n_refresh = n_refresh;
+    s.early = early;
+    for (int n = 0; n < 5; ++n) s.riters[n] = riters[n];
+    s.corrected = corrected;
+    s.forced = forced;
+    s.max_err = max_err;
+    s.avg_err = avg_err;
     s.t_end = gtimer();
-    if (c->early || c->failed) c->stop_major = 1;
+    if (early || failed) c->stop_major = 1;
 }
 // count_missing (grid.py:165-212): one block layer of the fresh audit grid
 // `a` around the particle's current block; true neighbours (fp64) missing
