@@ -58,6 +58,9 @@
 #ifndef RTS_MAJOR_FORK
 #define RTS_MAJOR_FORK 1  // major-step graph: gather || levels
 #endif
+#ifndef RTS_SETS_CAP
+#define RTS_SETS_CAP (148 * 32)
+#endif
 #ifndef RTS_PFOR_MINB
 #define RTS_PFOR_MINB 5
 #endif
@@ -1871,7 +1874,9 @@ int rts_pci_motion(const RtsParams *p, const RtsBuffers *b, int all, void *strea
 int rts_pci_sets(const RtsParams *p, const RtsBuffers *b, int row_mask, int all_pred,
                  void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
-    rts_note_launch(), k_sets<<<rts_blocks(p->n_fluid, 256, 148 * 4), 256, 0, s>>>(*p, *b, row_mask, all_pred);
+    // one trip of four particles per thread over the whole fluid
+    rts_note_launch(), k_sets<<<rts_blocks(((long long)p->n_fluid + 3) / 4, 256, RTS_SETS_CAP), 256, 0, s>>>(
+        *p, *b, row_mask, all_pred);
     RTS_LAUNCH_CHECK();
     return 0;
 }
