@@ -61,6 +61,9 @@
 #ifndef RTS_SETS_CAP
 #define RTS_SETS_CAP (148 * 32)
 #endif
+#ifndef RTS_RLIST_CAP
+#define RTS_RLIST_CAP (148 * 64)
+#endif
 #ifndef RTS_PFOR_MINB
 #define RTS_PFOR_MINB 5
 #endif
@@ -1849,7 +1852,9 @@ int rts_pci_refresh(const RtsParams *p, const RtsBuffers *b, int all, int two_la
                     void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
     cudaMemsetAsync(&b->ctr->n_compute, 0, sizeof(int), s);
-    rts_note_launch(), k_refresh_list<<<rts_blocks(p->n_fluid, 256, 148 * 4), 256, 0, s>>>(*p, *b, all);
+    // one 256-slot chunk per CTA over every CSR slot (fluid and walls)
+    rts_note_launch(), k_refresh_list<<<rts_blocks((long long)p->n_fluid + p->n_bound, 256,
+                                                   RTS_RLIST_CAP), 256, 0, s>>>(*p, *b, all);
     RTS_LAUNCH_CHECK();
     rts_note_launch(), k_refresh<<<pass_blocks(p), kThreads, 0, s>>>(*p, *b, two_layer_r1);
     RTS_LAUNCH_CHECK();
