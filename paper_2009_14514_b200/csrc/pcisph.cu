@@ -64,6 +64,9 @@
 #ifndef RTS_RLIST_CAP
 #define RTS_RLIST_CAP (148 * 64)
 #endif
+#ifndef RTS_INTEG_GRID4
+#define RTS_INTEG_GRID4 1
+#endif
 #ifndef RTS_PFOR_MINB
 #define RTS_PFOR_MINB 5
 #endif
@@ -1927,7 +1930,9 @@ int rts_pci_pforces(const RtsParams *p, const RtsBuffers *b, void *stream) {
 }
 
 int rts_pci_integrate(const RtsParams *p, const RtsBuffers *b, int countdown, void *stream) {
-    const int nb = rts_blocks(p->n_fluid, 256);
+    // four particles per thread without ghost rows, one with them
+    const int nb = rts_blocks(b->ghost || !RTS_INTEG_GRID4 ? p->n_fluid : ((long long)p->n_fluid + 3) / 4,
+                              256);
     cudaStream_t s = (cudaStream_t)stream;
     if (countdown & 2)
         rts_note_launch(), k_integrate<true><<<nb, 256, 0, s>>>(*p, *b, countdown);
