@@ -13,6 +13,10 @@
 // reference's from a common state; only the final fp32 store rounds.
 #include "common.cuh"
 
+#ifndef RTS_WINT_GRID4
+#define RTS_WINT_GRID4 1
+#endif
+
 // WCSPH force pass: table entries per gather chunk (1 = one at a time;
 // scripts/build_variant.sh A/B)
 #ifndef RTS_WF_CH
@@ -555,7 +559,9 @@ int rts_wcsph_forces(const RtsParams *p, const RtsBuffers *b, void *stream) {
 
 int rts_wcsph_integrate(const RtsParams *p, const RtsBuffers *b, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
-    rts_note_launch(), k_integrate<<<rts_blocks(p->n_fluid, 256), 256, 0, s>>>(*p, *b);
+    // four particles per thread
+    rts_note_launch(), k_integrate<<<rts_blocks(((long long)p->n_fluid + 3) / (RTS_WINT_GRID4 ? 4 : 1), 256),
+                                     256, 0, s>>>(*p, *b);
     RTS_LAUNCH_CHECK();
     return 0;
 }
