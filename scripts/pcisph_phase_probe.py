@@ -15,7 +15,7 @@ import bench  # noqa: E402
 majors = int(sys.argv[1]) if len(sys.argv) > 1 else 6
 dev = torch.device("cuda", 0)
 s = bench.make_device_solver("pcisph", dev, os.environ.get("WL", "cfg2"))
-for _ in range(3):
+for _ in range(int(os.environ.get("WARM", "3"))):
     s.advance()
 torch.cuda.synchronize()
 st = torch.cuda.current_stream()
