@@ -876,8 +876,8 @@ def main():
         # go up before and come back after every advance().  One GPU: a fresh
         # solver from the same seeded start runs the same W + K majors as the
         # device-timed region (the e2e number covers the same stretch of the
-        # simulation as `value` and the reference arm); x-slab ranks: K' = 10
-        # majors of the running decomposition.
+        # simulation as `value` and the reference arm); x-slab ranks: K' =
+        # min(K, 10) majors of the running decomposition.
         e_solver = None
         if world == 1:
             e_solver = make_device_solver("pcisph", device, args.workload)
@@ -932,7 +932,7 @@ def main():
                "note": ("pinned host pos+vel uploaded before and downloaded after every "
                         "advance() (the two PCIe directions overlapped: HostRoundTrip); wall "
                         "clock; " + ("a fresh solver over the same W + K majors as `value`"
-                                     if world == 1 else "10 majors after the timed region"))}
+                                     if world == 1 else "min(K, 10) majors after the timed region"))}
         del e_solver
 
     # ---- WCSPH extra (configs[2]: the 1M scene, RTS-WCSPH vs the global -------
