@@ -265,6 +265,27 @@ RTS_DEV void cswap(int &a, int &b) {
     a = lo;
     b = hi;
 }
+RTS_DEV void cswap(long long &a, long long &b) {
+    const long long lo = min(a, b), hi = max(a, b);
+    a = lo;
+    b = hi;
+}
+// ascending bitonic sorting network over N registers (N a power of two)
+template <int N, class T>
+RTS_DEV void bitonic(T (&v)[N]) {
+#pragma unroll
+    for (int k = 2; k <= N; k <<= 1)
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1)
+#pragma unroll
+            for (int q = 0; q < N; ++q) {
+                const int r = q ^ j;
+                if (r > q) {
+                    if ((q & k) == 0) cswap(v[q], v[r]);
+                    else cswap(v[r], v[q]);
+                }
+            }
+}
 
 __global__ void k_sort_runs(const __grid_constant__ RtsParams p, RtsBuffers b) {
     if (fatal(b.ctr)) return;
@@ -344,16 +365,22 @@ __global__ void k_sort_runs_keyed(const __grid_constant__ RtsParams p, RtsBuffer
         auto key = [&](int i) {
             return ((long long)b.sort_key[i] << 32) | (unsigned)i;
         };
-        if (n <= 32) {
+        if (n <= 16) {  // (global id, row) keys through register bitonic networks
+            long long v[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) v[q] = q < n ? key(run[q]) : 0x7fffffffffffffffll;
+            bitonic<16>(v);
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+                if (q < n) run[q] = (int)(v[q] & 0xffffffffll);
+        } else if (n <= 32) {
             long long v[32];
-            for (int q = 0; q < n; ++q) v[q] = key(run[q]);
-            for (int q = 1; q < n; ++q) {
-                const long long k = v[q];
-                int r = q - 1;
-                while (r >= 0 && v[r] > k) { v[r + 1] = v[r]; --r; }
-                v[r + 1] = k;
-            }
-            for (int q = 0; q < n; ++q) run[q] = (int)(v[q] & 0xffffffffll);
+#pragma unroll
+            for (int q = 0; q < 32; ++q) v[q] = q < n ? key(run[q]) : 0x7fffffffffffffffll;
+            bitonic<32>(v);
+#pragma unroll
+            for (int q = 0; q < 32; ++q)
+                if (q < n) run[q] = (int)(v[q] & 0xffffffffll);
         } else {
             for (int q = 1; q < n; ++q) {
                 const int x = run[q];
