@@ -26,7 +26,7 @@
 #define RTS_DENS_PF 1
 #endif
 #ifndef RTS_DENS_CH
-#define RTS_DENS_CH 3
+#define RTS_DENS_CH 2
 #endif
 #ifndef RTS_DENS_MINB
 #define RTS_DENS_MINB 8
@@ -38,7 +38,7 @@
 #define RTS_LG_CH 3
 #endif
 #ifndef RTS_PFOR_CH
-#define RTS_PFOR_CH 3
+#define RTS_PFOR_CH 2
 #endif
 #ifndef RTS_RF_TWO_PHASE
 #define RTS_RF_TWO_PHASE 1  // one-thread refresh: slots in the scan, ids + f_ext in a second loop
@@ -68,7 +68,7 @@
 #define RTS_INTEG_GRID4 1
 #endif
 #ifndef RTS_PFOR_MINB
-#define RTS_PFOR_MINB 5
+#define RTS_PFOR_MINB 7
 #endif
 
 using namespace rts;
