@@ -1892,7 +1892,7 @@ int rts_pci_sets(const RtsParams *p, const RtsBuffers *b, int row_mask, int all_
 int rts_pci_density(const RtsParams *p, const RtsBuffers *b, void *stream) {
     const int nb = pass_blocks(p);
     cudaStream_t s = (cudaStream_t)stream;
-    // 4-deep chunks, <= 48 registers: 10 CTAs of 128 threads per SM
+    // 2-chunk gather pipeline, 64 registers: 8 CTAs of 128 threads per SM
     rts_note_launch(), k_density<RTS_DENS_CH, RTS_DENS_MINB><<<nb, kThreads, 0, s>>>(*p, *b);
     RTS_LAUNCH_CHECK();
     return 0;
