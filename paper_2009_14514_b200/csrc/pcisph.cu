@@ -70,6 +70,12 @@
 #ifndef RTS_PFOR_MINB
 #define RTS_PFOR_MINB 7
 #endif
+#ifndef RTS_PAIR_CARVEOUT
+#define RTS_PAIR_CARVEOUT 0  // shared-memory carveout (%) asked for the pair passes (0: largest L1; -1: driver default)
+#endif
+#ifndef RTS_PAIR_CAP
+#define RTS_PAIR_CAP (148 * 32)  // grid cap of the pair passes (CTAs of kThreads)
+#endif
 
 using namespace rts;
 
@@ -855,7 +861,15 @@ constexpr int kPG = 8;
 // chains per thread) serve latency-bound desk-scale runs.  Large scenes are
 // unaffected (the cap binds).
 static inline int pass_blocks(const RtsParams *p) {
-    return rts_blocks((long long)p->n_fluid * kPG, kThreads);
+    return rts_blocks((long long)p->n_fluid * kPG, kThreads, RTS_PAIR_CAP);
+}
+
+// the pair passes use no shared memory: ask for the largest L1 once
+template <class K>
+static inline void pair_carveout(K kernel) {
+    if (RTS_PAIR_CARVEOUT >= 0)
+        cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             RTS_PAIR_CARVEOUT);
 }
 
 
@@ -1893,6 +1907,8 @@ int rts_pci_density(const RtsParams *p, const RtsBuffers *b, void *stream) {
     const int nb = pass_blocks(p);
     cudaStream_t s = (cudaStream_t)stream;
     // 2-chunk gather pipeline, 64 registers: 8 CTAs of 128 threads per SM
+    static bool once = (pair_carveout(k_density<RTS_DENS_CH, RTS_DENS_MINB>), true);
+    (void)once;
     rts_note_launch(), k_density<RTS_DENS_CH, RTS_DENS_MINB><<<nb, kThreads, 0, s>>>(*p, *b);
     RTS_LAUNCH_CHECK();
     return 0;
@@ -1924,6 +1940,8 @@ int rts_pci_sob(const RtsParams *p, const RtsBuffers *b, void *stream) {
 int rts_pci_pforces(const RtsParams *p, const RtsBuffers *b, void *stream) {
     const int nb = pass_blocks(p);
     cudaStream_t s = (cudaStream_t)stream;
+    static bool once = (pair_carveout(k_pforces<RTS_PFOR_CH, RTS_PFOR_MINB>), true);
+    (void)once;
     rts_note_launch(), k_pforces<RTS_PFOR_CH, RTS_PFOR_MINB><<<nb, kThreads, 0, s>>>(*p, *b);
     RTS_LAUNCH_CHECK();
     return 0;
