@@ -8,6 +8,8 @@ these buffers is a librtssph kernel.
 from __future__ import annotations
 
 import ctypes
+import functools
+import os
 
 import numpy as np
 import torch
@@ -27,6 +29,28 @@ def raw_stream(index: int) -> int:
     if _raw_stream is not None:
         return _raw_stream(index)
     return torch.cuda.current_stream(index).cuda_stream
+
+
+NVTX = os.environ.get("RTS_SPH_NVTX", "0") not in ("", "0")
+
+
+def nvtx_range(name: str):
+    """Decorator: an NVTX range around a host-side phase (major step, base
+    step, slab exchange) when RTS_SPH_NVTX=1, so a timeline capture shows the
+    solver's phases over its kernels; the undecorated function otherwise."""
+    def wrap(fn):
+        if not NVTX:
+            return fn
+
+        @functools.wraps(fn)
+        def inner(*a, **kw):
+            torch.cuda.nvtx.range_push(name)
+            try:
+                return fn(*a, **kw)
+            finally:
+                torch.cuda.nvtx.range_pop()
+        return inner
+    return wrap
 
 
 def device_index(device: torch.device) -> int:

@@ -31,7 +31,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from ._device import device_index, raw_stream
+from ._device import device_index, nvtx_range, raw_stream
 from .errors import ConfigError, NumericalError
 from .scene import Scene, seed_particles
 
@@ -717,6 +717,7 @@ class _ResidentRank:
             self._one_round = min(widths) > self.part.halo + 1
         return self._one_round
 
+    @nvtx_range("rts_slab.exchange")
     def _exchange(self) -> None:
         """Migration + fresh ghost band (one round when ``_single_round``)."""
         if getattr(self, "_force_two_rounds", False) or not self._single_round():

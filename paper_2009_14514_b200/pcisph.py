@@ -26,7 +26,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from ._device import raise_on_errors
+from ._device import nvtx_range, raise_on_errors
 from .errors import ConfigError, NumericalError
 from .scene import Scene
 from .stats import StepStats
@@ -487,6 +487,7 @@ class PcisphSolver(_DeviceSolver):
         N.call("rts_memset", self.arena.buf.f_p, 0, 12 * nf, s) if nf else None
 
     # -- synchronous baselines (pcisph.py:376-476) ------------------------------
+    @nvtx_range("rts_pcisph.sync_step")
     def sync_step(self) -> StepStats:
         """Synchronous baseline step (pcisph.py:376-419): rebuild, full
         search + external forces, the standard correction loop (device
@@ -551,6 +552,7 @@ class PcisphSolver(_DeviceSolver):
             self.dt = max(self.dt * 0.8, 0.1 * self.scene.const_dt())
 
     # -- regional mode (pcisph.py:482-768) -----------------------------------
+    @nvtx_range("rts_pcisph.major_step")
     def major_step(self) -> list[StepStats]:
         """One major step of N minor steps (pcisph.py:482-505).  With
         ``use_graphs`` (default) the whole major -- rebuild, region

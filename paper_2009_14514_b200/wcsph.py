@@ -27,8 +27,8 @@ import numpy as np
 import torch
 
 from . import _native as N
-from ._device import (Arena, Counters, PhaseTimer, device_index, raise_on_errors, raw_stream,
-                      require_cuda)
+from ._device import (Arena, Counters, PhaseTimer, device_index, nvtx_range, raise_on_errors,
+                      raw_stream, require_cuda)
 from .grid import BlockGrid
 from .kernels import KernelSet
 from .scene import TAIT_GAMMA, Scene, seed_particles
@@ -392,6 +392,7 @@ class WcsphSolver(_DeviceSolver):
     def advance(self) -> list[StepStats]:
         return [self.step()]
 
+    @nvtx_range("rts_wcsph.step")
     def step(self) -> StepStats:
         if self.mode == "rts":
             dt = self.dt_base

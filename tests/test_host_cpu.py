@@ -212,3 +212,18 @@ def test_schedule_validation_matches_the_reference_rules_on_random_schedules():
         assert a == b, (sch, a, b)
         legal += a is None
     assert legal > 0
+
+
+def test_nvtx_ranges_are_opt_in():
+    """RTS_SPH_NVTX unset: the solvers' phase methods are the plain functions
+    (no wrapper on the hot host path); set: each is wrapped in an NVTX range."""
+    import subprocess
+    import sys
+    code = ("import paper_2009_14514_b200.pcisph as P, paper_2009_14514_b200.wcsph as W;"
+            "print(hasattr(P.PcisphSolver.major_step, '__wrapped__'),"
+            " hasattr(W.WcsphSolver.step, '__wrapped__'))")
+    for flag, want in (("0", "False False"), ("1", "True True")):
+        env = dict(os.environ, RTS_SPH_NVTX=flag)
+        out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                             check=True, cwd=os.path.dirname(os.path.dirname(__file__)))
+        assert out.stdout.strip() == want
